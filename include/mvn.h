@@ -1,0 +1,191 @@
+/*
+ * mvn.h — C ABI of libmvn.so, the B200-native (sm_100a) hot path of arXiv 2405.14892:
+ * confidence-region detection from high-dimensional multivariate normal (MVN) probabilities.
+ *
+ *   geometry, theta = (sigma^2, beta, nu), u, 1-alpha            (problem statement)
+ *     -> mvn_marginal_order   p_M, descending order, limits      (Alg. 1 l.3-6)
+ *     -> mvn_cov_matern       Sigma tiles in sorted order         (Eq. 6; Alg. 1 l.2)
+ *     -> mvn_potrf            Sigma = L L^T in place              (Alg. 1 l.8)
+ *     -> mvn_sov_prefix       one SOV/QMC sweep -> per-prefix     (Alg. 2-3; Eq. 2-3)
+ *                             log-sum-exp partials (M_k, S_k)
+ *     -> mvn_prefix_finalize  log P_k                             (Alg. 2 l.19 mean(p))
+ *     -> mvn_confidence_region k*(1-alpha)                        (Eq. 4-5)
+ *
+ * Citations: P:n = PAPER.md line n; R-numbers = readings in DESIGN.md §2.
+ *
+ * Conventions (all functions):
+ *  - Ownership: the caller owns every buffer passed in. "d_" pointers are device pointers (e.g. a
+ *    torch tensor's data_ptr()), everything else is host memory. The context owns only its
+ *    internal workspace (Y-history scratch, block partials, lattice generators, device scalars).
+ *  - Streams: every device operation is enqueued on the context's stream (mvn_create /
+ *    mvn_set_stream). Functions returning host values (info, k_out, mvn_crd) synchronise it.
+ *  - Errors are returned, never thrown or printed; mvn_last_error() has the message. No CPU
+ *    fallback exists: without a usable sm_100a device, mvn_create fails with MVN_E_CUDA.
+ *  - Threading: a context is single-threaded; use one context per host thread / device.
+ *  - Precision: fp64 throughout.
+ */
+#ifndef MVN_H
+#define MVN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MVN_OK = 0,
+    MVN_E_USAGE = 1,    /* invalid argument (sizes, NaN limits, a_k > b_k, conf not in (0,1), ...) */
+    MVN_E_NUMERIC = 2,  /* Sigma not positive definite: see info (first failing 0-based row)       */
+    MVN_E_IO = 3,       /* reserved (file I/O lives above the ABI)                                  */
+    MVN_E_CUDA = 4,     /* CUDA runtime error or no usable device                                   */
+    MVN_E_NCCL = 5,     /* reserved: collectives live in the Python layer (torch.distributed)       */
+    MVN_E_NOMEM = 6     /* device or host allocation failed                                         */
+} mvn_status;
+
+typedef struct mvn_ctx mvn_ctx;
+
+/* Create a context bound to CUDA device `device` and stream `cuda_stream` (a cudaStream_t; NULL =
+ * the legacy default stream). Fails with MVN_E_CUDA unless the device is compute capability 10.0
+ * (B200, sm_100a — the only architecture this library is built for). */
+mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out);
+void mvn_destroy(mvn_ctx *ctx);
+mvn_status mvn_set_stream(mvn_ctx *ctx, void *cuda_stream);
+const char *mvn_last_error(const mvn_ctx *ctx);
+const char *mvn_version(void);
+/* Release the context's cached workspace (Y history, partials). */
+mvn_status mvn_trim(mvn_ctx *ctx);
+
+/* ---------------------------------------------------------------------------------------------
+ * Lower tile-packed symmetric storage (Chameleon-style tile descriptor, restated).
+ * nt = ceil(n/nb) tiles per side; tile (i,j), i >= j, starts at ((i*(i+1))/2 + j) * nb*nb doubles
+ * and is an nb x nb column-major block. The row panel of tile-row i is contiguous. Edge tiles are
+ * padded: padded diagonal entries are 1, padded off-diagonal entries 0, so the padded matrix is
+ * SPD with L's padding equal to the identity. nb must be 128 in this build (MVN_E_USAGE
+ * otherwise).                                                                                   */
+typedef struct {
+    int64_t n;   /* matrix order, >= 1 */
+    int64_t nb;  /* tile size (128) */
+} mvn_tiles;
+
+int64_t mvn_tiles_count(mvn_tiles t);   /* nt*(nt+1)/2, or -1 if invalid */
+size_t mvn_tiles_bytes(mvn_tiles t);    /* 8 * nb*nb * count, 0 if invalid */
+
+/* dense column-major (leading dimension ld >= n, device) <-> tile-packed (device). pack reads the
+ * lower triangle only and writes the padding; unpack writes the lower triangle and zeroes the
+ * strict upper triangle of the dense matrix. */
+mvn_status mvn_pack_lower(mvn_ctx *ctx, mvn_tiles t, const double *d_dense, int64_t ld, double *d_tiles);
+mvn_status mvn_unpack_lower(mvn_ctx *ctx, mvn_tiles t, const double *d_tiles, double *d_dense, int64_t ld);
+
+/* ---------------------------------------------------------------------------------------------
+ * a1. Marginal probabilities and order (Alg. 1 l.3-6; readings R2, R13). HOST.
+ *   z_i = (mu_i - u)/sqrt(var_i), p_M[i] = Phi(z_i) = P(X_i > u);
+ *   order = indices sorted by z descending, ties by ascending index (stable);
+ *   a_sorted[k] = u - mu[order[k]]  (lower limit of the k-th sorted location; b = +inf, R2).
+ * mu, var_diag: n doubles (var_diag = Sigma_ii = sigma^2 + nugget). order: n int64 (out),
+ * a_sorted: n doubles (out), pM: n doubles (out, nullable, original order).
+ * MVN_E_USAGE if n < 1, any input is NaN, or any var <= 0.                                      */
+mvn_status mvn_marginal_order(int64_t n, const double *mu, const double *var_diag, double u,
+                              int64_t *order, double *a_sorted, double *pM);
+
+/* ---------------------------------------------------------------------------------------------
+ * a2. Matérn covariance tiles (Eq. 6, as printed: no sqrt(2 nu) scaling, R14):
+ *   Sigma_kl = sigma2 * M_nu(h/beta) + nugget * delta_kl,  h = ||x_k - x_l||_2  (Euclidean)
+ *   nu = 0.5: e^{-x};  nu = 1.5: (1+x) e^{-x};  nu = 2.5: (1 + x + x^2/3) e^{-x}.
+ * d_xy: n x 2 row-major device doubles, ALREADY in sorted order (x_{o(k)}). d_tiles: device,
+ * mvn_tiles_bytes(t) bytes, fully written (including padding). Exactly symmetric.
+ * MVN_E_USAGE for sigma2 <= 0, beta <= 0, nugget < 0, or nu not in {0.5, 1.5, 2.5}.            */
+mvn_status mvn_cov_matern(mvn_ctx *ctx, mvn_tiles t, const double *d_xy, double sigma2, double beta,
+                          double nu, double nugget, double *d_tiles);
+
+/* ---------------------------------------------------------------------------------------------
+ * a3. Tiled right-looking Cholesky in place (Alg. 1 l.8 "L <- dpotrf(Sigma)"; box (a) of
+ * P:319): for k: POTRF(A_kk) -> TRSM(A_ik, i>k) -> SYRK/GEMM(A_ij, i>=j>k) on fp64 DMMA.
+ * d_tiles: in Sigma (lower tiles), out L (lower tiles; strict upper part of diagonal tiles
+ * zeroed). *info (host, out): -1 on success, else the 0-based global row of the first
+ * non-positive pivot, with MVN_E_NUMERIC returned (reading R17; no jitter retry). Synchronises. */
+mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
+
+/* ---------------------------------------------------------------------------------------------
+ * a5. QMC point set (reading R8). The global sample index g in [0, N*R) maps to shift r = g / N
+ * and lattice index j = g % N + 1 (1-based). Row k (0-based, sorted order) of sample g uses
+ *   X = (j * G_k + D_k^r) mod 2^64,  w = (floor(X / 2^12) + 1/2) * 2^-52,
+ *   G_k = floor(frac(sqrt(p_{k+1})) * 2^64)  (p_1 = 2: k-th prime),
+ *   D_k^r = SplitMix64_mix(seed + 0x9E3779B97F4A7C15 * (r * 2^32 + k + 1))  (mod 2^64).
+ * mvn_lattice_generators: HOST, writes gen[0..n). mvn_lattice_shifts: HOST, D[r*n + k].       */
+mvn_status mvn_lattice_generators(int64_t n, uint64_t *gen);
+mvn_status mvn_lattice_shifts(uint64_t seed, int32_t R, int64_t n, uint64_t *D);
+
+typedef struct {
+    int64_t N;             /* lattice points per shift, >= 1 */
+    int32_t R;             /* random shifts, >= 1 */
+    uint64_t seed;         /* shift seed */
+    int64_t sample_begin;  /* global sample range [begin, end) processed by this call */
+    int64_t sample_end;    /*   0 <= begin < end <= N*R  (a rank's shard, or everything) */
+} mvn_qmc;
+
+/* ---------------------------------------------------------------------------------------------
+ * a5-a8. One SOV sweep over all n rows for every sample in the range (Alg. 2, with
+ * the QMC tile kernel Alg. 3; Eq. 2-3; prefixes collapsed into one sweep,
+ * reading R1). Per sample, for k = 0..n-1:
+ *   s = sum_{t<k} L_kt y_t;  a' = (a_k - s)/L_kk;  b' = (b_k - s)/L_kk;
+ *   (log q, y_k) = tail-aware Phi / Phi^{-1} step of reading R9;  ell_k = ell_{k-1} + log q.
+ * Output: for every prefix k, over the samples of the range,
+ *   d_M[k] = max_g ell_k(g),  d_S[k] = sum_g exp(ell_k(g) - d_M[k])
+ * (M = -inf, S = 0 if every sample has probability 0). Deterministic for a given range, n and
+ * device (fixed sample blocking, fixed combine order).
+ * d_L: tile-packed L from mvn_potrf. d_a: n device doubles (-inf allowed). d_b: n device doubles
+ * or NULL for b = +inf (every BASELINE config). MVN_E_USAGE if the range is empty/out of bounds,
+ * or n, N, R < 1.                                                                              */
+mvn_status mvn_sov_prefix(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_a,
+                          const double *d_b, const mvn_qmc *q, double *d_M, double *d_S);
+
+/* Multi-GPU combine helpers (reading R11): after all_reduce(MAX) of M into d_Mglob,
+ *   S <- S * exp(M - Mglob), M <- Mglob  (elementwise, device; S = 0 where M = -inf).
+ * Then all_reduce(SUM) of S and mvn_prefix_finalize.                                           */
+mvn_status mvn_prefix_rescale(mvn_ctx *ctx, int64_t n, const double *d_Mglob, double *d_M, double *d_S);
+
+/* a8. log P_k = M_k + log S_k - log(NR) (the mean of Alg. 2 l.19 over all NR samples), device. */
+mvn_status mvn_prefix_finalize(mvn_ctx *ctx, int64_t n, int64_t NR, const double *d_M,
+                               const double *d_S, double *d_logP);
+
+/* ---------------------------------------------------------------------------------------------
+ * a10. Confidence regions (Eq. 4-5; readings R12, R16). HOST.
+ * logP: n host doubles in sorted order. Running minimum first (ulp guard), then for each level
+ * c = conf[i] in (0,1): k_out[i] = max{k : log P_k >= log c} (0 if none); the region is
+ * order[0 .. k_out[i]). near_tie[i] (nullable) = 1 if |log P_{k*} - log c| <= 1e-8 or
+ * |log P_{k*+1} - log c| <= 1e-8. The confidence function F(o(k)) = P_k (Eq. 5).             */
+mvn_status mvn_confidence_region(int64_t n, const double *logP, const double *conf, int64_t nconf,
+                                 int64_t *k_out, int32_t *near_tie);
+
+/* ---------------------------------------------------------------------------------------------
+ * End-to-end CRD (Alg. 1) on one GPU with HOST buffers: upload, a1..a10, download.
+ * This is the call a user makes; bench.py's "e2e" number times it.                             */
+typedef struct {
+    int64_t n;
+    const double *xy;      /* host, n x 2 row-major, original order */
+    const double *mu;      /* host, n, original order */
+    double sigma2, beta, nu, nugget, u;
+    int64_t N;
+    int32_t R;
+    uint64_t seed;
+    const double *conf;    /* host, nconf levels in (0,1) */
+    int64_t nconf;
+} mvn_crd_problem;
+
+typedef struct {
+    int64_t *order;        /* host out, n: original index of sorted position k */
+    double *logP;          /* host out, n: log P_k (sorted order, before running min) */
+    int64_t *k_star;       /* host out, nconf */
+    int32_t *near_tie;     /* host out, nconf (nullable) */
+    int64_t info;          /* -1 or first failing Cholesky row */
+    double ms_stage[6];    /* device time per stage: upload, cov, potrf, sov, finalize, download */
+} mvn_crd_result;
+
+mvn_status mvn_crd(mvn_ctx *ctx, const mvn_crd_problem *p, mvn_crd_result *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MVN_H */

@@ -1,0 +1,325 @@
+"""paper_2405_14892_b200 — B200-native (sm_100a) confidence-region detection from high-dimensional
+MVN probabilities (arXiv 2405.14892), as a thin ctypes binding over libmvn.so (include/mvn.h).
+
+The binding only marshals arguments: every step of the hot path runs in the CUDA library. There
+is no CPU fallback — if libmvn.so or an sm_100a device is missing, the calls raise.
+PyTorch provides device memory, streams and (in bench.py / parallel.py) torch.distributed.
+
+Function names follow the C ABI (mvn_cov_matern, mvn_potrf, mvn_sov_prefix, ...). Device
+arguments are CUDA torch tensors (float64 / int64 / uint64 as documented in include/mvn.h);
+host arguments are numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmvn.so")
+TILE = 128
+
+MVN_OK, MVN_E_USAGE, MVN_E_NUMERIC, MVN_E_IO, MVN_E_CUDA, MVN_E_NCCL, MVN_E_NOMEM = range(7)
+_STATUS = {0: "OK", 1: "USAGE", 2: "NUMERIC", 3: "IO", 4: "CUDA", 5: "NCCL", 6: "NOMEM"}
+
+# every symbol declared in include/mvn.h (tests/test_abi.py checks the header against this list)
+ABI_SYMBOLS = [
+    "mvn_create", "mvn_destroy", "mvn_set_stream", "mvn_last_error", "mvn_version", "mvn_trim",
+    "mvn_tiles_count", "mvn_tiles_bytes", "mvn_pack_lower", "mvn_unpack_lower",
+    "mvn_marginal_order", "mvn_cov_matern", "mvn_potrf", "mvn_lattice_generators",
+    "mvn_lattice_shifts", "mvn_sov_prefix", "mvn_prefix_rescale", "mvn_prefix_finalize",
+    "mvn_confidence_region", "mvn_crd",
+]
+
+
+class MvnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libmvn {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class mvn_tiles(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nb", ctypes.c_int64)]
+
+
+class mvn_qmc(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("R", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("sample_begin", ctypes.c_int64), ("sample_end", ctypes.c_int64)]
+
+
+class mvn_crd_problem(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("xy", ctypes.c_void_p), ("mu", ctypes.c_void_p),
+                ("sigma2", ctypes.c_double), ("beta", ctypes.c_double), ("nu", ctypes.c_double),
+                ("nugget", ctypes.c_double), ("u", ctypes.c_double), ("N", ctypes.c_int64),
+                ("R", ctypes.c_int32), ("seed", ctypes.c_uint64), ("conf", ctypes.c_void_p),
+                ("nconf", ctypes.c_int64)]
+
+
+class mvn_crd_result(ctypes.Structure):
+    _fields_ = [("order", ctypes.c_void_p), ("logP", ctypes.c_void_p), ("k_star", ctypes.c_void_p),
+                ("near_tie", ctypes.c_void_p), ("info", ctypes.c_int64), ("ms_stage", ctypes.c_double * 6)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libmvn.so (built by __graft_entry__.build() / _build.py). Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libmvn.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, U64, D, S = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64,
+                              ctypes.c_double, ctypes.c_int)
+    T = mvn_tiles
+    sig = {
+        "mvn_create": (S, [ctypes.c_int, P, ctypes.POINTER(P)]),
+        "mvn_destroy": (None, [P]),
+        "mvn_set_stream": (S, [P, P]),
+        "mvn_last_error": (ctypes.c_char_p, [P]),
+        "mvn_version": (ctypes.c_char_p, []),
+        "mvn_trim": (S, [P]),
+        "mvn_tiles_count": (I64, [T]),
+        "mvn_tiles_bytes": (ctypes.c_size_t, [T]),
+        "mvn_pack_lower": (S, [P, T, P, I64, P]),
+        "mvn_unpack_lower": (S, [P, T, P, P, I64]),
+        "mvn_marginal_order": (S, [I64, P, P, D, P, P, P]),
+        "mvn_cov_matern": (S, [P, T, P, D, D, D, D, P]),
+        "mvn_potrf": (S, [P, T, P, ctypes.POINTER(I64)]),
+        "mvn_lattice_generators": (S, [I64, P]),
+        "mvn_lattice_shifts": (S, [U64, I32, I64, P]),
+        "mvn_sov_prefix": (S, [P, T, P, P, P, ctypes.POINTER(mvn_qmc), P, P]),
+        "mvn_prefix_rescale": (S, [P, I64, P, P, P]),
+        "mvn_prefix_finalize": (S, [P, I64, I64, P, P, P]),
+        "mvn_confidence_region": (S, [I64, P, P, I64, P, P]),
+        "mvn_crd": (S, [P, ctypes.POINTER(mvn_crd_problem), ctypes.POINTER(mvn_crd_result)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _np_ptr(a: np.ndarray) -> int:
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data
+
+
+def _dev_ptr(t, dtype=None) -> int:
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise TypeError("expected a CUDA torch tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t.data_ptr()
+
+
+class Context:
+    """An mvn_ctx bound to one CUDA device; follows torch's current stream on every call."""
+
+    _by_device: dict[int, "Context"] = {}
+
+    def __init__(self, device: int = 0):
+        import torch
+        self.device = device
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            st = lib().mvn_create(device, ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream), ctypes.byref(h))
+        if st != MVN_OK:
+            raise MvnError(st, f"mvn_create(device={device}) failed (needs a B200 / sm_100 device)")
+        self.h = h
+
+    @classmethod
+    def get(cls, device: int | None = None) -> "Context":
+        import torch
+        if device is None:
+            device = torch.cuda.current_device()
+        if device not in cls._by_device:
+            cls._by_device[device] = Context(device)
+        c = cls._by_device[device]
+        lib().mvn_set_stream(c.h, ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream))
+        return c
+
+    def check(self, st: int, what: str):
+        if st != MVN_OK:
+            raise MvnError(st, f"{what}: {lib().mvn_last_error(self.h).decode()}")
+
+    def trim(self):
+        self.check(lib().mvn_trim(self.h), "mvn_trim")
+
+
+def tiles(n: int) -> mvn_tiles:
+    return mvn_tiles(n, TILE)
+
+
+def mvn_tiles_count(n: int) -> int:
+    return int(lib().mvn_tiles_count(tiles(n)))
+
+
+def mvn_tiles_bytes(n: int) -> int:
+    return int(lib().mvn_tiles_bytes(tiles(n)))
+
+
+def alloc_tiles(n: int, device=None):
+    import torch
+    return torch.empty(mvn_tiles_bytes(n) // 8, dtype=torch.float64, device=device or "cuda")
+
+
+def mvn_pack_lower(dense, n: int, out=None):
+    """dense: (n, n) CUDA float64, read as column-major with ld = n (a C-order tensor's transpose is
+    the same memory, and only the lower triangle of a symmetric matrix matters)."""
+    c = Context.get(dense.device.index)
+    out = alloc_tiles(n, dense.device) if out is None else out
+    c.check(lib().mvn_pack_lower(c.h, tiles(n), _dev_ptr(dense), n, _dev_ptr(out)), "mvn_pack_lower")
+    return out
+
+
+def mvn_unpack_lower(t, n: int, out=None):
+    """Returns an (n, n) CUDA float64 tensor M whose memory is column-major L, i.e. M.T == L."""
+    import torch
+    c = Context.get(t.device.index)
+    out = torch.zeros((n, n), dtype=torch.float64, device=t.device) if out is None else out
+    c.check(lib().mvn_unpack_lower(c.h, tiles(n), _dev_ptr(t), _dev_ptr(out), n), "mvn_unpack_lower")
+    return out
+
+
+def mvn_marginal_order(mu: np.ndarray, var_diag: np.ndarray, u: float):
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    var = np.ascontiguousarray(var_diag, dtype=np.float64)
+    n = mu.shape[0]
+    order = np.empty(n, dtype=np.int64)
+    a = np.empty(n)
+    pM = np.empty(n)
+    st = lib().mvn_marginal_order(n, _np_ptr(mu), _np_ptr(var), float(u), _np_ptr(order), _np_ptr(a), _np_ptr(pM))
+    if st != MVN_OK:
+        raise MvnError(st, "mvn_marginal_order")
+    return order, a, pM
+
+
+def mvn_cov_matern(xy_sorted, sigma2: float, beta: float, nu: float, nugget: float, out=None):
+    """xy_sorted: (n, 2) CUDA float64 in sorted order. Returns the tile-packed Sigma."""
+    import torch
+    n = xy_sorted.shape[0]
+    c = Context.get(xy_sorted.device.index)
+    out = alloc_tiles(n, xy_sorted.device) if out is None else out
+    c.check(lib().mvn_cov_matern(c.h, tiles(n), _dev_ptr(xy_sorted, torch.float64), float(sigma2), float(beta),
+                                 float(nu), float(nugget), _dev_ptr(out, torch.float64)), "mvn_cov_matern")
+    return out
+
+
+def mvn_potrf(t, n: int, raise_on_numeric: bool = True) -> int:
+    """In-place tiled Cholesky. Returns info (-1 ok, else first failing 0-based row)."""
+    c = Context.get(t.device.index)
+    info = ctypes.c_int64(-1)
+    st = lib().mvn_potrf(c.h, tiles(n), _dev_ptr(t), ctypes.byref(info))
+    if st == MVN_E_NUMERIC and not raise_on_numeric:
+        return int(info.value)
+    c.check(st, "mvn_potrf")
+    return int(info.value)
+
+
+def mvn_lattice_generators(n: int) -> np.ndarray:
+    g = np.empty(n, dtype=np.uint64)
+    st = lib().mvn_lattice_generators(n, _np_ptr(g))
+    if st != MVN_OK:
+        raise MvnError(st, "mvn_lattice_generators")
+    return g
+
+
+def mvn_lattice_shifts(seed: int, R: int, n: int) -> np.ndarray:
+    D = np.empty((R, n), dtype=np.uint64)
+    st = lib().mvn_lattice_shifts(int(seed), int(R), n, _np_ptr(D))
+    if st != MVN_OK:
+        raise MvnError(st, "mvn_lattice_shifts")
+    return D
+
+
+def mvn_sov_prefix(L, n: int, a, N: int, R: int, seed: int, begin: int = 0, end: int | None = None,
+                   b=None, M=None, S=None):
+    """One SOV/QMC sweep over global samples [begin, end). Returns CUDA (M, S), n each."""
+    import torch
+    c = Context.get(L.device.index)
+    end = N * R if end is None else end
+    M = torch.empty(n, dtype=torch.float64, device=L.device) if M is None else M
+    S = torch.empty(n, dtype=torch.float64, device=L.device) if S is None else S
+    q = mvn_qmc(int(N), int(R), int(seed), int(begin), int(end))
+    c.check(lib().mvn_sov_prefix(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64),
+                                 None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q),
+                                 _dev_ptr(M), _dev_ptr(S)), "mvn_sov_prefix")
+    return M, S
+
+
+def mvn_prefix_rescale(Mglob, M, S):
+    c = Context.get(M.device.index)
+    c.check(lib().mvn_prefix_rescale(c.h, M.numel(), _dev_ptr(Mglob), _dev_ptr(M), _dev_ptr(S)), "mvn_prefix_rescale")
+
+
+def mvn_prefix_finalize(M, S, NR: int, out=None):
+    import torch
+    c = Context.get(M.device.index)
+    out = torch.empty_like(M) if out is None else out
+    c.check(lib().mvn_prefix_finalize(c.h, M.numel(), int(NR), _dev_ptr(M), _dev_ptr(S), _dev_ptr(out)),
+            "mvn_prefix_finalize")
+    return out
+
+
+def mvn_confidence_region(logP: np.ndarray, conf):
+    lp = np.ascontiguousarray(logP, dtype=np.float64)
+    cf = np.ascontiguousarray(conf, dtype=np.float64)
+    k = np.empty(len(cf), dtype=np.int64)
+    tie = np.empty(len(cf), dtype=np.int32)
+    st = lib().mvn_confidence_region(lp.shape[0], _np_ptr(lp) if lp.size else None, _np_ptr(cf) if cf.size else None,
+                                     len(cf), _np_ptr(k) if cf.size else None, _np_ptr(tie) if cf.size else None)
+    if st != MVN_OK:
+        raise MvnError(st, "mvn_confidence_region")
+    return k, tie.astype(bool)
+
+
+@dataclass
+class CrdOutput:
+    order: np.ndarray
+    logP: np.ndarray
+    k_star: np.ndarray
+    near_tie: np.ndarray
+    info: int
+    ms_stage: tuple
+
+
+def mvn_crd(xy: np.ndarray, mu: np.ndarray, sigma2, beta, nu, nugget, u, N, R, seed, conf, device: int = 0,
+            pinned_out=None) -> CrdOutput:
+    """End-to-end Alg. 1 through the C ABI with HOST buffers (upload, a1..a10, download)."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    cf = np.ascontiguousarray(conf, dtype=np.float64)
+    n = mu.shape[0]
+    c = Context.get(device)
+    order = np.empty(n, dtype=np.int64)
+    logP = np.empty(n)
+    k = np.empty(max(len(cf), 1), dtype=np.int64)
+    tie = np.empty(max(len(cf), 1), dtype=np.int32)
+    prob = mvn_crd_problem(n, _np_ptr(xy), _np_ptr(mu), sigma2, beta, nu, nugget, u, int(N), int(R), int(seed),
+                           _np_ptr(cf) if cf.size else None, len(cf))
+    res = mvn_crd_result(_np_ptr(order), _np_ptr(logP), _np_ptr(k), _np_ptr(tie), -1)
+    c.check(lib().mvn_crd(c.h, ctypes.byref(prob), ctypes.byref(res)), "mvn_crd")
+    return CrdOutput(order, logP, k[:len(cf)], tie[:len(cf)].astype(bool), int(res.info), tuple(res.ms_stage))
+
+
+def running_min(logP: np.ndarray) -> np.ndarray:
+    return np.minimum.accumulate(np.asarray(logP, dtype=np.float64))
+
+
+def lower_dense_from_unpacked(M) -> np.ndarray:
+    """mvn_unpack_lower output (column-major memory) -> row-major numpy L."""
+    return M.T.contiguous().cpu().numpy() if hasattr(M, "cpu") else np.ascontiguousarray(M.T)
+
+
+__all__ = [n for n in dir() if n.startswith("mvn_")] + ["Context", "MvnError", "lib", "TILE", "alloc_tiles"]

@@ -1,0 +1,184 @@
+// K2-K4 — right-looking tiled Cholesky Sigma = L L^T (Alg. 1 line 8; box (a) of P:319).
+//
+// Per step k (nt steps, 128x128 tiles, lower tile-packed storage):
+//   K2 k_potrf_diag : A_kk = L_kk L_kk^T in shared memory (one CTA), pivot check -> info
+//   K3 k_trsm       : L_ik = A_ik L_kk^{-T}, i > k (one CTA per tile, one thread per row)
+//   K4 k_update     : A_ij -= L_ik L_jk^T, i >= j > k (DMMA GEMM, two 64x128 CTAs per tile)
+// The paper's StarPU task DAG becomes stream order; the K4 GEMM carries
+// n^3/3 of the n^3/3 + O(n^2 nb) flops.
+#include "common.cuh"
+#include "gemm_dmma.cuh"
+#include "mvn_internal.h"
+
+namespace mvn {
+
+// ------------------------------------------------------------------------------------------ K2
+// Unblocked right-looking Cholesky of one 128x128 tile held in shared memory (column-major).
+// The first non-positive (or NaN) pivot writes its global row to *info (only if no earlier step
+// failed) and stops the factorisation of this tile.
+__global__ void __launch_bounds__(512) k_potrf_diag(double *__restrict__ tiles, int k, int64_t *__restrict__ info) {
+    extern __shared__ double A[];  // 128 x 128, column-major
+    __shared__ int failed;
+    double *T = tiles + tile_offset(k, k);
+    const int tid = threadIdx.x, nth = blockDim.x;
+    for (int e = tid; e < kTile * kTile / 2; e += nth)
+        reinterpret_cast<double2 *>(A)[e] = reinterpret_cast<const double2 *>(T)[e];
+    if (tid == 0) failed = (*info >= 0);  // an earlier step already failed: leave tiles as they are
+    __syncthreads();
+    if (failed) return;
+    const int warp = tid >> 5, lane = tid & 31, nwarp = nth >> 5;
+    for (int c = 0; c < kTile; ++c) {
+        if (tid == 0) {
+            const double d = A[c * kTile + c];
+            if (!(d > 0.0)) {
+                failed = 1;
+                *info = (int64_t)k * kTile + c;
+            } else {
+                A[c * kTile + c] = sqrt(d);
+            }
+        }
+        __syncthreads();
+        if (failed) return;
+        const double piv = A[c * kTile + c];
+        for (int i = c + 1 + tid; i < kTile; i += nth) A[c * kTile + i] /= piv;
+        __syncthreads();
+        // trailing update of the lower triangle: column j handled by warp (j - c - 1) % nwarp
+        for (int j = c + 1 + warp; j < kTile; j += nwarp) {
+            const double ljc = A[c * kTile + j];
+            for (int i = j + lane; i < kTile; i += 32) A[j * kTile + i] -= A[c * kTile + i] * ljc;
+        }
+        __syncthreads();
+    }
+    // write back L_kk with the strict upper triangle zeroed
+    for (int e = tid; e < kTile * kTile; e += nth) {
+        const int col = e >> 7, row = e & 127;
+        T[e] = (row >= col) ? A[e] : 0.0;
+    }
+}
+
+// ------------------------------------------------------------------------------------------ K3
+// L_ik = A_ik L_kk^{-T}: row r of the tile solves x L_kk^T = a by forward substitution,
+// x_j = (a_j - sum_{t<j} x_t L_kk(j,t)) / L_kk(j,j). Thread r owns row r; its x lives in a
+// column-major shared copy of the tile (conflict-free), L_kk(j,t) is a warp-uniform broadcast.
+__global__ void __launch_bounds__(128) k_trsm(double *__restrict__ tiles, int k, int nt) {
+    extern __shared__ double X[];  // 128 x 128 column-major: X[col*128 + row]
+    const int i = k + 1 + blockIdx.x;
+    double *T = tiles + tile_offset(i, k);
+    const double *__restrict__ Lkk = tiles + tile_offset(k, k);
+    const int r = threadIdx.x;
+    for (int e = r; e < kTile * kTile / 2; e += 128)
+        reinterpret_cast<double2 *>(X)[e] = reinterpret_cast<const double2 *>(T)[e];
+    __syncthreads();
+    for (int j = 0; j < kTile; ++j) {
+        double s0 = X[j * kTile + r], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int t = 0;
+        for (; t + 4 <= j; t += 4) {
+            s0 -= X[(t + 0) * kTile + r] * __ldg(Lkk + (t + 0) * kTile + j);
+            s1 -= X[(t + 1) * kTile + r] * __ldg(Lkk + (t + 1) * kTile + j);
+            s2 -= X[(t + 2) * kTile + r] * __ldg(Lkk + (t + 2) * kTile + j);
+            s3 -= X[(t + 3) * kTile + r] * __ldg(Lkk + (t + 3) * kTile + j);
+        }
+        for (; t < j; ++t) s0 -= X[t * kTile + r] * __ldg(Lkk + t * kTile + j);
+        X[j * kTile + r] = ((s0 + s1) + (s2 + s3)) / __ldg(Lkk + j * kTile + j);
+    }
+    __syncthreads();
+    for (int e = r; e < kTile * kTile / 2; e += 128)
+        reinterpret_cast<double2 *>(T)[e] = reinterpret_cast<const double2 *>(X)[e];
+}
+
+// ------------------------------------------------------------------------------------------ K4
+// Trailing update, one CTA per (tile (i,j), row half h): C(64x128) -= L_ik[h-half] * L_jk^T.
+// 4 warps as 2 (M) x 2 (N), warp tile 32x64 = 4x8 DMMA blocks (64 fp64 accumulators / thread).
+namespace upd {
+constexpr int BM = 64, BN = 128, BK = 16, STAGES = 3;
+constexpr int SA = BM + 4, SB = BN + 4;  // == 4 (mod 16)
+constexpr int WM = 4, WN = 8;
+constexpr int SMEM = STAGES * BK * (SA + SB) * 8;
+}  // namespace upd
+
+__global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, int k, int nt) {
+    using namespace upd;
+    extern __shared__ double sm[];
+    double *As = sm;
+    double *Bs = sm + STAGES * BK * SA;
+    const int64_t id = blockIdx.x >> 1;
+    const int h = blockIdx.x & 1;
+    // id -> (ii, jj), 0 <= jj <= ii < T, row-major lower enumeration; tile (k+1+ii, k+1+jj)
+    int ii = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
+    while ((int64_t)ii * (ii + 1) / 2 > id) --ii;
+    while ((int64_t)(ii + 1) * (ii + 2) / 2 <= id) ++ii;
+    const int jj = (int)(id - (int64_t)ii * (ii + 1) / 2);
+    const int ti = k + 1 + ii, tj = k + 1 + jj;
+    const double *__restrict__ Lik = tiles + tile_offset(ti, k) + h * BM;   // column stride 128
+    const double *__restrict__ Ljk = tiles + tile_offset(tj, k);
+    double *C = tiles + tile_offset(ti, tj) + h * BM;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 64;
+    double acc[WM][WN][2];
+#pragma unroll
+    for (int a = 0; a < WM; ++a)
+#pragma unroll
+        for (int b = 0; b < WN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    auto load = [&](int ch, int st) {
+        const int kc = ch * BK;
+        double *as = As + st * BK * SA;
+        double *bs = Bs + st * BK * SB;
+        // A: 16 columns x 64 rows -> 512 x 16B; 4 per thread
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = q * 128 + tid;       // 0..511
+            const int col = e >> 5, seg = e & 31;
+            cp_async16(as + col * SA + seg * 2, Lik + (int64_t)(kc + col) * kTile + seg * 2);
+        }
+        // B: 16 columns x 128 rows -> 1024 x 16B; 8 per thread
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = q * 128 + tid;
+            const int col = e >> 6, seg = e & 63;
+            cp_async16(bs + col * SB + seg * 2, Ljk + (int64_t)(kc + col) * kTile + seg * 2);
+        }
+    };
+    gemm_mainloop<BK, STAGES, SA, SB, WM, WN>(kTile / BK, As, Bs, wm0, wn0, lane, acc, load);
+
+    // epilogue: C[row][col] -= acc, C column-major (column stride 128)
+#pragma unroll
+    for (int a = 0; a < WM; ++a) {
+        const int row = wm0 + a * 8 + (lane >> 2);
+#pragma unroll
+        for (int b = 0; b < WN; ++b) {
+            const int col = wn0 + b * 8 + 2 * (lane & 3);
+            double *p0 = C + (int64_t)col * kTile + row;
+            double *p1 = p0 + kTile;
+            *p0 -= acc[a][b][0];
+            *p1 -= acc[a][b][1];
+        }
+    }
+}
+
+cudaError_t potrf_init() {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * kTile * 8))) return e;
+    if ((e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * kTile * 8))) return e;
+    if ((e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, upd::SMEM))) return e;
+    return cudaSuccess;
+}
+
+cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st) {
+    const int nt = (int)((n + kTile - 1) / kTile);
+    for (int k = 0; k < nt; ++k) {
+        k_potrf_diag<<<1, 512, kTile * kTile * 8, st>>>(tiles, k, d_info);
+        const int T = nt - k - 1;
+        if (T > 0) {
+            k_trsm<<<T, 128, kTile * kTile * 8, st>>>(tiles, k, nt);
+            const int64_t ntile = (int64_t)T * (T + 1) / 2;
+            k_update<<<(unsigned)(2 * ntile), 128, upd::SMEM, st>>>(tiles, k, nt);
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace mvn

@@ -1,0 +1,368 @@
+// libmvn C ABI (include/mvn.h): argument validation, workspace, lattice tables, host steps
+// (a1 marginal order, a10 regions) and launch orchestration. No Python, no CPU fallback.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/mvn.h"
+#include "mvn_internal.h"
+
+struct mvn_ctx {
+    int device = 0;
+    int nsm = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    // workspace (device)
+    void *Y = nullptr; size_t Y_cap = 0;
+    void *part = nullptr; size_t part_cap = 0;
+    uint64_t *G = nullptr; int64_t G_n = 0;
+    int64_t *d_info = nullptr;
+    // mvn_crd buffers
+    void *crd_L = nullptr; size_t crd_L_cap = 0;
+    void *crd_vec = nullptr; size_t crd_vec_cap = 0;
+};
+
+namespace {
+
+mvn_status fail(mvn_ctx *c, mvn_status s, const std::string &msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+mvn_status cuda_fail(mvn_ctx *c, cudaError_t e, const char *where) {
+    return fail(c, MVN_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define MVN_CUDA(ctx, call)                                              \
+    do {                                                                 \
+        cudaError_t _e = (call);                                         \
+        if (_e != cudaSuccess) return cuda_fail((ctx), _e, #call);       \
+    } while (0)
+
+mvn_status ensure(mvn_ctx *c, void **buf, size_t *cap, size_t bytes) {
+    if (*cap >= bytes) return MVN_OK;
+    if (*buf) {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(*buf);
+        *buf = nullptr;
+        *cap = 0;
+    }
+    cudaError_t e = cudaMalloc(buf, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, MVN_E_NOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+    }
+    *cap = bytes;
+    return MVN_OK;
+}
+
+bool tiles_ok(mvn_tiles t) { return t.n >= 1 && t.nb == mvn::kTile; }
+
+// ----------------------------------------------------------------------------- lattice (R8)
+std::vector<uint64_t> first_primes(int64_t n) {
+    std::vector<uint64_t> out;
+    if (n <= 0) return out;
+    const double ln = std::log((double)std::max<int64_t>(n, 6));
+    const uint64_t bound = n < 6 ? 15 : (uint64_t)(n * (ln + std::log(ln))) + 1;
+    std::vector<uint8_t> comp(bound + 1, 0);
+    for (uint64_t c = 2; c <= bound && (int64_t)out.size() < n; ++c) {
+        if (comp[c]) continue;
+        out.push_back(c);
+        for (uint64_t m = c * c; m <= bound; m += c) comp[m] = 1;
+    }
+    return out;
+}
+
+// floor(frac(sqrt(p)) * 2^64) = floor(sqrt(p * 2^128)) mod 2^64 by a bitwise search on the fraction
+// b: the largest b with (a 2^64 + b)^2 <= p 2^128, a = floor(sqrt p), tested exactly in 128-bit
+// integers as 2ab + floor(b^2 / 2^64) + frac <= (p - a^2) 2^64.
+uint64_t sqrt_frac64(uint64_t p) {
+    uint64_t a = (uint64_t)std::sqrt((double)p);
+    while (a * a > p) --a;
+    while ((a + 1) * (a + 1) <= p) ++a;
+    const unsigned __int128 c = (unsigned __int128)(p - a * a) << 64;
+    uint64_t b = 0;
+    for (int bit = 63; bit >= 0; --bit) {
+        const uint64_t cand = b | (1ull << bit);
+        const unsigned __int128 sq = (unsigned __int128)cand * cand;
+        const uint64_t hi = (uint64_t)(sq >> 64), lo = (uint64_t)sq;
+        const unsigned __int128 X = (unsigned __int128)2 * a * cand + hi;
+        const bool ok = X < c || (X == c && lo == 0);
+        if (ok) b = cand;
+    }
+    return b;
+}
+
+uint64_t shift64(uint64_t seed, uint64_t r, uint64_t k) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * ((r << 32) + k + 1ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+mvn_status ensure_generators(mvn_ctx *c, int64_t n) {
+    if (c->G_n >= n) return MVN_OK;
+    std::vector<uint64_t> g((size_t)n);
+    mvn_status s = mvn_lattice_generators(n, g.data());
+    if (s != MVN_OK) return fail(c, s, "lattice generators");
+    if (c->G) { cudaStreamSynchronize(c->stream); cudaFree(c->G); c->G = nullptr; c->G_n = 0; }
+    MVN_CUDA(c, cudaMalloc(&c->G, sizeof(uint64_t) * (size_t)n));
+    MVN_CUDA(c, cudaMemcpy(c->G, g.data(), sizeof(uint64_t) * (size_t)n, cudaMemcpyHostToDevice));
+    c->G_n = n;
+    return MVN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mvn_version(void) { return "mvn-b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
+    if (!out) return MVN_E_USAGE;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { cudaGetLastError(); return MVN_E_CUDA; }
+    if (device < 0 || device >= ndev) return MVN_E_USAGE;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return MVN_E_CUDA;
+    if (prop.major != 10 || prop.minor != 0) return MVN_E_CUDA;   // sm_100a binary only
+    if (cudaSetDevice(device) != cudaSuccess) return MVN_E_CUDA;
+    mvn_ctx *c = new mvn_ctx();
+    c->device = device;
+    c->nsm = prop.multiProcessorCount;
+    c->stream = (cudaStream_t)cuda_stream;
+    if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess ||
+        cudaMalloc(&c->d_info, sizeof(int64_t)) != cudaSuccess) {
+        delete c;
+        return MVN_E_CUDA;
+    }
+    *out = c;
+    return MVN_OK;
+}
+
+void mvn_destroy(mvn_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (void *p : {c->Y, c->part, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec})
+        if (p) cudaFree(p);
+    delete c;
+}
+
+mvn_status mvn_set_stream(mvn_ctx *c, void *s) {
+    if (!c) return MVN_E_USAGE;
+    c->stream = (cudaStream_t)s;
+    return MVN_OK;
+}
+
+const char *mvn_last_error(const mvn_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+mvn_status mvn_trim(mvn_ctx *c) {
+    if (!c) return MVN_E_USAGE;
+    cudaStreamSynchronize(c->stream);
+    for (void **p : {&c->Y, &c->part, &c->crd_L, &c->crd_vec})
+        if (*p) { cudaFree(*p); *p = nullptr; }
+    c->Y_cap = c->part_cap = c->crd_L_cap = c->crd_vec_cap = 0;
+    return MVN_OK;
+}
+
+int64_t mvn_tiles_count(mvn_tiles t) {
+    if (!tiles_ok(t)) return -1;
+    const int64_t nt = (t.n + t.nb - 1) / t.nb;
+    return nt * (nt + 1) / 2;
+}
+
+size_t mvn_tiles_bytes(mvn_tiles t) {
+    const int64_t c = mvn_tiles_count(t);
+    return c < 0 ? 0 : (size_t)c * (size_t)(t.nb * t.nb) * sizeof(double);
+}
+
+mvn_status mvn_pack_lower(mvn_ctx *c, mvn_tiles t, const double *d_dense, int64_t ld, double *d_tiles) {
+    if (!c || !tiles_ok(t) || !d_dense || !d_tiles || ld < t.n) return fail(c, MVN_E_USAGE, "mvn_pack_lower: bad arguments");
+    MVN_CUDA(c, mvn::launch_pack(t.n, d_dense, ld, d_tiles, true, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_unpack_lower(mvn_ctx *c, mvn_tiles t, const double *d_tiles, double *d_dense, int64_t ld) {
+    if (!c || !tiles_ok(t) || !d_dense || !d_tiles || ld < t.n) return fail(c, MVN_E_USAGE, "mvn_unpack_lower: bad arguments");
+    MVN_CUDA(c, mvn::launch_pack(t.n, d_dense, ld, const_cast<double *>(d_tiles), false, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_marginal_order(int64_t n, const double *mu, const double *var, double u, int64_t *order,
+                              double *a_sorted, double *pM) {
+    if (n < 1 || !mu || !var || !order || !a_sorted || std::isnan(u)) return MVN_E_USAGE;
+    std::vector<double> z((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (std::isnan(mu[i]) || !(var[i] > 0.0)) return MVN_E_USAGE;
+        z[i] = (mu[i] - u) / std::sqrt(var[i]);
+    }
+    std::vector<int64_t> o((size_t)n);
+    std::iota(o.begin(), o.end(), 0);
+    std::stable_sort(o.begin(), o.end(), [&](int64_t x, int64_t y) { return z[x] > z[y]; });
+    for (int64_t k = 0; k < n; ++k) {
+        order[k] = o[k];
+        a_sorted[k] = u - mu[o[k]];
+    }
+    if (pM)
+        for (int64_t i = 0; i < n; ++i) pM[i] = 0.5 * std::erfc(-z[i] * 0.70710678118654752440);
+    return MVN_OK;
+}
+
+mvn_status mvn_cov_matern(mvn_ctx *c, mvn_tiles t, const double *d_xy, double sigma2, double beta, double nu,
+                          double nugget, double *d_tiles) {
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !d_xy || !d_tiles || !(sigma2 > 0) || !(beta > 0) || !(nugget >= 0) ||
+        !(nu == 0.5 || nu == 1.5 || nu == 2.5))
+        return fail(c, MVN_E_USAGE, "mvn_cov_matern: need nb=128, sigma2>0, beta>0, nugget>=0, nu in {0.5,1.5,2.5}");
+    MVN_CUDA(c, mvn::launch_cov_matern(t.n, d_xy, sigma2, beta, nu, nugget, d_tiles, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_potrf(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t *info) {
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !d_tiles || !info) return fail(c, MVN_E_USAGE, "mvn_potrf: bad arguments");
+    const int64_t minus1 = -1;
+    MVN_CUDA(c, cudaMemcpyAsync(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, mvn::launch_potrf(t.n, d_tiles, c->d_info, c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(info, c->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (*info >= 0 && *info < t.n)
+        return fail(c, MVN_E_NUMERIC, "mvn_potrf: matrix not positive definite at row " + std::to_string(*info));
+    if (*info >= t.n) *info = -1;   // cannot happen (padding is the identity)
+    return MVN_OK;
+}
+
+mvn_status mvn_lattice_generators(int64_t n, uint64_t *gen) {
+    if (n < 1 || !gen) return MVN_E_USAGE;
+    std::vector<uint64_t> p = first_primes(n);
+    if ((int64_t)p.size() != n) return MVN_E_USAGE;
+    for (int64_t k = 0; k < n; ++k) gen[k] = sqrt_frac64(p[k]);
+    return MVN_OK;
+}
+
+mvn_status mvn_lattice_shifts(uint64_t seed, int32_t R, int64_t n, uint64_t *D) {
+    if (n < 1 || R < 1 || !D) return MVN_E_USAGE;
+    for (int64_t r = 0; r < R; ++r)
+        for (int64_t k = 0; k < n; ++k) D[r * n + k] = shift64(seed, (uint64_t)r, (uint64_t)k);
+    return MVN_OK;
+}
+
+mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
+                          const mvn_qmc *q, double *d_M, double *d_S) {
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !d_L || !d_a || !q || !d_M || !d_S || q->N < 1 || q->R < 1 || q->sample_begin < 0 ||
+        q->sample_end <= q->sample_begin || q->sample_end > q->N * (int64_t)q->R)
+        return fail(c, MVN_E_USAGE, "mvn_sov_prefix: bad arguments (need nb=128, 0 <= begin < end <= N*R)");
+    mvn_status s;
+    if ((s = ensure_generators(c, t.n)) != MVN_OK) return s;
+    const int64_t nsamp = q->sample_end - q->sample_begin;
+    mvn::SovLaunch L;
+    L.L = d_L; L.n = t.n; L.a = d_a; L.b = d_b; L.G = c->G; L.N = q->N; L.seed = q->seed;
+    L.g_begin = q->sample_begin; L.g_end = q->sample_end;
+    L.nb = mvn::sov_pick_nb(nsamp, t.n, c->nsm);
+    L.nblk = (nsamp + L.nb - 1) / L.nb;
+    L.grid = (int)std::min<int64_t>(L.nblk, c->nsm);
+    const int64_t n_pad = (t.n + 63) / 64 * 64;
+    if ((s = ensure(c, &c->Y, &c->Y_cap, (size_t)L.grid * n_pad * L.nb * sizeof(double))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->part, &c->part_cap, (size_t)L.nblk * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
+    L.Y = (double *)c->Y; L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S;
+    MVN_CUDA(c, mvn::launch_sov(L, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_prefix_rescale(mvn_ctx *c, int64_t n, const double *d_Mglob, double *d_M, double *d_S) {
+    if (!c || n < 1 || !d_Mglob || !d_M || !d_S) return fail(c, MVN_E_USAGE, "mvn_prefix_rescale: bad arguments");
+    MVN_CUDA(c, mvn::launch_rescale(n, d_Mglob, d_M, d_S, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_prefix_finalize(mvn_ctx *c, int64_t n, int64_t NR, const double *d_M, const double *d_S, double *d_logP) {
+    if (!c || n < 1 || NR < 1 || !d_M || !d_S || !d_logP) return fail(c, MVN_E_USAGE, "mvn_prefix_finalize: bad arguments");
+    MVN_CUDA(c, mvn::launch_finalize(n, NR, d_M, d_S, d_logP, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_confidence_region(int64_t n, const double *logP, const double *conf, int64_t nconf, int64_t *k_out,
+                                 int32_t *near_tie) {
+    if (n < 0 || (n > 0 && !logP) || nconf < 0 || (nconf > 0 && (!conf || !k_out))) return MVN_E_USAGE;
+    std::vector<double> lp((size_t)n);
+    double run = INFINITY;
+    for (int64_t k = 0; k < n; ++k) {
+        if (std::isnan(logP[k])) return MVN_E_USAGE;
+        run = std::min(run, logP[k]);
+        lp[k] = run;
+    }
+    for (int64_t i = 0; i < nconf; ++i) {
+        if (!(conf[i] > 0.0 && conf[i] < 1.0)) return MVN_E_USAGE;
+        const double lc = std::log(conf[i]);
+        // lp is non-increasing: k* = number of prefixes with log P_k >= log c
+        const int64_t k = std::partition_point(lp.begin(), lp.end(), [&](double v) { return v >= lc; }) - lp.begin();
+        k_out[i] = k;
+        if (near_tie)
+            near_tie[i] = ((k > 0 && std::fabs(lp[k - 1] - lc) <= 1e-8) || (k < n && std::fabs(lp[k] - lc) <= 1e-8)) ? 1 : 0;
+    }
+    return MVN_OK;
+}
+
+mvn_status mvn_crd(mvn_ctx *c, const mvn_crd_problem *p, mvn_crd_result *out) {
+    if (!c) return MVN_E_USAGE;
+    if (!p || !out || p->n < 1 || !p->xy || !p->mu || !out->order || !out->logP || (p->nconf > 0 && !out->k_star))
+        return fail(c, MVN_E_USAGE, "mvn_crd: bad arguments");
+    const int64_t n = p->n;
+    mvn_tiles t{n, mvn::kTile};
+    cudaEvent_t ev[7];
+    for (auto &e : ev) MVN_CUDA(c, cudaEventCreate(&e));
+    struct EvGuard { cudaEvent_t *e; ~EvGuard() { for (int i = 0; i < 7; ++i) cudaEventDestroy(e[i]); } } guard{ev};
+
+    // a1 (host): marginals, order, limits, sorted locations
+    std::vector<double> var((size_t)n, p->sigma2 + p->nugget), a((size_t)n), xys((size_t)(2 * n));
+    mvn_status s = mvn_marginal_order(n, p->mu, var.data(), p->u, out->order, a.data(), nullptr);
+    if (s != MVN_OK) return fail(c, s, "mvn_crd: invalid mu / sigma2 / u");
+    for (int64_t k = 0; k < n; ++k) {
+        xys[2 * k] = p->xy[2 * out->order[k]];
+        xys[2 * k + 1] = p->xy[2 * out->order[k] + 1];
+    }
+    if ((s = ensure(c, &c->crd_L, &c->crd_L_cap, mvn_tiles_bytes(t))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->crd_vec, &c->crd_vec_cap, sizeof(double) * (size_t)n * 6)) != MVN_OK) return s;
+    double *dL = (double *)c->crd_L;
+    double *dxy = (double *)c->crd_vec, *da = dxy + 2 * n, *dM = da + n, *dS = dM + n, *dlp = dS + n;
+
+    MVN_CUDA(c, cudaEventRecord(ev[0], c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(dxy, xys.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(da, a.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, cudaEventRecord(ev[1], c->stream));
+    if ((s = mvn_cov_matern(c, t, dxy, p->sigma2, p->beta, p->nu, p->nugget, dL)) != MVN_OK) return s;
+    MVN_CUDA(c, cudaEventRecord(ev[2], c->stream));
+    int64_t info = -1;
+    s = mvn_potrf(c, t, dL, &info);
+    out->info = info;
+    if (s != MVN_OK) return s;
+    MVN_CUDA(c, cudaEventRecord(ev[3], c->stream));
+    mvn_qmc q{p->N, p->R, p->seed, 0, p->N * (int64_t)p->R};
+    if ((s = mvn_sov_prefix(c, t, dL, da, nullptr, &q, dM, dS)) != MVN_OK) return s;
+    MVN_CUDA(c, cudaEventRecord(ev[4], c->stream));
+    if ((s = mvn_prefix_finalize(c, n, q.N * (int64_t)q.R, dM, dS, dlp)) != MVN_OK) return s;
+    MVN_CUDA(c, cudaEventRecord(ev[5], c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(out->logP, dlp, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaEventRecord(ev[6], c->stream));
+    MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < 6; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+        out->ms_stage[i] = ms;
+    }
+    if (p->nconf > 0)
+        if ((s = mvn_confidence_region(n, out->logP, p->conf, p->nconf, out->k_star, out->near_tie)) != MVN_OK)
+            return fail(c, s, "mvn_crd: invalid confidence levels");
+    return MVN_OK;
+}
+
+}  // extern "C"

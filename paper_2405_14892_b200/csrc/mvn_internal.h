@@ -1,0 +1,38 @@
+// Internal declarations shared by the libmvn translation units (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mvn {
+
+constexpr int kTile = 128;  // storage tile (mvn_tiles.nb)
+
+cudaError_t launch_cov_matern(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
+                              double *tiles, cudaStream_t st);
+cudaError_t launch_pack(int64_t n, const double *dense, int64_t ld, double *tiles, bool to_tiles, cudaStream_t st);
+cudaError_t launch_rescale(int64_t n, const double *Mg, double *M, double *S, cudaStream_t st);
+cudaError_t launch_finalize(int64_t n, int64_t NR, const double *M, const double *S, double *logP, cudaStream_t st);
+
+cudaError_t potrf_init();
+cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st);
+
+struct SovLaunch {
+    const double *L;
+    int64_t n;
+    const double *a, *b;
+    const uint64_t *G;
+    int64_t N;
+    uint64_t seed;
+    int64_t g_begin, g_end;
+    int nb;          // samples per block (128..256, multiple of 32)
+    int64_t nblk;    // sample blocks
+    int grid;        // persistent CTAs (<= SM count)
+    double *Y;       // [grid][ceil(n/64)*64][nb]
+    double *part;    // [nblk][ceil(n/64)*64][2]
+    double *Mout, *Sout;
+};
+cudaError_t sov_init();
+int sov_pick_nb(int64_t nsamp, int64_t n, int nsm);
+cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
+
+}  // namespace mvn

@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Tolerances (north_star): |log P_k^gpu - log P_k^cpu| <= 1e-8 for every prefix k,
+Cholesky residual ||L L^T - Sigma||_F / ||Sigma||_F <= 1e-12, identical region sizes; Matérn
+entries within 1e-14 relative (closed form vs Bessel K_nu in the oracle); integer / index outputs
+bit-exact."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import lattice
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+LOGP_TOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def torch_cuda(cuda_device):
+    import torch
+    return torch
+
+
+def mvn():
+    import paper_2405_14892_b200 as m
+    return m
+
+
+def to_dense_lower(tiles_t, n):
+    """GPU tile-packed L -> host row-major lower (numpy), via mvn_unpack_lower."""
+    M = mvn().mvn_unpack_lower(tiles_t, n)
+    return M.T.contiguous().cpu().numpy()
+
+
+def sorted_inputs(cfg):
+    inp = W.make_inputs(cfg)
+    c = inp.cfg
+    var = np.full(c.n, c.sigma2 + c.nugget)
+    order, a, _ = oracle.marginal_order(inp.mu, var, c.u)
+    return inp, order, a
+
+
+def gpu_cov(torch, xy_sorted, c):
+    d_xy = torch.from_numpy(np.ascontiguousarray(xy_sorted)).cuda()
+    return mvn().mvn_cov_matern(d_xy, c.sigma2, c.beta, c.nu, c.nugget)
+
+
+# ------------------------------------------------------------------------------------ K1
+@pytest.mark.parametrize("n,nu,beta", [(400, 0.5, 0.1), (1000, 1.5, 0.05), (129, 2.5, 0.2), (1, 0.5, 0.1)])
+def test_matern_tiles_vs_oracle(torch_cuda, n, nu, beta):
+    torch = torch_cuda
+    xy = np.random.default_rng(n).uniform(size=(n, 2))
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.3, beta, nu, 1e-8)
+    G = to_dense_lower(T, n)
+    S = oracle.covariance(xy, 1.3, beta, nu, 1e-8)
+    low = np.tril(S)
+    rel = np.abs(G - low) / np.maximum(np.abs(low), 1e-300)
+    assert np.max(np.where(low != 0, rel, np.abs(G))) <= 2e-14
+    assert np.array_equal(np.diag(G), np.diag(S))
+    # padding of the last diagonal tile is the identity
+    nt = -(-n // 128)
+    Th = T.cpu().numpy()
+    last = Th[((nt - 1) * nt // 2 + nt - 1) * 128 * 128:][: 128 * 128].reshape(128, 128).T   # row-major view
+    r = n - (nt - 1) * 128
+    if r < 128:
+        assert np.array_equal(last[r:, r:], np.eye(128 - r))
+        assert not np.any(last[r:, :r])
+
+
+# ------------------------------------------------------------------------------------ K2-K4
+@pytest.mark.parametrize("n,nu", [(1, 0.5), (127, 0.5), (128, 1.5), (129, 0.5), (400, 0.5), (1000, 1.5), (2000, 0.5)])
+def test_potrf_vs_oracle(torch_cuda, n, nu):
+    torch = torch_cuda
+    xy = np.random.default_rng(7 + n).uniform(size=(n, 2))
+    beta = 0.1 if nu == 0.5 else 0.05
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, beta, nu, 1e-8)
+    info = mvn().mvn_potrf(T, n)
+    assert info == -1
+    Lg = to_dense_lower(T, n)
+    S = oracle.covariance(xy, 1.0, beta, nu, 1e-8)
+    Lo, info_o = oracle.cholesky(S, nthreads=8)
+    assert info_o == -1
+    res = np.linalg.norm(Lg @ Lg.T - S) / np.linalg.norm(S)
+    assert res <= 1e-12, res
+    # elementwise vs the oracle's factor: both are backward stable; bound by cond-scaled eps
+    cond = np.linalg.cond(S) if n <= 2000 else 1e8
+    assert np.max(np.abs(Lg - Lo)) <= max(1e-13, 50 * cond * 2.2e-16)
+
+
+def test_potrf_not_spd_reports_row(torch_cuda):
+    torch = torch_cuda
+    n = 300
+    A = np.eye(n)
+    A[200, 200] = -1.0
+    T = mvn().mvn_pack_lower(torch.from_numpy(A).cuda(), n)
+    info = mvn().mvn_potrf(T, n, raise_on_numeric=False)
+    assert info == 200
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_potrf(mvn().mvn_pack_lower(torch.from_numpy(A).cuda(), n), n)
+    B = np.array([[1.0, 2.0], [2.0, 1.0]])
+    assert mvn().mvn_potrf(mvn().mvn_pack_lower(torch.from_numpy(B).cuda(), 2), 2, raise_on_numeric=False) == 1
+
+
+def test_pack_unpack_roundtrip(torch_cuda):
+    torch = torch_cuda
+    n = 300
+    A = np.random.default_rng(1).standard_normal((n, n))
+    A = A + A.T
+    T = mvn().mvn_pack_lower(torch.from_numpy(A).cuda(), n)
+    assert np.array_equal(to_dense_lower(T, n), np.tril(A))
+
+
+# ------------------------------------------------------------------------------------ K5/K6
+def gpu_sov(torch, T, n, a, N, R, seed, begin=0, end=None, b=None):
+    d_a = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    d_b = None if b is None else torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    M, S = mvn().mvn_sov_prefix(T, n, d_a, N, R, seed, begin, end, b=d_b)
+    return M.cpu().numpy(), S.cpu().numpy()
+
+
+def oracle_range(L, a, b, N, R, seed, begin, end, nthreads=16):
+    """Oracle (M, S) over global samples [begin, end): per-shift units."""
+    n = L.shape[0]
+    G = lattice.generators(n)
+    D = lattice.shifts(seed, R, n)
+    parts = []
+    g = begin
+    while g < end:
+        r = g // N
+        j0 = g % N + 1
+        J = min(end - g, N - (j0 - 1))
+        J1 = J
+        # split big units so the oracle's threads have work
+        step = max(64, -(-J1 // nthreads))
+        off = 0
+        while off < J1:
+            jj = min(step, J1 - off)
+            MS, _, _ = oracle.sov_unit(L, a, b, G, D[r], j0 + off, jj)
+            parts.append(MS)
+            off += jj
+        g += J
+    return oracle.combine_units(np.array(parts))
+
+
+def logp_from(M, S, NR):
+    with np.errstate(divide="ignore"):
+        return np.where(S > 0, M + np.log(S) - math.log(NR), -np.inf)
+
+
+@pytest.mark.parametrize("cfgname,g,N,R,begin,end", [
+    ("A", 20, 10_000, 10, 0, None),          # config A in full
+    ("A", 9, 300, 4, 0, None),               # n = 81 (< one row block)
+    ("A", 19, 500, 3, 123, 1_377),           # ragged range across shifts, n = 361
+    ("C", 23, 200, 2, 0, None),              # nu = 3/2, u = 0.5, n = 529
+])
+def test_sov_shared_L_vs_oracle(torch_cuda, cfgname, g, N, R, begin, end):
+    torch = torch_cuda
+    cfg = W.small_config(f"{cfgname}{g}", g, N, R, base=cfgname)
+    inp, order, a = sorted_inputs(cfg)
+    n = cfg.n
+    T = gpu_cov(torch, inp.xy[order], cfg)
+    assert mvn().mvn_potrf(T, n) == -1
+    end = N * R if end is None else end
+    M, S = gpu_sov(torch, T, n, a, N, R, cfg.seed_lattice, begin, end)
+    L = to_dense_lower(T, n)
+    Mo, So = oracle_range(L, a, np.full(n, np.inf), N, R, cfg.seed_lattice, begin, end)
+    lp_g = logp_from(M, S, end - begin)
+    lp_o = logp_from(Mo, So, end - begin)
+    assert np.max(np.abs(lp_g - lp_o)) <= LOGP_TOL
+    assert np.max(np.abs(lp_g - lp_o)) <= 1e-11      # shared L: summation order only (expected ~1e-13)
+
+
+def test_sov_finite_b_and_tails(torch_cuda):
+    torch = torch_cuda
+    rng = np.random.default_rng(3)
+    n = 200
+    xy = rng.uniform(size=(n, 2))
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, 0.1, 0.5, 1e-8)
+    mvn().mvn_potrf(T, n)
+    L = to_dense_lower(T, n)
+    a = rng.uniform(-1.0, 0.5, n)
+    b = a + rng.uniform(0.2, 3.0, n)
+    b[::4] = np.inf
+    a[::7] = -np.inf
+    a[5] = 38.0 * L[5, 5]     # far upper tail on row 5 (log-space branch)
+    b[5] = np.inf
+    N, R = 300, 2
+    M, S = gpu_sov(torch, T, n, a, N, R, 99, b=b)
+    Mo, So = oracle_range(L, a, b, N, R, 99, 0, N * R)
+    lp_g, lp_o = logp_from(M, S, N * R), logp_from(Mo, So, N * R)
+    assert np.all(np.isfinite(lp_g))
+    assert np.max(np.abs(lp_g - lp_o)) <= 1e-10
+
+
+def test_sov_identity_closed_form(torch_cuda):
+    torch = torch_cuda
+    n = 300
+    T = mvn().mvn_pack_lower(torch.from_numpy(np.eye(n)).cuda(), n)
+    mvn().mvn_potrf(T, n)
+    a = np.full(n, -np.inf)
+    b = np.zeros(n)
+    M, S = gpu_sov(torch, T, n, a, 100, 2, 5, b=b)
+    lp = logp_from(M, S, 200)
+    assert np.max(np.abs(lp + np.arange(1, n + 1) * math.log(2))) <= 1e-12
+
+
+def test_sov_range_split_combines(torch_cuda):
+    """Sharding logic of the multi-GPU path on one device: two disjoint ranges, rescaled and summed,
+    equal the single call (up to rounding of the combine)."""
+    torch = torch_cuda
+    cfg = W.small_config("A15", 15, 1000, 4)
+    inp, order, a = sorted_inputs(cfg)
+    n = cfg.n
+    T = gpu_cov(torch, inp.xy[order], cfg)
+    mvn().mvn_potrf(T, n)
+    d_a = torch.from_numpy(a).cuda()
+    NR = cfg.NR
+    M, S = mvn().mvn_sov_prefix(T, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, 0, NR)
+    M1, S1 = mvn().mvn_sov_prefix(T, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, 0, 1500)
+    M2, S2 = mvn().mvn_sov_prefix(T, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, 1500, NR)
+    Mg = torch.maximum(M1, M2)
+    mvn().mvn_prefix_rescale(Mg, M1, S1)
+    mvn().mvn_prefix_rescale(Mg, M2, S2)
+    lp_split = mvn().mvn_prefix_finalize(Mg, S1 + S2, NR).cpu().numpy()
+    lp_one = mvn().mvn_prefix_finalize(M, S, NR).cpu().numpy()
+    assert np.max(np.abs(lp_split - lp_one)) <= 1e-13
+    # determinism: same call twice is bitwise identical
+    M3, S3 = mvn().mvn_sov_prefix(T, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, 0, NR)
+    assert torch.equal(M3, M) and torch.equal(S3, S)
+
+
+# ------------------------------------------------------------------------------------ end to end
+def test_crd_config_A_independent_vs_oracle(torch_cuda):
+    cfg = W.CONFIGS["A"]
+    inp = W.make_inputs(cfg)
+    out = mvn().mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                        cfg.seed_lattice, cfg.conf)
+    ref = oracle.crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                     cfg.seed_lattice, cfg.conf, chunk=625, nthreads=16)
+    assert out.info == -1
+    assert np.array_equal(out.order, ref.order)
+    assert np.max(np.abs(out.logP - ref.logp)) <= LOGP_TOL
+    assert np.array_equal(out.k_star, ref.k_star)
+    assert not np.any(ref.near_tie)
+
+
+@pytest.mark.slow
+def test_crd_config_B_independent_vs_oracle(torch_cuda):
+    """Config B (n = 4,900) end to end; the oracle runs all 1e5 samples on the host cores."""
+    cfg = W.CONFIGS["B"]
+    inp = W.make_inputs(cfg)
+    out = mvn().mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                        cfg.seed_lattice, cfg.conf)
+    ref = oracle.crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                     cfg.seed_lattice, cfg.conf, chunk=500, nthreads=0)
+    assert np.array_equal(out.order, ref.order)
+    assert np.max(np.abs(out.logP - ref.logp)) <= LOGP_TOL
+    assert np.array_equal(out.k_star, ref.k_star)
