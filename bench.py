@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""bench.py — one JSON line for the driver (contract in the task statement).
+
+A step is one pass of the whole hot path on one workload:
+  Matérn tiles -> tiled DMMA Cholesky -> (N>1: broadcast L) -> SOV/QMC prefix sweep over this
+  rank's samples -> (N>1: allreduce combine) -> log P_k -> confidence regions (host).
+Inputs (sorted locations, limits) are resident in HBM when the timed region starts; the e2e number
+times the public C-ABI call mvn_crd with host buffers (H2D and D2H inside).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config D] [--impl ours|reference]
+
+metric: BASELINE.json's "SOV-QMC n·N sample-dims/s" (value = n*N*R / step time, whole job), with
+the other two BASELINE metrics (Cholesky fp64 TFLOP/s, end-to-end region time) as extra keys.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PEAK_FP64_TFLOPS = 37.07          # measured DMMA peak on this pool (profiles/r01_fp64_calibration.md)
+METRIC = "SOV-QMC n·N sample-dims/s"
+UNIT = "sample-dims/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# --------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (SM clock, throttle reasons)."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------- oracle (CPU)
+def oracle_sample(cfg, n_sub: int, J: int, threads: int):
+    """The oracle on a bounded sample of the workload: the leading n_sub sorted locations (the first
+    n_sub prefixes are exactly the first n_sub rows of the full sweep, reading R1) with J samples of
+    shift 0. Returns (seconds, details) and the full-workload time extrapolated by operation count:
+    Cholesky (n/n_sub)^3, SOV (n/n_sub)^2 * NR/J."""
+    import oracle
+    inp = W.make_inputs(cfg)
+    var = np.full(cfg.n, cfg.sigma2 + cfg.nugget)
+    order, a, _ = oracle.marginal_order(inp.mu, var, cfg.u)
+    sel = order[:n_sub]
+    t0 = time.perf_counter()
+    S = oracle.covariance(inp.xy[sel], cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    t1 = time.perf_counter()
+    L, info = oracle.cholesky(S, nthreads=threads)
+    t2 = time.perf_counter()
+    G = oracle.generators(n_sub)
+    D = oracle.shifts(cfg.seed_lattice, 1, n_sub)
+    chunk = max(1, -(-J // threads))
+    parts = oracle.sov_units(L, a[:n_sub], np.full(n_sub, np.inf), G, D, J, 1, chunk, nthreads=threads)
+    M, Ssum = oracle.combine_units(parts)
+    oracle.prefix_logp(M, Ssum, J)
+    t3 = time.perf_counter()
+    n, NR = cfg.n, cfg.NR
+    t_full = (t1 - t0) * (n / n_sub) ** 2 + (t2 - t1) * (n / n_sub) ** 3 + (t3 - t2) * (n / n_sub) ** 2 * (NR / J)
+    return t3 - t0, t_full, {"cov_s": t1 - t0, "chol_s": t2 - t1, "sov_s": t3 - t2}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_plan(cfg):
+    """(n_sub, J) so that one oracle sample is ~10-20 s on ~16 cores."""
+    n_sub = min(cfg.n, 2048)
+    J = min(cfg.NR, 4096)
+    return n_sub, J
+
+
+# --------------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    thr = cpu_threads()
+    n_sub, J = oracle_plan(cfg)
+    for _ in range(args.warmup):
+        oracle_sample(cfg, min(n_sub, 256), min(J, 256), thr)
+    times, fulls = [], []
+    for _ in range(args.steps):
+        t, tf, det = oracle_sample(cfg, n_sub, J, thr)
+        times.append(t)
+        fulls.append(tf)
+    t_full = float(np.mean(fulls))
+    value = cfg.n * cfg.NR / t_full
+    sample = (f"oracle (oracle/, C -O2 + numpy) on the leading {n_sub} of {cfg.n} sorted locations x {J} samples "
+              f"of shift 0 per step; full-workload time extrapolated by op count (Cholesky x(n/n')^3, SOV x(n/n')^2*NR/J)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {cfg.name}", "n": cfg.n, "N": cfg.N, "R": cfg.R},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample,
+                             "measured_s_per_step": float(np.mean(times))},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="D", choices=sorted(W.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200 import parallel
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+
+    # ---- untimed setup: host inputs, a1 (marginal order), upload
+    inp = W.make_inputs(cfg)
+    n, NR = cfg.n, cfg.NR
+    var = np.full(n, cfg.sigma2 + cfg.nugget)
+    order, a, _ = mvn.mvn_marginal_order(inp.mu, var, cfg.u)
+    d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+    d_a = torch.from_numpy(a).cuda()
+    L = mvn.alloc_tiles(n)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
+
+    def step(events=None):
+        logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events)
+        lp = logp.cpu().numpy()                          # a10 on the host: regions
+        k, _ = mvn.mvn_confidence_region(lp, cfg.conf)
+        return lp, k
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, stage = [], {}
+    for _ in range(args.steps):
+        flush.zero_()                                    # L2 flush between timed iterations (untimed)
+        ev = []
+        lp, k = step(events=ev)
+        e_end = torch.cuda.Event(enable_timing=True)
+        e_end.record()
+        torch.cuda.synchronize()
+        names = [x[0] for x in ev]
+        for (nm0, e0), (nm1, e1) in zip(ev[:-1], ev[1:]):
+            stage.setdefault(nm1, []).append(e0.elapsed_time(e1))
+        stage.setdefault("region", []).append(ev[-1][1].elapsed_time(e_end))
+        step_ms.append(ev[0][1].elapsed_time(e_end))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        st = torch.tensor([np.mean(stage[k]) for k in sorted(stage)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        stage_mean = dict(zip(sorted(stage), st.cpu().tolist()))
+    else:
+        stage_mean = {k: float(np.mean(v)) for k, v in stage.items()}
+    ms_per_step = total_ms / args.steps
+    value = n * NR / (ms_per_step / 1e3)
+
+    # ---- e2e through the public C API with host buffers (N = 1: mvn_crd)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        ts = []
+        for it in range(2):                      # one warm-up call (allocations), one timed
+            t0 = time.perf_counter()
+            out = mvn.mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                              cfg.seed_lattice, cfg.conf)
+            t1 = time.perf_counter()
+            if it > 0:
+                ts.append(t1 - t0)
+        e2e = {"value": n * NR / float(np.mean(ts)), "unit": UNIT, "h2d_bytes_per_step": 24 * n,
+               "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)),
+               "k_star_matches_device_path": bool(np.array_equal(out.k_star, k))}
+    elif world > 1:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * n,
+               "note": "multi-GPU e2e not measured this round (mvn_crd is the single-GPU public call)"}
+
+    # ---- roofline of the dominant kernel (k_sov, SOV GEMM + chain), from the live stage times
+    sov_ms = stage_mean["sov"]
+    my_begin, my_end = parallel.shard_range(NR, rank, world)
+    my_samples = my_end - my_begin
+    sov_flops = float(n) * (n - 1) * my_samples       # algorithmic: sum_k 2(k-1) per sample (a6 + in-block dot)
+    achieved = sov_flops / (sov_ms / 1e3) / 1e12
+    nt = -(-n // 128)
+    launches = 1 + (nt + 2 * (nt - 1)) + 2 + 1 + (1 if world > 1 else 0)
+    potrf_ms = stage_mean["potrf"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {cfg.name}: n={n} ({cfg.g}x{cfg.g} jittered grid), Matern "
+                               f"(s2={cfg.sigma2}, beta={cfg.beta}, nu={cfg.nu}) + nugget {cfg.nugget}, u={cfg.u}, "
+                               f"N={cfg.N} x R={cfg.R} QMC", "n": n, "N": cfg.N, "R": cfg.R,
+                   "parallelism": f"samples sharded over {world} GPU(s), L broadcast from rank 0",
+                   "l2": "flushed between timed steps (256 MB write); L itself is "
+                         f"{mvn.mvn_tiles_bytes(n) / 1e9:.2f} GB"},
+        "cholesky_tflops": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12,
+        "sov_sample_dims_per_s": n * my_samples / (sov_ms / 1e3),
+        "region_time_ms": ms_per_step,
+        "stage_ms": stage_mean,
+        "roofline": {"kernel": "k_sov (SOV DMMA GEMM + Phi chain)", "bound": "tensor", "achieved": achieved,
+                     "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
+                     "traffic": None,
+                     "peak_source": "measured fp64 DMMA peak (tools/calib_fp64.cu, profiles/r01_fp64_calibration.md); "
+                                    "MEASURED_PEAKS.json has no fp64 entry",
+                     "algorithmic": f"n(n-1) flops per sample x {my_samples} samples"},
+        "potrf_roofline": {"achieved": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12, "peak": PEAK_FP64_TFLOPS,
+                           "frac": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12 / PEAK_FP64_TFLOPS},
+        "clocks": clk,
+        "gpu_launches": launches * args.steps,
+        "e2e": e2e,
+        "k_star": [int(x) for x in k],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        thr = cpu_threads()
+        n_sub, J = oracle_plan(cfg)
+        t, t_full, det = oracle_sample(cfg, n_sub, J, thr)
+        line["cpu_baseline"] = {"value": n * NR / t_full, "unit": UNIT, "cores": thr, "kind": "oracle",
+                                "sample": f"leading {n_sub} of {n} sorted locations x {J} samples of shift 0 "
+                                          f"(cov+Cholesky+SOV, {t:.1f} s measured); full-workload time "
+                                          f"{t_full:.0f} s extrapolated by op count",
+                                "measured": det}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
