@@ -1,22 +1,27 @@
 // K5/K6 — the SOV sweep with Richtmyer-lattice QMC (Alg. 2 PMVN; Alg. 3 QMC tile
 // kernel; Eq. 2-3), all prefixes in one sweep (reading R1).
 //
-// Work decomposition (B200-first, not the paper's tile-task DAG):
-//   * The parallel axis is the sample ("MC chain"). A CTA owns a block of NB consecutive
-//     global samples and sweeps all n rows in row blocks of 64; CTAs are persistent (one per SM).
-//   * Row block r (rows [64r, 64r+64)):
-//       (a6) S = L[rows, 0:64r] * Y[0:64r, block]  — left-looking fp64 DMMA GEMM (box (c), one
-//            product serves a' and b', reading R7), operands streamed by a 3-stage cp.async
-//            pipeline: L panel from L2 (all CTAs sweep the same rows), Y history from this CTA's
-//            HBM scratch.
-//       (a7) the in-block recursion of Alg. 3 per sample (thread j = sample j): in sub-blocks of
-//            8 rows, s += in-block dot, Phi/Phi^{-1} step (normal.cuh), log-weight ell += log q,
-//            y written to the Y history (coalesced) and folded into the remaining rows of S.
-//       (a8) per-row log-sum-exp over the block's samples (warp shuffles) -> (M, S) partial per
-//            (sample block, row).
+// B200-first decomposition (not the paper's tile-task DAG):
+//   * The parallel axis is the sample ("MC chain"). Persistent CTAs, one per SM; CTA c owns
+//     a balanced contiguous range of global samples (NR/148 each), swept as blocks of <= 128
+//     samples (the last block of a CTA is narrowed to a multiple of 32, so no CTA idles in a tail
+//     wave). Each block sweeps all n rows in row blocks of 64.
+//   * Warp specialisation (416 threads):
+//       warp 12    (producer): streams 16-column K-chunks of the L row panel (from L2 — all CTAs
+//                  sweep the same rows) and 16-row chunks of the Y history (this CTA's HBM scratch)
+//                  into a 4-stage shared-memory ring with TMA bulk copies (cp.async.bulk, mbarrier
+//                  complete_tx); full/empty mbarriers, no CTA-wide barrier in the main loop.
+//       warps 0-7  (GEMM): (a6) S_r = L[rows r, 0:64r] * Y[0:64r, block] on fp64 DMMA. The part
+//                  of S_{r+1} that only needs Y[0:64r] is computed WHILE the chain warps run row
+//                  block r; only the last 64 columns wait for Y_r.
+//       warps 8-11 (chain): (a7) Alg. 3's in-block recursion, one thread per sample: sub-blocks of
+//                  8 rows, s += in-block dot, Phi/Phi^{-1} step (normal.cuh), ell += log q, y to
+//                  the Y history (coalesced) and folded into the remaining rows of S;
+//                  (a8) per-row log-sum-exp over the block's samples (warp shuffles).
+//     Hand-off through named barriers: S_FULL (GEMM -> chain), Y_READY (chain -> GEMM).
 //   * k_reduce_blocks combines the block partials of every prefix in fixed order (deterministic).
-// The lattice point w (reading R8) is generated in registers from 64-bit integers; the n x NR
-// matrices R, A, B of Alg. 2 are never materialised.
+// The lattice point w (reading R8) is generated in registers; the n x NR matrices R, A, B of
+// Alg. 2 are never materialised.
 #include "common.cuh"
 #include "gemm_dmma.cuh"
 #include "mvn_internal.h"
@@ -24,19 +29,54 @@
 
 namespace mvn {
 namespace sovk {
-constexpr int M = 64;              // SOV row block
-constexpr int BK = 16, STAGES = 3;
-constexpr int SA = M + 4;          // 68 == 4 (mod 16)
-constexpr int NT = 256;            // threads per CTA
-template <int NB> struct Cfg {
-    static constexpr int SB = NB + 4;      // pipeline B stride, == 4 (mod 16) for NB % 16 == 0
-    static constexpr int SS = NB + 8;      // S / ell tile stride (16-byte stores conflict-free)
-    static constexpr int WN = NB / 32;     // 8-column DMMA blocks per warp (warp tile 32 x NB/4)
-    static constexpr int PIPE = STAGES * BK * (SA + SB);
-    static constexpr int UNION = (PIPE > M * SS) ? PIPE : M * SS;
-    static constexpr int SMEM = (UNION + M * M + 3 * M) * 8;
-};
+constexpr int M = 64;                    // SOV row block
+constexpr int NB = 128;                  // max samples per block (= chain threads)
+constexpr int BK = 16, STAGES = 4;
+constexpr int SA = M + 4;                // 68  == 4 (mod 16): conflict-free DMMA fragment loads
+constexpr int SB = NB + 4;               // 132 == 4 (mod 16)
+constexpr int SS = NB + 8;               // S tile stride (16-byte fragment stores conflict-free)
+constexpr int NGEMM = 256, NCHAIN = NB, NPROD = 32, NT = NGEMM + NCHAIN + NPROD;
+constexpr int STAGE = BK * (SA + SB);                    // doubles per pipeline stage
+constexpr int OFF_S = STAGES * STAGE;                    // S[64][SS]: s, then y, of the row block
+constexpr int OFF_LD = OFF_S + M * SS;                   // Ld[64 cols][64 rows] (column-major)
+constexpr int OFF_PS = OFF_LD + M * M;                   // per-row, per-chain-warp (max, sum) [64][4][2]
+constexpr int OFF_AG = OFF_PS + M * 4 * 2;               // [3][64]: a, b, G (as double bits)
+constexpr int OFF_BAR = OFF_AG + 3 * M;                  // full[STAGES], empty[STAGES] mbarriers
+constexpr int SMEM = (OFF_BAR + 2 * STAGES) * 8;
+constexpr int CPB = M / BK;                              // K-chunks per row block
+enum : int { BAR_SFULL = 1, BAR_YREADY = 2, BAR_CHAIN = 3 };
+constexpr int N_SFULL = NGEMM + NCHAIN, N_YREADY = NCHAIN + NPROD;
 }  // namespace sovk
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// TMA-engine bulk copy global -> shared, completion counted on an mbarrier (SASS UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes));
+}
 
 __device__ __forceinline__ uint64_t lattice_shift(uint64_t seed, uint64_t r, uint64_t k) {
     // SplitMix64 output function of the counter seed + GAMMA * (r*2^32 + k + 1) (reading R8)
@@ -54,159 +94,274 @@ __device__ __forceinline__ double lattice_w(uint64_t j, uint64_t G, uint64_t D) 
 struct SovArgs {
     const double *L;
     int64_t n;
-    int nrb;                 // row blocks of 64 (ceil(n/64))
-    const double *a, *b;     // b may be null (+inf)
+    int nrb;                  // row blocks of 64 (ceil(n/64))
+    const double *a, *b;      // b may be null (+inf)
     const uint64_t *G;
     int64_t N;
     uint64_t seed;
-    int64_t g_begin, g_end;  // global sample range
-    int64_t nblk;            // sample blocks
-    int64_t n_pad;           // Y-history rows per slot (nrb*64)
-    double *Y;               // [gridDim][n_pad][NB]
-    double *part;            // [nblk][n_pad][2]
+    const int64_t *cta;       // [grid][3]: first global sample, sample count, first block index
+    int64_t n_pad;            // Y-history rows per slot (nrb*64)
+    double *Y;                // [grid][n_pad][NB]
+    double *part;             // [nblk][n_pad][2]
 };
 
-template <int NB, bool HAS_B>
-__global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
+__device__ __forceinline__ int block_width(int64_t count, int b) {
+    const int64_t rem = count - (int64_t)b * sovk::NB;
+    const int cnt = rem < sovk::NB ? (int)rem : sovk::NB;
+    return cnt;
+}
+
+// ------------------------------------------------------------------------------------ producer
+// One warp streams K-chunks (16 columns of the L row panel + 16 rows of the Y history) into the
+// STAGES-deep ring with TMA bulk copies: lanes 0-15 copy one 512-byte L column segment each,
+// lanes 16-31 one Y row (w samples) each. The chunk of row block r whose Y rows come from row
+// block r-1 is only issued after the chain warps have published Y_{r-1} (barrier Y_READY).
+__device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const double *Yslot, int64_t count, int nblk,
+                                             int lane) {
     using namespace sovk;
-    using C = Cfg<NB>;
-    extern __shared__ double sm[];
-    double *As = sm;                                    // pipeline (union with S)
-    double *Bs = sm + STAGES * BK * SA;
-    double *S = sm;                                     // M x SS: s, then ell
-    double *Ld = sm + C::UNION;                         // 64 x 64 diagonal block of L, row-major
-    double *a_s = Ld + M * M;
-    double *b_s = a_s + M;
-    uint64_t *G_s = reinterpret_cast<uint64_t *>(b_s + M);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * (NB / 4);
-    double *Yslot = p.Y + (int64_t)blockIdx.x * p.n_pad * NB;
-
-    for (int64_t blk = blockIdx.x; blk < p.nblk; blk += gridDim.x) {
-        const int64_t g0 = p.g_begin + blk * NB;
-        const int64_t rem = p.g_end - g0;
-        const int cnt = rem < NB ? (int)rem : NB;
-        const int j = tid;                               // sample within block (tid < NB)
-        const uint64_t g = (uint64_t)(g0 + (j < NB ? j : 0));
-        const uint64_t r = g / (uint64_t)p.N;
-        const uint64_t jl = g - r * (uint64_t)p.N + 1ull;   // 1-based lattice index
-        double ell = 0.0;
-
-        for (int rb = 0; rb < p.nrb; ++rb) {
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
+    uint64_t *empty = full + STAGES;
+    uint32_t q = 0;
+    for (int b = 0; b < nblk; ++b) {
+        const int w = (block_width(count, b) + 31) & ~31;
+        for (int rb = 1; rb < p.nrb; ++rb) {
             const int64_t row0 = (int64_t)rb * M;
             const int R = (int)(row0 / kTile), hh = (int)(row0 % kTile);
-            // ---------------------------------------------------------------- (a6) GEMM
-            if (rb > 0) {
-                double acc[4][C::WN][2];
-#pragma unroll
-                for (int x = 0; x < 4; ++x)
-#pragma unroll
-                    for (int y = 0; y < C::WN; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-                auto load = [&](int ch, int st) {
-                    const int64_t kc = (int64_t)ch * BK;              // first column of the chunk
-                    const int T = (int)(kc / kTile), cc = (int)(kc % kTile);
-                    const double *Lsrc = p.L + tile_offset(R, T) + (int64_t)cc * kTile + hh;
-                    double *as = As + st * BK * SA;
-                    double *bs = Bs + st * BK * C::SB;
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {                     // 16 cols x 64 rows
-                        const int e = q * NT + tid;
-                        const int col = e >> 5, seg = e & 31;
-                        cp_async16(as + col * SA + seg * 2, Lsrc + (int64_t)col * kTile + seg * 2);
-                    }
-                    const double *Ysrc = Yslot + kc * NB;               // 16 rows x NB, contiguous
-#pragma unroll
-                    for (int q = 0; q < NB / 32; ++q) {
-                        const int e = q * NT + tid;
-                        const int row = e / (NB / 2), seg = e % (NB / 2);
-                        cp_async16(bs + row * C::SB + seg * 2, Ysrc + (int64_t)row * NB + seg * 2);
-                    }
-                };
-                gemm_mainloop<BK, STAGES, SA, C::SB, 4, C::WN>((int)(row0 / BK), As, Bs, wm0, wn0, lane, acc, load);
-#pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                    const int row = wm0 + x * 8 + (lane >> 2);
-#pragma unroll
-                    for (int y = 0; y < C::WN; ++y) {
-                        const int col = wn0 + y * 8 + 2 * (lane & 3);
-                        *reinterpret_cast<double2 *>(S + row * C::SS + col) = make_double2(acc[x][y][0], acc[x][y][1]);
-                    }
-                }
-            } else {
-                for (int e = tid; e < M * C::SS; e += NT) S[e] = 0.0;
-            }
-            // diagonal block L[row0:+64, row0:+64] (row-major in smem), limits, generators
-            {
-                const double *Dsrc = p.L + tile_offset(R, R) + (int64_t)hh * kTile + hh;
-                for (int e = tid; e < M * M; e += NT) {
-                    const int col = e >> 6, row = e & 63;            // coalesced along rows
-                    Ld[row * M + col] = Dsrc[(int64_t)col * kTile + row];
-                }
-                if (tid < M) {
-                    const int64_t k = row0 + tid;
-                    a_s[tid] = k < p.n ? p.a[k] : 0.0;
-                    b_s[tid] = (HAS_B && k < p.n) ? p.b[k] : CUDART_INF;
-                    G_s[tid] = k < p.n ? p.G[k] : 0ull;
+            for (int c = 0; c < CPB * rb; ++c, ++q) {
+                if (c == CPB * (rb - 1)) named_sync(BAR_YREADY, N_YREADY);   // Y_{rb-1} published
+                const int st = q % STAGES;
+                mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
+                const int64_t kc = (int64_t)c * BK;
+                double *as = sm + st * STAGE;
+                double *bs = as + BK * SA;
+                if (lane == 0) mbar_arrive_expect_tx(&full[st], (unsigned)(BK * M * 8 + BK * w * 8));
+                __syncwarp();
+                if (lane < 16) {
+                    const int T = (int)(kc / kTile), cc = (int)(kc % kTile) + lane;
+                    bulk_g2s(as + lane * SA, p.L + tile_offset(R, T) + (int64_t)cc * kTile + hh, M * 8, &full[st]);
+                } else {
+                    const int row = lane - 16;
+                    bulk_g2s(bs + row * SB, Yslot + (kc + row) * NB, (unsigned)(w * 8), &full[st]);
                 }
             }
-            __syncthreads();
-            // ---------------------------------------------------------------- (a7) chain
-            if (j < NB) {
-#pragma unroll 1
-                for (int sb = 0; sb < M / 8; ++sb) {
-                    const int rb0 = sb * 8;
-                    double s[8], yv[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) s[i] = S[(rb0 + i) * C::SS + j];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int li = rb0 + i;
-                        const int64_t k = row0 + li;
-                        double y = 0.0;
-                        if (k < p.n) {
-                            const double lkk = Ld[li * M + li];
-                            const double ap = (a_s[li] - s[i]) / lkk;
-                            const double w = lattice_w(jl, G_s[li], lattice_shift(p.seed, r, (uint64_t)k));
-                            double lq;
-                            if (HAS_B) sov_step(ap, (b_s[li] - s[i]) / lkk, w, lq, y);
-                            else sov_step_upper(ap, w, lq, y);
-                            ell += lq;
-                        }
-                        yv[i] = y;
-                        S[li * C::SS + j] = ell;
-                        Yslot[k * NB + j] = y;
-#pragma unroll
-                        for (int i2 = i + 1; i2 < 8; ++i2) s[i2] += Ld[(rb0 + i2) * M + li] * y;
-                    }
-                    for (int li = rb0 + 8; li < M; ++li) {
-                        double t = S[li * C::SS + j];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) t += Ld[li * M + rb0 + i] * yv[i];
-                        S[li * C::SS + j] = t;
-                    }
-                }
-            }
-            __threadfence_block();
-            __syncthreads();
-            // ---------------------------------------------------------------- (a8) per-row lse
-            for (int li = warp; li < M; li += NT / 32) {
-                const int64_t k = row0 + li;
-                if (k >= p.n) break;
-                double m = -CUDART_INF;
-                for (int jj = lane; jj < cnt; jj += 32) m = fmax(m, S[li * C::SS + jj]);
-#pragma unroll
-                for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-                double sum = 0.0;
-                if (m != -CUDART_INF)
-                    for (int jj = lane; jj < cnt; jj += 32) sum += exp(S[li * C::SS + jj] - m);
-#pragma unroll
-                for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-                if (lane == 0)
-                    *reinterpret_cast<double2 *>(p.part + (blk * p.n_pad + k) * 2) = make_double2(m, sum);
-            }
-            __syncthreads();
         }
+        named_sync(BAR_YREADY, N_YREADY);                     // the block's last chain is done
+    }
+}
+
+// ------------------------------------------------------------------------------------ GEMM warps
+// S_r (64 x w) = L[rows r, 0:64r] * Y[0:64r, block]: 8 warps as 2 (rows) x 4 (columns), warp tile
+// 32 x 8*WN, fp64 DMMA.8x8x4 from conflict-free shared-memory fragments.
+template <int WN>
+__device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, uint32_t &q) {
+    using namespace sovk;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
+    uint64_t *empty = full + STAGES;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * (WN * 8);
+    double acc[4][WN][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int c = 0; c < CPB * rb; ++c, ++q) {
+        const int st = q % STAGES;
+        mbar_wait(&full[st], (q / STAGES) & 1);
+        const double *as = sm + st * STAGE;
+        const double *bs = as + BK * SA;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double fa[4], fb[WN];
+            const int kr = kk + (lane & 3);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) fa[i] = as[kr * SA + wm0 + i * 8 + (lane >> 2)];
+#pragma unroll
+            for (int j = 0; j < WN; ++j) fb[j] = bs[kr * SB + wn0 + j * 8 + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < WN; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    double *S = sm + OFF_S;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = wm0 + i * 8 + (lane >> 2);
+#pragma unroll
+        for (int j = 0; j < WN; ++j) {
+            const int col = wn0 + j * 8 + 2 * (lane & 3);
+            *reinterpret_cast<double2 *>(S + row * SS + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------ chain warps
+// Diagonal block L[row0:+64, row0:+64] (column-major, Ld[col*64 + row]) and the limits / generators
+// of the row block, by cp.async (zero-filled past n).
+template <bool HAS_B>
+__device__ __forceinline__ void chain_load(const SovArgs &p, double *sm, int rb, int ct) {
+    using namespace sovk;
+    const int64_t row0 = (int64_t)rb * M;
+    const int R = (int)(row0 / kTile), hh = (int)(row0 % kTile);
+    const double *Dsrc = p.L + tile_offset(R, R) + (int64_t)hh * kTile + hh;
+    double *Ld = sm + OFF_LD;
+#pragma unroll
+    for (int qq = 0; qq < 16; ++qq) {                    // 64 cols x 64 rows = 2048 x 16 B
+        const int e = qq * NCHAIN + ct;
+        const int col = e >> 5, seg = e & 31;
+        cp_async16(Ld + col * M + seg * 2, Dsrc + (int64_t)col * kTile + seg * 2);
+    }
+    double *ag = sm + OFF_AG;
+    if (ct < 96) {                                       // a, b, G: 3 x 32 segments of 2 values
+        const int which = ct >> 5, seg = ct & 31;
+        const int64_t k = row0 + seg * 2;
+        const int valid = k + 1 < p.n ? 16 : (k < p.n ? 8 : 0);
+        const int64_t kk = valid ? k : 0;
+        const void *src = which == 0 ? (const void *)(p.a + kk)
+                                     : which == 1 ? (const void *)(HAS_B ? p.b + kk : p.a + kk) : (const void *)(p.G + kk);
+        cp_async16_zfill(ag + which * M + seg * 2, src, (which == 1 && !HAS_B) ? 0 : valid);
+    }
+}
+
+// Alg. 3 on one row block for sample j (thread j of the chain group). s for row li arrives in
+// S[li][j] (GEMM part + in-block contributions so far) and y_li overwrites it. Sub-blocks of 8
+// rows: rows inside a sub-block update each other directly, the remaining rows of the block get
+// the sub-block's 8 y values in one pass (8 FMAs per shared-memory read/write). After each row the
+// warp reduces (max, sum exp) of its 32 samples' log weights into ps[row][warp].
+template <bool HAS_B>
+__device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, double *Yslot, int rb, int j, int cnt,
+                                               uint64_t r, uint64_t jl, double &ell) {
+    using namespace sovk;
+    const int64_t row0 = (int64_t)rb * M;
+    double *S = sm + OFF_S;
+    const double *Ld = sm + OFF_LD;
+    double *ps = sm + OFF_PS;
+    const double *a_s = sm + OFF_AG;
+    const double *b_s = a_s + M;
+    const uint64_t *G_s = reinterpret_cast<const uint64_t *>(a_s + 2 * M);
+    const int lane = j & 31, cw = j >> 5;
+    const bool valid = j < cnt;
+    if (rb == 0)                                          // S_0 = 0: no GEMM for the first row block
+        for (int li = 0; li < M; ++li) S[li * SS + j] = 0.0;
+#pragma unroll 1
+    for (int sb = 0; sb < M / 8; ++sb) {
+        const int rb0 = sb * 8;
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i) {
+            const int li = rb0 + i;
+            const int64_t k = row0 + li;
+            if (k >= p.n) break;                          // uniform: padded rows need no y
+            const double s = S[li * SS + j];
+            const double lkk = Ld[li * M + li];
+            const double ap = (a_s[li] - s) / lkk;
+            const double wq = lattice_w(jl, G_s[li], lattice_shift(p.seed, r, (uint64_t)k));
+            double lq, y;
+            if (HAS_B) sov_step(ap, (b_s[li] - s) / lkk, wq, lq, y);
+            else sov_step_upper(ap, wq, lq, y);
+            ell += lq;
+            S[li * SS + j] = y;
+            Yslot[k * NB + j] = y;
+#pragma unroll 1
+            for (int i2 = li + 1; i2 < rb0 + 8; ++i2) S[i2 * SS + j] += Ld[li * M + i2] * y;
+            // per-row log-sum-exp over this warp's samples
+            double m = valid ? ell : -CUDART_INF;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            double e = (valid && m != -CUDART_INF) ? exp(ell - m) : 0.0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+            if (lane == 0) *reinterpret_cast<double2 *>(ps + (li * 4 + cw) * 2) = make_double2(m, e);
+        }
+        double yv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) yv[i] = S[(rb0 + i) * SS + j];
+#pragma unroll 2
+        for (int li = rb0 + 8; li < M; ++li) {
+            double t = S[li * SS + j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t += Ld[(rb0 + i) * M + li] * yv[i];
+            S[li * SS + j] = t;
+        }
+    }
+}
+
+template <bool HAS_B>
+__global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
+    using namespace sovk;
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x;
+    const int64_t g_first = p.cta[blockIdx.x * 3], count = p.cta[blockIdx.x * 3 + 1], blk_first = p.cta[blockIdx.x * 3 + 2];
+    const int nblk = (int)((count + NB - 1) / NB);
+    double *Yslot = p.Y + (int64_t)blockIdx.x * p.n_pad * NB;
+    if (tid == 0) {
+        uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&full[STAGES + s], NGEMM / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (tid < NGEMM) {
+        // ============================================================ GEMM warps
+        uint32_t q = 0;
+        for (int b = 0; b < nblk; ++b) {
+            const int w = (block_width(count, b) + 31) & ~31;
+            for (int rb = 1; rb < p.nrb; ++rb) {
+                switch (w >> 5) {
+                    case 1: sov_gemm_rowblock<1>(sm, rb, tid, q); break;
+                    case 2: sov_gemm_rowblock<2>(sm, rb, tid, q); break;
+                    case 3: sov_gemm_rowblock<3>(sm, rb, tid, q); break;
+                    default: sov_gemm_rowblock<4>(sm, rb, tid, q); break;
+                }
+                named_arrive(BAR_SFULL, N_SFULL);
+            }
+        }
+    } else if (tid < NGEMM + NCHAIN) {
+        // ============================================================ chain warps
+        const int j = tid - NGEMM;
+        for (int b = 0; b < nblk; ++b) {
+            const int64_t g0 = g_first + (int64_t)b * NB;
+            const int cnt = block_width(count, b);
+            const int w = (cnt + 31) & ~31;
+            const uint64_t g = (uint64_t)(g0 + (j < cnt ? j : 0));
+            const uint64_t r = g / (uint64_t)p.N;
+            const uint64_t jl = g - r * (uint64_t)p.N + 1ull;    // 1-based lattice index
+            const int64_t blk = blk_first + b;
+            double ell = 0.0;
+            for (int rb = 0; rb < p.nrb; ++rb) {
+                chain_load<HAS_B>(p, sm, rb, j);                  // Ld / a / G of this row block
+                cp_async_commit();
+                if (rb > 0) named_sync(BAR_SFULL, N_SFULL);       // S_rb written by the GEMM warps
+                cp_async_wait<0>();
+                named_sync(BAR_CHAIN, NCHAIN);
+                if (j < w) chain_rowblock<HAS_B>(p, sm, Yslot, rb, j, cnt, r, jl, ell);
+                __threadfence();                                  // Y_rb: generic-proxy writes ...
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");   // ... visible to the TMA reads
+                named_arrive(BAR_YREADY, N_YREADY);
+                named_sync(BAR_CHAIN, NCHAIN);                   // ps complete, Ld / S free
+                if (j < M) {
+                    const int64_t k = (int64_t)rb * M + j;
+                    if (k < p.n) {
+                        const double *ps = sm + OFF_PS + j * 8;
+                        const int nw = w >> 5;
+                        double mm = -CUDART_INF;
+                        for (int qq = 0; qq < nw; ++qq) mm = fmax(mm, ps[2 * qq]);
+                        double ss = 0.0;
+                        if (mm != -CUDART_INF)
+                            for (int qq = 0; qq < nw; ++qq)
+                                if (ps[2 * qq] != -CUDART_INF) ss += ps[2 * qq + 1] * exp(ps[2 * qq] - mm);
+                        *reinterpret_cast<double2 *>(p.part + (blk * p.n_pad + k) * 2) = make_double2(mm, ss);
+                    }
+                }
+            }
+        }
+    } else {
+        // ============================================================ producer warp
+        sov_producer(p, sm, Yslot, count, nblk, tid & 31);
     }
 }
 
@@ -227,63 +382,37 @@ __global__ void k_reduce_blocks(const double *__restrict__ part, int64_t nblk, i
     So[k] = s;
 }
 
-template <int NB, bool HB>
-static cudaError_t set_attr() {
-    return cudaFuncSetAttribute(k_sov<NB, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sovk::Cfg<NB>::SMEM);
-}
-
 cudaError_t sov_init() {
-    cudaError_t e = cudaSuccess;
-#define MVN_SOV_ATTR(NB)                               \
-    if ((e = set_attr<NB, false>()) != cudaSuccess) return e; \
-    if ((e = set_attr<NB, true>()) != cudaSuccess) return e;
-    MVN_SOV_ATTR(128) MVN_SOV_ATTR(160) MVN_SOV_ATTR(192) MVN_SOV_ATTR(224) MVN_SOV_ATTR(256)
-#undef MVN_SOV_ATTR
-    return e;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_sov<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sovk::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_sov<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sovk::SMEM))) return e;
+    return cudaSuccess;
 }
 
-int sov_pick_nb(int64_t nsamp, int64_t n, int nsm) {
-    static const int cand[5] = {256, 224, 192, 160, 128};
-    int best = 256;
-    double bestc = 1e300;
-    const double chain = (double)((n + 63) / 64) * 64.0 * 1500.0;   // latency-bound chain clk per block
-    for (int c : cand) {
-        const int64_t nblk = (nsamp + c - 1) / c;
-        const int64_t waves = (nblk + nsm - 1) / nsm;
-        const double gemm = (double)c * (double)n * (double)n / 128.0;  // DMMA clk per block at full rate
-        const double cost = (double)waves * (gemm + chain);
-        if (cost < bestc * (1 - 1e-9)) { bestc = cost; best = c; }
-    }
-    return best;
-}
+int sov_block_samples() { return sovk::NB; }
 
-size_t sov_smem_bytes(int nb) {
-    switch (nb) {
-        case 128: return sovk::Cfg<128>::SMEM;
-        case 160: return sovk::Cfg<160>::SMEM;
-        case 192: return sovk::Cfg<192>::SMEM;
-        case 224: return sovk::Cfg<224>::SMEM;
-        default: return sovk::Cfg<256>::SMEM;
+// Balanced partition of [g_begin, g_end) over `grid` CTAs: CTA c gets a contiguous share of
+// floor/ceil(nsamp/grid) samples, processed as blocks of 128 (last one narrowed to 32k).
+int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta) {
+    const int64_t ns = g_end - g_begin, base = ns / grid, rem = ns % grid;
+    int64_t blk = 0, g = g_begin;
+    for (int c = 0; c < grid; ++c) {
+        const int64_t cnt = base + (c < rem ? 1 : 0);
+        cta[3 * c] = g;
+        cta[3 * c + 1] = cnt;
+        cta[3 * c + 2] = blk;
+        g += cnt;
+        blk += (cnt + sovk::NB - 1) / sovk::NB;
     }
+    return blk;
 }
 
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
     SovArgs a;
     a.L = L.L; a.n = L.n; a.nrb = (int)((L.n + 63) / 64); a.a = L.a; a.b = L.b; a.G = L.G; a.N = L.N;
-    a.seed = L.seed; a.g_begin = L.g_begin; a.g_end = L.g_end; a.nblk = L.nblk; a.n_pad = (int64_t)a.nrb * 64;
-    a.Y = L.Y; a.part = L.part;
-    const dim3 grid(L.grid), block(sovk::NT);
-    const size_t sm = sov_smem_bytes(L.nb);
-#define MVN_SOV_LAUNCH(NB)                                                               \
-    case NB:                                                                             \
-        if (L.b) k_sov<NB, true><<<grid, block, sm, st>>>(a);                            \
-        else k_sov<NB, false><<<grid, block, sm, st>>>(a);                               \
-        break;
-    switch (L.nb) {
-        MVN_SOV_LAUNCH(128) MVN_SOV_LAUNCH(160) MVN_SOV_LAUNCH(192) MVN_SOV_LAUNCH(224) MVN_SOV_LAUNCH(256)
-        default: return cudaErrorInvalidValue;
-    }
-#undef MVN_SOV_LAUNCH
+    a.seed = L.seed; a.cta = L.cta; a.n_pad = (int64_t)a.nrb * 64; a.Y = L.Y; a.part = L.part;
+    if (L.b) k_sov<true><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
+    else k_sov<false><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     k_reduce_blocks<<<(unsigned)((L.n + 255) / 256), 256, 0, st>>>(L.part, L.nblk, L.n, a.n_pad, L.Mout, L.Sout);

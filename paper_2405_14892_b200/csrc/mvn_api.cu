@@ -21,6 +21,7 @@ struct mvn_ctx {
     // workspace (device)
     void *Y = nullptr; size_t Y_cap = 0;
     void *part = nullptr; size_t part_cap = 0;
+    void *cta = nullptr; size_t cta_cap = 0;
     uint64_t *G = nullptr; int64_t G_n = 0;
     int64_t *d_info = nullptr;
     // mvn_crd buffers
@@ -151,7 +152,7 @@ void mvn_destroy(mvn_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (void *p : {c->Y, c->part, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec})
+    for (void *p : {c->Y, c->part, c->cta, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec})
         if (p) cudaFree(p);
     delete c;
 }
@@ -167,9 +168,9 @@ const char *mvn_last_error(const mvn_ctx *c) { return c ? c->err.c_str() : "null
 mvn_status mvn_trim(mvn_ctx *c) {
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->crd_L, &c->crd_vec})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->crd_L, &c->crd_vec})
         if (*p) { cudaFree(*p); *p = nullptr; }
-    c->Y_cap = c->part_cap = c->crd_L_cap = c->crd_vec_cap = 0;
+    c->Y_cap = c->part_cap = c->cta_cap = c->crd_L_cap = c->crd_vec_cap = 0;
     return MVN_OK;
 }
 
@@ -267,12 +268,16 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
     mvn::SovLaunch L;
     L.L = d_L; L.n = t.n; L.a = d_a; L.b = d_b; L.G = c->G; L.N = q->N; L.seed = q->seed;
     L.g_begin = q->sample_begin; L.g_end = q->sample_end;
-    L.nb = mvn::sov_pick_nb(nsamp, t.n, c->nsm);
-    L.nblk = (nsamp + L.nb - 1) / L.nb;
-    L.grid = (int)std::min<int64_t>(L.nblk, c->nsm);
+    L.grid = (int)std::min<int64_t>(nsamp, c->nsm);
+    std::vector<int64_t> cta((size_t)L.grid * 3);
+    L.nblk = mvn::sov_partition(q->sample_begin, q->sample_end, L.grid, cta.data());
     const int64_t n_pad = (t.n + 63) / 64 * 64;
-    if ((s = ensure(c, &c->Y, &c->Y_cap, (size_t)L.grid * n_pad * L.nb * sizeof(double))) != MVN_OK) return s;
+    const int nb = mvn::sov_block_samples();
+    if ((s = ensure(c, &c->Y, &c->Y_cap, (size_t)L.grid * n_pad * nb * sizeof(double))) != MVN_OK) return s;
     if ((s = ensure(c, &c->part, &c->part_cap, (size_t)L.nblk * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->cta, &c->cta_cap, cta.size() * sizeof(int64_t))) != MVN_OK) return s;
+    MVN_CUDA(c, cudaMemcpyAsync(c->cta, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    L.cta = (const int64_t *)c->cta;
     L.Y = (double *)c->Y; L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S;
     MVN_CUDA(c, mvn::launch_sov(L, c->stream));
     return MVN_OK;

@@ -24,15 +24,16 @@ struct SovLaunch {
     int64_t N;
     uint64_t seed;
     int64_t g_begin, g_end;
-    int nb;          // samples per block (128..256, multiple of 32)
-    int64_t nblk;    // sample blocks
-    int grid;        // persistent CTAs (<= SM count)
-    double *Y;       // [grid][ceil(n/64)*64][nb]
+    const int64_t *cta;  // device [grid][3]: first sample, count, first block (sov_partition)
+    int64_t nblk;        // sample blocks
+    int grid;            // persistent CTAs (<= SM count)
+    double *Y;           // [grid][ceil(n/64)*64][128]
     double *part;    // [nblk][ceil(n/64)*64][2]
     double *Mout, *Sout;
 };
 cudaError_t sov_init();
-int sov_pick_nb(int64_t nsamp, int64_t n, int nsm);
+int sov_block_samples();
+int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta);
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
 
 }  // namespace mvn
