@@ -6,6 +6,8 @@
 //   K4 k_update     : A_ij -= L_ik L_jk^T, i >= j > k (DMMA GEMM, two 64x128 CTAs per tile)
 // The paper's StarPU task DAG becomes stream order; the K4 GEMM carries
 // n^3/3 of the n^3/3 + O(n^2 nb) flops.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gemm_dmma.cuh"
 #include "mvn_internal.h"
@@ -142,17 +144,161 @@ __global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, i
     };
     gemm_mainloop<BK, STAGES, SA, SB, WM, WN>(kTile / BK, As, Bs, wm0, wn0, lane, acc, load);
 
-    // epilogue: C[row][col] -= acc, C column-major (column stride 128)
+    // epilogue: C[row][col] -= acc, C column-major (column stride 128); loads batched per row block
 #pragma unroll
     for (int a = 0; a < WM; ++a) {
         const int row = wm0 + a * 8 + (lane >> 2);
+        double cv[WN][2];
 #pragma unroll
         for (int b = 0; b < WN; ++b) {
-            const int col = wn0 + b * 8 + 2 * (lane & 3);
-            double *p0 = C + (int64_t)col * kTile + row;
-            double *p1 = p0 + kTile;
-            *p0 -= acc[a][b][0];
-            *p1 -= acc[a][b][1];
+            const double *p0 = C + (int64_t)(wn0 + b * 8 + 2 * (lane & 3)) * kTile + row;
+            cv[b][0] = p0[0];
+            cv[b][1] = p0[kTile];
+        }
+#pragma unroll
+        for (int b = 0; b < WN; ++b) {
+            double *p0 = C + (int64_t)(wn0 + b * 8 + 2 * (lane & 3)) * kTile + row;
+            p0[0] = cv[b][0] - acc[a][b][0];
+            p0[kTile] = cv[b][1] - acc[a][b][1];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------ K4
+// Persistent trailing update (the hot loop of the Cholesky): CTA c processes tiles
+// c, c + grid, ... of the trailing lower triangle (column by column, so the next panel's column
+// k+1 is finished first). Per tile C_ij -= L_ik L_jk^T (128 x 128 x 128):
+//   warp 8 (producer): per 16-column K-chunk, the 16 columns of L_ik and L_jk (cp.async, completion
+//                     tracked on the stage's mbarrier) into a 5-stage ring (full/empty mbarriers), and
+//                     a bulk L2 prefetch of the C tile;
+//   warps 0-7        : 2 (rows) x 4 (cols) warps, warp tile 64 x 32 = 8 x 4 DMMA.8x8x4 blocks
+//                      (64 fp64 accumulators / thread, 12 fragment loads per 32 DMMA), then the
+//                      read-modify-write epilogue of their fragments (C prefetched into L2).
+// The producer runs ahead across tiles, so the next tile's operands stream in during the epilogue.
+namespace upd2 {
+constexpr int BK = 16, STAGES = 5;
+constexpr int SP = kTile + 4;                       // 132 == 4 (mod 16)
+constexpr int STAGE = 2 * BK * SP;                  // A and B chunks
+constexpr int NCONS = 256, NT = NCONS + 32;
+constexpr int OFF_BAR = STAGES * STAGE;
+constexpr int SMEM = (OFF_BAR + 2 * STAGES) * 8;
+constexpr int CHUNKS = kTile / BK;
+}  // namespace upd2
+
+__device__ __forceinline__ void upd_item(int64_t item, int T, int &ii, int &jj, int64_t &base, int &col) {
+    // column-major enumeration of the T x T lower triangle: column jj holds T - jj tiles
+    while (item >= base + (T - col)) { base += T - col; ++col; }
+    jj = col;
+    ii = col + (int)(item - base);
+}
+
+__global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int nt) {
+    using namespace upd2;
+    extern __shared__ double sm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
+    uint64_t *empty = full + STAGES;
+    const int tid = threadIdx.x;
+    const int T = nt - k - 1;
+    const int64_t nitems = (int64_t)T * (T + 1) / 2;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCONS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    int64_t base = 0;
+    int col = 0;
+    uint32_t q = 0;
+    if (tid >= NCONS) {
+        // ------------------------------------------------------------ producer warp
+        const int lane = tid & 31;
+        for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+            int ii, jj;
+            upd_item(item, T, ii, jj, base, col);
+            const int ti = k + 1 + ii, tj = k + 1 + jj;
+            const double *Lik = tiles + tile_offset(ti, k);
+            const double *Ljk = tiles + tile_offset(tj, k);
+            if (lane == 0) {
+                const double *C = tiles + tile_offset(ti, tj);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) bulk_prefetch_l2(C + h * 4096, 32768);
+            }
+            for (int c = 0; c < CHUNKS; ++c, ++q) {
+                const int st = q % STAGES;
+                mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
+                double *as = sm + st * STAGE;
+                double *bs = as + BK * SP;
+                // 16 columns of L_ik and of L_jk (1 KB each) into padded rows: cp.async, 16 B per lane
+                const double *a0 = Lik + (int64_t)c * BK * kTile + lane * 2;
+                const double *b0 = Ljk + (int64_t)c * BK * kTile + lane * 2;
+#pragma unroll
+                for (int t = 0; t < BK; ++t)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {                // 1 KB column = 2 x 32 lanes x 16 B
+                        cp_async16(as + t * SP + h * 64 + lane * 2, a0 + (int64_t)t * kTile + h * 64);
+                        cp_async16(bs + t * SP + h * 64 + lane * 2, b0 + (int64_t)t * kTile + h * 64);
+                    }
+                cp_async_mbar_arrive(&full[st]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[st]);
+            }
+        }
+        return;
+    }
+    // ---------------------------------------------------------------- consumer warps
+    const int lane = tid & 31, warp = tid >> 5;
+    const int wm0 = (warp & 1) * 64, wn0 = (warp >> 1) * 32;
+    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        int ii, jj;
+        upd_item(item, T, ii, jj, base, col);
+        const int ti = k + 1 + ii, tj = k + 1 + jj;
+        double acc[8][4][2];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int c = 0; c < CHUNKS; ++c, ++q) {
+            const int st = q % STAGES;
+            mbar_wait(&full[st], (q / STAGES) & 1);
+            const double *as = sm + st * STAGE;
+            const double *bs = as + BK * SP;
+#pragma unroll
+            for (int kk = 0; kk < BK; kk += 4) {
+                double fa[8], fb[4];
+                const int kr = kk + (lane & 3);
+#pragma unroll
+                for (int a = 0; a < 8; ++a) fa[a] = as[kr * SP + wm0 + a * 8 + (lane >> 2)];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) fb[b] = bs[kr * SP + wn0 + b * 8 + (lane >> 2)];
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        // epilogue C -= acc: loads batched per 8-row block (8 independent loads in flight before
+        // the dependent stores), otherwise possible aliasing serialises every load-store pair
+        double *C = tiles + tile_offset(ti, tj);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int row = wm0 + a * 8 + (lane >> 2);
+            double cv[4][2];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double *p0 = C + (int64_t)(wn0 + b * 8 + 2 * (lane & 3)) * kTile + row;
+                cv[b][0] = p0[0];
+                cv[b][1] = p0[kTile];
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                double *p0 = C + (int64_t)(wn0 + b * 8 + 2 * (lane & 3)) * kTile + row;
+                p0[0] = cv[b][0] - acc[a][b][0];
+                p0[kTile] = cv[b][1] - acc[a][b][1];
+            }
         }
     }
 }
@@ -162,18 +308,27 @@ cudaError_t potrf_init() {
     if ((e = cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * kTile * 8))) return e;
     if ((e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * kTile * 8))) return e;
     if ((e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, upd::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, upd2::SMEM))) return e;
     return cudaSuccess;
 }
 
 cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    static const bool use_persistent = [] { const char *e = getenv("MVN_POTRF_PERSISTENT"); return !(e && e[0] == '0'); }();
     for (int k = 0; k < nt; ++k) {
         k_potrf_diag<<<1, 512, kTile * kTile * 8, st>>>(tiles, k, d_info);
         const int T = nt - k - 1;
         if (T > 0) {
             k_trsm<<<T, 128, kTile * kTile * 8, st>>>(tiles, k, nt);
             const int64_t ntile = (int64_t)T * (T + 1) / 2;
-            k_update<<<(unsigned)(2 * ntile), 128, upd::SMEM, st>>>(tiles, k, nt);
+            if (use_persistent && ntile >= 2 * nsm) {
+                k_update2<<<nsm, upd2::NT, upd2::SMEM, st>>>(tiles, k, nt);
+            } else {
+                k_update<<<(unsigned)(2 * ntile), 128, upd::SMEM, st>>>(tiles, k, nt);
+            }
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

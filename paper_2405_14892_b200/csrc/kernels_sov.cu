@@ -33,7 +33,7 @@ constexpr int M = 64;                    // SOV row block
 constexpr int NB = 128;                  // max samples per block (= chain threads)
 constexpr int BK = 16, STAGES = 4;
 constexpr int SA = M + 4;                // 68  == 4 (mod 16): conflict-free DMMA fragment loads
-constexpr int SB = NB + 4;               // 132 == 4 (mod 16)
+constexpr int SB = NB + 4;               // 132 == 4 (mod 16); also the Y-history row stride
 constexpr int SS = NB + 8;               // S tile stride (16-byte fragment stores conflict-free)
 constexpr int NGEMM = 256, NCHAIN = NB, NPROD = 32, NT = NGEMM + NCHAIN + NPROD;
 constexpr int STAGE = BK * (SA + SB);                    // doubles per pipeline stage
@@ -41,38 +41,14 @@ constexpr int OFF_S = STAGES * STAGE;                    // S[64][SS]: s, then y
 constexpr int OFF_LD = OFF_S + M * SS;                   // Ld[64 cols][64 rows] (column-major)
 constexpr int OFF_PS = OFF_LD + M * M;                   // per-row, per-chain-warp (max, sum) [64][4][2]
 constexpr int OFF_AG = OFF_PS + M * 4 * 2;               // [3][64]: a, b, G (as double bits)
-constexpr int OFF_BAR = OFF_AG + 3 * M;                  // full[STAGES], empty[STAGES] mbarriers
+constexpr int OFF_DINV = OFF_AG + 3 * M;                 // [64]: 1 / L_kk of the row block
+constexpr int OFF_ELL8 = OFF_DINV + M;                   // [8][NB]: log weights of the current 8-row sub-block
+constexpr int OFF_BAR = OFF_ELL8 + 8 * NB;               // full[STAGES], empty[STAGES] mbarriers
 constexpr int SMEM = (OFF_BAR + 2 * STAGES) * 8;
 constexpr int CPB = M / BK;                              // K-chunks per row block
 enum : int { BAR_SFULL = 1, BAR_YREADY = 2, BAR_CHAIN = 3 };
 constexpr int N_SFULL = NGEMM + NCHAIN, N_YREADY = NCHAIN + NPROD;
 }  // namespace sovk
-
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-// TMA-engine bulk copy global -> shared, completion counted on an mbarrier (SASS UBLKCP).
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
 
 __device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, int src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes));
@@ -101,7 +77,7 @@ struct SovArgs {
     uint64_t seed;
     const int64_t *cta;       // [grid][3]: first global sample, sample count, first block index
     int64_t n_pad;            // Y-history rows per slot (nrb*64)
-    double *Y;                // [grid][n_pad][NB]
+    double *Y;                // [grid][n_pad][SB] (row stride SB: padded for conflict-free DMMA loads)
     double *part;             // [nblk][n_pad][2]
 };
 
@@ -134,14 +110,17 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
                 const int64_t kc = (int64_t)c * BK;
                 double *as = sm + st * STAGE;
                 double *bs = as + BK * SA;
-                if (lane == 0) mbar_arrive_expect_tx(&full[st], (unsigned)(BK * M * 8 + BK * w * 8));
+                // A: 16 L columns x 64 rows (512 B each, 1 KB apart) by cp.async, one 16 B piece per lane
+                const int T = (int)(kc / kTile), cc = (int)(kc % kTile);
+                const double *Lsrc = p.L + tile_offset(R, T) + (int64_t)cc * kTile + hh + lane * 2;
+#pragma unroll
+                for (int t = 0; t < BK; ++t) cp_async16(as + t * SA + lane * 2, Lsrc + (int64_t)t * kTile);
+                cp_async_mbar_arrive(&full[st]);
                 __syncwarp();
-                if (lane < 16) {
-                    const int T = (int)(kc / kTile), cc = (int)(kc % kTile) + lane;
-                    bulk_g2s(as + lane * SA, p.L + tile_offset(R, T) + (int64_t)cc * kTile + hh, M * 8, &full[st]);
-                } else {
-                    const int row = lane - 16;
-                    bulk_g2s(bs + row * SB, Yslot + (kc + row) * NB, (unsigned)(w * 8), &full[st]);
+                // B: 16 Y-history rows, contiguous thanks to the padded row stride SB: one TMA bulk copy
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[st], BK * SB * 8);
+                    bulk_g2s(bs, Yslot + kc * SB, BK * SB * 8, &full[st]);
                 }
             }
         }
@@ -227,9 +206,10 @@ __device__ __forceinline__ void chain_load(const SovArgs &p, double *sm, int rb,
 
 // Alg. 3 on one row block for sample j (thread j of the chain group). s for row li arrives in
 // S[li][j] (GEMM part + in-block contributions so far) and y_li overwrites it. Sub-blocks of 8
-// rows: rows inside a sub-block update each other directly, the remaining rows of the block get
-// the sub-block's 8 y values in one pass (8 FMAs per shared-memory read/write). After each row the
-// warp reduces (max, sum exp) of its 32 samples' log weights into ps[row][warp].
+// rows: rows inside a sub-block update each other directly (7 predicated, independent FMAs), the
+// remaining rows of the block get the sub-block's 8 y values in one pass (8 FMAs per shared-memory
+// read/write). After each sub-block every warp reduces (max, sum exp) of its 32 samples' log
+// weights for the 8 rows at once (8 independent shuffle trees) into ps[row][warp].
 template <bool HAS_B>
 __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, double *Yslot, int rb, int j, int cnt,
                                                uint64_t r, uint64_t jl, double &ell) {
@@ -241,6 +221,8 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
     const double *a_s = sm + OFF_AG;
     const double *b_s = a_s + M;
     const uint64_t *G_s = reinterpret_cast<const uint64_t *>(a_s + 2 * M);
+    const double *dinv = sm + OFF_DINV;
+    double *ELL8 = sm + OFF_ELL8;
     const int lane = j & 31, cw = j >> 5;
     const bool valid = j < cnt;
     if (rb == 0)                                          // S_0 = 0: no GEMM for the first row block
@@ -248,31 +230,47 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
 #pragma unroll 1
     for (int sb = 0; sb < M / 8; ++sb) {
         const int rb0 = sb * 8;
+        const int64_t left = p.n - (row0 + rb0);
+        if (left <= 0) break;                             // uniform: padded rows need no y
+        const int nrows = left < 8 ? (int)left : 8;
 #pragma unroll 1
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < nrows; ++i) {
             const int li = rb0 + i;
             const int64_t k = row0 + li;
-            if (k >= p.n) break;                          // uniform: padded rows need no y
             const double s = S[li * SS + j];
-            const double lkk = Ld[li * M + li];
-            const double ap = (a_s[li] - s) / lkk;
+            const double ap = (a_s[li] - s) * dinv[li];
             const double wq = lattice_w(jl, G_s[li], lattice_shift(p.seed, r, (uint64_t)k));
             double lq, y;
-            if (HAS_B) sov_step(ap, (b_s[li] - s) / lkk, wq, lq, y);
+            if (HAS_B) sov_step(ap, (b_s[li] - s) * dinv[li], wq, lq, y);
             else sov_step_upper(ap, wq, lq, y);
             ell += lq;
             S[li * SS + j] = y;
-            Yslot[k * NB + j] = y;
-#pragma unroll 1
-            for (int i2 = li + 1; i2 < rb0 + 8; ++i2) S[i2 * SS + j] += Ld[li * M + i2] * y;
-            // per-row log-sum-exp over this warp's samples
-            double m = valid ? ell : -CUDART_INF;
+            ELL8[i * NB + j] = ell;
+            Yslot[k * SB + j] = y;
 #pragma unroll
-            for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-            double e = (valid && m != -CUDART_INF) ? exp(ell - m) : 0.0;
+            for (int d = 1; d < 8; ++d)
+                if (i + d < 8) S[(li + d) * SS + j] += Ld[li * M + li + d] * y;
+        }
+        // per-row log-sum-exp over this warp's samples, 8 rows at once
+        double m[8], e[8];
 #pragma unroll
-            for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-            if (lane == 0) *reinterpret_cast<double2 *>(ps + (li * 4 + cw) * 2) = make_double2(m, e);
+        for (int i = 0; i < 8; ++i) m[i] = (valid && i < nrows) ? ELL8[i * NB + j] : -CUDART_INF;
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m[i] = fmax(m[i], __shfl_xor_sync(0xffffffffu, m[i], o));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) e[i] = (valid && i < nrows && m[i] != -CUDART_INF) ? exp(ELL8[i * NB + j] - m[i]) : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) e[i] += __shfl_xor_sync(0xffffffffu, e[i], o);
+        if (lane < nrows) {
+            double mi = m[0], ei = e[0];
+#pragma unroll
+            for (int i = 1; i < 8; ++i)
+                if (lane == i) { mi = m[i]; ei = e[i]; }
+            *reinterpret_cast<double2 *>(ps + ((rb0 + lane) * 4 + cw) * 2) = make_double2(mi, ei);
         }
         double yv[8];
 #pragma unroll
@@ -294,11 +292,11 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
     const int tid = threadIdx.x;
     const int64_t g_first = p.cta[blockIdx.x * 3], count = p.cta[blockIdx.x * 3 + 1], blk_first = p.cta[blockIdx.x * 3 + 2];
     const int nblk = (int)((count + NB - 1) / NB);
-    double *Yslot = p.Y + (int64_t)blockIdx.x * p.n_pad * NB;
+    double *Yslot = p.Y + (int64_t)blockIdx.x * p.n_pad * SB;
     if (tid == 0) {
         uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1);                      // + 32 cp.async arrivals + bulk tx bytes
             mbar_init(&full[STAGES + s], NGEMM / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -337,6 +335,8 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
                 cp_async_commit();
                 if (rb > 0) named_sync(BAR_SFULL, N_SFULL);       // S_rb written by the GEMM warps
                 cp_async_wait<0>();
+                named_sync(BAR_CHAIN, NCHAIN);
+                if (j < M) sm[OFF_DINV + j] = 1.0 / sm[OFF_LD + j * M + j];
                 named_sync(BAR_CHAIN, NCHAIN);
                 if (j < w) chain_rowblock<HAS_B>(p, sm, Yslot, rb, j, cnt, r, jl, ell);
                 __threadfence();                                  // Y_rb: generic-proxy writes ...
@@ -390,6 +390,7 @@ cudaError_t sov_init() {
 }
 
 int sov_block_samples() { return sovk::NB; }
+int sov_y_stride() { return sovk::SB; }
 
 // Balanced partition of [g_begin, g_end) over `grid` CTAs: CTA c gets a contiguous share of
 // floor/ceil(nsamp/grid) samples, processed as blocks of 128 (last one narrowed to 32k).

@@ -272,8 +272,8 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
     std::vector<int64_t> cta((size_t)L.grid * 3);
     L.nblk = mvn::sov_partition(q->sample_begin, q->sample_end, L.grid, cta.data());
     const int64_t n_pad = (t.n + 63) / 64 * 64;
-    const int nb = mvn::sov_block_samples();
-    if ((s = ensure(c, &c->Y, &c->Y_cap, (size_t)L.grid * n_pad * nb * sizeof(double))) != MVN_OK) return s;
+    const int ys = mvn::sov_y_stride();
+    if ((s = ensure(c, &c->Y, &c->Y_cap, (size_t)L.grid * n_pad * ys * sizeof(double))) != MVN_OK) return s;
     if ((s = ensure(c, &c->part, &c->part_cap, (size_t)L.nblk * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
     if ((s = ensure(c, &c->cta, &c->cta_cap, cta.size() * sizeof(int64_t))) != MVN_OK) return s;
     MVN_CUDA(c, cudaMemcpyAsync(c->cta, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));

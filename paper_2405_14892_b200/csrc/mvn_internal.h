@@ -27,12 +27,13 @@ struct SovLaunch {
     const int64_t *cta;  // device [grid][3]: first sample, count, first block (sov_partition)
     int64_t nblk;        // sample blocks
     int grid;            // persistent CTAs (<= SM count)
-    double *Y;           // [grid][ceil(n/64)*64][128]
+    double *Y;           // [grid][ceil(n/64)*64][sov_y_stride()]
     double *part;    // [nblk][ceil(n/64)*64][2]
     double *Mout, *Sout;
 };
 cudaError_t sov_init();
 int sov_block_samples();
+int sov_y_stride();
 int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta);
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
 
