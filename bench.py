@@ -130,7 +130,7 @@ def cpu_threads() -> int:
 
 def oracle_plan(cfg):
     """(n_sub, J) so that one oracle sample is ~10-20 s on ~16 cores."""
-    n_sub = min(cfg.n, 2048)
+    n_sub = min(cfg.n, 8192)
     J = min(cfg.NR, 4096)
     return n_sub, J
 

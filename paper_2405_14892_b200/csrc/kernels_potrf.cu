@@ -6,6 +6,7 @@
 //   K4 k_update     : A_ij -= L_ik L_jk^T, i >= j > k (DMMA GEMM, two 64x128 CTAs per tile)
 // The paper's StarPU task DAG becomes stream order; the K4 GEMM carries
 // n^3/3 of the n^3/3 + O(n^2 nb) flops.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -88,6 +89,156 @@ __global__ void __launch_bounds__(128) k_trsm(double *__restrict__ tiles, int k,
         reinterpret_cast<double2 *>(T)[e] = reinterpret_cast<const double2 *>(X)[e];
 }
 
+// ------------------------------------------------------------------------------------------ K2/K3
+// Blocked versions (32-column blocks) of the diagonal POTRF and the panel TRSM. Shared-memory
+// matrices are column-major with a padded column stride (== 4 mod 16 doubles) so that the DMMA
+// fragment loads are conflict-free. Per 32-column block: a DMMA GEMM applies the already
+// finished columns (K = 32 cb), then a short 32-column substitution finishes the block.
+namespace blk {
+constexpr int SP = kTile + 4;    // 132: diagonal tile / L_kk in smem
+constexpr int SPX = 64 + 4;      // 68: a 64-row half of a panel tile
+}
+
+// X[m0.., c0..c0+32) -= X[m0.., 0..K) * B(K x 32), B(k, n) = Bm[k * ldb + b0 + n]; rows [r0, r1)
+// of the output in 16-row x 16-column warp tiles (DMMA.8x8x4, 2 x 2 blocks per warp).
+__device__ __forceinline__ void blk_gemm_sub(double *X, int ldx, int r0, int r1, int c0, int K, const double *Bm, int ldb,
+                                             int b0, int warp, int nwarp, int lane) {
+    const int mt = (r1 - r0) / 16;
+    for (int t = warp; t < mt * 2; t += nwarp) {
+        const int m0 = r0 + (t >> 1) * 16, n0 = (t & 1) * 16;
+        double acc[2][2][2] = {};
+        for (int k = 0; k < K; k += 4) {
+            const int kr = k + (lane & 3);
+            double fa[2], fb[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) fa[i] = X[kr * ldx + m0 + i * 8 + (lane >> 2)];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) fb[j] = Bm[kr * ldb + b0 + n0 + j * 8 + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int m = m0 + i * 8 + (lane >> 2), n = c0 + n0 + j * 8 + 2 * (lane & 3);
+                X[n * ldx + m] -= acc[i][j][0];
+                X[(n + 1) * ldx + m] -= acc[i][j][1];
+            }
+    }
+}
+
+// Rows r of X (columns c0..c0+32) solve x L_cc^T = x: x_j = (x_j - sum_{t<j} x_t L(j,t)) / L(j,j),
+// L(j,t) = Lm[(lc + t) * ldl + lc + j] (warp-uniform broadcast). One thread per row.
+__device__ __forceinline__ void blk_solve32(double *X, int ldx, int c0, int r, const double *Lm, int ldl, int lc) {
+    for (int j = 0; j < 32; ++j) {
+        double s0 = X[(c0 + j) * ldx + r], s1 = 0.0;
+        int t = 0;
+        for (; t + 2 <= j; t += 2) {
+            s0 -= X[(c0 + t) * ldx + r] * Lm[(lc + t) * ldl + lc + j];
+            s1 -= X[(c0 + t + 1) * ldx + r] * Lm[(lc + t + 1) * ldl + lc + j];
+        }
+        if (t < j) s0 -= X[(c0 + t) * ldx + r] * Lm[(lc + t) * ldl + lc + j];
+        X[(c0 + j) * ldx + r] = (s0 + s1) / Lm[(lc + j) * ldl + lc + j];
+    }
+}
+
+// K2 (blocked): POTRF of the 128 x 128 diagonal tile k in shared memory. Per 32-column block cb:
+// DMMA update of rows >= 32cb by the finished columns, one-warp factorisation of the 32 x 32
+// diagonal block (first non-positive pivot -> *info, global row), substitution of the rows below.
+__global__ void __launch_bounds__(256) k_potrf_diag2(double *__restrict__ tiles, int k, int64_t *__restrict__ info) {
+    using namespace blk;
+    extern __shared__ double A[];          // [128 cols][SP]
+    __shared__ int failed;
+    double *T = tiles + tile_offset(k, k);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < kTile * kTile / 2; e += 256) {
+        const int col = e >> 6, seg = e & 63;
+        cp_async16(A + col * SP + seg * 2, T + col * kTile + seg * 2);
+    }
+    cp_async_commit();
+    if (tid == 0) failed = (*info >= 0);
+    cp_async_wait<0>();
+    __syncthreads();
+    if (failed) return;
+    for (int cb = 0; cb < 4; ++cb) {
+        const int c0 = cb * 32;
+        if (cb > 0) {
+            blk_gemm_sub(A, SP, c0, kTile, c0, c0, A, SP, c0, warp, 8, lane);
+            __syncthreads();
+        }
+        if (warp == 0) {                   // 32 x 32 diagonal block, lane = row
+            for (int j = 0; j < 32; ++j) {
+                const double d = A[(c0 + j) * SP + c0 + j];
+                const bool bad = !(d > 0.0);
+                if (bad) {
+                    if (lane == 0) { failed = 1; *info = (int64_t)k * kTile + c0 + j; }
+                    break;
+                }
+                const double ljj = sqrt(d);
+                __syncwarp();
+                if (lane == j) A[(c0 + j) * SP + c0 + j] = ljj;
+                double lij = 0.0;
+                if (lane > j) {
+                    lij = A[(c0 + j) * SP + c0 + lane] / ljj;
+                    A[(c0 + j) * SP + c0 + lane] = lij;
+                }
+                __syncwarp();
+                if (lane > j)
+                    for (int q = j + 1; q <= lane; ++q) A[(c0 + q) * SP + c0 + lane] -= lij * A[(c0 + j) * SP + c0 + q];
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        if (failed) return;
+        const int r = c0 + 32 + tid;
+        if (r < kTile) blk_solve32(A, SP, c0, r, A, SP, c0);
+        __syncthreads();
+    }
+    for (int e = tid; e < kTile * kTile; e += 256) {
+        const int col = e >> 7, row = e & 127;
+        T[e] = (row >= col) ? A[col * SP + row] : 0.0;
+    }
+}
+
+// K3 (blocked): L_ik = A_ik L_kk^{-T} for one 64-row half of panel tile i (grid: 2 CTAs per tile).
+__global__ void __launch_bounds__(256) k_trsm2(double *__restrict__ tiles, int k) {
+    using namespace blk;
+    extern __shared__ double sh[];
+    double *X = sh;                        // [128 cols][SPX]: rows h*64 .. h*64+63 of A_ik
+    double *Lk = sh + kTile * SPX;         // [128 cols][SP]
+    const int i = k + 1 + (blockIdx.x >> 1), h = blockIdx.x & 1;
+    double *Ti = tiles + tile_offset(i, k) + h * 64;
+    const double *Lkk = tiles + tile_offset(k, k);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < kTile * 32; e += 256) {           // 128 cols x 32 pieces
+        const int col = e >> 5, seg = e & 31;
+        cp_async16(X + col * SPX + seg * 2, Ti + col * kTile + seg * 2);
+    }
+    for (int e = tid; e < kTile * 64; e += 256) {           // 128 cols x 64 pieces
+        const int col = e >> 6, seg = e & 63;
+        cp_async16(Lk + col * SP + seg * 2, Lkk + col * kTile + seg * 2);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int cb = 0; cb < 4; ++cb) {
+        const int c0 = cb * 32;
+        if (cb > 0) {
+            blk_gemm_sub(X, SPX, 0, 64, c0, c0, Lk, SP, c0, warp, 8, lane);
+            __syncthreads();
+        }
+        if (tid < 64) blk_solve32(X, SPX, c0, tid, Lk, SP, c0);
+        __syncthreads();
+    }
+    for (int e = tid; e < kTile * 32; e += 256) {
+        const int col = e >> 5, seg = e & 31;
+        *reinterpret_cast<double2 *>(Ti + col * kTile + seg * 2) = *reinterpret_cast<const double2 *>(X + col * SPX + seg * 2);
+    }
+}
+
 // ------------------------------------------------------------------------------------------ K4
 // Trailing update, one CTA per (tile (i,j), row half h): C(64x128) -= L_ik[h-half] * L_jk^T.
 // 4 warps as 2 (M) x 2 (N), warp tile 32x64 = 4x8 DMMA blocks (64 fp64 accumulators / thread).
@@ -98,18 +249,27 @@ constexpr int WM = 4, WN = 8;
 constexpr int SMEM = STAGES * BK * (SA + SB) * 8;
 }  // namespace upd
 
-__global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, int k, int nt) {
+__global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, int k, int nt, int mode) {
     using namespace upd;
     extern __shared__ double sm[];
     double *As = sm;
     double *Bs = sm + STAGES * BK * SA;
     const int64_t id = blockIdx.x >> 1;
     const int h = blockIdx.x & 1;
-    // id -> (ii, jj), 0 <= jj <= ii < T, row-major lower enumeration; tile (k+1+ii, k+1+jj)
-    int ii = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
-    while ((int64_t)ii * (ii + 1) / 2 > id) --ii;
-    while ((int64_t)(ii + 1) * (ii + 2) / 2 <= id) ++ii;
-    const int jj = (int)(id - (int64_t)ii * (ii + 1) / 2);
+    // id -> (ii, jj), 0 <= jj <= ii < T, row-major lower enumeration; tile (k+1+ii, k+1+jj).
+    // mode 1: only column k+1 (the next panel), ii = id, jj = 0.
+    // mode 2: the rest (columns >= k+2): the same enumeration shifted by one tile.
+    int ii, jj;
+    if (mode == 1) {
+        ii = (int)id;
+        jj = 0;
+    } else {
+        ii = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
+        while ((int64_t)ii * (ii + 1) / 2 > id) --ii;
+        while ((int64_t)(ii + 1) * (ii + 2) / 2 <= id) ++ii;
+        jj = (int)(id - (int64_t)ii * (ii + 1) / 2);
+        if (mode == 2) { ++ii; ++jj; }
+    }
     const int ti = k + 1 + ii, tj = k + 1 + jj;
     const double *__restrict__ Lik = tiles + tile_offset(ti, k) + h * BM;   // column stride 128
     const double *__restrict__ Ljk = tiles + tile_offset(tj, k);
@@ -192,13 +352,13 @@ __device__ __forceinline__ void upd_item(int64_t item, int T, int &ii, int &jj, 
     ii = col + (int)(item - base);
 }
 
-__global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int nt) {
+__global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int nt, int off) {
     using namespace upd2;
     extern __shared__ double sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
     uint64_t *empty = full + STAGES;
     const int tid = threadIdx.x;
-    const int T = nt - k - 1;
+    const int T = nt - k - 1 - off;          // off = 1: skip column k+1 (done by the lookahead stream)
     const int64_t nitems = (int64_t)T * (T + 1) / 2;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -217,7 +377,7 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
             int ii, jj;
             upd_item(item, T, ii, jj, base, col);
-            const int ti = k + 1 + ii, tj = k + 1 + jj;
+            const int ti = k + 1 + off + ii, tj = k + 1 + off + jj;
             const double *Lik = tiles + tile_offset(ti, k);
             const double *Ljk = tiles + tile_offset(tj, k);
             if (lane == 0) {
@@ -253,7 +413,7 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         int ii, jj;
         upd_item(item, T, ii, jj, base, col);
-        const int ti = k + 1 + ii, tj = k + 1 + jj;
+        const int ti = k + 1 + off + ii, tj = k + 1 + off + jj;
         double acc[8][4][2];
 #pragma unroll
         for (int a = 0; a < 8; ++a)
@@ -309,8 +469,39 @@ cudaError_t potrf_init() {
     if ((e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * kTile * 8))) return e;
     if ((e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, upd::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, upd2::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_potrf_diag2, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * blk::SP * 8))) return e;
+    if ((e = cudaFuncSetAttribute(k_trsm2, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * (blk::SP + blk::SPX) * 8))) return e;
     return cudaSuccess;
 }
+
+// Right-looking factorisation with one step of lookahead on two streams:
+//   panel stream (high priority): column update of tile column k+1 -> POTRF(k+1) -> TRSM(k+1)
+//   main stream                 : persistent update of the rest of the trailing matrix (columns >= k+2),
+//                                 on all but kPanelSMs SMs, so the panel work of step k+1 runs beside it.
+// Events order the two (panel k before update k; update k-1 before the column update of step k).
+namespace {
+constexpr int kPanelSMs = 8;
+struct PotrfStreams {
+    int dev = -1;
+    cudaStream_t sp = nullptr;
+    cudaEvent_t ev_panel[2] = {}, ev_rest[2] = {}, ev_start = nullptr;
+};
+PotrfStreams g_ps;
+cudaError_t potrf_streams(int dev) {
+    if (g_ps.dev == dev) return cudaSuccess;
+    int lo = 0, hi = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithPriority(&g_ps.sp, cudaStreamNonBlocking, hi))) return e;
+    for (int i = 0; i < 2; ++i) {
+        if ((e = cudaEventCreateWithFlags(&g_ps.ev_panel[i], cudaEventDisableTiming))) return e;
+        if ((e = cudaEventCreateWithFlags(&g_ps.ev_rest[i], cudaEventDisableTiming))) return e;
+    }
+    if ((e = cudaEventCreateWithFlags(&g_ps.ev_start, cudaEventDisableTiming))) return e;
+    g_ps.dev = dev;
+    return cudaSuccess;
+}
+}  // namespace
 
 cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
@@ -318,22 +509,42 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     static const bool use_persistent = [] { const char *e = getenv("MVN_POTRF_PERSISTENT"); return !(e && e[0] == '0'); }();
-    for (int k = 0; k < nt; ++k) {
-        k_potrf_diag<<<1, 512, kTile * kTile * 8, st>>>(tiles, k, d_info);
-        const int T = nt - k - 1;
-        if (T > 0) {
-            k_trsm<<<T, 128, kTile * kTile * 8, st>>>(tiles, k, nt);
-            const int64_t ntile = (int64_t)T * (T + 1) / 2;
-            if (use_persistent && ntile >= 2 * nsm) {
-                k_update2<<<nsm, upd2::NT, upd2::SMEM, st>>>(tiles, k, nt);
+    cudaError_t e = potrf_streams(dev);
+    if (e != cudaSuccess) return e;
+    cudaStream_t sp = g_ps.sp;
+    const size_t sm_diag = kTile * blk::SP * 8, sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
+    // the panel stream starts after everything already queued on the main stream (Sigma)
+    if ((e = cudaEventRecord(g_ps.ev_start, st))) return e;
+    if ((e = cudaStreamWaitEvent(sp, g_ps.ev_start, 0))) return e;
+    k_potrf_diag2<<<1, 256, sm_diag, sp>>>(tiles, 0, d_info);
+    if (nt > 1) k_trsm2<<<2 * (nt - 1), 256, sm_trsm, sp>>>(tiles, 0);
+    if ((e = cudaEventRecord(g_ps.ev_panel[0], sp))) return e;
+    for (int k = 0; k + 1 < nt; ++k) {
+        const int T = nt - k - 1;                       // trailing tile rows/cols after step k
+        // main stream: update columns >= k+2 with panel k
+        if ((e = cudaStreamWaitEvent(st, g_ps.ev_panel[k & 1], 0))) return e;
+        if (T > 1) {
+            const int Tr = T - 1;
+            const int64_t items = (int64_t)Tr * (Tr + 1) / 2;
+            if (use_persistent && items >= 2 * nsm) {
+                const int grid = (int)std::min<int64_t>(items, nsm - kPanelSMs);
+                k_update2<<<grid, upd2::NT, upd2::SMEM, st>>>(tiles, k, nt, 1);
             } else {
-                k_update<<<(unsigned)(2 * ntile), 128, upd::SMEM, st>>>(tiles, k, nt);
+                k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(tiles, k, nt, 2);
             }
         }
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
+        if ((e = cudaEventRecord(g_ps.ev_rest[k & 1], st))) return e;
+        // panel stream: column k+1, then POTRF / TRSM of panel k+1
+        if (k >= 1 && (e = cudaStreamWaitEvent(sp, g_ps.ev_rest[(k - 1) & 1], 0))) return e;
+        k_update<<<(unsigned)(2 * T), 128, upd::SMEM, sp>>>(tiles, k, nt, 1);
+        k_potrf_diag2<<<1, 256, sm_diag, sp>>>(tiles, k + 1, d_info);
+        if (T > 1) k_trsm2<<<2 * (T - 1), 256, sm_trsm, sp>>>(tiles, k + 1);
+        if ((e = cudaEventRecord(g_ps.ev_panel[(k + 1) & 1], sp))) return e;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    return cudaSuccess;
+    // join: the main stream waits for the last panel
+    if ((e = cudaStreamWaitEvent(st, g_ps.ev_panel[(nt - 1) & 1], 0))) return e;
+    return cudaGetLastError();
 }
 
 }  // namespace mvn
