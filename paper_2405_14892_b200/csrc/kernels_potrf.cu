@@ -326,21 +326,23 @@ __global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, i
 
 // ------------------------------------------------------------------------------------------ K4
 // Persistent trailing update (the hot loop of the Cholesky): CTA c processes tiles
-// c, c + grid, ... of the trailing lower triangle (column by column, so the next panel's column
-// k+1 is finished first). Per tile C_ij -= L_ik L_jk^T (128 x 128 x 128):
-//   warp 8 (producer): per 16-column K-chunk, the 16 columns of L_ik and L_jk (cp.async, completion
-//                     tracked on the stage's mbarrier) into a 5-stage ring (full/empty mbarriers), and
-//                     a bulk L2 prefetch of the C tile;
-//   warps 0-7        : 2 (rows) x 4 (cols) warps, warp tile 64 x 32 = 8 x 4 DMMA.8x8x4 blocks
-//                      (64 fp64 accumulators / thread, 12 fragment loads per 32 DMMA), then the
-//                      read-modify-write epilogue of their fragments (C prefetched into L2).
+// c, c + grid, ... of the trailing lower triangle (column by column). Per tile C_ij -= L_ik L_jk^T
+// (128 x 128 x 128):
+//   warp 8 (producer): per 8-column K-chunk, the 8 columns of L_ik and L_jk (cp.async, completion
+//                     tracked on the stage's mbarrier) into a 4-stage ring (full/empty mbarriers);
+//   warps 0-7        : warp w owns 16 full columns of the tile (warp tile 128 x 16 = 16 x 2
+//                      DMMA.8x8x4 blocks, 64 fp64 accumulators / thread). Epilogue: -acc is
+//                      written to the warp's 16 KB staging buffer in the tile's column-major
+//                      layout and ONE TMA bulk reduction (cp.reduce.async.bulk .add.f64) adds it
+//                      to C in L2 — no global loads, nothing to wait for before the next tile.
 // The producer runs ahead across tiles, so the next tile's operands stream in during the epilogue.
 namespace upd2 {
-constexpr int BK = 16, STAGES = 5;
+constexpr int BK = 8, STAGES = 4;
 constexpr int SP = kTile + 4;                       // 132 == 4 (mod 16)
 constexpr int STAGE = 2 * BK * SP;                  // A and B chunks
 constexpr int NCONS = 256, NT = NCONS + 32;
-constexpr int OFF_BAR = STAGES * STAGE;
+constexpr int OFF_STG = STAGES * STAGE;             // [8 warps][16 cols][128 rows]
+constexpr int OFF_BAR = OFF_STG + 8 * 16 * kTile;
 constexpr int SMEM = (OFF_BAR + 2 * STAGES) * 8;
 constexpr int CHUNKS = kTile / BK;
 }  // namespace upd2
@@ -351,6 +353,14 @@ __device__ __forceinline__ void upd_item(int64_t item, int T, int &ii, int &jj, 
     jj = col;
     ii = col + (int)(item - base);
 }
+
+__device__ __forceinline__ void bulk_reduce_add_f64(double *gdst, const double *ssrc, unsigned bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n"
+                 ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int nt, int off) {
     using namespace upd2;
@@ -380,17 +390,12 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
             const int ti = k + 1 + off + ii, tj = k + 1 + off + jj;
             const double *Lik = tiles + tile_offset(ti, k);
             const double *Ljk = tiles + tile_offset(tj, k);
-            if (lane == 0) {
-                const double *C = tiles + tile_offset(ti, tj);
-#pragma unroll
-                for (int h = 0; h < 4; ++h) bulk_prefetch_l2(C + h * 4096, 32768);
-            }
             for (int c = 0; c < CHUNKS; ++c, ++q) {
                 const int st = q % STAGES;
                 mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
                 double *as = sm + st * STAGE;
                 double *bs = as + BK * SP;
-                // 16 columns of L_ik and of L_jk (1 KB each) into padded rows: cp.async, 16 B per lane
+                // 8 columns of L_ik and of L_jk (1 KB each) into padded rows: cp.async, 16 B per lane
                 const double *a0 = Lik + (int64_t)c * BK * kTile + lane * 2;
                 const double *b0 = Ljk + (int64_t)c * BK * kTile + lane * 2;
 #pragma unroll
@@ -409,16 +414,17 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
     }
     // ---------------------------------------------------------------- consumer warps
     const int lane = tid & 31, warp = tid >> 5;
-    const int wm0 = (warp & 1) * 64, wn0 = (warp >> 1) * 32;
+    const int wn0 = warp * 16;                       // 16 full columns per warp
+    double *stg = sm + OFF_STG + warp * 16 * kTile;   // column-major [16][128]
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         int ii, jj;
         upd_item(item, T, ii, jj, base, col);
         const int ti = k + 1 + off + ii, tj = k + 1 + off + jj;
-        double acc[8][4][2];
+        double acc[16][2][2];
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
+        for (int a = 0; a < 16; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+            for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
         for (int c = 0; c < CHUNKS; ++c, ++q) {
             const int st = q % STAGES;
             mbar_wait(&full[st], (q / STAGES) & 1);
@@ -426,41 +432,38 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
             const double *bs = as + BK * SP;
 #pragma unroll
             for (int kk = 0; kk < BK; kk += 4) {
-                double fa[8], fb[4];
+                double fa[16], fb[2];
                 const int kr = kk + (lane & 3);
 #pragma unroll
-                for (int a = 0; a < 8; ++a) fa[a] = as[kr * SP + wm0 + a * 8 + (lane >> 2)];
+                for (int b = 0; b < 2; ++b) fb[b] = bs[kr * SP + wn0 + b * 8 + (lane >> 2)];
 #pragma unroll
-                for (int b = 0; b < 4; ++b) fb[b] = bs[kr * SP + wn0 + b * 8 + (lane >> 2)];
+                for (int a = 0; a < 16; ++a) fa[a] = as[kr * SP + a * 8 + (lane >> 2)];
 #pragma unroll
-                for (int a = 0; a < 8; ++a)
+                for (int a = 0; a < 16; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+                    for (int b = 0; b < 2; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
         }
-        // epilogue C -= acc: loads batched per 8-row block (8 independent loads in flight before
-        // the dependent stores), otherwise possible aliasing serialises every load-store pair
-        double *C = tiles + tile_offset(ti, tj);
+        // epilogue: the previous tile's reduction must have finished reading the staging buffer
+        if (lane == 0) bulk_wait_read_all();
+        __syncwarp();
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int row = wm0 + a * 8 + (lane >> 2);
-            double cv[4][2];
+        for (int a = 0; a < 16; ++a) {
+            const int row = a * 8 + (lane >> 2);
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const double *p0 = C + (int64_t)(wn0 + b * 8 + 2 * (lane & 3)) * kTile + row;
-                cv[b][0] = p0[0];
-                cv[b][1] = p0[kTile];
-            }
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                double *p0 = C + (int64_t)(wn0 + b * 8 + 2 * (lane & 3)) * kTile + row;
-                p0[0] = cv[b][0] - acc[a][b][0];
-                p0[kTile] = cv[b][1] - acc[a][b][1];
+            for (int b = 0; b < 2; ++b) {
+                const int cl = b * 8 + 2 * (lane & 3);
+                stg[cl * kTile + row] = -acc[a][b][0];
+                stg[(cl + 1) * kTile + row] = -acc[a][b][1];
             }
         }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> async proxy
+        __syncwarp();
+        if (lane == 0) bulk_reduce_add_f64(tiles + tile_offset(ti, tj) + (int64_t)wn0 * kTile, stg, 16 * kTile * 8);
     }
+    if (lane == 0) bulk_wait_all();
 }
 
 cudaError_t potrf_init() {

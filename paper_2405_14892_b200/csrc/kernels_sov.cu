@@ -233,11 +233,13 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
         const int64_t left = p.n - (row0 + rb0);
         if (left <= 0) break;                             // uniform: padded rows need no y
         const int nrows = left < 8 ? (int)left : 8;
+        double s = S[rb0 * SS + j];                       // row rb0: GEMM part + earlier sub-blocks
 #pragma unroll 1
         for (int i = 0; i < nrows; ++i) {
             const int li = rb0 + i;
             const int64_t k = row0 + li;
-            const double s = S[li * SS + j];
+            // next row's s without the current row's term, read before y exists (off the critical path)
+            const double s_next = (i + 1 < 8) ? S[(li + 1) * SS + j] : 0.0;
             const double ap = (a_s[li] - s) * dinv[li];
             const double wq = lattice_w(jl, G_s[li], lattice_shift(p.seed, r, (uint64_t)k));
             double lq, y;
@@ -247,8 +249,9 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
             S[li * SS + j] = y;
             ELL8[i * NB + j] = ell;
             Yslot[k * SB + j] = y;
+            if (i + 1 < 8) s = s_next + Ld[li * M + li + 1] * y;   // row li+1 carried in a register
 #pragma unroll
-            for (int d = 1; d < 8; ++d)
+            for (int d = 2; d < 8; ++d)
                 if (i + d < 8) S[(li + d) * SS + j] += Ld[li * M + li + d] * y;
         }
         // per-row log-sum-exp over this warp's samples, 8 rows at once

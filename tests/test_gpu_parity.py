@@ -260,3 +260,72 @@ def test_crd_config_B_independent_vs_oracle(torch_cuda):
     assert np.array_equal(out.order, ref.order)
     assert np.max(np.abs(out.logP - ref.logp)) <= LOGP_TOL
     assert np.array_equal(out.k_star, ref.k_star)
+
+
+# ------------------------------------------------------------------------------------ full-size configs
+def tile_rows(T, n, rows, ncols):
+    """Rows `rows` of the tile-packed lower L (first ncols columns) as a dense host array."""
+    import torch
+    nt = -(-n // 128)
+    V = T.view(-1, 128, 128)                               # [tile][col][row]
+    out = np.zeros((len(rows), ncols))
+    for q, i in enumerate(rows):
+        I, r = divmod(int(i), 128)
+        J = min(I, (ncols - 1) // 128)
+        idx = torch.arange(I * (I + 1) // 2, I * (I + 1) // 2 + J + 1, device=T.device)
+        v = V[idx, :, r].reshape(-1).cpu().numpy()
+        m = min(ncols, v.shape[0], i + 1)
+        out[q, :m] = v[:m]
+    return out
+
+
+def leading_block(T, n, m):
+    """Dense L[0:m, 0:m] (host) from the tile-packed factor."""
+    import torch
+    nb = -(-m // 128)
+    V = T.view(-1, 128, 128)
+    D = torch.zeros((nb * 128, nb * 128), dtype=torch.float64, device=T.device)
+    for I in range(nb):
+        for J in range(I + 1):
+            D[I * 128:(I + 1) * 128, J * 128:(J + 1) * 128] = V[I * (I + 1) // 2 + J].T
+    return torch.tril(D[:m, :m]).cpu().numpy()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C", "D"])
+def test_full_config_sampled_parity(torch_cuda, name):
+    """BASELINE configs C (n = 16,384, nu = 3/2) and D (n = 65,536) at full size, in the launch
+    configuration bench.py times: (1) Cholesky residual on 1,000 sampled entries (L L^T)_ij vs the
+    oracle's Matérn Sigma_ij; (2) the leading 4,096 x 4,096 block of L vs the oracle's own Cholesky of
+    the leading block of Sigma (independent mode; a leading principal block factors on its own);
+    (3) log P_k for the first 4,096 prefixes over 256 samples (two ranges across a shift boundary):
+    shared-L mode |dlog P| <= 1e-10, independent mode <= 1e-8."""
+    torch = torch_cuda
+    cfg = W.CONFIGS[name]
+    inp, order, a = sorted_inputs(cfg)
+    n = cfg.n
+    xy = inp.xy[order]
+    T = gpu_cov(torch, xy, cfg)
+    assert mvn().mvn_potrf(T, n) == -1
+    rng = np.random.default_rng(5)
+    ii = np.sort(rng.integers(0, n, 1000))
+    jj = np.array([rng.integers(0, i + 1) for i in ii])
+    Ri = tile_rows(T, n, ii, n)
+    Rj = tile_rows(T, n, jj, n)
+    got = np.einsum("ij,ij->i", Ri, Rj)
+    h = np.sqrt(((xy[ii] - xy[jj]) ** 2).sum(1))
+    want = oracle.matern(h, cfg.sigma2, cfg.beta, cfg.nu) + np.where(ii == jj, cfg.nugget, 0.0)
+    assert np.max(np.abs(got - want)) <= 1e-12 * (cfg.sigma2 + cfg.nugget)
+    m = 4096
+    Lg = leading_block(T, n, m)
+    So = oracle.covariance(xy[:m], cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    Lo, info = oracle.cholesky(So, nthreads=16)
+    assert info == -1
+    assert np.linalg.norm(Lg @ Lg.T - So) / np.linalg.norm(So) <= 1e-12
+    for begin, end in [(0, 128), (cfg.N - 64, cfg.N + 64)]:
+        M, S = gpu_sov(torch, T, n, a, cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+        lp_g = logp_from(M, S, end - begin)[:m]
+        Ms, Ss = oracle_range(Lg, a[:m], np.full(m, np.inf), cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+        assert np.max(np.abs(lp_g - logp_from(Ms, Ss, end - begin))) <= 1e-10
+        Mo, So_ = oracle_range(Lo, a[:m], np.full(m, np.inf), cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+        assert np.max(np.abs(lp_g - logp_from(Mo, So_, end - begin))) <= LOGP_TOL
