@@ -174,6 +174,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--potrf", default="auto", choices=["auto", "rank0", "dist"],
+                    help="N>1: factor on rank 0 + broadcast L, or distributed (NEXT-1); auto = dist")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":
@@ -203,7 +205,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
 
     def step(events=None):
-        logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events)
+        logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events, potrf=args.potrf)
         lp = logp.cpu().numpy()                          # a10 on the host: regions
         k, _ = mvn.mvn_confidence_region(lp, cfg.conf)
         return lp, k
@@ -248,7 +250,9 @@ def main():
     ms_per_step = total_ms / args.steps
     value = n * NR / (ms_per_step / 1e3)
 
-    # ---- e2e through the public C API with host buffers (N = 1: mvn_crd)
+    # ---- e2e through the public API with host buffers. N = 1: the C-ABI call mvn_crd (a1 on the
+    # host, H2D of sorted locations and limits, a2..a8, D2H of log P, a10). N > 1: the same steps
+    # through parallel.crd_step on every rank from pinned host buffers, max over ranks.
     e2e = None
     if not args.no_e2e and world == 1:
         ts = []
@@ -260,11 +264,31 @@ def main():
             if it > 0:
                 ts.append(t1 - t0)
         e2e = {"value": n * NR / float(np.mean(ts)), "unit": UNIT, "h2d_bytes_per_step": 24 * n,
-               "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)),
+               "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)), "api": "mvn_crd (C ABI)",
                "k_star_matches_device_path": bool(np.array_equal(out.k_star, k))}
-    elif world > 1:
-        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * n,
-               "note": "multi-GPU e2e not measured this round (mvn_crd is the single-GPU public call)"}
+    elif not args.no_e2e:
+        import torch as _t
+        h_xy = _t.empty((n, 2), dtype=_t.float64).pin_memory()
+        h_a = _t.empty(n, dtype=_t.float64).pin_memory()
+        h_lp = _t.empty(n, dtype=_t.float64).pin_memory()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        o2, a2, _ = mvn.mvn_marginal_order(inp.mu, var, cfg.u)              # a1 (host)
+        h_xy.numpy()[:] = inp.xy[o2]
+        h_a.numpy()[:] = a2
+        d_xy.copy_(h_xy, non_blocking=True)
+        d_a.copy_(h_a, non_blocking=True)
+        logp = parallel.crd_step(d_xy, d_a, L, cfg, potrf=args.potrf)
+        h_lp.copy_(logp, non_blocking=True)
+        torch.cuda.synchronize()
+        k2, _ = mvn.mvn_confidence_region(h_lp.numpy(), cfg.conf)          # a10 (host)
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * NR / float(t.item()), "unit": UNIT, "h2d_bytes_per_step": 24 * n,
+               "d2h_bytes_per_step": 8 * n, "s_per_call": float(t.item()),
+               "api": "parallel.crd_step from pinned host buffers, max over ranks",
+               "k_star_matches_device_path": bool(np.array_equal(k2, k))}
 
     # ---- roofline of the dominant kernel (k_sov, SOV GEMM + chain), from the live stage times
     sov_ms = stage_mean["sov"]
@@ -272,8 +296,12 @@ def main():
     my_samples = my_end - my_begin
     sov_flops = float(n) * (n - 1) * my_samples       # algorithmic: sum_k 2(k-1) per sample (a6 + in-block dot)
     achieved = sov_flops / (sov_ms / 1e3) / 1e12
-    nt = -(-n // 128)
-    launches = 1 + (nt + 2 * (nt - 1)) + 2 + 1 + (1 if world > 1 else 0)
+    mode = ("dist" if world > 1 else "rank0") if args.potrf == "auto" else args.potrf
+    if mode == "dist":
+        n_potrf = parallel.potrf_launches(n, world, rank)
+    else:
+        n_potrf = parallel.potrf_launches(n) if rank == 0 else 0
+    launches = (1 if (mode == "dist" or rank == 0) else 0) + n_potrf + 2 + 1 + (1 if world > 1 else 0)
     potrf_ms = stage_mean["potrf"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -282,7 +310,9 @@ def main():
         "config": {"workload": f"config {cfg.name}: n={n} ({cfg.g}x{cfg.g} jittered grid), Matern "
                                f"(s2={cfg.sigma2}, beta={cfg.beta}, nu={cfg.nu}) + nugget {cfg.nugget}, u={cfg.u}, "
                                f"N={cfg.N} x R={cfg.R} QMC", "n": n, "N": cfg.N, "R": cfg.R,
-                   "parallelism": f"samples sharded over {world} GPU(s), L broadcast from rank 0",
+                   "parallelism": (f"samples sharded over {world} GPU(s); " +
+                                   ("Cholesky 1-D block-cyclic over the GPUs (NEXT-1)" if mode == "dist" and world > 1
+                                    else "Cholesky on rank 0, L broadcast" if world > 1 else "one GPU")),
                    "l2": "flushed between timed steps (256 MB write); L itself is "
                          f"{mvn.mvn_tiles_bytes(n) / 1e9:.2f} GB"},
         "cholesky_tflops": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12,

@@ -108,6 +108,38 @@ mvn_status mvn_cov_matern(mvn_ctx *ctx, mvn_tiles t, const double *d_xy, double 
 mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
 
 /* ---------------------------------------------------------------------------------------------
+ * NEXT-1: building blocks of the distributed tiled Cholesky, 1-D
+ * block-cyclic over tile columns (tile column j is owned by rank j mod W). The step loop and the
+ * NCCL panel broadcasts are in the Python layer (paper_2405_14892_b200/parallel.py,
+ * potrf_distributed); the right-looking recurrence is the one of mvn_potrf (Alg. 1 l.8, P:233;
+ * the paper runs it distributed on Chameleon/StarPU). Per step k:
+ *   owner(k):  mvn_potrf_panel(k)  -> mvn_panel_pack(k)  -> broadcast panel k
+ *   others:    receive panel k     -> mvn_panel_unpack(k)
+ *   all:       mvn_potrf_update(k, own columns > k)
+ * A panel is the nt-k tiles (k..nt-1, k) stored contiguously: (nt-k) * nb*nb doubles, device.
+ * All calls are asynchronous on the context's stream; pivots are checked on the device and
+ * collected by mvn_potrf_info.                                                                  */
+
+/* POTRF of diagonal tile k and TRSM of the tiles below it (A_ik <- A_ik L_kk^{-T}), in place.
+ * Tile column k must already carry every update from panels 0..k-1. A non-positive pivot records
+ * its 0-based global row in the context's device info (first failure only) and leaves the tile. */
+mvn_status mvn_potrf_panel(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t k);
+
+/* Trailing update with panel k: A_ij -= L_ik L_jk^T for every tile column j in
+ * {col_first, col_first + col_stride, ...} (< nt) and every i >= j. Requires k < col_first and
+ * col_stride >= 1. sm_reserve SMs are left free for concurrent panel work (0..nsm-1).          */
+mvn_status mvn_potrf_update(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t k, int64_t col_first,
+                            int64_t col_stride, int32_t sm_reserve);
+
+/* Tile column k <-> contiguous panel buffer of (nt-k) * nb*nb doubles (device, caller-owned). */
+mvn_status mvn_panel_pack(mvn_ctx *ctx, mvn_tiles t, const double *d_tiles, int64_t k, double *d_panel);
+mvn_status mvn_panel_unpack(mvn_ctx *ctx, mvn_tiles t, const double *d_panel, int64_t k, double *d_tiles);
+
+/* Reads (synchronising the stream) the device info of mvn_potrf_panel: -1 if every pivot so far
+ * was positive, else the first failing 0-based row. reset != 0 sets it back to -1 afterwards.  */
+mvn_status mvn_potrf_info(mvn_ctx *ctx, int64_t *info, int32_t reset);
+
+/* ---------------------------------------------------------------------------------------------
  * a5. QMC point set (reading R8). The global sample index g in [0, N*R) maps to shift r = g / N
  * and lattice index j = g % N + 1 (1-based). Row k (0-based, sorted order) of sample g uses
  *   X = (j * G_k + D_k^r) mod 2^64,  w = (floor(X / 2^12) + 1/2) * 2^-52,

@@ -31,7 +31,8 @@ ABI_SYMBOLS = [
     "mvn_tiles_count", "mvn_tiles_bytes", "mvn_pack_lower", "mvn_unpack_lower",
     "mvn_marginal_order", "mvn_cov_matern", "mvn_potrf", "mvn_lattice_generators",
     "mvn_lattice_shifts", "mvn_sov_prefix", "mvn_prefix_rescale", "mvn_prefix_finalize",
-    "mvn_confidence_region", "mvn_crd",
+    "mvn_confidence_region", "mvn_crd", "mvn_potrf_panel", "mvn_potrf_update", "mvn_panel_pack",
+    "mvn_panel_unpack", "mvn_potrf_info",
 ]
 
 
@@ -98,6 +99,11 @@ def lib() -> ctypes.CDLL:
         "mvn_prefix_finalize": (S, [P, I64, I64, P, P, P]),
         "mvn_confidence_region": (S, [I64, P, P, I64, P, P]),
         "mvn_crd": (S, [P, ctypes.POINTER(mvn_crd_problem), ctypes.POINTER(mvn_crd_result)]),
+        "mvn_potrf_panel": (S, [P, T, P, I64]),
+        "mvn_potrf_update": (S, [P, T, P, I64, I64, I64, I32]),
+        "mvn_panel_pack": (S, [P, T, P, I64, P]),
+        "mvn_panel_unpack": (S, [P, T, P, I64, P]),
+        "mvn_potrf_info": (S, [P, ctypes.POINTER(I64), I32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -139,14 +145,16 @@ class Context:
         self.h = h
 
     @classmethod
-    def get(cls, device: int | None = None) -> "Context":
+    def get(cls, device: int | None = None, stream=None) -> "Context":
+        """The device's context, bound to `stream` (a torch.cuda.Stream) or torch's current stream."""
         import torch
         if device is None:
             device = torch.cuda.current_device()
         if device not in cls._by_device:
             cls._by_device[device] = Context(device)
         c = cls._by_device[device]
-        lib().mvn_set_stream(c.h, ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream))
+        st = stream if stream is not None else torch.cuda.current_stream(device)
+        lib().mvn_set_stream(c.h, ctypes.c_void_p(st.cuda_stream))
         return c
 
     def check(self, st: int, what: str):
@@ -224,6 +232,42 @@ def mvn_potrf(t, n: int, raise_on_numeric: bool = True) -> int:
     if st == MVN_E_NUMERIC and not raise_on_numeric:
         return int(info.value)
     c.check(st, "mvn_potrf")
+    return int(info.value)
+
+
+# ---- NEXT-1: building blocks of the distributed factorisation (driven by parallel.potrf_distributed)
+def mvn_potrf_panel(t, n: int, k: int, stream=None):
+    """POTRF of diagonal tile k + TRSM of the tiles below it, in place (asynchronous)."""
+    c = Context.get(t.device.index, stream)
+    c.check(lib().mvn_potrf_panel(c.h, tiles(n), _dev_ptr(t), int(k)), "mvn_potrf_panel")
+
+
+def mvn_potrf_update(t, n: int, k: int, col_first: int, col_stride: int = 1, sm_reserve: int = 0, stream=None):
+    """A_ij -= L_ik L_jk^T for tile columns j = col_first, col_first + col_stride, ... (asynchronous)."""
+    c = Context.get(t.device.index, stream)
+    c.check(lib().mvn_potrf_update(c.h, tiles(n), _dev_ptr(t), int(k), int(col_first), int(col_stride),
+                                   int(sm_reserve)), "mvn_potrf_update")
+
+
+def panel_numel(n: int, k: int) -> int:
+    nt = -(-n // TILE)
+    return (nt - k) * TILE * TILE
+
+
+def mvn_panel_pack(t, n: int, k: int, panel, stream=None):
+    c = Context.get(t.device.index, stream)
+    c.check(lib().mvn_panel_pack(c.h, tiles(n), _dev_ptr(t), int(k), _dev_ptr(panel)), "mvn_panel_pack")
+
+
+def mvn_panel_unpack(panel, n: int, k: int, t, stream=None):
+    c = Context.get(t.device.index, stream)
+    c.check(lib().mvn_panel_unpack(c.h, tiles(n), _dev_ptr(panel), int(k), _dev_ptr(t)), "mvn_panel_unpack")
+
+
+def mvn_potrf_info(device: int = 0, reset: bool = True, stream=None) -> int:
+    c = Context.get(device, stream)
+    info = ctypes.c_int64(-1)
+    c.check(lib().mvn_potrf_info(c.h, ctypes.byref(info), 1 if reset else 0), "mvn_potrf_info")
     return int(info.value)
 
 

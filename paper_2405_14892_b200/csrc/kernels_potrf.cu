@@ -240,8 +240,21 @@ __global__ void __launch_bounds__(256) k_trsm2(double *__restrict__ tiles, int k
 }
 
 // ------------------------------------------------------------------------------------------ K4
-// Trailing update, one CTA per (tile (i,j), row half h): C(64x128) -= L_ik[h-half] * L_jk^T.
-// 4 warps as 2 (M) x 2 (N), warp tile 32x64 = 4x8 DMMA blocks (64 fp64 accumulators / thread).
+// Column-major enumeration of the trailing tiles (ti, tj), ti >= tj, over the tile columns
+// tj = c0, c0 + cs, c0 + 2 cs, ... < nt (column tj holds nt - tj tiles). `base` / `col` carry the
+// scan between calls (items of one CTA increase monotonically).
+__device__ __forceinline__ void upd_item(int64_t item, int nt, int c0, int cs, int &ti, int &tj, int64_t &base, int &col) {
+    while (item >= base + (nt - (c0 + col * cs))) { base += nt - (c0 + col * cs); ++col; }
+    tj = c0 + col * cs;
+    ti = tj + (int)(item - base);
+}
+
+__host__ __device__ inline int64_t upd_items(int nt, int c0, int cs) {
+    int64_t s = 0;
+    for (int c = c0; c < nt; c += cs) s += nt - c;
+    return s;
+}
+
 namespace upd {
 constexpr int BM = 64, BN = 128, BK = 16, STAGES = 3;
 constexpr int SA = BM + 4, SB = BN + 4;  // == 4 (mod 16)
@@ -249,28 +262,20 @@ constexpr int WM = 4, WN = 8;
 constexpr int SMEM = STAGES * BK * (SA + SB) * 8;
 }  // namespace upd
 
-__global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, int k, int nt, int mode) {
+// Trailing update, one CTA per (tile (i,j), row half h): C(64x128) -= L_ik[h-half] * L_jk^T.
+// 4 warps as 2 (M) x 2 (N), warp tile 32x64 = 4x8 DMMA blocks (64 fp64 accumulators / thread).
+__global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, int k, int nt, int c0, int cs) {
     using namespace upd;
     extern __shared__ double sm[];
     double *As = sm;
     double *Bs = sm + STAGES * BK * SA;
     const int64_t id = blockIdx.x >> 1;
     const int h = blockIdx.x & 1;
-    // id -> (ii, jj), 0 <= jj <= ii < T, row-major lower enumeration; tile (k+1+ii, k+1+jj).
-    // mode 1: only column k+1 (the next panel), ii = id, jj = 0.
-    // mode 2: the rest (columns >= k+2): the same enumeration shifted by one tile.
-    int ii, jj;
-    if (mode == 1) {
-        ii = (int)id;
-        jj = 0;
-    } else {
-        ii = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
-        while ((int64_t)ii * (ii + 1) / 2 > id) --ii;
-        while ((int64_t)(ii + 1) * (ii + 2) / 2 <= id) ++ii;
-        jj = (int)(id - (int64_t)ii * (ii + 1) / 2);
-        if (mode == 2) { ++ii; ++jj; }
-    }
-    const int ti = k + 1 + ii, tj = k + 1 + jj;
+    // id -> tile (ti, tj) of the column-major enumeration over tile columns c0, c0 + cs, ... (> k):
+    // c0 = k+1, cs >= nt: the next panel column only (lookahead); c0 = k+2, cs = 1: the rest.
+    int ti, tj, col = 0;
+    int64_t base = 0;
+    upd_item(id, nt, c0, cs, ti, tj, base, col);
     const double *__restrict__ Lik = tiles + tile_offset(ti, k) + h * BM;   // column stride 128
     const double *__restrict__ Ljk = tiles + tile_offset(tj, k);
     double *C = tiles + tile_offset(ti, tj) + h * BM;
@@ -347,13 +352,6 @@ constexpr int SMEM = (OFF_BAR + 2 * STAGES) * 8;
 constexpr int CHUNKS = kTile / BK;
 }  // namespace upd2
 
-__device__ __forceinline__ void upd_item(int64_t item, int T, int &ii, int &jj, int64_t &base, int &col) {
-    // column-major enumeration of the T x T lower triangle: column jj holds T - jj tiles
-    while (item >= base + (T - col)) { base += T - col; ++col; }
-    jj = col;
-    ii = col + (int)(item - base);
-}
-
 __device__ __forceinline__ void bulk_reduce_add_f64(double *gdst, const double *ssrc, unsigned bytes) {
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n"
                  ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
@@ -362,14 +360,16 @@ __device__ __forceinline__ void bulk_reduce_add_f64(double *gdst, const double *
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
-__global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int nt, int off) {
+// Updates with panel k the tile columns c0, c0 + cs, ... (c0 > k): c0 = k+2, cs = 1 on one GPU
+// (column k+1 is the lookahead stream's); cs = world size for the 1-D block-cyclic distributed
+// factorisation (mvn_potrf_update).
+__global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int nt, int c0, int cs,
+                                                        int64_t nitems) {
     using namespace upd2;
     extern __shared__ double sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
     uint64_t *empty = full + STAGES;
     const int tid = threadIdx.x;
-    const int T = nt - k - 1 - off;          // off = 1: skip column k+1 (done by the lookahead stream)
-    const int64_t nitems = (int64_t)T * (T + 1) / 2;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -385,9 +385,8 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
         // ------------------------------------------------------------ producer warp
         const int lane = tid & 31;
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-            int ii, jj;
-            upd_item(item, T, ii, jj, base, col);
-            const int ti = k + 1 + off + ii, tj = k + 1 + off + jj;
+            int ti, tj;
+            upd_item(item, nt, c0, cs, ti, tj, base, col);
             const double *Lik = tiles + tile_offset(ti, k);
             const double *Ljk = tiles + tile_offset(tj, k);
             for (int c = 0; c < CHUNKS; ++c, ++q) {
@@ -417,9 +416,8 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
     const int wn0 = warp * 16;                       // 16 full columns per warp
     double *stg = sm + OFF_STG + warp * 16 * kTile;   // column-major [16][128]
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-        int ii, jj;
-        upd_item(item, T, ii, jj, base, col);
-        const int ti = k + 1 + off + ii, tj = k + 1 + off + jj;
+        int ti, tj;
+        upd_item(item, nt, c0, cs, ti, tj, base, col);
         double acc[16][2][2];
 #pragma unroll
         for (int a = 0; a < 16; ++a)
@@ -531,15 +529,15 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
             const int64_t items = (int64_t)Tr * (Tr + 1) / 2;
             if (use_persistent && items >= 2 * nsm) {
                 const int grid = (int)std::min<int64_t>(items, nsm - kPanelSMs);
-                k_update2<<<grid, upd2::NT, upd2::SMEM, st>>>(tiles, k, nt, 1);
+                k_update2<<<grid, upd2::NT, upd2::SMEM, st>>>(tiles, k, nt, k + 2, 1, items);
             } else {
-                k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(tiles, k, nt, 2);
+                k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(tiles, k, nt, k + 2, 1);
             }
         }
         if ((e = cudaEventRecord(g_ps.ev_rest[k & 1], st))) return e;
         // panel stream: column k+1, then POTRF / TRSM of panel k+1
         if (k >= 1 && (e = cudaStreamWaitEvent(sp, g_ps.ev_rest[(k - 1) & 1], 0))) return e;
-        k_update<<<(unsigned)(2 * T), 128, upd::SMEM, sp>>>(tiles, k, nt, 1);
+        k_update<<<(unsigned)(2 * T), 128, upd::SMEM, sp>>>(tiles, k, nt, k + 1, nt);
         k_potrf_diag2<<<1, 256, sm_diag, sp>>>(tiles, k + 1, d_info);
         if (T > 1) k_trsm2<<<2 * (T - 1), 256, sm_trsm, sp>>>(tiles, k + 1);
         if ((e = cudaEventRecord(g_ps.ev_panel[(k + 1) & 1], sp))) return e;
@@ -547,6 +545,57 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
     }
     // join: the main stream waits for the last panel
     if ((e = cudaStreamWaitEvent(st, g_ps.ev_panel[(nt - 1) & 1], 0))) return e;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------ NEXT-1
+// Building blocks of the distributed (1-D block-cyclic over tile columns) factorisation; the step
+// loop and the NCCL panel broadcasts live in paper_2405_14892_b200/parallel.py (collectives stay
+// above the ABI). Every rank keeps a full tile-packed buffer; it updates only the tile columns it
+// owns and receives every other column as a finished panel, so each rank ends with all of L.
+
+// Panel copy: tiles (k..nt-1, k) <-> contiguous panel[(i - k) * nb^2]. One CTA per (tile, 1/8).
+__global__ void __launch_bounds__(256) k_panel_copy(double *__restrict__ tiles, int k, double *__restrict__ panel,
+                                                   int to_panel) {
+    const int i = k + blockIdx.y;
+    double2 *t = reinterpret_cast<double2 *>(tiles + tile_offset(i, k));
+    double2 *p = reinterpret_cast<double2 *>(panel + (int64_t)blockIdx.y * kTile * kTile);
+    constexpr int PER = kTile * kTile / 2 / 8;             // double2 per CTA
+    const int e0 = blockIdx.x * PER;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < PER; e += 256) {
+        if (to_panel) p[e0 + e] = t[e0 + e];
+        else t[e0 + e] = p[e0 + e];
+    }
+}
+
+cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int64_t *d_info, cudaStream_t st) {
+    const int nt = (int)((n + kTile - 1) / kTile);
+    const size_t sm_diag = kTile * blk::SP * 8, sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
+    k_potrf_diag2<<<1, 256, sm_diag, st>>>(tiles, k, d_info);
+    if (nt - k - 1 > 0) k_trsm2<<<2 * (nt - k - 1), 256, sm_trsm, st>>>(tiles, k);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int c0, int cs, int sm_reserve, cudaStream_t st) {
+    const int nt = (int)((n + kTile - 1) / kTile);
+    if (c0 >= nt) return cudaSuccess;
+    const int64_t items = upd_items(nt, c0, cs);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int avail = std::max(1, nsm - sm_reserve);
+    if (items >= 2 * avail) {
+        k_update2<<<avail, upd2::NT, upd2::SMEM, st>>>(tiles, k, nt, c0, cs, items);
+    } else {
+        k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(tiles, k, nt, c0, cs);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, double *panel, bool to_panel, cudaStream_t st) {
+    const int nt = (int)((n + kTile - 1) / kTile);
+    k_panel_copy<<<dim3(8, nt - k), 256, 0, st>>>(tiles, k, panel, to_panel ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -144,6 +144,11 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
         delete c;
         return MVN_E_CUDA;
     }
+    const int64_t minus1 = -1;
+    if (cudaMemcpy(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+        delete c;
+        return MVN_E_CUDA;
+    }
     *out = c;
     return MVN_OK;
 }
@@ -238,6 +243,53 @@ mvn_status mvn_potrf(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t *info) {
     if (*info >= 0 && *info < t.n)
         return fail(c, MVN_E_NUMERIC, "mvn_potrf: matrix not positive definite at row " + std::to_string(*info));
     if (*info >= t.n) *info = -1;   // cannot happen (padding is the identity)
+    return MVN_OK;
+}
+
+mvn_status mvn_potrf_panel(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k) {
+    if (!c) return MVN_E_USAGE;
+    const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
+    if (!nt || !d_tiles || k < 0 || k >= nt) return fail(c, MVN_E_USAGE, "mvn_potrf_panel: bad arguments");
+    MVN_CUDA(c, mvn::launch_potrf_panel(t.n, d_tiles, (int)k, c->d_info, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_potrf_update(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k, int64_t col_first, int64_t col_stride,
+                            int32_t sm_reserve) {
+    if (!c) return MVN_E_USAGE;
+    const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
+    if (!nt || !d_tiles || k < 0 || col_first <= k || col_stride < 1 || sm_reserve < 0 || sm_reserve >= c->nsm)
+        return fail(c, MVN_E_USAGE, "mvn_potrf_update: bad arguments (need 0 <= k < col_first, col_stride >= 1)");
+    if (col_first >= nt) return MVN_OK;
+    MVN_CUDA(c, mvn::launch_potrf_update(t.n, d_tiles, (int)k, (int)col_first, (int)std::min<int64_t>(col_stride, nt),
+                                         sm_reserve, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_panel_pack(mvn_ctx *c, mvn_tiles t, const double *d_tiles, int64_t k, double *d_panel) {
+    if (!c) return MVN_E_USAGE;
+    const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
+    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt) return fail(c, MVN_E_USAGE, "mvn_panel_pack: bad arguments");
+    MVN_CUDA(c, mvn::launch_panel_copy(t.n, const_cast<double *>(d_tiles), (int)k, d_panel, true, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_panel_unpack(mvn_ctx *c, mvn_tiles t, const double *d_panel, int64_t k, double *d_tiles) {
+    if (!c) return MVN_E_USAGE;
+    const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
+    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt) return fail(c, MVN_E_USAGE, "mvn_panel_unpack: bad arguments");
+    MVN_CUDA(c, mvn::launch_panel_copy(t.n, d_tiles, (int)k, const_cast<double *>(d_panel), false, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_potrf_info(mvn_ctx *c, int64_t *info, int32_t reset) {
+    if (!c || !info) return fail(c, MVN_E_USAGE, "mvn_potrf_info: bad arguments");
+    MVN_CUDA(c, cudaMemcpyAsync(info, c->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    if (reset) {
+        const int64_t minus1 = -1;
+        MVN_CUDA(c, cudaMemcpyAsync(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    }
+    MVN_CUDA(c, cudaStreamSynchronize(c->stream));
     return MVN_OK;
 }
 

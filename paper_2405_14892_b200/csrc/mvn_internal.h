@@ -15,6 +15,10 @@ cudaError_t launch_finalize(int64_t n, int64_t NR, const double *M, const double
 
 cudaError_t potrf_init();
 cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st);
+// distributed-factorisation building blocks (NEXT-1)
+cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int64_t *d_info, cudaStream_t st);
+cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int c0, int cs, int sm_reserve, cudaStream_t st);
+cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, double *panel, bool to_panel, cudaStream_t st);
 
 struct SovLaunch {
     const double *L;

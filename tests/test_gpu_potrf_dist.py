@@ -1,0 +1,164 @@
+"""NEXT-1 on one GPU: the building blocks of the distributed Cholesky (mvn_potrf_panel,
+mvn_potrf_update with a column filter, mvn_panel_pack / unpack) and the schedule of
+parallel.potrf_dist_schedule for W = 1, 2, 3, 4 virtual ranks.
+
+The virtual ranks are NOT co-resident processes waiting on each other: one process steps the W
+generators in lockstep, each rank with its own streams and its own full tile buffer, and the
+panel "broadcast" is a device copy ordered by events exactly like an NCCL broadcast (receivers
+copy on their side stream after the owner packed; the owner's next write to the panel slot waits
+for the copies). No kernel ever spins on another rank's kernel.
+
+Parity: every rank's L must equal the single-GPU mvn_potrf factor bit for bit (each tile receives
+the same updates, in the same order, from the same kernels), which the oracle pins via
+test_gpu_parity.test_potrf_vs_oracle; the residual is checked here as well."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+NB = 128
+
+
+@pytest.fixture(scope="module")
+def torch(cuda_device):
+    import torch as t
+    return t
+
+
+def mvn():
+    import paper_2405_14892_b200 as m
+    return m
+
+
+def dense(T, n):
+    return mvn().mvn_unpack_lower(T, n).T.contiguous().cpu().numpy()
+
+
+def sigma(torch, n, nu=0.5, seed=0):
+    xy = np.random.default_rng(seed + n).uniform(size=(n, 2))
+    beta = 0.1 if nu == 0.5 else 0.05
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, beta, nu, 1e-8)
+    return T, oracle.covariance(xy, 1.0, beta, nu, 1e-8)
+
+
+def emulate(torch, tiles, n):
+    """Run potrf_dist_schedule for len(tiles) virtual ranks on one device (see module doc)."""
+    from paper_2405_14892_b200.parallel import CudaPotrfOps, potrf_dist_schedule
+    W = len(tiles)
+    torch.cuda.synchronize()
+    mvn().mvn_potrf_info(0, reset=True)
+    ops = [CudaPotrfOps(tiles[r], n, main=torch.cuda.Stream()) for r in range(W)]
+    gens = [potrf_dist_schedule(ops[r], r, W) for r in range(W)]
+    reqs = [next(g) for g in gens]
+    while True:
+        assert len({q[1:] for q in reqs}) == 1, reqs        # every rank is at the same broadcast
+        _, k, src = reqs[0]
+        ev_src = ops[src].record("side")
+        handles = [None] * W
+        for r in range(W):
+            if r == src:
+                continue
+            ops[r].side.wait_event(ev_src)
+            with torch.cuda.stream(ops[r].side):
+                ops[r].panel_buf(k).copy_(ops[src].panel_buf(k))
+            handles[r] = ops[r].record("side")
+            ops[src].side.wait_event(handles[r])            # the owner's slot is free after the copies
+        handles[src] = ops[src].record("side")
+        nxt = []
+        for r, g in enumerate(gens):
+            try:
+                nxt.append(g.send(handles[r]))
+            except StopIteration:
+                nxt.append(None)
+        if all(q is None for q in nxt):
+            break
+        assert all(q is not None for q in nxt)
+        reqs = nxt
+    for o in ops:
+        torch.cuda.current_stream().wait_stream(o.main)
+    torch.cuda.synchronize()
+    return mvn().mvn_potrf_info(0, reset=True)
+
+
+def test_panel_pack_unpack(torch):
+    n = 5 * NB + 3
+    T, _ = sigma(torch, n)
+    for k in (0, 2, 5):
+        buf = torch.empty(mvn().panel_numel(n, k), dtype=torch.float64, device="cuda")
+        mvn().mvn_panel_pack(T, n, k, buf)
+        nt = -(-n // NB)
+        Th = T.cpu().numpy()
+        for i in range(k, nt):
+            off = (i * (i + 1) // 2 + k) * NB * NB
+            assert np.array_equal(buf[(i - k) * NB * NB:(i - k + 1) * NB * NB].cpu().numpy(), Th[off:off + NB * NB])
+        T2 = torch.zeros_like(T)
+        mvn().mvn_panel_unpack(buf, n, k, T2)
+        T2h = T2.cpu().numpy()
+        for i in range(k, nt):
+            off = (i * (i + 1) // 2 + k) * NB * NB
+            assert np.array_equal(T2h[off:off + NB * NB], Th[off:off + NB * NB])
+
+
+@pytest.mark.parametrize("c0,cs", [(1, 1), (2, 3), (4, 2), (3, 100)])
+def test_update_column_filter(torch, c0, cs):
+    """mvn_potrf_update(k=0, c0, cs) on a random tile buffer == numpy A_ij -= L_i0 L_j0^T on the
+    selected tile columns, untouched elsewhere (small k so that the persistent kernel, taken for
+    >= 2*(148-8) tiles, is exercised at n = 40 tiles)."""
+    for ntile in (7, 40):
+        n = ntile * NB
+        cnt = ntile * (ntile + 1) // 2
+        rng = np.random.default_rng(ntile + c0)
+        host = rng.standard_normal(cnt * NB * NB)
+        T = torch.from_numpy(host.copy()).cuda()
+        mvn().mvn_potrf_update(T, n, 0, c0, cs, 8)
+        got = T.cpu().numpy()
+
+        def tile(a, i, j):
+            off = (i * (i + 1) // 2 + j) * NB * NB
+            return a[off:off + NB * NB].reshape(NB, NB).T          # column-major -> logical
+
+        for j in range(ntile):
+            for i in range(j, ntile):
+                want = tile(host, i, j)
+                if j >= c0 and (j - c0) % cs == 0:
+                    want = want - tile(host, i, 0) @ tile(host, j, 0).T
+                    assert np.max(np.abs(tile(got, i, j) - want)) <= 1e-12 * NB
+                else:
+                    assert np.array_equal(tile(got, i, j), want)
+
+
+@pytest.mark.parametrize("n,nu,W", [(1000, 0.5, 1), (1000, 0.5, 2), (2000, 1.5, 3), (4000, 0.5, 4), (5000, 0.5, 2),
+                                    (130, 0.5, 3), (40 * NB + 77, 0.5, 3)])
+def test_emulated_distributed_potrf_matches_single_gpu(torch, n, nu, W):
+    T, S = sigma(torch, n, nu)
+    ref = T.clone()
+    assert mvn().mvn_potrf(ref, n) == -1
+    Lref = dense(ref, n)
+    copies = [T.clone() for _ in range(W)]
+    info = emulate(torch, copies, n)
+    assert info == -1
+    for r in range(W):
+        assert torch.equal(copies[r], ref), f"rank {r}: max diff {float((copies[r] - ref).abs().max())}"
+    res = np.linalg.norm(Lref @ Lref.T - S) / np.linalg.norm(S)
+    assert res <= 1e-12
+
+
+def test_emulated_distributed_potrf_reports_first_failure(torch):
+    n, W = 600, 3
+    A = np.eye(n)
+    A[333, 333] = -1.0
+    copies = [mvn().mvn_pack_lower(torch.from_numpy(A).cuda(), n) for _ in range(W)]
+    assert emulate(torch, copies, n) == 333
+
+
+def test_potrf_distributed_single_process(torch):
+    """potrf_distributed without a process group (world 1) == mvn_potrf bit for bit."""
+    from paper_2405_14892_b200.parallel import potrf_distributed
+    n = 3000
+    T, _ = sigma(torch, n, 1.5)
+    ref = T.clone()
+    mvn().mvn_potrf(ref, n)
+    assert potrf_distributed(T, n) == -1
+    torch.cuda.synchronize()
+    assert torch.equal(T, ref)
