@@ -192,6 +192,38 @@ mvn_status mvn_confidence_region(int64_t n, const double *logP, const double *co
                                  int64_t *k_out, int32_t *near_tie);
 
 /* ---------------------------------------------------------------------------------------------
+ * NEXT-2: Monte-Carlo validation of the confidence regions ("draws
+ * N samples from the fitted distribution, where N_s represents the number of samples exceeding a
+ * given threshold ... p_hat(alpha) = N_s/N"; supplement P:20-23). Reading R20:
+ * sample s (global index, 0-based) draws, for every sorted row k,
+ *   z_k = Phi^{-1}(w),  w = (floor(X / 2^12) + 1/2) 2^-52,
+ *   X = SplitMix64_mix(seed + 0x9E3779B97F4A7C15 * (s * 2^32 + k + 1))  (mod 2^64),
+ * and the field in sorted order is mu + L z. It exceeds u on the region o(1..k*) iff
+ * (L z)_k > a_k for all k < k*, so one pass records its first failing row
+ *   f_s = min{k : (L z)_k <= a_k}   (n if none),
+ * and p_hat(k*) = #{s : f_s >= k*} / N for every level at once.                                 */
+typedef struct {
+    uint64_t seed;         /* z-generator seed */
+    int64_t sample_begin;  /* global sample range [begin, end) of this call (a rank's shard) */
+    int64_t sample_end;
+} mvn_mc;
+
+/* d_L: tile-packed L (mvn_potrf), d_a: n device doubles (the limits a_k of the sweep).
+ * d_count: n+1 device uint64, ACCUMULATED (count[f] += samples with first failing row f), so
+ * chunks and ranks add up (all_reduce SUM across ranks). d_first: nullable, device int32 per
+ * sample of the range (f_s). Work: n(n+1) fp64 flops per sample on DMMA (X = L Z, never stored).
+ * Internal workspace: the Z block (<= ~8 GB; samples are processed in chunks).
+ * MVN_E_USAGE for an empty / negative range.                                                    */
+mvn_status mvn_mc_validate(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_a, const mvn_mc *m,
+                           uint64_t *d_count, int32_t *d_first);
+
+/* HOST. p_hat[i] = #{s : f_s >= k_star[i]} / N_total from the histogram count[0..n] (the
+ * confidence level the MC draws give the region of size k_star[i]). MVN_E_USAGE if
+ * N_total < 1 or a k_star is outside [0, n].                                                   */
+mvn_status mvn_mc_levels(int64_t n, const uint64_t *count, int64_t N_total, const int64_t *k_star, int64_t nconf,
+                         double *p_hat);
+
+/* ---------------------------------------------------------------------------------------------
  * End-to-end CRD (Alg. 1) on one GPU with HOST buffers: upload, a1..a10, download.
  * This is the call a user makes; bench.py's "e2e" number times it.                             */
 typedef struct {

@@ -55,6 +55,9 @@ def lib() -> ctypes.CDLL:
             ("orc_cholesky", i64, [i64, dp, i]),
             ("orc_sov_unit", i, [i64, dp, i64, dp, dp, u64p, u64p, i64, i64, dp, dp, dp]),
             ("orc_sov_units", i, [i64, dp, i64, dp, dp, u64p, u64p, i64, i64, i64, i64, i64, dp, i]),
+            ("orc_mc_mix", ctypes.c_uint64, [ctypes.c_uint64] * 3),
+            ("orc_mc_z", d, [ctypes.c_uint64] * 3),
+            ("orc_mc_first", i, [i64, dp, i64, dp, ctypes.c_uint64, i64, i64, dp, dp, dp, i]),
         ]:
             f = getattr(L, name)
             f.restype = res
@@ -73,3 +76,4 @@ from .pipeline import (  # noqa: E402
     Phi, Phibar, Phiinv, sov_step, cholesky, marginal_order, sov_units, sov_unit,
     combine_units, prefix_logp, per_shift_logp, region, crd,
 )
+from .mcval import mc_z, mc_first, mc_counts, mc_levels  # noqa: E402

@@ -276,3 +276,63 @@ int orc_sov_units(long long n, const double *L, long long ldl, const double *a, 
     }
     return err;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* NEXT-2: Monte-Carlo validation of the confidence regions ("draws N samples from the    */
+/* fitted distribution, where N_s represents the number of samples exceeding a given threshold */
+/* ... p_hat(alpha) = N_s/N"; supplement P:20-23).                                              */
+/* Sample s (global index) draws z_k = Phi^{-1}(w_{k,s}) for k = 0..n-1 with                   */
+/*   X = SplitMix64-mix(seed + GAMMA (s 2^32 + k + 1)),  w = (floor(X / 2^12) + 1/2) 2^-52      */
+/* (reading R20), forms x_k = sum_{t<=k} L_kt z_t (ascending t; x = L z, so mu + x is a draw of */
+/* the field in sorted order) and records its first failing row                                */
+/*   first[s - s0] = min{k : x_k <= a_k}  (n if x_k > a_k for every k),                         */
+/* i.e. the sample exceeds u on the region o(1..k*) iff first >= k*. If margin is non-NULL it  */
+/* receives x_f - a_f at the reported row (0 when first = n) for tie diagnostics.              */
+/* ------------------------------------------------------------------------------------------ */
+uint64_t orc_mc_mix(uint64_t seed, uint64_t s, uint64_t k)
+{
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * ((s << 32) + k + 1ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+double orc_mc_z(uint64_t seed, uint64_t s, uint64_t k)
+{
+    uint64_t X = orc_mc_mix(seed, s, k);
+    double w = ((double)(X >> 12) + 0.5) * 0x1p-52;
+    return w <= 0.5 ? orc_Phiinv_lower(w) : -orc_Phiinv_lower(1.0 - w);
+}
+
+int orc_mc_first(long long n, const double *L, long long ldl, const double *a, uint64_t seed, long long s0,
+                 long long ns, int *first, double *margin, double *min_gap, int nthreads)
+{
+    int err = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel for schedule(dynamic, 16) reduction(| : err)
+    for (long long s = 0; s < ns; ++s) {
+        double *z = (double *)malloc(sizeof(double) * (size_t)n);
+        if (!z) { err |= 1; continue; }
+        int f = (int)n;
+        double gap = INFINITY;            /* smallest |x_k - a_k| over rows k <= f */
+        double mg = 0.0;
+        for (long long k = 0; k < n; ++k) {
+            z[k] = orc_mc_z(seed, (uint64_t)(s0 + s), (uint64_t)k);
+            const double *Lk = L + k * ldl;
+            double x = 0.0;
+            for (long long t = 0; t <= k; ++t) x += Lk[t] * z[t];
+            double d = fabs(x - a[k]) / (1.0 + fabs(a[k]));
+            if (d < gap) gap = d;
+            if (!(x > a[k])) { f = (int)k; mg = x - a[k]; break; }
+        }
+        first[s] = f;
+        if (margin) margin[s] = mg;
+        if (min_gap) min_gap[s] = gap;
+        free(z);
+    }
+    return err;
+}

@@ -32,7 +32,7 @@ ABI_SYMBOLS = [
     "mvn_marginal_order", "mvn_cov_matern", "mvn_potrf", "mvn_lattice_generators",
     "mvn_lattice_shifts", "mvn_sov_prefix", "mvn_prefix_rescale", "mvn_prefix_finalize",
     "mvn_confidence_region", "mvn_crd", "mvn_potrf_panel", "mvn_potrf_update", "mvn_panel_pack",
-    "mvn_panel_unpack", "mvn_potrf_info",
+    "mvn_panel_unpack", "mvn_potrf_info", "mvn_mc_validate", "mvn_mc_levels",
 ]
 
 
@@ -49,6 +49,10 @@ class mvn_tiles(ctypes.Structure):
 class mvn_qmc(ctypes.Structure):
     _fields_ = [("N", ctypes.c_int64), ("R", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("sample_begin", ctypes.c_int64), ("sample_end", ctypes.c_int64)]
+
+
+class mvn_mc(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("sample_begin", ctypes.c_int64), ("sample_end", ctypes.c_int64)]
 
 
 class mvn_crd_problem(ctypes.Structure):
@@ -104,6 +108,8 @@ def lib() -> ctypes.CDLL:
         "mvn_panel_pack": (S, [P, T, P, I64, P]),
         "mvn_panel_unpack": (S, [P, T, P, I64, P]),
         "mvn_potrf_info": (S, [P, ctypes.POINTER(I64), I32]),
+        "mvn_mc_validate": (S, [P, T, P, P, ctypes.POINTER(mvn_mc), P, P]),
+        "mvn_mc_levels": (S, [I64, P, I64, P, I64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -326,6 +332,34 @@ def mvn_confidence_region(logP: np.ndarray, conf):
     if st != MVN_OK:
         raise MvnError(st, "mvn_confidence_region")
     return k, tie.astype(bool)
+
+
+# ---- NEXT-2: Monte-Carlo validation of the regions
+def mvn_mc_validate(L, n: int, a, seed: int, begin: int, end: int, count=None, first=None):
+    """Draws samples [begin, end) of mu + L z (reading R20) and accumulates the histogram of their
+    first failing rows into `count` (CUDA uint64, n+1; created zeroed if None). `first`: optional
+    CUDA int32 of end-begin, receives f_s. Returns count."""
+    import torch
+    c = Context.get(L.device.index)
+    if count is None:
+        count = torch.zeros(n + 1, dtype=torch.uint64, device=L.device)
+    m = mvn_mc(int(seed), int(begin), int(end))
+    c.check(lib().mvn_mc_validate(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64), ctypes.byref(m),
+                                  _dev_ptr(count, torch.uint64), None if first is None else _dev_ptr(first, torch.int32)),
+            "mvn_mc_validate")
+    return count
+
+
+def mvn_mc_levels(count: np.ndarray, N_total: int, k_star) -> np.ndarray:
+    """p_hat(k*) = #{f >= k*} / N_total (host)."""
+    cnt = np.ascontiguousarray(count, dtype=np.uint64)
+    ks = np.ascontiguousarray(k_star, dtype=np.int64)
+    out = np.empty(len(ks))
+    st = lib().mvn_mc_levels(cnt.shape[0] - 1, _np_ptr(cnt), int(N_total), _np_ptr(ks) if ks.size else None, len(ks),
+                             _np_ptr(out) if ks.size else None)
+    if st != MVN_OK:
+        raise MvnError(st, "mvn_mc_levels")
+    return out
 
 
 @dataclass

@@ -27,6 +27,9 @@ struct mvn_ctx {
     // mvn_crd buffers
     void *crd_L = nullptr; size_t crd_L_cap = 0;
     void *crd_vec = nullptr; size_t crd_vec_cap = 0;
+    // mvn_mc_validate
+    void *mcZ = nullptr; size_t mcZ_cap = 0;
+    void *mcF = nullptr; size_t mcF_cap = 0;
 };
 
 namespace {
@@ -139,7 +142,7 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
     c->device = device;
     c->nsm = prop.multiProcessorCount;
     c->stream = (cudaStream_t)cuda_stream;
-    if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess ||
+    if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess || mvn::mc_init() != cudaSuccess ||
         cudaMalloc(&c->d_info, sizeof(int64_t)) != cudaSuccess) {
         delete c;
         return MVN_E_CUDA;
@@ -157,7 +160,7 @@ void mvn_destroy(mvn_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (void *p : {c->Y, c->part, c->cta, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec})
+    for (void *p : {c->Y, c->part, c->cta, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF})
         if (p) cudaFree(p);
     delete c;
 }
@@ -173,9 +176,9 @@ const char *mvn_last_error(const mvn_ctx *c) { return c ? c->err.c_str() : "null
 mvn_status mvn_trim(mvn_ctx *c) {
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->cta, &c->crd_L, &c->crd_vec})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF})
         if (*p) { cudaFree(*p); *p = nullptr; }
-    c->Y_cap = c->part_cap = c->cta_cap = c->crd_L_cap = c->crd_vec_cap = 0;
+    c->Y_cap = c->part_cap = c->cta_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
     return MVN_OK;
 }
 
@@ -365,6 +368,42 @@ mvn_status mvn_confidence_region(int64_t n, const double *logP, const double *co
         k_out[i] = k;
         if (near_tie)
             near_tie[i] = ((k > 0 && std::fabs(lp[k - 1] - lc) <= 1e-8) || (k < n && std::fabs(lp[k] - lc) <= 1e-8)) ? 1 : 0;
+    }
+    return MVN_OK;
+}
+
+mvn_status mvn_mc_validate(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const mvn_mc *m,
+                           uint64_t *d_count, int32_t *d_first) {
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !d_L || !d_a || !m || !d_count || m->sample_begin < 0 || m->sample_end <= m->sample_begin)
+        return fail(c, MVN_E_USAGE, "mvn_mc_validate: bad arguments (need nb=128, 0 <= begin < end)");
+    const int64_t total = m->sample_end - m->sample_begin;
+    const int64_t n_pad = (t.n + t.nb - 1) / t.nb * t.nb;
+    // chunk: as many 128-sample blocks as fit ~8 GB of Z, at least one
+    const int64_t per_blk = mvn::mc_z_doubles(t.n, 128) * (int64_t)sizeof(double);
+    int64_t blocks = std::max<int64_t>(1, (int64_t)(8ll << 30) / per_blk);
+    int64_t chunk = std::min<int64_t>(total, blocks * 128);
+    (void)n_pad;
+    mvn_status s;
+    if ((s = ensure(c, &c->mcZ, &c->mcZ_cap, (size_t)mvn::mc_z_doubles(t.n, chunk) * sizeof(double))) != MVN_OK) return s;
+    if (!d_first && (s = ensure(c, &c->mcF, &c->mcF_cap, (size_t)chunk * sizeof(int32_t))) != MVN_OK) return s;
+    for (int64_t s0 = 0; s0 < total; s0 += chunk) {
+        const int64_t ns = std::min(chunk, total - s0);
+        int *first = d_first ? (int *)d_first + s0 : (int *)c->mcF;
+        MVN_CUDA(c, mvn::launch_mc_chunk(t.n, d_L, d_a, m->seed, m->sample_begin + s0, ns, (double *)c->mcZ, first,
+                                         (unsigned long long *)d_count, c->nsm, c->stream));
+    }
+    return MVN_OK;
+}
+
+mvn_status mvn_mc_levels(int64_t n, const uint64_t *count, int64_t N_total, const int64_t *k_star, int64_t nconf,
+                         double *p_hat) {
+    if (n < 1 || !count || N_total < 1 || nconf < 0 || (nconf > 0 && (!k_star || !p_hat))) return MVN_E_USAGE;
+    std::vector<uint64_t> tail((size_t)n + 2, 0);
+    for (int64_t k = n; k >= 0; --k) tail[(size_t)k] = tail[(size_t)k + 1] + count[k];
+    for (int64_t i = 0; i < nconf; ++i) {
+        if (k_star[i] < 0 || k_star[i] > n) return MVN_E_USAGE;
+        p_hat[i] = (double)tail[(size_t)k_star[i]] / (double)N_total;
     }
     return MVN_OK;
 }

@@ -41,4 +41,10 @@ int sov_y_stride();
 int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta);
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
 
+// NEXT-2: Monte-Carlo validation
+cudaError_t mc_init();
+int64_t mc_z_doubles(int64_t n, int64_t ns);
+cudaError_t launch_mc_chunk(int64_t n, const double *tiles, const double *a, uint64_t seed, int64_t s0, int64_t ns,
+                            double *Z, int *first, unsigned long long *count, int nsm, cudaStream_t st);
+
 }  // namespace mvn

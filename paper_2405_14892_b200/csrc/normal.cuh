@@ -17,12 +17,12 @@ __device__ __forceinline__ double Phi_lo(double x) { return 0.5 * erfc(-x * kRsq
 __device__ __forceinline__ double Phi_hi(double x) { return 0.5 * erfc(x * kRsqrt2); }    // P(Z > x)
 
 // log P(Z > x) for x >= kFarTail: P(Z > x) = erfcx(x/sqrt2)/2 * exp(-x^2/2)
-__device__ __noinline__ double log_Phi_hi_far(double x) { return log(0.5 * erfcx(x * kRsqrt2)) - 0.5 * x * x; }
+static __device__ __noinline__ double log_Phi_hi_far(double x) { return log(0.5 * erfcx(x * kRsqrt2)) - 0.5 * x * x; }
 
 // Solve log P(Z > y) = T for y >= x0 (x0 >= kFarTail, log P(Z > x0) >= T). Newton from the left
 // end point; the function is concave decreasing, so after one step the iterates decrease
 // monotonically onto the root and stay in the far-tail domain.
-__device__ __noinline__ double Phi_hi_inv_far(double T, double x0) {
+static __device__ __noinline__ double Phi_hi_inv_far(double T, double x0) {
     double y = x0;
     for (int it = 0; it < 60; ++it) {
         double g = log_Phi_hi_far(y) - T;
@@ -34,7 +34,7 @@ __device__ __noinline__ double Phi_hi_inv_far(double T, double x0) {
     return y;
 }
 
-__device__ __noinline__ void sov_step_far_upper(double ap, double bp, double w, double &logq, double &y) {
+static __device__ __noinline__ void sov_step_far_upper(double ap, double bp, double w, double &logq, double &y) {
     double la = log_Phi_hi_far(ap);
     double lb = isinf(bp) ? -CUDART_INF : log_Phi_hi_far(bp);
     logq = isinf(lb) ? la : la + log1p(-exp(lb - la));

@@ -1,0 +1,136 @@
+"""NEXT-2 on the GPU: mvn_mc_validate (Monte-Carlo validation of the regions) against the
+oracle (oracle/mcval.py) on the same seeded draws (reading R20).
+
+Per-sample first failing rows f_s are integers decided by floating point: the GPU forms (L z)_k
+with DMMA sums, the oracle with an ascending dot, and z comes from two independent Phi^{-1}
+implementations (AS 241 vs Halley), so a decision x_k <= a_k may legitimately differ where
+|x_k - a_k| is at rounding level. The bar: f_s identical for every sample whose oracle margin
+min_k |x_k - a_k| / (1 + |a_k|) over the rows it examined exceeds 1e-9; the histogram equals the
+bincount of the GPU's own f_s exactly; p_hat levels follow from the histogram exactly."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+GAP = 1e-9
+
+
+@pytest.fixture(scope="module")
+def torch(cuda_device):
+    import torch as t
+    return t
+
+
+def mvn():
+    import paper_2405_14892_b200 as m
+    return m
+
+
+def dense(T, n):
+    return mvn().mvn_unpack_lower(T, n).T.contiguous().cpu().numpy()
+
+
+def factor(torch, cfg):
+    inp = W.make_inputs(cfg)
+    var = np.full(cfg.n, cfg.sigma2 + cfg.nugget)
+    order, a, _ = oracle.marginal_order(inp.mu, var, cfg.u)
+    T = mvn().mvn_cov_matern(torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda(), cfg.sigma2, cfg.beta,
+                             cfg.nu, cfg.nugget)
+    assert mvn().mvn_potrf(T, cfg.n) == -1
+    return T, a
+
+
+def gpu_first(torch, T, n, a, seed, begin, end):
+    d_a = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    first = torch.empty(end - begin, dtype=torch.int32, device="cuda")
+    count = mvn().mvn_mc_validate(T, n, d_a, seed, begin, end, first=first)
+    return first.cpu().numpy(), count.cpu().numpy().astype(np.int64)
+
+
+def check_against_oracle(fg, L, a, seed, begin, end):
+    fo, _, gap = oracle.mc_first(L, a, seed, begin, end - begin, nthreads=16, diagnostics=True)
+    diff = fg != fo
+    assert not np.any(diff & (gap > GAP)), np.flatnonzero(diff & (gap > GAP))[:10]
+    return fo, int(diff.sum())
+
+
+@pytest.mark.parametrize("g,base,begin,end", [(20, "A", 0, 4096), (9, "A", 5, 700), (23, "C", 1000, 3333),
+                                              (11, "A", 0, 129)])
+def test_mc_first_vs_oracle(torch, g, base, begin, end):
+    cfg = W.small_config(f"mc{g}", g, 100, 1, base=base)
+    T, a = factor(torch, cfg)
+    n = cfg.n
+    fg, count = gpu_first(torch, T, n, a, 1234, begin, end)
+    assert np.array_equal(count, np.bincount(fg, minlength=n + 1))
+    fo, nd = check_against_oracle(fg, dense(T, n), a, 1234, begin, end)
+    assert nd <= max(1, (end - begin) // 1000)
+
+
+def test_mc_multiple_row_tiles_and_far_rows(torch):
+    """n = 1,000 (8 row tiles, ragged last) with limits pushed low so that draws survive deep into
+    the sweep and the later row tiles decide."""
+    cfg = W.small_config("mc-deep", 31, 100, 1, base="A")   # n = 961
+    T, a = factor(torch, cfg)
+    n = cfg.n
+    a = a - 3.5
+    fg, count = gpu_first(torch, T, n, a, 77, 0, 2000)
+    assert fg.max() > 600                                   # the deep tiles were exercised
+    check_against_oracle(fg, dense(T, n), a, 77, 0, 2000)
+
+
+def test_mc_chunks_accumulate_and_split(torch):
+    cfg = W.small_config("mc-split", 15, 100, 1, base="A")
+    T, a = factor(torch, cfg)
+    n = cfg.n
+    d_a = torch.from_numpy(a).cuda()
+    c1 = mvn().mvn_mc_validate(T, n, d_a, 5, 0, 3000)
+    c2 = mvn().mvn_mc_validate(T, n, d_a, 5, 0, 1111)
+    mvn().mvn_mc_validate(T, n, d_a, 5, 1111, 3000, count=c2)
+    assert torch.equal(c1, c2)
+    c3 = mvn().mvn_mc_validate(T, n, d_a, 5, 0, 3000)
+    assert torch.equal(c1, c3)                                # deterministic
+
+
+def test_mc_identity_closed_form(torch):
+    n, N = 300, 100_000
+    T = mvn().mvn_pack_lower(torch.from_numpy(np.eye(n)).cuda(), n)
+    a = np.full(n, -2.5)
+    a[:3] = [-0.5, 0.0, -1.0]
+    cnt = mvn().mvn_mc_validate(T, n, torch.from_numpy(a).cuda(), 3, 0, N).cpu().numpy()
+    from scipy.special import ndtr
+    ks = [1, 2, 3, 10, 100, 300]
+    ph = mvn().mvn_mc_levels(cnt, N, ks)
+    for k, p_hat in zip(ks, ph):
+        p = float(np.prod(1 - ndtr(a[:k])))
+        assert abs(p_hat - p) <= 4 * math.sqrt(p * (1 - p) / N) + 1e-12, (k, p_hat, p)
+
+
+def test_mc_levels_host():
+    cnt = np.array([3, 0, 2, 5], dtype=np.uint64)
+    assert list(mvn().mvn_mc_levels(cnt, 10, [0, 1, 2, 3])) == [1.0, 0.7, 0.7, 0.5]
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_mc_levels(cnt, 10, [4])
+
+
+@pytest.mark.slow
+def test_mc_full_config_D_sampled(torch):
+    """Config D (n = 65,536) at full size: 2,048 draws through the bench launch configuration; the
+    oracle decides each draw from the leading 4,096 x 4,096 block of L (a draw whose first failure
+    lies in the block is decided there; the GPU must then agree; draws that survive the block
+    must also survive it on the GPU)."""
+    import test_gpu_parity as P
+    cfg = W.CONFIGS["D"]
+    T, a = factor(torch, cfg)
+    n, m = cfg.n, 4096
+    fg, count = gpu_first(torch, T, n, a, 42, 10_000, 12_048)
+    Lm = P.leading_block(T, n, m)
+    fo, _, gap = oracle.mc_first(Lm, a[:m], 42, 10_000, 2048, nthreads=16, diagnostics=True)
+    decided = fo < m
+    assert decided.mean() > 0.9
+    bad = decided & (fg != fo) & (gap > GAP)
+    assert not np.any(bad)
+    assert np.all(fg[~decided] >= m)
