@@ -35,6 +35,17 @@ METRIC = "SOV-QMC n·N sample-dims/s"
 UNIT = "sample-dims/s"
 
 
+def committed_traffic(cfg_name: str, kernel: str):
+    """DRAM bytes per launch of `kernel` at this config from the committed ncu capture
+    (profiles/traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(cfg_name)
+        return float(t["bytes"]) if t and t.get("kernel") == kernel else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -164,6 +175,92 @@ def run_reference(args, cfg):
     return 0
 
 
+# --------------------------------------------------------------------------------- NEXT-2 workload
+def mc_chunks(n: int, draws: int) -> int:
+    """Chunks mvn_mc_validate splits `draws` into (as many 128-draw blocks as fit 8 GiB of Z)."""
+    n_pad = -(-n // 128) * 128
+    blocks = max(1, (8 << 30) // (n_pad * 132 * 8))
+    return -(-draws // (blocks * 128))
+
+
+def run_mc(args, cfg):
+    """MC validation of the regions on one workload: untimed cov + potrf + one CRD sweep for
+    the regions k*, then K timed passes of mvn_mc_validate over --mc-samples draws (sharded over
+    the ranks, counts all_reduce'd). Prints one JSON line (not the driver's headline)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200 import parallel
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    inp = W.make_inputs(cfg)
+    n = cfg.n
+    var = np.full(n, cfg.sigma2 + cfg.nugget)
+    order, a, _ = mvn.mvn_marginal_order(inp.mu, var, cfg.u)
+    d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+    d_a = torch.from_numpy(a).cuda()
+    L = mvn.alloc_tiles(n)
+    logp = parallel.crd_step(d_xy, d_a, L, cfg, potrf=args.potrf)      # untimed: L and the regions
+    k_star, _ = mvn.mvn_confidence_region(logp.cpu().numpy(), cfg.conf)
+    Ns = args.mc_samples
+    b, e = parallel.shard_range(Ns, rank, world)
+    count = torch.zeros(n + 1, dtype=torch.uint64, device="cuda")
+    for _ in range(args.warmup):
+        count.zero_()
+        mvn.mvn_mc_validate(L, n, d_a, 777, b, e, count=count)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ms = []
+    for _ in range(args.steps):
+        count.zero_()
+        ev0.record()
+        mvn.mvn_mc_validate(L, n, d_a, 777, b, e, count=count)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms.append(ev0.elapsed_time(ev1))
+    clk = clocks.stop()
+    t = float(np.sum(ms))
+    if world > 1:
+        c64 = count.to(torch.int64)
+        dist.all_reduce(c64)
+        count = c64
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    ms_step = t / args.steps
+    p_hat = mvn.mvn_mc_levels(count.cpu().numpy().astype(np.uint64), Ns, k_star)
+    flops = float(n) * (n + 1) * (e - b)
+    achieved = flops / (ms_step / 1e3) / 1e12
+    line = {"metric": "MC validation draw-dims/s (NEXT-2)", "value": n * Ns / (ms_step / 1e3), "unit": "draw-dims/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {cfg.name}: MC validation, {Ns} draws of mu + L z", "n": n, "draws": Ns},
+            "roofline": {"kernel": "k_mc_trmm (X = L Z on DMMA + first-failure epilogue)", "bound": "tensor",
+                         "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
+                         "algorithmic": f"n(n+1) flops per draw x {e - b} draws"},
+            "levels": [float(c) for c in cfg.conf], "k_star": [int(k) for k in k_star],
+            "p_hat": [float(p) for p in p_hat],
+            "one_minus_alpha_minus_p_hat": [float(c - p) for c, p in zip(cfg.conf, p_hat)],
+            "mc_se": [float(math.sqrt(max(p * (1 - p), 0.0) / Ns)) for p in p_hat],
+            "clocks": clk, "gpu_launches": 4 * args.steps * mc_chunks(n, e - b)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # --------------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -176,10 +273,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--potrf", default="auto", choices=["auto", "rank0", "dist"],
                     help="N>1: factor on rank 0 + broadcast L, or distributed (NEXT-1); auto = dist")
+    ap.add_argument("--workload", default="crd", choices=["crd", "mc"],
+                    help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions")
+    ap.add_argument("--mc-samples", type=int, default=50_000, help="--workload mc: draws (paper: N = 50,000, P:595)")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.workload == "mc":
+        return run_mc(args, cfg)
 
     import torch
     import torch.distributed as dist
@@ -321,7 +423,7 @@ def main():
         "stage_ms": stage_mean,
         "roofline": {"kernel": "k_sov (SOV DMMA GEMM + Phi chain)", "bound": "tensor", "achieved": achieved,
                      "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
-                     "traffic": None,
+                     "traffic": committed_traffic(cfg.name, "k_sov"),
                      "peak_source": "measured fp64 DMMA peak (tools/calib_fp64.cu, profiles/r01_fp64_calibration.md); "
                                     "MEASURED_PEAKS.json has no fp64 entry",
                      "algorithmic": f"n(n-1) flops per sample x {my_samples} samples"},

@@ -173,7 +173,7 @@ def potrf_dist_schedule(ops, rank: int, world: int):
             first = owned_first(k + 1, rank, world)
             if first == k + 1 and rank == owner(k + 1):
                 first += world
-            ops.update(k, first, world, "main")
+            ops.update(k, first, world, "main", side_busy=(rank == owner(k + 1)))
     ops.join()
 
 
@@ -215,10 +215,11 @@ class CudaPotrfOps:
         from . import mvn_panel_unpack
         mvn_panel_unpack(self.panel_buf(k), self.n, k, self.L, stream=self._st(on))
 
-    def update(self, k, c0, cs, on):
+    def update(self, k, c0, cs, on, side_busy=True):
         from . import mvn_potrf_update
         if c0 < self.nt:
-            mvn_potrf_update(self.L, self.n, k, c0, cs, self.SIDE_SMS if on == "main" else 0, stream=self._st(on))
+            reserve = self.SIDE_SMS if (on == "main" and side_busy) else 0
+            mvn_potrf_update(self.L, self.n, k, c0, cs, reserve, stream=self._st(on))
 
     def record(self, on):
         ev = self.torch.cuda.Event()

@@ -65,7 +65,7 @@ class NumpyPotrfOps:
         for i in range(k, self.nt):
             self.T[tidx(i, k)] = self.bufs[k & 1][i - k]
 
-    def update(self, k, c0, cs, on):
+    def update(self, k, c0, cs, on, side_busy=True):
         self.log.append(("update", k, c0, cs, on))
         for j in range(c0, self.nt, cs):
             for i in range(j, self.nt):
