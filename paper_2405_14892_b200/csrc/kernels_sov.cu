@@ -54,6 +54,27 @@ __device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, i
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes));
 }
 
+// L2 residency: the L panel is shared by every CTA (keep it: evict_last), the Y history is private
+// streaming data read once per row block (evict_first), so the L rows of the current row blocks
+// survive the ~2 TB/s of Y traffic that passes through L2.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void cp_async16_hint(void *smem, const void *gmem, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "l"(pol));
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, unsigned bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ uint64_t lattice_shift(uint64_t seed, uint64_t r, uint64_t k) {
     // SplitMix64 output function of the counter seed + GAMMA * (r*2^32 + k + 1) (reading R8)
     uint64_t z = seed + 0x9E3779B97F4A7C15ull * ((r << 32) + k + 1ull);
@@ -79,6 +100,12 @@ struct SovArgs {
     int64_t n_pad;            // Y-history rows per slot (nrb*64)
     double *Y;                // [grid][n_pad][SB] (row stride SB: padded for conflict-free DMMA loads)
     double *part;             // [nblk][n_pad][2]
+    // soft grid lockstep (L panel reuse in L2): producer of step s = b*nrb + rb waits until every CTA
+    // that has step s - lag has issued it; step_done[s] counts issuers, need[b] = CTAs with > b blocks.
+    int lag;                  // 0 = off
+    int *step_done;           // [max blocks][nrb]
+    const int *need;          // [max blocks]
+    int hints;                // L2 cache-policy hints on the producer's copies
 };
 
 __device__ __forceinline__ int block_width(int64_t count, int b) {
@@ -98,11 +125,28 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
     uint64_t *empty = full + STAGES;
     uint32_t q = 0;
+    const uint64_t pol_L = policy_evict_last(), pol_Y = policy_evict_first();
     for (int b = 0; b < nblk; ++b) {
         const int w = (block_width(count, b) + 31) & ~31;
+        if (p.lag > 0 && lane == 0) atomicAdd(p.step_done + (int64_t)b * p.nrb, 1);   // row block 0: no GEMM
         for (int rb = 1; rb < p.nrb; ++rb) {
             const int64_t row0 = (int64_t)rb * M;
             const int R = (int)(row0 / kTile), hh = (int)(row0 % kTile);
+            if (p.lag > 0) {
+                const int64_t s_wait = (int64_t)b * p.nrb + rb - p.lag;
+                if (lane == 0 && s_wait >= 0) {
+                    const int bw = (int)(s_wait / p.nrb);
+                    const int need = p.need[bw];
+                    const int *cnt = p.step_done + s_wait;
+                    int v;
+                    while (true) {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+                        if (v >= need) break;
+                        __nanosleep(100);
+                    }
+                }
+                __syncwarp();
+            }
             for (int c = 0; c < CPB * rb; ++c, ++q) {
                 if (c == CPB * (rb - 1)) named_sync(BAR_YREADY, N_YREADY);   // Y_{rb-1} published
                 const int st = q % STAGES;
@@ -113,16 +157,23 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
                 // A: 16 L columns x 64 rows (512 B each, 1 KB apart) by cp.async, one 16 B piece per lane
                 const int T = (int)(kc / kTile), cc = (int)(kc % kTile);
                 const double *Lsrc = p.L + tile_offset(R, T) + (int64_t)cc * kTile + hh + lane * 2;
+                if (p.hints) {
 #pragma unroll
-                for (int t = 0; t < BK; ++t) cp_async16(as + t * SA + lane * 2, Lsrc + (int64_t)t * kTile);
+                    for (int t = 0; t < BK; ++t) cp_async16_hint(as + t * SA + lane * 2, Lsrc + (int64_t)t * kTile, pol_L);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < BK; ++t) cp_async16(as + t * SA + lane * 2, Lsrc + (int64_t)t * kTile);
+                }
                 cp_async_mbar_arrive(&full[st]);
                 __syncwarp();
                 // B: 16 Y-history rows, contiguous thanks to the padded row stride SB: one TMA bulk copy
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[st], BK * SB * 8);
-                    bulk_g2s(bs, Yslot + kc * SB, BK * SB * 8, &full[st]);
+                    if (p.hints) bulk_g2s_hint(bs, Yslot + kc * SB, BK * SB * 8, &full[st], pol_Y);
+                    else bulk_g2s(bs, Yslot + kc * SB, BK * SB * 8, &full[st]);
                 }
             }
+            if (p.lag > 0 && lane == 0) atomicAdd(p.step_done + (int64_t)b * p.nrb + rb, 1);
         }
         named_sync(BAR_YREADY, N_YREADY);                     // the block's last chain is done
     }
@@ -415,6 +466,11 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
     SovArgs a;
     a.L = L.L; a.n = L.n; a.nrb = (int)((L.n + 63) / 64); a.a = L.a; a.b = L.b; a.G = L.G; a.N = L.N;
     a.seed = L.seed; a.cta = L.cta; a.n_pad = (int64_t)a.nrb * 64; a.Y = L.Y; a.part = L.part;
+    a.lag = L.lag; a.step_done = L.step_done; a.need = L.need; a.hints = L.hints;
+    if (a.lag > 0) {
+        cudaError_t e = cudaMemsetAsync(L.step_done, 0, sizeof(int) * (size_t)L.max_blocks * a.nrb, st);
+        if (e != cudaSuccess) return e;
+    }
     if (L.b) k_sov<true><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
     else k_sov<false><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
     cudaError_t e = cudaGetLastError();

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -22,6 +23,7 @@ struct mvn_ctx {
     void *Y = nullptr; size_t Y_cap = 0;
     void *part = nullptr; size_t part_cap = 0;
     void *cta = nullptr; size_t cta_cap = 0;
+    void *sync = nullptr; size_t sync_cap = 0;   // SOV lockstep counters + need[]
     uint64_t *G = nullptr; int64_t G_n = 0;
     int64_t *d_info = nullptr;
     // mvn_crd buffers
@@ -160,7 +162,7 @@ void mvn_destroy(mvn_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (void *p : {c->Y, c->part, c->cta, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF})
+    for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF})
         if (p) cudaFree(p);
     delete c;
 }
@@ -176,9 +178,9 @@ const char *mvn_last_error(const mvn_ctx *c) { return c ? c->err.c_str() : "null
 mvn_status mvn_trim(mvn_ctx *c) {
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->cta, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF})
         if (*p) { cudaFree(*p); *p = nullptr; }
-    c->Y_cap = c->part_cap = c->cta_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
+    c->Y_cap = c->part_cap = c->cta_cap = c->sync_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
     return MVN_OK;
 }
 
@@ -331,6 +333,23 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
     if ((s = ensure(c, &c->Y, &c->Y_cap, (size_t)L.grid * n_pad * ys * sizeof(double))) != MVN_OK) return s;
     if ((s = ensure(c, &c->part, &c->part_cap, (size_t)L.nblk * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
     if ((s = ensure(c, &c->cta, &c->cta_cap, cta.size() * sizeof(int64_t))) != MVN_OK) return s;
+    // soft lockstep: need[b] = CTAs with more than b sample blocks; counters [max_blocks][nrb]
+    static const int env_lag = [] { const char *e = getenv("MVN_SOV_LAG"); return e ? atoi(e) : 2; }();
+    static const int env_hints = [] { const char *e = getenv("MVN_SOV_HINTS"); return e ? atoi(e) : 1; }();
+    const int bs = mvn::sov_block_samples();
+    int max_blocks = 0;
+    for (int g = 0; g < L.grid; ++g) max_blocks = std::max<int>(max_blocks, (int)((cta[3 * g + 1] + bs - 1) / bs));
+    std::vector<int> sync_host((size_t)max_blocks, 0);
+    for (int g = 0; g < L.grid; ++g)
+        for (int b = 0; b < (int)((cta[3 * g + 1] + bs - 1) / bs); ++b) ++sync_host[(size_t)b];
+    const int64_t nrb = (t.n + 63) / 64;
+    const size_t sync_bytes = sizeof(int) * ((size_t)max_blocks * nrb + max_blocks);
+    if ((s = ensure(c, &c->sync, &c->sync_cap, sync_bytes)) != MVN_OK) return s;
+    int *d_sync = (int *)c->sync;
+    MVN_CUDA(c, cudaMemcpyAsync(d_sync + (size_t)max_blocks * nrb, sync_host.data(), sizeof(int) * max_blocks,
+                                cudaMemcpyHostToDevice, c->stream));
+    L.lag = env_lag; L.step_done = d_sync; L.need = d_sync + (size_t)max_blocks * nrb; L.max_blocks = max_blocks;
+    L.hints = env_hints;
     MVN_CUDA(c, cudaMemcpyAsync(c->cta, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     L.cta = (const int64_t *)c->cta;
     L.Y = (double *)c->Y; L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S;

@@ -34,6 +34,11 @@ struct SovLaunch {
     double *Y;           // [grid][ceil(n/64)*64][sov_y_stride()]
     double *part;    // [nblk][ceil(n/64)*64][2]
     double *Mout, *Sout;
+    int lag = 0;             // soft grid lockstep distance in row blocks (0 = off)
+    int *step_done = nullptr;  // [max_blocks][nrb] counters (zeroed by launch_sov)
+    const int *need = nullptr; // [max_blocks]: CTAs with more than b blocks
+    int max_blocks = 0;
+    int hints = 1;           // L2 cache-policy hints
 };
 cudaError_t sov_init();
 int sov_block_samples();

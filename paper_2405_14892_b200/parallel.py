@@ -256,7 +256,9 @@ def potrf_distributed(L, n: int, group=None, ops=None) -> int:
     while req is not None:
         _, k, src = req
         h = None
-        if world > 1:
+        if world == 1:
+            h = ops.record("side")               # the panel chain ran on the side stream
+        else:
             buf = ops.panel_buf(k)
             if getattr(ops, "side", None) is not None:
                 with torch.cuda.stream(ops.side):
