@@ -111,23 +111,58 @@ __device__ __forceinline__ void sov_step(double ap, double bp, double w, double 
     y = (plo < phi) ? Phi_inv_lower(plo) : -Phi_inv_lower(phi);
 }
 
+// Phi^{-1}(p) for 0 < p <= 1/2, the same AS 241 rational approximations as Phi_inv_lower but
+// evaluated without branches: the central and the tail forms are both computed and selected, the
+// two tail coefficient sets (r <= 5, r > 5) are selected per lane. In a warp whose lanes fall in
+// different regions this costs one evaluation of each form instead of a divergent replay, and it
+// needs one division instead of two.
+__device__ __forceinline__ double Phi_inv_lower_nb(double p) {
+    const double q = p - 0.5;
+    const double rc = 0.180625 - q * q;
+    const double numc = ((((((2.5090809287301226727e+3 * rc + 3.3430575583588128105e+4) * rc + 6.7265770927008700853e+4) * rc +
+                            4.5921953931549871457e+4) * rc + 1.3731693765509461125e+4) * rc + 1.9715909503065514427e+3) * rc +
+                          1.3314166789178437745e+2) * rc + 3.3871328727963666080e0;
+    const double denc = ((((((5.2264952788528545610e+3 * rc + 2.8729085735721942674e+4) * rc + 3.9307895800092710610e+4) * rc +
+                            2.1213794301586595867e+4) * rc + 5.3941960214247511077e+3) * rc + 6.8718700749205790830e+2) * rc +
+                          4.2313330701600911252e+1) * rc + 1.0;
+    const double rt = sqrt(-log(p));
+    const bool far = rt > 5.0;
+    const double x = rt - (far ? 5.0 : 1.6);
+#define MVN_SEL(a2, a3) (far ? (a3) : (a2))
+    const double numt =
+        ((((((MVN_SEL(7.74545014278341407640e-4, 2.01033439929228813265e-7) * x + MVN_SEL(2.27238449892691845833e-2, 2.71155556874348757815e-5)) * x +
+             MVN_SEL(2.41780725177450611770e-1, 1.24266094738807843860e-3)) * x + MVN_SEL(1.27045825245236838258e0, 2.65321895265761230930e-2)) * x +
+           MVN_SEL(3.64784832476320460504e0, 2.96560571828504891230e-1)) * x + MVN_SEL(5.76949722146069140550e0, 1.78482653991729133580e0)) * x +
+         MVN_SEL(4.63033784615654529590e0, 5.46378491116411436990e0)) * x + MVN_SEL(1.42343711074968357734e0, 6.65790464350110377720e0);
+    const double dent =
+        ((((((MVN_SEL(1.05075007164441684324e-9, 2.04426310338993978564e-15) * x + MVN_SEL(5.47593808499534494600e-4, 1.42151175831644588870e-7)) * x +
+             MVN_SEL(1.51986665636164571966e-2, 1.84631831751005468180e-5)) * x + MVN_SEL(1.48103976427480074590e-1, 7.86869131145613259100e-4)) * x +
+           MVN_SEL(6.89767334985100004550e-1, 1.48753612908506148525e-2)) * x + MVN_SEL(1.67638483018380384940e0, 1.36929880922735805310e-1)) * x +
+         MVN_SEL(2.05319162663775882187e0, 5.99832206555887937690e-1)) * x + 1.0;
+#undef MVN_SEL
+    const bool central = fabs(q) <= 0.425;
+    return (central ? q * numc : -numt) / (central ? denc : dent);
+}
+
 // Upper-exceedance fast path (b = +inf, every BASELINE config): Phibar(b') = 0.
+// One erfc for both signs of a' (t = Phibar(|a'|)), one log, one Phi^{-1} call site:
+//   a' >= 0: q = t,      log q = log t,             y = -Phi^{-1}((1-w) q)
+//   a' <  0: q = 1 - t,  log q = log1p(-t),          y = Phi^{-1}(min(t + w q, (1-w) q)) (signed)
+// log1p(-t) is formed as log(v) - delta (2 - v) with v = fl(1 - t) in [1/2, 1) and
+// delta = (v - 1) + t the exact rounding error of 1 - t (first-order correction; error <= 2^-55
+// absolute), so both signs share one log.
 __device__ __forceinline__ void sov_step_upper(double ap, double w, double &logq, double &y) {
     if (ap >= kFarTail) { sov_step_far_upper(ap, CUDART_INF, w, logq, y); return; }
-    double plo, phi;
-    if (ap >= 0.0) {
-        const double q = Phi_hi(ap);
-        logq = log(q);
-        plo = 1.0;                       // p_lo >= 1/2 >= p_hi: take the upper branch
-        phi = (1.0 - w) * q;
-    } else {
-        const double d = isinf(ap) ? 0.0 : Phi_lo(ap);
-        const double q = 1.0 - d;
-        logq = log1p(-d);               // q > 1/2 here
-        plo = d + w * q;
-        phi = (1.0 - w) * q;
-    }
-    y = (plo < phi) ? Phi_inv_lower(plo) : -Phi_inv_lower(phi);
+    const bool pos = ap >= 0.0;
+    const double t = isinf(ap) ? 0.0 : 0.5 * erfc(fabs(ap) * kRsqrt2);
+    const double v = pos ? t : 1.0 - t;                  // q
+    const double delta = pos ? 0.0 : (v - 1.0) + t;
+    logq = log(v) - delta * (2.0 - v);
+    const double phi = (1.0 - w) * v;
+    const double plo = pos ? 1.0 : t + w * v;            // a' >= 0: p_lo >= 1/2 >= p_hi
+    const bool lower = plo < phi;
+    const double r = Phi_inv_lower_nb(lower ? plo : phi);
+    y = lower ? r : -r;
 }
 
 }  // namespace mvn

@@ -68,3 +68,19 @@ def test_far_tail_threshold_consistent_with_oracle():
     k = float(re.search(r"kFarTail = ([0-9.]+)", SRC).group(1))
     osrc = open(os.path.join(ROOT, "oracle", "csrc", "oracle.c")).read()
     assert float(re.search(r"#define ORC_FAR_TAIL ([0-9.]+)", osrc).group(1)) == k == 35.0
+
+
+def test_branch_free_ppnd16_uses_same_coefficients():
+    """Phi_inv_lower_nb (the SOV fast path) selects per lane among the same AS 241 coefficient sets
+    as Phi_inv_lower (pinned above against mpmath)."""
+    ref = _blocks()
+    C, i = [], 0
+    for blk in range(3):
+        C.append(ref[i:i + 8]); i += 8
+        C.append(ref[i:i + 7]); i += 7
+    body = SRC[SRC.index("double Phi_inv_lower_nb"):SRC.index("// Upper-exceedance fast path")]
+    nums = [float(x) for x in re.findall(r"[0-9]\.[0-9]+e[+-]?[0-9]+", body)]
+    assert nums[:8] == C[0] and nums[8:15] == C[1]
+    sel = nums[15:]
+    assert sel[0:16:2] == C[2] and sel[1:16:2] == C[4]          # numerator: (r <= 5, r > 5) pairs
+    assert sel[16:30:2] == C[3] and sel[17:30:2] == C[5]        # denominator
