@@ -109,31 +109,40 @@ mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
 
 /* ---------------------------------------------------------------------------------------------
  * NEXT-1: building blocks of the distributed tiled Cholesky, 1-D
- * block-cyclic over tile columns (tile column j is owned by rank j mod W). The step loop and the
+ * block-cyclic over super-panels of kp tile columns (super-panel s = tile columns s*kp ..
+ * s*kp+kp-1 is owned by rank s mod W; kp = mvn_potrf_panel_width(), 2). The step loop and the
  * NCCL panel broadcasts are in the Python layer (paper_2405_14892_b200/parallel.py,
- * potrf_distributed); the right-looking recurrence is the one of mvn_potrf (Alg. 1 l.8, P:233;
- * the paper runs it distributed on Chameleon/StarPU). Per step k:
- *   owner(k):  mvn_potrf_panel(k)  -> mvn_panel_pack(k)  -> broadcast panel k
- *   others:    receive panel k     -> mvn_panel_unpack(k)
- *   all:       mvn_potrf_update(k, own columns > k)
- * A panel is the nt-k tiles (k..nt-1, k) stored contiguously: (nt-k) * nb*nb doubles, device.
- * All calls are asynchronous on the context's stream; pivots are checked on the device and
- * collected by mvn_potrf_info.                                                                  */
+ * potrf_distributed); the right-looking recurrence is the one of mvn_potrf, which is built from
+ * the same two calls (Alg. 1 l.8; the paper runs it distributed on Chameleon/StarPU, P:81,
+ * P:609-645), so both produce bit-identical factors. Per super-step s (k = s*kp):
+ *   owner(s):  mvn_potrf_panel(k, kp)  -> mvn_panel_pack(k, kp)  -> broadcast
+ *   others:    receive                 -> mvn_panel_unpack(k, kp)
+ *   all:       mvn_potrf_update(k, kp, own columns >= k+kp)
+ * A panel of (k, kp) is the tiles (k+j .. nt-1, k+j), j < kp, stored contiguously column after
+ * column: sum_j (nt-k-j) * nb*nb doubles, device. All calls are asynchronous on the context's
+ * stream; pivots are checked on the device and collected by mvn_potrf_info.                    */
 
-/* POTRF of diagonal tile k and TRSM of the tiles below it (A_ik <- A_ik L_kk^{-T}), in place.
- * Tile column k must already carry every update from panels 0..k-1. A non-positive pivot records
- * its 0-based global row in the context's device info (first failure only) and leaves the tile. */
-mvn_status mvn_potrf_panel(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t k);
+/* Tile columns per super-panel used by mvn_potrf (and expected by potrf_distributed). */
+int64_t mvn_potrf_panel_width(void);
 
-/* Trailing update with panel k: A_ij -= L_ik L_jk^T for every tile column j in
- * {col_first, col_first + col_stride, ...} (< nt) and every i >= j. Requires k < col_first and
- * col_stride >= 1. sm_reserve SMs are left free for concurrent panel work (0..nsm-1).          */
-mvn_status mvn_potrf_update(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t k, int64_t col_first,
-                            int64_t col_stride, int32_t sm_reserve);
+/* Factor the kp (1..4; clipped at nt) tile columns k .. k+kp-1 in place: POTRF of the diagonal tile
+ * and TRSM of the tiles below, column by column, each further column first updated with the
+ * previous columns of the super-panel. All updates from columns < k must have been applied. A
+ * non-positive pivot records its 0-based global row in the context's device info (first failure
+ * only) and leaves its tile.                                                                     */
+mvn_status mvn_potrf_panel(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t k, int64_t kp);
 
-/* Tile column k <-> contiguous panel buffer of (nt-k) * nb*nb doubles (device, caller-owned). */
-mvn_status mvn_panel_pack(mvn_ctx *ctx, mvn_tiles t, const double *d_tiles, int64_t k, double *d_panel);
-mvn_status mvn_panel_unpack(mvn_ctx *ctx, mvn_tiles t, const double *d_panel, int64_t k, double *d_tiles);
+/* Trailing update with the super-panel (k, kp): A_ij -= sum_{c=k}^{k+kp-1} L_ic L_jc^T for every
+ * i >= j and every tile column j = col_first + m*col_stride + b (m >= 0, 0 <= b < col_block, j < nt)
+ * — blocks of col_block columns every col_stride columns (1, 1: all columns from col_first).
+ * Requires k + kp <= col_first, 1 <= col_block <= col_stride. sm_reserve SMs are left free for
+ * concurrent panel work (0..nsm-1).                                                              */
+mvn_status mvn_potrf_update(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t k, int64_t kp, int64_t col_first,
+                            int64_t col_stride, int64_t col_block, int32_t sm_reserve);
+
+/* Super-panel (k, kp) <-> contiguous panel buffer (device, caller-owned, size above). */
+mvn_status mvn_panel_pack(mvn_ctx *ctx, mvn_tiles t, const double *d_tiles, int64_t k, int64_t kp, double *d_panel);
+mvn_status mvn_panel_unpack(mvn_ctx *ctx, mvn_tiles t, const double *d_panel, int64_t k, int64_t kp, double *d_tiles);
 
 /* Reads (synchronising the stream) the device info of mvn_potrf_panel: -1 if every pivot so far
  * was positive, else the first failing 0-based row. reset != 0 sets it back to -1 afterwards.  */
@@ -222,6 +231,38 @@ mvn_status mvn_mc_validate(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const d
  * N_total < 1 or a k_star is outside [0, n].                                                   */
 mvn_status mvn_mc_levels(int64_t n, const uint64_t *count, int64_t N_total, const int64_t *k_star, int64_t nconf,
                          double *p_hat);
+
+/* ---------------------------------------------------------------------------------------------
+ * NEXT-4: posterior conditioning before Alg. 1 (§V-A):
+ * m noisy observations y = A x + N(0, tau^2 I) of the field at sites obs give
+ *   Sigma_post = (Sigma^{-1} + tau^{-2} A^T A)^{-1}          (Eq. 7)
+ *   mu_post    = mu + tau^{-2} Sigma_post A^T (y - A mu)     (Eq. 8)
+ * which "can be used as input to Algorithm 1 (line 2) ... to update the a vector".
+ * Computed as the Schur complement left by a partial tiled Cholesky of the augmented matrix
+ * [[Sigma_oo + tau^2 I, Sigma_{o,:}, r], [Sigma_{:,o}, Sigma, 0], [r^T, 0, 1]], r = y - mu_o
+ * (reading R21): the trailing block is Sigma_post, the last row is -(mu_post - mu).
+ * Use: mvn_posterior -> mvn_marginal_order(mu_post, var_post, u) -> mvn_posterior_tiles(order)
+ * -> mvn_potrf -> mvn_sov_prefix -> ...                                                          */
+typedef struct {
+    int64_t n;             /* sites */
+    const double *xy;      /* host, n x 2 row-major, original order */
+    const double *mu;      /* host, n prior mean */
+    int64_t m;             /* observations, >= 1 */
+    const int64_t *obs;    /* host, m distinct site indices in [0, n) */
+    const double *y;       /* host, m observed values */
+    double sigma2, beta, nu, nugget;   /* Matérn of the field (Eq. 6, R14) */
+    double tau;            /* observation noise standard deviation (> 0; the paper uses 0.5) */
+} mvn_posterior_problem;
+
+/* Conditions the field; writes mu_post and var_post = diag(Sigma_post) (host, n each, original
+ * order) and keeps Sigma_post in the context's workspace ((m_pad + n + 1)^2 / 2 doubles, m_pad =
+ * m rounded up to 128) for mvn_posterior_tiles. *info (host): -1, or the first failing row of the
+ * observation block (MVN_E_NUMERIC). MVN_E_USAGE for bad sizes / indices / tau <= 0.            */
+mvn_status mvn_posterior(mvn_ctx *ctx, const mvn_posterior_problem *p, double *mu_post, double *var_post, int64_t *info);
+
+/* Writes Sigma_post permuted to `order` (host, n: sorted position -> site, e.g. from
+ * mvn_marginal_order) into the tile-packed d_tiles (t.n = the n of the last mvn_posterior).      */
+mvn_status mvn_posterior_tiles(mvn_ctx *ctx, mvn_tiles t, const int64_t *order, double *d_tiles);
 
 /* ---------------------------------------------------------------------------------------------
  * End-to-end CRD (Alg. 1) on one GPU with HOST buffers: upload, a1..a10, download.

@@ -175,3 +175,24 @@ def crd(xy, mu, sigma2, beta, nu, nugget, u, N, R, seed, conf, chunk=None, nthre
     logp = prefix_logp(M, Ssum, N * R)
     ks, ties = region(logp, conf)
     return CrdResult(order, a, L, logp, ks, ties, parts, info)
+
+
+def crd_cov(Sigma, mu, u, N, R, seed, conf, chunk=None, nthreads=0):
+    """Alg. 1 end to end for a given covariance in the original site order (e.g. Sigma_post of
+    Eq. 7 with mu_post of Eq. 8): marginals from diag(Sigma), order, Sigma permuted to sorted
+    order (R1), Cholesky, one sweep, regions."""
+    Sigma = np.asarray(Sigma, dtype=np.float64)
+    n = Sigma.shape[0]
+    order, a, _ = marginal_order(mu, np.diag(Sigma).copy(), u)
+    L, info = cholesky(Sigma[np.ix_(order, order)], nthreads)
+    if info >= 0:
+        raise FloatingPointError(f"Sigma not positive definite at row {info}")
+    b = np.full(n, np.inf)
+    G = generators(n)
+    D = shifts(seed, R, n)
+    chunk = chunk or N
+    parts = sov_units(L, a, b, G, D, N, R, chunk, nthreads=nthreads)
+    M, Ssum = combine_units(parts)
+    logp = prefix_logp(M, Ssum, N * R)
+    ks, ties = region(logp, conf)
+    return CrdResult(order, a, L, logp, ks, ties, parts, info)

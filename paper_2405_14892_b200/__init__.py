@@ -32,7 +32,8 @@ ABI_SYMBOLS = [
     "mvn_marginal_order", "mvn_cov_matern", "mvn_potrf", "mvn_lattice_generators",
     "mvn_lattice_shifts", "mvn_sov_prefix", "mvn_prefix_rescale", "mvn_prefix_finalize",
     "mvn_confidence_region", "mvn_crd", "mvn_potrf_panel", "mvn_potrf_update", "mvn_panel_pack",
-    "mvn_panel_unpack", "mvn_potrf_info", "mvn_mc_validate", "mvn_mc_levels",
+    "mvn_panel_unpack", "mvn_potrf_info", "mvn_mc_validate", "mvn_mc_levels", "mvn_potrf_panel_width",
+    "mvn_posterior", "mvn_posterior_tiles",
 ]
 
 
@@ -53,6 +54,13 @@ class mvn_qmc(ctypes.Structure):
 
 class mvn_mc(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("sample_begin", ctypes.c_int64), ("sample_end", ctypes.c_int64)]
+
+
+class mvn_posterior_problem(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("xy", ctypes.c_void_p), ("mu", ctypes.c_void_p), ("m", ctypes.c_int64),
+                ("obs", ctypes.c_void_p), ("y", ctypes.c_void_p), ("sigma2", ctypes.c_double),
+                ("beta", ctypes.c_double), ("nu", ctypes.c_double), ("nugget", ctypes.c_double),
+                ("tau", ctypes.c_double)]
 
 
 class mvn_crd_problem(ctypes.Structure):
@@ -103,13 +111,16 @@ def lib() -> ctypes.CDLL:
         "mvn_prefix_finalize": (S, [P, I64, I64, P, P, P]),
         "mvn_confidence_region": (S, [I64, P, P, I64, P, P]),
         "mvn_crd": (S, [P, ctypes.POINTER(mvn_crd_problem), ctypes.POINTER(mvn_crd_result)]),
-        "mvn_potrf_panel": (S, [P, T, P, I64]),
-        "mvn_potrf_update": (S, [P, T, P, I64, I64, I64, I32]),
-        "mvn_panel_pack": (S, [P, T, P, I64, P]),
-        "mvn_panel_unpack": (S, [P, T, P, I64, P]),
+        "mvn_potrf_panel": (S, [P, T, P, I64, I64]),
+        "mvn_potrf_update": (S, [P, T, P, I64, I64, I64, I64, I64, I32]),
+        "mvn_potrf_panel_width": (I64, []),
+        "mvn_panel_pack": (S, [P, T, P, I64, I64, P]),
+        "mvn_panel_unpack": (S, [P, T, P, I64, I64, P]),
         "mvn_potrf_info": (S, [P, ctypes.POINTER(I64), I32]),
         "mvn_mc_validate": (S, [P, T, P, P, ctypes.POINTER(mvn_mc), P, P]),
         "mvn_mc_levels": (S, [I64, P, I64, P, I64, P]),
+        "mvn_posterior": (S, [P, ctypes.POINTER(mvn_posterior_problem), P, P, ctypes.POINTER(I64)]),
+        "mvn_posterior_tiles": (S, [P, T, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -242,32 +253,39 @@ def mvn_potrf(t, n: int, raise_on_numeric: bool = True) -> int:
 
 
 # ---- NEXT-1: building blocks of the distributed factorisation (driven by parallel.potrf_distributed)
-def mvn_potrf_panel(t, n: int, k: int, stream=None):
-    """POTRF of diagonal tile k + TRSM of the tiles below it, in place (asynchronous)."""
+def mvn_potrf_panel_width() -> int:
+    """kp: tile columns per super-panel of mvn_potrf (the distributed schedule uses the same)."""
+    return int(lib().mvn_potrf_panel_width())
+
+
+def mvn_potrf_panel(t, n: int, k: int, kp: int = 1, stream=None):
+    """Factor tile columns k .. k+kp-1 in place (asynchronous)."""
     c = Context.get(t.device.index, stream)
-    c.check(lib().mvn_potrf_panel(c.h, tiles(n), _dev_ptr(t), int(k)), "mvn_potrf_panel")
+    c.check(lib().mvn_potrf_panel(c.h, tiles(n), _dev_ptr(t), int(k), int(kp)), "mvn_potrf_panel")
 
 
-def mvn_potrf_update(t, n: int, k: int, col_first: int, col_stride: int = 1, sm_reserve: int = 0, stream=None):
-    """A_ij -= L_ik L_jk^T for tile columns j = col_first, col_first + col_stride, ... (asynchronous)."""
+def mvn_potrf_update(t, n: int, k: int, kp: int, col_first: int, col_stride: int = 1, col_block: int = 1,
+                     sm_reserve: int = 0, stream=None):
+    """A_ij -= sum_{c<kp} L_i,k+c L_j,k+c^T for tile columns j = col_first + m col_stride + b, b < col_block."""
     c = Context.get(t.device.index, stream)
-    c.check(lib().mvn_potrf_update(c.h, tiles(n), _dev_ptr(t), int(k), int(col_first), int(col_stride),
-                                   int(sm_reserve)), "mvn_potrf_update")
+    c.check(lib().mvn_potrf_update(c.h, tiles(n), _dev_ptr(t), int(k), int(kp), int(col_first), int(col_stride),
+                                   int(col_block), int(sm_reserve)), "mvn_potrf_update")
 
 
-def panel_numel(n: int, k: int) -> int:
+def panel_numel(n: int, k: int, kp: int = 1) -> int:
     nt = -(-n // TILE)
-    return (nt - k) * TILE * TILE
+    kp = min(kp, nt - k)
+    return sum(nt - k - j for j in range(kp)) * TILE * TILE
 
 
-def mvn_panel_pack(t, n: int, k: int, panel, stream=None):
+def mvn_panel_pack(t, n: int, k: int, kp: int, panel, stream=None):
     c = Context.get(t.device.index, stream)
-    c.check(lib().mvn_panel_pack(c.h, tiles(n), _dev_ptr(t), int(k), _dev_ptr(panel)), "mvn_panel_pack")
+    c.check(lib().mvn_panel_pack(c.h, tiles(n), _dev_ptr(t), int(k), int(kp), _dev_ptr(panel)), "mvn_panel_pack")
 
 
-def mvn_panel_unpack(panel, n: int, k: int, t, stream=None):
+def mvn_panel_unpack(panel, n: int, k: int, kp: int, t, stream=None):
     c = Context.get(t.device.index, stream)
-    c.check(lib().mvn_panel_unpack(c.h, tiles(n), _dev_ptr(panel), int(k), _dev_ptr(t)), "mvn_panel_unpack")
+    c.check(lib().mvn_panel_unpack(c.h, tiles(n), _dev_ptr(panel), int(k), int(kp), _dev_ptr(t)), "mvn_panel_unpack")
 
 
 def mvn_potrf_info(device: int = 0, reset: bool = True, stream=None) -> int:
@@ -360,6 +378,49 @@ def mvn_mc_levels(count: np.ndarray, N_total: int, k_star) -> np.ndarray:
     if st != MVN_OK:
         raise MvnError(st, "mvn_mc_levels")
     return out
+
+
+# ---- NEXT-4: posterior conditioning (Eq. 7-8)
+def mvn_posterior(xy, mu, obs, y, sigma2, beta, nu, nugget, tau, device: int = 0):
+    """Returns host (mu_post, var_post); Sigma_post stays in the context for mvn_posterior_tiles."""
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    obs = np.ascontiguousarray(obs, dtype=np.int64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n, m = mu.shape[0], obs.shape[0]
+    c = Context.get(device)
+    mp, vp = np.empty(n), np.empty(n)
+    info = ctypes.c_int64(-1)
+    prob = mvn_posterior_problem(n, _np_ptr(xy), _np_ptr(mu), m, _np_ptr(obs), _np_ptr(y), float(sigma2), float(beta),
+                                 float(nu), float(nugget), float(tau))
+    c.check(lib().mvn_posterior(c.h, ctypes.byref(prob), _np_ptr(mp), _np_ptr(vp), ctypes.byref(info)), "mvn_posterior")
+    return mp, vp
+
+
+def mvn_posterior_tiles(order: np.ndarray, out=None, device: int = 0):
+    """Sigma_post of the last mvn_posterior, permuted to `order`, as a tile-packed CUDA tensor."""
+    order = np.ascontiguousarray(order, dtype=np.int64)
+    n = order.shape[0]
+    c = Context.get(device)
+    out = alloc_tiles(n, f"cuda:{device}") if out is None else out
+    c.check(lib().mvn_posterior_tiles(c.h, tiles(n), _np_ptr(order), _dev_ptr(out)), "mvn_posterior_tiles")
+    return out
+
+
+def crd_posterior(xy, mu, obs, y, sigma2, beta, nu, nugget, tau, u, N, R, seed, conf, device: int = 0):
+    """Alg. 1 on the posterior field: condition (Eq. 7-8), order by the posterior marginals,
+    factor Sigma_post in sorted order, one SOV sweep, regions. Every step runs in libmvn."""
+    import torch
+    mp, vp = mvn_posterior(xy, mu, obs, y, sigma2, beta, nu, nugget, tau, device)
+    order, a, _ = mvn_marginal_order(mp, vp, u)
+    T = mvn_posterior_tiles(order, device=device)
+    n = mp.shape[0]
+    info = mvn_potrf(T, n)
+    d_a = torch.from_numpy(a).to(f"cuda:{device}")
+    M, S = mvn_sov_prefix(T, n, d_a, N, R, seed)
+    logp = mvn_prefix_finalize(M, S, N * R).cpu().numpy()
+    k, tie = mvn_confidence_region(logp, conf)
+    return CrdOutput(order, logp, k, tie, info, ()), mp, vp, T
 
 
 @dataclass

@@ -241,17 +241,22 @@ __global__ void __launch_bounds__(256) k_trsm2(double *__restrict__ tiles, int k
 
 // ------------------------------------------------------------------------------------------ K4
 // Column-major enumeration of the trailing tiles (ti, tj), ti >= tj, over the tile columns
-// tj = c0, c0 + cs, c0 + 2 cs, ... < nt (column tj holds nt - tj tiles). `base` / `col` carry the
-// scan between calls (items of one CTA increase monotonically).
-__device__ __forceinline__ void upd_item(int64_t item, int nt, int c0, int cs, int &ti, int &tj, int64_t &base, int &col) {
-    while (item >= base + (nt - (c0 + col * cs))) { base += nt - (c0 + col * cs); ++col; }
-    tj = c0 + col * cs;
+//   tj = c0 + m*cs + b,  m >= 0, 0 <= b < cb,  tj < nt
+// (blocks of cb consecutive columns every cs columns; cb = cs = 1: every column from c0; the
+// distributed factorisation passes cb = kp, cs = kp * W). Column tj holds nt - tj tiles. `base` /
+// `col` carry the scan between calls (the items of one CTA increase monotonically).
+__host__ __device__ inline int upd_col(int idx, int c0, int cs, int cb) { return c0 + (idx / cb) * cs + idx % cb; }
+
+__device__ __forceinline__ void upd_item(int64_t item, int nt, int c0, int cs, int cb, int &ti, int &tj, int64_t &base,
+                                         int &col) {
+    while (item >= base + (nt - upd_col(col, c0, cs, cb))) { base += nt - upd_col(col, c0, cs, cb); ++col; }
+    tj = upd_col(col, c0, cs, cb);
     ti = tj + (int)(item - base);
 }
 
-__host__ __device__ inline int64_t upd_items(int nt, int c0, int cs) {
+__host__ __device__ inline int64_t upd_items(int nt, int c0, int cs, int cb) {
     int64_t s = 0;
-    for (int c = c0; c < nt; c += cs) s += nt - c;
+    for (int idx = 0; upd_col(idx, c0, cs, cb) < nt; ++idx) s += nt - upd_col(idx, c0, cs, cb);
     return s;
 }
 
@@ -264,18 +269,19 @@ constexpr int SMEM = STAGES * BK * (SA + SB) * 8;
 
 // Trailing update, one CTA per (tile (i,j), row half h): C(64x128) -= L_ik[h-half] * L_jk^T.
 // 4 warps as 2 (M) x 2 (N), warp tile 32x64 = 4x8 DMMA blocks (64 fp64 accumulators / thread).
-__global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, int k, int nt, int c0, int cs) {
+__global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, int k, int kp, int nt, int c0, int cs,
+                                                   int cb) {
     using namespace upd;
     extern __shared__ double sm[];
     double *As = sm;
     double *Bs = sm + STAGES * BK * SA;
     const int64_t id = blockIdx.x >> 1;
     const int h = blockIdx.x & 1;
-    // id -> tile (ti, tj) of the column-major enumeration over tile columns c0, c0 + cs, ... (> k):
-    // c0 = k+1, cs >= nt: the next panel column only (lookahead); c0 = k+2, cs = 1: the rest.
+    // id -> tile (ti, tj) of the column-major enumeration over the selected tile columns (> k+kp-1);
+    // the panel is the kp tile columns k .. k+kp-1 (K = 128 kp; tiles (ti, k..k+kp-1) are contiguous).
     int ti, tj, col = 0;
     int64_t base = 0;
-    upd_item(id, nt, c0, cs, ti, tj, base, col);
+    upd_item(id, nt, c0, cs, cb, ti, tj, base, col);
     const double *__restrict__ Lik = tiles + tile_offset(ti, k) + h * BM;   // column stride 128
     const double *__restrict__ Ljk = tiles + tile_offset(tj, k);
     double *C = tiles + tile_offset(ti, tj) + h * BM;
@@ -307,7 +313,7 @@ __global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, i
             cp_async16(bs + col * SB + seg * 2, Ljk + (int64_t)(kc + col) * kTile + seg * 2);
         }
     };
-    gemm_mainloop<BK, STAGES, SA, SB, WM, WN>(kTile / BK, As, Bs, wm0, wn0, lane, acc, load);
+    gemm_mainloop<BK, STAGES, SA, SB, WM, WN>(kp * (kTile / BK), As, Bs, wm0, wn0, lane, acc, load);
 
     // epilogue: C[row][col] -= acc, C column-major (column stride 128); loads batched per row block
 #pragma unroll
@@ -363,8 +369,8 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // Updates with panel k the tile columns c0, c0 + cs, ... (c0 > k): c0 = k+2, cs = 1 on one GPU
 // (column k+1 is the lookahead stream's); cs = world size for the 1-D block-cyclic distributed
 // factorisation (mvn_potrf_update).
-__global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int nt, int c0, int cs,
-                                                        int64_t nitems) {
+__global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int kp, int nt, int c0,
+                                                        int cs, int cb, int64_t nitems) {
     using namespace upd2;
     extern __shared__ double sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
@@ -386,10 +392,10 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
         const int lane = tid & 31;
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
             int ti, tj;
-            upd_item(item, nt, c0, cs, ti, tj, base, col);
-            const double *Lik = tiles + tile_offset(ti, k);
+            upd_item(item, nt, c0, cs, cb, ti, tj, base, col);
+            const double *Lik = tiles + tile_offset(ti, k);    // kp consecutive tiles (row panels are contiguous)
             const double *Ljk = tiles + tile_offset(tj, k);
-            for (int c = 0; c < CHUNKS; ++c, ++q) {
+            for (int c = 0; c < kp * CHUNKS; ++c, ++q) {
                 const int st = q % STAGES;
                 mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
                 double *as = sm + st * STAGE;
@@ -417,13 +423,13 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
     double *stg = sm + OFF_STG + warp * 16 * kTile;   // column-major [16][128]
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         int ti, tj;
-        upd_item(item, nt, c0, cs, ti, tj, base, col);
+        upd_item(item, nt, c0, cs, cb, ti, tj, base, col);
         double acc[16][2][2];
 #pragma unroll
         for (int a = 0; a < 16; ++a)
 #pragma unroll
             for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-        for (int c = 0; c < CHUNKS; ++c, ++q) {
+        for (int c = 0; c < kp * CHUNKS; ++c, ++q) {
             const int st = q % STAGES;
             mbar_wait(&full[st], (q / STAGES) & 1);
             const double *as = sm + st * STAGE;
@@ -475,11 +481,7 @@ cudaError_t potrf_init() {
     return cudaSuccess;
 }
 
-// Right-looking factorisation with one step of lookahead on two streams:
-//   panel stream (high priority): column update of tile column k+1 -> POTRF(k+1) -> TRSM(k+1)
-//   main stream                 : persistent update of the rest of the trailing matrix (columns >= k+2),
-//                                 on all but kPanelSMs SMs, so the panel work of step k+1 runs beside it.
-// Events order the two (panel k before update k; update k-1 before the column update of step k).
+// Streams and events of the single-GPU lookahead schedule (launch_potrf).
 namespace {
 constexpr int kPanelSMs = 8;
 struct PotrfStreams {
@@ -504,61 +506,110 @@ cudaError_t potrf_streams(int dev) {
 }
 }  // namespace
 
-cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st) {
+// ---- building blocks shared by mvn_potrf and the distributed factorisation (identical arithmetic)
+// Factor the kp tile columns k .. k+kp-1 (all updates from columns < k applied): POTRF + TRSM of
+// column k; for each further column k+j: update it with columns k .. k+j-1 (K = 128 j), POTRF, TRSM.
+cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int kp, int64_t *d_info, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
+    kp = std::min(kp, nt - k);
+    const size_t sm_diag = kTile * blk::SP * 8, sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
+    for (int j = 0; j < kp; ++j) {
+        const int c = k + j;
+        if (j > 0) k_update<<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tiles, k, j, nt, c, nt, 1);
+        k_potrf_diag2<<<1, 256, sm_diag, st>>>(tiles, c, d_info);
+        if (nt - c - 1 > 0) k_trsm2<<<2 * (nt - c - 1), 256, sm_trsm, st>>>(tiles, c);
+    }
+    return cudaGetLastError();
+}
+
+// A_ij -= sum_{c=k}^{k+kp-1} L_ic L_jc^T for the tile columns j = c0 + m cs + b (0 <= b < cb) and
+// i >= j: the persistent kernel (on nsm - sm_reserve SMs) when there are >= 2 tiles per CTA, else
+// two CTAs per tile.
+cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0, int cs, int cb, int sm_reserve,
+                                cudaStream_t st) {
+    const int nt = (int)((n + kTile - 1) / kTile);
+    if (c0 >= nt) return cudaSuccess;
+    kp = std::min(kp, nt - k);
+    const int64_t items = upd_items(nt, c0, cs, cb);
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     static const bool use_persistent = [] { const char *e = getenv("MVN_POTRF_PERSISTENT"); return !(e && e[0] == '0'); }();
+    const int avail = std::max(1, nsm - sm_reserve);
+    if (use_persistent && items >= 2 * avail) {
+        k_update2<<<avail, upd2::NT, upd2::SMEM, st>>>(tiles, k, kp, nt, c0, cs, cb, items);
+    } else {
+        k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(tiles, k, kp, nt, c0, cs, cb);
+    }
+    return cudaGetLastError();
+}
+
+int potrf_panel_width() {
+    static const int kp = [] { const char *e = getenv("MVN_POTRF_KP"); const int v = e ? atoi(e) : 2; return v >= 1 && v <= 4 ? v : 2; }();
+    return kp;
+}
+
+// Right-looking factorisation over super-panels of kp = potrf_panel_width() tile columns (K = 128 kp
+// per trailing update: half the update passes and epilogues of a 128-wide step), with one step of
+// lookahead on two streams:
+//   panel stream (high priority): update of the next super-panel's columns with super-panel s, then
+//                                 its factorisation (launch_potrf_panel);
+//   main stream                 : persistent update of the columns after the next super-panel, on
+//                                 all but kPanelSMs SMs, so the panel work runs beside it.
+// Events order the two (panel s before update s; update s-1 before the panel-stream update of s).
+cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols) {
+    const int nt = (int)((n + kTile - 1) / kTile);
+    if (ncols <= 0 || ncols > nt) ncols = nt;      // ncols < nt: partial factorisation (Schur complement left)
+    const int KP = potrf_panel_width();
+    const int S = (ncols + KP - 1) / KP;
+    int dev = 0;
+    cudaGetDevice(&dev);
     cudaError_t e = potrf_streams(dev);
     if (e != cudaSuccess) return e;
     cudaStream_t sp = g_ps.sp;
-    const size_t sm_diag = kTile * blk::SP * 8, sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
     // the panel stream starts after everything already queued on the main stream (Sigma)
     if ((e = cudaEventRecord(g_ps.ev_start, st))) return e;
     if ((e = cudaStreamWaitEvent(sp, g_ps.ev_start, 0))) return e;
-    k_potrf_diag2<<<1, 256, sm_diag, sp>>>(tiles, 0, d_info);
-    if (nt > 1) k_trsm2<<<2 * (nt - 1), 256, sm_trsm, sp>>>(tiles, 0);
+    if ((e = launch_potrf_panel(n, tiles, 0, std::min(KP, ncols), d_info, sp))) return e;
     if ((e = cudaEventRecord(g_ps.ev_panel[0], sp))) return e;
-    for (int k = 0; k + 1 < nt; ++k) {
-        const int T = nt - k - 1;                       // trailing tile rows/cols after step k
-        // main stream: update columns >= k+2 with panel k
-        if ((e = cudaStreamWaitEvent(st, g_ps.ev_panel[k & 1], 0))) return e;
-        if (T > 1) {
-            const int Tr = T - 1;
-            const int64_t items = (int64_t)Tr * (Tr + 1) / 2;
-            if (use_persistent && items >= 2 * nsm) {
-                const int grid = (int)std::min<int64_t>(items, nsm - kPanelSMs);
-                k_update2<<<grid, upd2::NT, upd2::SMEM, st>>>(tiles, k, nt, k + 2, 1, items);
-            } else {
-                k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(tiles, k, nt, k + 2, 1);
-            }
+    for (int s = 0; s < S; ++s) {
+        const int k = s * KP, w = std::min(KP, ncols - k);
+        const int kn = k + w;
+        if ((e = cudaStreamWaitEvent(st, g_ps.ev_panel[s & 1], 0))) return e;
+        if (s + 1 == S) {
+            // last super-panel: the trailing (Schur complement) block of a partial factorisation
+            if (kn < nt && (e = launch_potrf_update(n, tiles, k, w, kn, 1, 1, 0, st))) return e;
+            break;
         }
-        if ((e = cudaEventRecord(g_ps.ev_rest[k & 1], st))) return e;
-        // panel stream: column k+1, then POTRF / TRSM of panel k+1
-        if (k >= 1 && (e = cudaStreamWaitEvent(sp, g_ps.ev_rest[(k - 1) & 1], 0))) return e;
-        k_update<<<(unsigned)(2 * T), 128, upd::SMEM, sp>>>(tiles, k, nt, k + 1, nt);
-        k_potrf_diag2<<<1, 256, sm_diag, sp>>>(tiles, k + 1, d_info);
-        if (T > 1) k_trsm2<<<2 * (T - 1), 256, sm_trsm, sp>>>(tiles, k + 1);
-        if ((e = cudaEventRecord(g_ps.ev_panel[(k + 1) & 1], sp))) return e;
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        const int wn = std::min(KP, ncols - kn);
+        // main stream: columns >= kn + wn with super-panel s
+        if ((e = launch_potrf_update(n, tiles, k, w, kn + wn, 1, 1, kPanelSMs, st))) return e;
+        if ((e = cudaEventRecord(g_ps.ev_rest[s & 1], st))) return e;
+        // panel stream: columns kn .. kn+wn-1 with super-panel s, then factor super-panel s+1
+        if (s >= 1 && (e = cudaStreamWaitEvent(sp, g_ps.ev_rest[(s - 1) & 1], 0))) return e;
+        if ((e = launch_potrf_update(n, tiles, k, w, kn, nt, wn, 0, sp))) return e;
+        if ((e = launch_potrf_panel(n, tiles, kn, wn, d_info, sp))) return e;
+        if ((e = cudaEventRecord(g_ps.ev_panel[(s + 1) & 1], sp))) return e;
     }
-    // join: the main stream waits for the last panel
-    if ((e = cudaStreamWaitEvent(st, g_ps.ev_panel[(nt - 1) & 1], 0))) return e;
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------------ NEXT-1
-// Building blocks of the distributed (1-D block-cyclic over tile columns) factorisation; the step
-// loop and the NCCL panel broadcasts live in paper_2405_14892_b200/parallel.py (collectives stay
-// above the ABI). Every rank keeps a full tile-packed buffer; it updates only the tile columns it
-// owns and receives every other column as a finished panel, so each rank ends with all of L.
+// Building blocks of the distributed (1-D block-cyclic over super-panels of kp tile columns)
+// factorisation; the step loop and the NCCL panel broadcasts live in
+// paper_2405_14892_b200/parallel.py (collectives stay above the ABI). Every rank keeps a full
+// tile-packed buffer; it updates only the tile columns it owns and receives every other super-panel
+// finished, so each rank ends with all of L. launch_potrf_panel / launch_potrf_update above are the
+// arithmetic; this adds the panel copy.
 
-// Panel copy: tiles (k..nt-1, k) <-> contiguous panel[(i - k) * nb^2]. One CTA per (tile, 1/8).
-__global__ void __launch_bounds__(256) k_panel_copy(double *__restrict__ tiles, int k, double *__restrict__ panel,
+// Panel copy: tiles (k+j .. nt-1, k+j) for j < kp <-> contiguous panel (column k first, then k+1, ...).
+// grid (8, tiles of the super-panel): one CTA per (tile, 1/8).
+__global__ void __launch_bounds__(256) k_panel_copy(double *__restrict__ tiles, int k, int nt, double *__restrict__ panel,
                                                    int to_panel) {
-    const int i = k + blockIdx.y;
-    double2 *t = reinterpret_cast<double2 *>(tiles + tile_offset(i, k));
+    int idx = blockIdx.y, c = k;
+    while (idx >= nt - c) { idx -= nt - c; ++c; }
+    const int i = c + idx;
+    double2 *t = reinterpret_cast<double2 *>(tiles + tile_offset(i, c));
     double2 *p = reinterpret_cast<double2 *>(panel + (int64_t)blockIdx.y * kTile * kTile);
     constexpr int PER = kTile * kTile / 2 / 8;             // double2 per CTA
     const int e0 = blockIdx.x * PER;
@@ -569,33 +620,12 @@ __global__ void __launch_bounds__(256) k_panel_copy(double *__restrict__ tiles, 
     }
 }
 
-cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int64_t *d_info, cudaStream_t st) {
+cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, int kp, double *panel, bool to_panel, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
-    const size_t sm_diag = kTile * blk::SP * 8, sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
-    k_potrf_diag2<<<1, 256, sm_diag, st>>>(tiles, k, d_info);
-    if (nt - k - 1 > 0) k_trsm2<<<2 * (nt - k - 1), 256, sm_trsm, st>>>(tiles, k);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int c0, int cs, int sm_reserve, cudaStream_t st) {
-    const int nt = (int)((n + kTile - 1) / kTile);
-    if (c0 >= nt) return cudaSuccess;
-    const int64_t items = upd_items(nt, c0, cs);
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int avail = std::max(1, nsm - sm_reserve);
-    if (items >= 2 * avail) {
-        k_update2<<<avail, upd2::NT, upd2::SMEM, st>>>(tiles, k, nt, c0, cs, items);
-    } else {
-        k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(tiles, k, nt, c0, cs);
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, double *panel, bool to_panel, cudaStream_t st) {
-    const int nt = (int)((n + kTile - 1) / kTile);
-    k_panel_copy<<<dim3(8, nt - k), 256, 0, st>>>(tiles, k, panel, to_panel ? 1 : 0);
+    kp = std::min(kp, nt - k);
+    int ntiles = 0;
+    for (int j = 0; j < kp; ++j) ntiles += nt - k - j;
+    k_panel_copy<<<dim3(8, ntiles), 256, 0, st>>>(tiles, k, nt, panel, to_panel ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -29,6 +29,10 @@ struct mvn_ctx {
     // mvn_crd buffers
     void *crd_L = nullptr; size_t crd_L_cap = 0;
     void *crd_vec = nullptr; size_t crd_vec_cap = 0;
+    // mvn_posterior: augmented matrix (Schur complement = Sigma_post) and small vectors
+    void *post = nullptr; size_t post_cap = 0;
+    void *postv = nullptr; size_t postv_cap = 0;
+    int64_t post_n = 0, post_off = 0;
     // mvn_mc_validate
     void *mcZ = nullptr; size_t mcZ_cap = 0;
     void *mcF = nullptr; size_t mcF_cap = 0;
@@ -162,7 +166,8 @@ void mvn_destroy(mvn_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF})
+    for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF,
+                    c->post, c->postv})
         if (p) cudaFree(p);
     delete c;
 }
@@ -178,9 +183,11 @@ const char *mvn_last_error(const mvn_ctx *c) { return c ? c->err.c_str() : "null
 mvn_status mvn_trim(mvn_ctx *c) {
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv})
         if (*p) { cudaFree(*p); *p = nullptr; }
     c->Y_cap = c->part_cap = c->cta_cap = c->sync_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
+    c->post_cap = c->postv_cap = 0;
+    c->post_n = c->post_off = 0;
     return MVN_OK;
 }
 
@@ -251,39 +258,44 @@ mvn_status mvn_potrf(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t *info) {
     return MVN_OK;
 }
 
-mvn_status mvn_potrf_panel(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k) {
+mvn_status mvn_potrf_panel(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k, int64_t kp) {
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
-    if (!nt || !d_tiles || k < 0 || k >= nt) return fail(c, MVN_E_USAGE, "mvn_potrf_panel: bad arguments");
-    MVN_CUDA(c, mvn::launch_potrf_panel(t.n, d_tiles, (int)k, c->d_info, c->stream));
+    if (!nt || !d_tiles || k < 0 || k >= nt || kp < 1 || kp > 4) return fail(c, MVN_E_USAGE, "mvn_potrf_panel: bad arguments");
+    MVN_CUDA(c, mvn::launch_potrf_panel(t.n, d_tiles, (int)k, (int)kp, c->d_info, c->stream));
     return MVN_OK;
 }
 
-mvn_status mvn_potrf_update(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k, int64_t col_first, int64_t col_stride,
-                            int32_t sm_reserve) {
+mvn_status mvn_potrf_update(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k, int64_t kp, int64_t col_first,
+                            int64_t col_stride, int64_t col_block, int32_t sm_reserve) {
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
-    if (!nt || !d_tiles || k < 0 || col_first <= k || col_stride < 1 || sm_reserve < 0 || sm_reserve >= c->nsm)
-        return fail(c, MVN_E_USAGE, "mvn_potrf_update: bad arguments (need 0 <= k < col_first, col_stride >= 1)");
+    if (!nt || !d_tiles || k < 0 || kp < 1 || kp > 4 || col_first < std::min(k + kp, nt) || col_stride < 1 ||
+        col_block < 1 || col_block > col_stride || sm_reserve < 0 || sm_reserve >= c->nsm)
+        return fail(c, MVN_E_USAGE, "mvn_potrf_update: bad arguments (need k + kp <= col_first, 1 <= col_block <= col_stride)");
     if (col_first >= nt) return MVN_OK;
-    MVN_CUDA(c, mvn::launch_potrf_update(t.n, d_tiles, (int)k, (int)col_first, (int)std::min<int64_t>(col_stride, nt),
-                                         sm_reserve, c->stream));
+    MVN_CUDA(c, mvn::launch_potrf_update(t.n, d_tiles, (int)k, (int)kp, (int)col_first, (int)std::min<int64_t>(col_stride, nt),
+                                         (int)std::min<int64_t>(col_block, nt), sm_reserve, c->stream));
     return MVN_OK;
 }
 
-mvn_status mvn_panel_pack(mvn_ctx *c, mvn_tiles t, const double *d_tiles, int64_t k, double *d_panel) {
+int64_t mvn_potrf_panel_width(void) { return mvn::potrf_panel_width(); }
+
+mvn_status mvn_panel_pack(mvn_ctx *c, mvn_tiles t, const double *d_tiles, int64_t k, int64_t kp, double *d_panel) {
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
-    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt) return fail(c, MVN_E_USAGE, "mvn_panel_pack: bad arguments");
-    MVN_CUDA(c, mvn::launch_panel_copy(t.n, const_cast<double *>(d_tiles), (int)k, d_panel, true, c->stream));
+    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 4)
+        return fail(c, MVN_E_USAGE, "mvn_panel_pack: bad arguments");
+    MVN_CUDA(c, mvn::launch_panel_copy(t.n, const_cast<double *>(d_tiles), (int)k, (int)kp, d_panel, true, c->stream));
     return MVN_OK;
 }
 
-mvn_status mvn_panel_unpack(mvn_ctx *c, mvn_tiles t, const double *d_panel, int64_t k, double *d_tiles) {
+mvn_status mvn_panel_unpack(mvn_ctx *c, mvn_tiles t, const double *d_panel, int64_t k, int64_t kp, double *d_tiles) {
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
-    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt) return fail(c, MVN_E_USAGE, "mvn_panel_unpack: bad arguments");
-    MVN_CUDA(c, mvn::launch_panel_copy(t.n, d_tiles, (int)k, const_cast<double *>(d_panel), false, c->stream));
+    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 4)
+        return fail(c, MVN_E_USAGE, "mvn_panel_unpack: bad arguments");
+    MVN_CUDA(c, mvn::launch_panel_copy(t.n, d_tiles, (int)k, (int)kp, const_cast<double *>(d_panel), false, c->stream));
     return MVN_OK;
 }
 
@@ -334,7 +346,7 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
     if ((s = ensure(c, &c->part, &c->part_cap, (size_t)L.nblk * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
     if ((s = ensure(c, &c->cta, &c->cta_cap, cta.size() * sizeof(int64_t))) != MVN_OK) return s;
     // soft lockstep: need[b] = CTAs with more than b sample blocks; counters [max_blocks][nrb]
-    static const int env_lag = [] { const char *e = getenv("MVN_SOV_LAG"); return e ? atoi(e) : 2; }();
+    static const int env_lag = [] { const char *e = getenv("MVN_SOV_LAG"); return e ? atoi(e) : 0; }();   // off: measured no gain (r01)
     static const int env_hints = [] { const char *e = getenv("MVN_SOV_HINTS"); return e ? atoi(e) : 1; }();
     const int bs = mvn::sov_block_samples();
     int max_blocks = 0;
@@ -424,6 +436,78 @@ mvn_status mvn_mc_levels(int64_t n, const uint64_t *count, int64_t N_total, cons
         if (k_star[i] < 0 || k_star[i] > n) return MVN_E_USAGE;
         p_hat[i] = (double)tail[(size_t)k_star[i]] / (double)N_total;
     }
+    return MVN_OK;
+}
+
+mvn_status mvn_posterior(mvn_ctx *c, const mvn_posterior_problem *p, double *mu_post, double *var_post, int64_t *info) {
+    if (!c) return MVN_E_USAGE;
+    if (!p || !mu_post || !var_post || !info || p->n < 1 || p->m < 1 || !p->xy || !p->mu || !p->obs || !p->y ||
+        !(p->tau > 0) || !(p->sigma2 > 0) || !(p->beta > 0) || !(p->nugget >= 0) || !(p->nu == 0.5 || p->nu == 1.5 || p->nu == 2.5))
+        return fail(c, MVN_E_USAGE, "mvn_posterior: bad arguments");
+    const int64_t n = p->n, m = p->m;
+    std::vector<char> seen((size_t)n, 0);
+    for (int64_t j = 0; j < m; ++j) {
+        if (p->obs[j] < 0 || p->obs[j] >= n || seen[(size_t)p->obs[j]] || std::isnan(p->y[j]))
+            return fail(c, MVN_E_USAGE, "mvn_posterior: observation indices must be distinct sites, y finite");
+        seen[(size_t)p->obs[j]] = 1;
+    }
+    const int64_t m_pad = (m + mvn::kTile - 1) / mvn::kTile * mvn::kTile;
+    const int64_t N = m_pad + n + 1, extra = m_pad + n;
+    mvn_tiles ta{N, mvn::kTile};
+    // augmented locations: observed sites, decoupled far points (padding), all sites, far point (r row)
+    std::vector<double> xy((size_t)(2 * N)), r((size_t)m);
+    for (int64_t j = 0; j < m; ++j) {
+        xy[2 * j] = p->xy[2 * p->obs[j]];
+        xy[2 * j + 1] = p->xy[2 * p->obs[j] + 1];
+        r[(size_t)j] = p->y[j] - p->mu[p->obs[j]];
+    }
+    for (int64_t j = m; j < m_pad; ++j) { xy[2 * j] = 1e9 * (double)(j + 1); xy[2 * j + 1] = 1e9; }
+    for (int64_t i = 0; i < n; ++i) { xy[2 * (m_pad + i)] = p->xy[2 * i]; xy[2 * (m_pad + i) + 1] = p->xy[2 * i + 1]; }
+    xy[2 * extra] = -1e9;
+    xy[2 * extra + 1] = -1e9;
+    mvn_status s;
+    if ((s = ensure(c, &c->post, &c->post_cap, mvn_tiles_bytes(ta))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->postv, &c->postv_cap, sizeof(double) * (size_t)(2 * N + m + 2 * n))) != MVN_OK) return s;
+    double *A = (double *)c->post, *d_xy = (double *)c->postv, *d_r = d_xy + 2 * N, *d_dg = d_r + m, *d_row = d_dg + n;
+    MVN_CUDA(c, cudaMemcpyAsync(d_xy, xy.data(), sizeof(double) * 2 * N, cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(d_r, r.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+    if ((s = mvn_cov_matern(c, ta, d_xy, p->sigma2, p->beta, p->nu, p->nugget, A)) != MVN_OK) return s;
+    MVN_CUDA(c, mvn::launch_add_diag(A, 0, m, p->tau * p->tau, c->stream));           // Sigma_oo + tau^2 I
+    MVN_CUDA(c, mvn::launch_set_row(A, extra, 0, m, d_r, c->stream));                 // r^T
+    const int64_t minus1 = -1;
+    MVN_CUDA(c, cudaMemcpyAsync(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, mvn::launch_potrf(N, A, c->d_info, c->stream, (int)(m_pad / mvn::kTile)));
+    MVN_CUDA(c, mvn::launch_get_diag(A, m_pad, n, d_dg, c->stream));
+    MVN_CUDA(c, mvn::launch_get_row(A, extra, m_pad, n, d_row, c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(var_post, d_dg, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(mu_post, d_row, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(info, c->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (*info >= 0) {
+        if (*info >= m) *info = -1;                       // cannot happen: padding is decoupled and positive
+        else return fail(c, MVN_E_NUMERIC, "mvn_posterior: observation covariance not positive definite at row " + std::to_string(*info));
+    }
+    for (int64_t i = 0; i < n; ++i) mu_post[i] = p->mu[i] - mu_post[i];   // the last row holds -(mu_post - mu)
+    c->post_n = n;
+    c->post_off = m_pad;
+    return MVN_OK;
+}
+
+mvn_status mvn_posterior_tiles(mvn_ctx *c, mvn_tiles t, const int64_t *order, double *d_tiles) {
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !order || !d_tiles || c->post_n != t.n || !c->post)
+        return fail(c, MVN_E_USAGE, "mvn_posterior_tiles: call mvn_posterior first (same n)");
+    const int64_t n = t.n;
+    std::vector<char> seen((size_t)n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        if (order[i] < 0 || order[i] >= n || seen[(size_t)order[i]]) return fail(c, MVN_E_USAGE, "mvn_posterior_tiles: order is not a permutation");
+        seen[(size_t)order[i]] = 1;
+    }
+    mvn_status s;
+    if ((s = ensure(c, &c->cta, &c->cta_cap, sizeof(int64_t) * (size_t)n)) != MVN_OK) return s;
+    MVN_CUDA(c, cudaMemcpyAsync(c->cta, order, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, mvn::launch_permute_sym((const double *)c->post, c->post_off, (const int64_t *)c->cta, n, d_tiles, c->stream));
+    MVN_CUDA(c, cudaStreamSynchronize(c->stream));
     return MVN_OK;
 }
 

@@ -14,11 +14,13 @@ cudaError_t launch_rescale(int64_t n, const double *Mg, double *M, double *S, cu
 cudaError_t launch_finalize(int64_t n, int64_t NR, const double *M, const double *S, double *logP, cudaStream_t st);
 
 cudaError_t potrf_init();
-cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st);
+cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols = 0);
 // distributed-factorisation building blocks (NEXT-1)
-cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int64_t *d_info, cudaStream_t st);
-cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int c0, int cs, int sm_reserve, cudaStream_t st);
-cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, double *panel, bool to_panel, cudaStream_t st);
+int potrf_panel_width();   // kp: tile columns per super-panel (2; MVN_POTRF_KP overrides)
+cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int kp, int64_t *d_info, cudaStream_t st);
+cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0, int cs, int cb, int sm_reserve,
+                                cudaStream_t st);
+cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, int kp, double *panel, bool to_panel, cudaStream_t st);
 
 struct SovLaunch {
     const double *L;
@@ -45,6 +47,13 @@ int sov_block_samples();
 int sov_y_stride();
 int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta);
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
+
+// NEXT-4: posterior conditioning helpers (kernels_post.cu)
+cudaError_t launch_add_diag(double *tiles, int64_t begin, int64_t end, double v, cudaStream_t st);
+cudaError_t launch_set_row(double *tiles, int64_t row, int64_t col0, int64_t ncols, const double *v, cudaStream_t st);
+cudaError_t launch_get_row(const double *tiles, int64_t row, int64_t col0, int64_t ncols, double *out, cudaStream_t st);
+cudaError_t launch_get_diag(const double *tiles, int64_t begin, int64_t n, double *out, cudaStream_t st);
+cudaError_t launch_permute_sym(const double *src, int64_t off, const int64_t *order, int64_t n, double *dst, cudaStream_t st);
 
 // NEXT-2: Monte-Carlo validation
 cudaError_t mc_init();

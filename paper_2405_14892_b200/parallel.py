@@ -11,8 +11,8 @@ The combine is written against an injectable `rescale` so the host logic is test
 gloo (tests/test_parallel_gloo.py); on the GPU path it is the CUDA kernel behind mvn_prefix_rescale.
 
 NEXT-1: `potrf_distributed` factors Sigma across the ranks instead of on
-rank 0 alone — 1-D block-cyclic over 128-wide tile columns (column j owned by rank j mod W), one
-step of lookahead, the finished panel of each step broadcast over NCCL while the ranks update
+rank 0 alone — 1-D block-cyclic over super-panels of kp = 2 tile columns (super-panel s owned by
+rank s mod W), one step of lookahead, the finished panel of each step broadcast over NCCL while the ranks update
 their own columns. Every rank ends with all of L, so the broadcast of L (C1) disappears.
 """
 from __future__ import annotations
@@ -104,29 +104,33 @@ def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg,
     return logp
 
 
-def potrf_launches(n: int, world: int = 1, rank: int = 0, nsm: int = 148) -> int:
-    """Kernels launched by one factorisation: mvn_potrf (world 1) or this rank's share of
-    potrf_distributed (panel = POTRF + TRSM, update, pack / unpack)."""
+def potrf_launches(n: int, world: int = 1, rank: int = 0, kp: int = 2, nsm: int = 148) -> int:
+    """Kernels launched by one factorisation with super-panels of kp columns: mvn_potrf (world 1)
+    or this rank's share of potrf_distributed (panel = per column [update] + POTRF [+ TRSM]; one
+    update per bulk / lookahead step; pack / unpack)."""
     nt = -(-n // TILE)
+    S = -(-nt // kp)
+
+    def panel(sp):
+        k, w = sp * kp, min(kp, nt - sp * kp)
+        return sum((1 if j else 0) + 1 + (1 if nt - k - j - 1 > 0 else 0) for j in range(w))
+
     if world == 1:
-        c = 1 + (1 if nt > 1 else 0)
-        for k in range(nt - 1):
-            T = nt - k - 1
-            c += (1 if T > 1 else 0) + 1 + 1 + (1 if T > 1 else 0)
+        c = panel(0)
+        for sp in range(S - 1):
+            kn, wn = (sp + 1) * kp, min(kp, nt - (sp + 1) * kp)
+            c += (1 if kn + wn < nt else 0) + 1 + panel(sp + 1)
         return c
     c = 0
-    for k in range(nt):
-        if k % world == rank:
-            c += 1 + (1 if k + 1 < nt else 0) + 1         # panel (potrf [+ trsm]) + pack
-        else:
-            c += 1                                        # unpack
-        if k + 1 < nt:
-            if (k + 1) % world == rank:
-                c += 1                                    # lookahead column update
-            first = owned_first(k + 1, rank, world)
-            if first == k + 1 and (k + 1) % world == rank:
+    for sp in range(S):
+        c += (panel(sp) + 1) if sp % world == rank else 1        # factor + pack, or unpack
+        if sp + 1 < S:
+            if (sp + 1) % world == rank:
+                c += 1                                            # lookahead update
+            first = owned_first(sp + 1, rank, world)
+            if first == sp + 1 and (sp + 1) % world == rank:
                 first += world
-            c += 1 if first < nt else 0
+            c += 1 if first * kp < nt else 0
     return c
 
 
@@ -134,46 +138,51 @@ def potrf_launches(n: int, world: int = 1, rank: int = 0, nsm: int = 148) -> int
 TILE = 128
 
 
-def owned_first(col: int, rank: int, world: int) -> int:
-    """Smallest tile column >= col owned by `rank` under the 1-D block-cyclic map j -> j mod world."""
-    return col + ((rank - col) % world)
+def owned_first(sp: int, rank: int, world: int) -> int:
+    """Smallest super-panel index >= sp owned by `rank` under the 1-D block-cyclic map s -> s mod world."""
+    return sp + ((rank - sp) % world)
 
 
 def potrf_dist_schedule(ops, rank: int, world: int):
     """The per-rank step loop of the distributed right-looking Cholesky, as a generator.
 
-    It yields ("bcast", k, src) whenever panel k (tile column k, packed into ops.panel_buf(k)) must
-    be broadcast from rank src, and is resumed with a handle that `ops.wait` understands. Runners:
-    `potrf_distributed` (torch.distributed, one generator per process) and the single-device
-    emulator in the tests (W generators stepped in lockstep). The recurrence is mvn_potrf's
-    (Alg. 1 l.8); only the ownership of the updates is split:
-      panel k   : owner(k) = k mod W runs POTRF(A_kk) + TRSM(A_ik) and packs the column;
-      lookahead : owner(k+1) updates column k+1 with panel k and factors panel k+1 on the side
-                  stream, whose broadcast then overlaps the bulk update of step k;
-      bulk      : every rank updates its own columns >= k+1 (minus the lookahead column).
+    Super-panels of kp = ops.kp tile columns (super-panel s = columns s*kp .. s*kp+kp-1) are owned
+    by rank s mod W. The generator yields ("bcast", s, src) whenever super-panel s (packed into
+    ops.panel_buf(s)) must be broadcast from rank src, and is resumed with a handle that `ops.wait`
+    understands. Runners: `potrf_distributed` (torch.distributed, one generator per process) and the
+    single-device emulator in the tests (W generators stepped in lockstep). The recurrence is
+    mvn_potrf's (Alg. 1 l.8, built from the same two library calls); only the ownership of
+    the updates is split:
+      panel s    : owner(s) factors super-panel s (mvn_potrf_panel) and packs it;
+      lookahead  : owner(s+1) updates super-panel s+1's columns with super-panel s and factors it
+                   on the side stream, whose broadcast then overlaps the bulk update of step s;
+      bulk       : every rank updates its own columns after super-panel s (minus the lookahead).
     """
-    nt = ops.nt
-    owner = lambda k: k % world
+    nt, kp = ops.nt, ops.kp
+    S = -(-nt // kp)
+    owner = lambda sp: sp % world
+    col = lambda sp: sp * kp
+    width = lambda sp: min(kp, nt - sp * kp)
     if rank == owner(0):
         ops.panel(0, "side")
         ops.pack(0, "side")
     h = yield ("bcast", 0, owner(0))
-    for k in range(nt):
-        ops.wait(h, "main")                      # panel k has arrived (or was produced here)
-        if rank != owner(k):
-            ops.unpack(k, "main")
+    for sp in range(S):
+        ops.wait(h, "main")                      # super-panel sp has arrived (or was produced here)
+        if rank != owner(sp):
+            ops.unpack(sp, "main")
         ev = ops.record("main")                  # also orders every earlier bulk update
-        if k + 1 < nt:
+        if sp + 1 < S:
             ops.wait(ev, "side")
-            if rank == owner(k + 1):
-                ops.update(k, k + 1, nt, "side")                 # column k+1 only
-                ops.panel(k + 1, "side")
-                ops.pack(k + 1, "side")
-            h = yield ("bcast", k + 1, owner(k + 1))
-            first = owned_first(k + 1, rank, world)
-            if first == k + 1 and rank == owner(k + 1):
+            if rank == owner(sp + 1):
+                ops.update(sp, col(sp + 1), nt, width(sp + 1), "side")      # the next super-panel only
+                ops.panel(sp + 1, "side")
+                ops.pack(sp + 1, "side")
+            h = yield ("bcast", sp + 1, owner(sp + 1))
+            first = owned_first(sp + 1, rank, world)
+            if first == sp + 1 and rank == owner(sp + 1):
                 first += world
-            ops.update(k, first, world, "main", side_busy=(rank == owner(k + 1)))
+            ops.update(sp, col(first), kp * world, kp, "main", side_busy=(rank == owner(sp + 1)))
     ops.join()
 
 
@@ -183,43 +192,44 @@ class CudaPotrfOps:
 
     SIDE_SMS = 8                                 # SMs left free for the panel chain (cf. kPanelSMs)
 
-    def __init__(self, L, n: int, main=None):
+    def __init__(self, L, n: int, main=None, kp: int | None = None):
         import torch
-        from . import panel_numel
+        from . import mvn_potrf_panel_width, panel_numel
         self.torch = torch
         self.L, self.n = L, n
         self.nt = -(-n // TILE)
+        self.kp = kp or mvn_potrf_panel_width()
         self.dev = L.device
         self.main = main if main is not None else torch.cuda.current_stream(self.dev)
         self.side = torch.cuda.Stream(device=self.dev, priority=-1)
         self.side.wait_stream(self.main)
-        m = panel_numel(n, 0)
+        m = panel_numel(n, 0, self.kp)
         self.bufs = [torch.empty(m, dtype=torch.float64, device=self.dev) for _ in range(2)]
 
     def _st(self, which):
         return self.main if which == "main" else self.side
 
-    def panel_buf(self, k: int):
+    def panel_buf(self, sp: int):
         from . import panel_numel
-        return self.bufs[k & 1][:panel_numel(self.n, k)]
+        return self.bufs[sp & 1][:panel_numel(self.n, sp * self.kp, self.kp)]
 
-    def panel(self, k, on):
+    def panel(self, sp, on):
         from . import mvn_potrf_panel
-        mvn_potrf_panel(self.L, self.n, k, stream=self._st(on))
+        mvn_potrf_panel(self.L, self.n, sp * self.kp, self.kp, stream=self._st(on))
 
-    def pack(self, k, on):
+    def pack(self, sp, on):
         from . import mvn_panel_pack
-        mvn_panel_pack(self.L, self.n, k, self.panel_buf(k), stream=self._st(on))
+        mvn_panel_pack(self.L, self.n, sp * self.kp, self.kp, self.panel_buf(sp), stream=self._st(on))
 
-    def unpack(self, k, on):
+    def unpack(self, sp, on):
         from . import mvn_panel_unpack
-        mvn_panel_unpack(self.panel_buf(k), self.n, k, self.L, stream=self._st(on))
+        mvn_panel_unpack(self.panel_buf(sp), self.n, sp * self.kp, self.kp, self.L, stream=self._st(on))
 
-    def update(self, k, c0, cs, on, side_busy=True):
+    def update(self, sp, c0, cs, cb, on, side_busy=True):
         from . import mvn_potrf_update
         if c0 < self.nt:
             reserve = self.SIDE_SMS if (on == "main" and side_busy) else 0
-            mvn_potrf_update(self.L, self.n, k, c0, cs, reserve, stream=self._st(on))
+            mvn_potrf_update(self.L, self.n, sp * self.kp, self.kp, c0, cs, cb, reserve, stream=self._st(on))
 
     def record(self, on):
         ev = self.torch.cuda.Event()

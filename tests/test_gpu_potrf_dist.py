@@ -81,55 +81,61 @@ def emulate(torch, tiles, n):
     return mvn().mvn_potrf_info(0, reset=True)
 
 
-def test_panel_pack_unpack(torch):
+@pytest.mark.parametrize("kp", [1, 2, 3])
+def test_panel_pack_unpack(torch, kp):
     n = 5 * NB + 3
     T, _ = sigma(torch, n)
+    nt = -(-n // NB)
+    Th = T.cpu().numpy()
     for k in (0, 2, 5):
-        buf = torch.empty(mvn().panel_numel(n, k), dtype=torch.float64, device="cuda")
-        mvn().mvn_panel_pack(T, n, k, buf)
-        nt = -(-n // NB)
-        Th = T.cpu().numpy()
-        for i in range(k, nt):
-            off = (i * (i + 1) // 2 + k) * NB * NB
-            assert np.array_equal(buf[(i - k) * NB * NB:(i - k + 1) * NB * NB].cpu().numpy(), Th[off:off + NB * NB])
+        buf = torch.empty(mvn().panel_numel(n, k, kp), dtype=torch.float64, device="cuda")
+        mvn().mvn_panel_pack(T, n, k, kp, buf)
         T2 = torch.zeros_like(T)
-        mvn().mvn_panel_unpack(buf, n, k, T2)
-        T2h = T2.cpu().numpy()
-        for i in range(k, nt):
-            off = (i * (i + 1) // 2 + k) * NB * NB
-            assert np.array_equal(T2h[off:off + NB * NB], Th[off:off + NB * NB])
+        mvn().mvn_panel_unpack(buf, n, k, kp, T2)
+        bh, T2h = buf.cpu().numpy(), T2.cpu().numpy()
+        q = 0
+        for c in range(k, min(k + kp, nt)):
+            for i in range(c, nt):
+                off = (i * (i + 1) // 2 + c) * NB * NB
+                assert np.array_equal(bh[q * NB * NB:(q + 1) * NB * NB], Th[off:off + NB * NB])
+                assert np.array_equal(T2h[off:off + NB * NB], Th[off:off + NB * NB])
+                q += 1
+        assert q * NB * NB == buf.numel()
 
 
-@pytest.mark.parametrize("c0,cs", [(1, 1), (2, 3), (4, 2), (3, 100)])
-def test_update_column_filter(torch, c0, cs):
-    """mvn_potrf_update(k=0, c0, cs) on a random tile buffer == numpy A_ij -= L_i0 L_j0^T on the
-    selected tile columns, untouched elsewhere (small k so that the persistent kernel, taken for
-    >= 2*(148-8) tiles, is exercised at n = 40 tiles)."""
+@pytest.mark.parametrize("kp,c0,cs,cb", [(1, 1, 1, 1), (1, 2, 3, 1), (2, 2, 1, 1), (2, 3, 4, 2), (2, 4, 100, 2),
+                                         (1, 3, 100, 1)])
+def test_update_column_filter(torch, kp, c0, cs, cb):
+    """mvn_potrf_update(k = 0, kp, c0, cs, cb) on a random tile buffer == numpy
+    A_ij -= sum_{c < kp} L_ic L_jc^T on the selected tile columns j = c0 + m cs + b (b < cb),
+    untouched elsewhere; 40 tile rows exercise the persistent kernel (>= 2 (148 - 8) tiles)."""
     for ntile in (7, 40):
         n = ntile * NB
         cnt = ntile * (ntile + 1) // 2
         rng = np.random.default_rng(ntile + c0)
         host = rng.standard_normal(cnt * NB * NB)
         T = torch.from_numpy(host.copy()).cuda()
-        mvn().mvn_potrf_update(T, n, 0, c0, cs, 8)
+        mvn().mvn_potrf_update(T, n, 0, kp, c0, cs, cb, 8)
         got = T.cpu().numpy()
 
         def tile(a, i, j):
             off = (i * (i + 1) // 2 + j) * NB * NB
             return a[off:off + NB * NB].reshape(NB, NB).T          # column-major -> logical
 
+        sel = {c0 + m * cs + b for m in range(ntile) for b in range(cb)}
         for j in range(ntile):
             for i in range(j, ntile):
                 want = tile(host, i, j)
-                if j >= c0 and (j - c0) % cs == 0:
-                    want = want - tile(host, i, 0) @ tile(host, j, 0).T
-                    assert np.max(np.abs(tile(got, i, j) - want)) <= 1e-12 * NB
+                if j in sel:
+                    for c in range(kp):
+                        want = want - tile(host, i, c) @ tile(host, j, c).T
+                    assert np.max(np.abs(tile(got, i, j) - want)) <= 1e-12 * NB * kp
                 else:
                     assert np.array_equal(tile(got, i, j), want)
 
 
 @pytest.mark.parametrize("n,nu,W", [(1000, 0.5, 1), (1000, 0.5, 2), (2000, 1.5, 3), (4000, 0.5, 4), (5000, 0.5, 2),
-                                    (130, 0.5, 3), (40 * NB + 77, 0.5, 3)])
+                                    (130, 0.5, 3), (40 * NB + 77, 0.5, 3), (300, 0.5, 2), (75 * NB, 0.5, 4)])
 def test_emulated_distributed_potrf_matches_single_gpu(torch, n, nu, W):
     T, S = sigma(torch, n, nu)
     ref = T.clone()

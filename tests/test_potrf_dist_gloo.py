@@ -24,11 +24,12 @@ def tidx(i, j):
 
 class NumpyPotrfOps:
     """Tile-packed lower storage as an array [tiles][nb][nb] (logical row-major tiles); the same
-    semantics as mvn_potrf_panel / mvn_potrf_update / mvn_panel_pack / mvn_panel_unpack."""
+    semantics as mvn_potrf_panel / mvn_potrf_update / mvn_panel_pack / mvn_panel_unpack with
+    super-panels of kp tile columns. `applied[(i, j)]` logs the columns applied to tile (i, j)."""
 
-    def __init__(self, A: np.ndarray):
+    def __init__(self, A: np.ndarray, kp: int = 2):
         n = A.shape[0]
-        self.n, self.nt = n, -(-n // NB)
+        self.n, self.nt, self.kp = n, -(-n // NB), kp
         npad = self.nt * NB
         P = np.eye(npad)
         P[:n, :n] = A
@@ -36,40 +37,65 @@ class NumpyPotrfOps:
         for i in range(self.nt):
             for j in range(i + 1):
                 self.T[tidx(i, j)] = P[i * NB:(i + 1) * NB, j * NB:(j + 1) * NB]
-        self.bufs = [np.zeros((self.nt, NB, NB)) for _ in range(2)]
+        self.bufs = [np.zeros((kp * self.nt, NB, NB)) for _ in range(2)]
         self.first_fail = -1
         self.log = []
+        self.applied = {}
 
-    def panel_buf(self, k):
-        return torch.from_numpy(self.bufs[k & 1][:self.nt - k])
+    def cols(self, sp):
+        k = sp * self.kp
+        return list(range(k, min(k + self.kp, self.nt)))
 
-    def panel(self, k, on):
-        self.log.append(("panel", k, on))
-        D = self.T[tidx(k, k)]
-        try:
-            Lkk = np.linalg.cholesky(D)
-        except np.linalg.LinAlgError:
-            if self.first_fail < 0:
-                d = np.linalg.eigvalsh(D)
-                self.first_fail = k * NB
-            return
-        self.T[tidx(k, k)] = Lkk
-        for i in range(k + 1, self.nt):
-            self.T[tidx(i, k)] = sla.solve_triangular(Lkk, self.T[tidx(i, k)].T, lower=True).T
+    def tiles_of(self, sp):
+        return [(i, c) for c in self.cols(sp) for i in range(c, self.nt)]
 
-    def pack(self, k, on):
-        for i in range(k, self.nt):
-            self.bufs[k & 1][i - k] = self.T[tidx(i, k)]
+    def panel_buf(self, sp):
+        return torch.from_numpy(self.bufs[sp & 1][:len(self.tiles_of(sp))])
 
-    def unpack(self, k, on):
-        for i in range(k, self.nt):
-            self.T[tidx(i, k)] = self.bufs[k & 1][i - k]
+    def _apply(self, i, j, cs):
+        for c in cs:
+            self.T[tidx(i, j)] -= self.T[tidx(i, c)] @ self.T[tidx(j, c)].T
+        self.applied.setdefault((i, j), []).extend(cs)
 
-    def update(self, k, c0, cs, on, side_busy=True):
-        self.log.append(("update", k, c0, cs, on))
-        for j in range(c0, self.nt, cs):
-            for i in range(j, self.nt):
-                self.T[tidx(i, j)] -= self.T[tidx(i, k)] @ self.T[tidx(j, k)].T
+    def panel(self, sp, on):
+        cs = self.cols(sp)
+        self.log.append(("panel", sp, on))
+        for q, c in enumerate(cs):
+            for i in range(c, self.nt):
+                if q:
+                    self._apply(i, c, cs[:q])
+            D = self.T[tidx(c, c)]
+            try:
+                Lcc = np.linalg.cholesky(D)
+            except np.linalg.LinAlgError:
+                if self.first_fail < 0:
+                    self.first_fail = c * NB
+                return
+            self.T[tidx(c, c)] = Lcc
+            for i in range(c + 1, self.nt):
+                self.T[tidx(i, c)] = sla.solve_triangular(Lcc, self.T[tidx(i, c)].T, lower=True).T
+
+    def pack(self, sp, on):
+        for q, (i, c) in enumerate(self.tiles_of(sp)):
+            self.bufs[sp & 1][q] = self.T[tidx(i, c)]
+
+    def unpack(self, sp, on):
+        for q, (i, c) in enumerate(self.tiles_of(sp)):
+            self.T[tidx(i, c)] = self.bufs[sp & 1][q]
+
+    def update(self, sp, c0, cs, cb, on, side_busy=True):
+        self.log.append(("update", sp, c0, cs, cb, on))
+        m = 0
+        while True:
+            base = c0 + m * cs
+            if base >= self.nt:
+                break
+            for b in range(cb):
+                j = base + b
+                if j < self.nt:
+                    for i in range(j, self.nt):
+                        self._apply(i, j, self.cols(sp))
+            m += 1
 
     def record(self, on):
         return None
@@ -100,42 +126,31 @@ def spd(n, seed=3):
 
 def test_owned_first():
     for world in (1, 2, 3, 8):
-        for col in range(20):
+        for sp in range(20):
             for r in range(world):
-                f = owned_first(col, r, world)
-                assert f >= col and f % world == r and f - col < world
+                f = owned_first(sp, r, world)
+                assert f >= sp and f % world == r and f - sp < world
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 5])
-def test_schedule_covers_every_update_once(world):
-    """Replays the schedule of all ranks in lockstep: each tile (i, j) receives the updates of
-    panels 0..j-1 exactly once, in ascending k, on the rank that owns column j, before column j
-    is factored; panels are factored in order by their owners."""
+@pytest.mark.parametrize("world,kp", [(1, 2), (2, 2), (3, 2), (5, 2), (3, 1), (2, 3)])
+def test_schedule_covers_every_update_once(world, kp):
+    """Replays each rank's schedule: every tile (i, j) of a column the rank owns receives the
+    updates of columns 0 .. j-1 exactly once, in ascending order, before column j is factored;
+    super-panels are factored by their owners, in order."""
     n = 9 * NB + 17
     nt = -(-n // NB)
-    logs = []
     for r in range(world):
-        ops = NumpyPotrfOps(np.eye(n))
-        g = potrf_dist_schedule(ops, r, world)
-        for _ in g:
+        ops = NumpyPotrfOps(np.eye(n), kp)
+        for _ in potrf_dist_schedule(ops, r, world):
             pass
-        logs.append(ops.log)
-    for r in range(world):
-        seen = {}
-        factored = set()
-        for ev in logs[r]:
-            if ev[0] == "panel":
-                k = ev[1]
-                assert k % world == r
-                assert all(seen.get((i, k), []) == list(range(k)) for i in range(k, nt))
-                factored.add(k)
-            else:
-                _, k, c0, cs, _ = ev
-                for j in range(c0, nt, cs):
-                    assert j % world == r and j > k
-                    for i in range(j, nt):
-                        seen.setdefault((i, j), []).append(k)
-        assert factored == {k for k in range(nt) if k % world == r}
+        owned_sp = [sp for sp in range(-(-nt // kp)) if sp % world == r]
+        assert [e[1] for e in ops.log if e[0] == "panel"] == owned_sp
+        for sp in owned_sp:
+            for j in ops.cols(sp):
+                for i in range(j, nt):
+                    assert ops.applied.get((i, j), []) == list(range(j)), (r, i, j, ops.applied.get((i, j)))
+        for (i, j), cs in ops.applied.items():
+            assert (j // kp) % world == r                     # only own columns are touched
 
 
 def _worker(rank, world, port, n, out, bad_row):
@@ -144,7 +159,7 @@ def _worker(rank, world, port, n, out, bad_row):
     A = spd(n)
     if bad_row is not None:
         A[bad_row, bad_row] = -1.0
-    ops = NumpyPotrfOps(A)
+    ops = NumpyPotrfOps(A, 2)
     info = potrf_distributed(None, n, ops=ops)
     out[rank] = (info, ops.dense_L())
     dist.destroy_process_group()
@@ -174,7 +189,7 @@ def test_distributed_potrf_gloo(world):
 
 
 def test_distributed_potrf_gloo_reports_failure():
-    n, world = 4 * NB, 2
+    n, world = 6 * NB, 2
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(world, free_port(), n, out, 2 * NB + 5), nprocs=world, join=True)

@@ -1,0 +1,33 @@
+"""Time mvn_potrf alone (CUDA events) on a BASELINE config: python tools/potrf_time.py D [reps].
+MVN_POTRF_KP (super-panel width) is read once per process, so A/B runs use separate processes."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2405_14892_b200 as mvn  # noqa: E402
+import workloads as W  # noqa: E402
+
+cfg = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "D"]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+inp = W.make_inputs(cfg)
+n = cfg.n
+order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
+d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+L = mvn.alloc_tiles(n)
+ts = []
+for it in range(reps + 1):
+    mvn.mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, out=L)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    info = mvn.mvn_potrf(L, n)
+    e1.record()
+    torch.cuda.synchronize()
+    assert info == -1
+    if it:
+        ts.append(e0.elapsed_time(e1))
+ms = float(np.mean(ts))
+print(f"cfg={cfg.name} kp={os.environ.get('MVN_POTRF_KP', 'def')} potrf_ms={ms:.1f} "
+      f"tflops={n ** 3 / 3 / (ms / 1e3) / 1e12:.2f} frac={n ** 3 / 3 / (ms / 1e3) / 1e12 / 37.07:.3f}", flush=True)

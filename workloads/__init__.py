@@ -107,3 +107,28 @@ def small_config(name: str, g: int, N: int, R: int, base: str = "A", **kw) -> Co
     d = dict(c.__dict__)
     d.update(name=name, g=g, N=N, R=R, **kw)
     return Config(**d)
+
+
+@dataclass
+class PosteriorInputs:
+    cfg: Config
+    xy: np.ndarray
+    mu: np.ndarray          # prior mean (0, the paper's choice "mu = 0")
+    obs: np.ndarray         # m distinct observed site indices (sorted)
+    y: np.ndarray           # m noisy observations
+    tau: float
+
+
+def make_posterior_inputs(cfg: Config | str, m: int, tau: float = 0.5, seed: int = 4242) -> PosteriorInputs:
+    """NEXT-4 workload (§V-A: "6,250 samples under the additive noise N(0, 0.5^2)
+    ... randomly selected"): the config's jittered grid, a zero prior mean, a hidden field drawn
+    from the same GP (random Fourier features, as for mu), m sites chosen uniformly without
+    replacement, y = field + N(0, tau^2) noise. Seeded; no method arithmetic."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    xy = jittered_grid(cfg.g, cfg.seed_geom)
+    field_ = gp_mean_draw(xy, cfg.sigma2, cfg.beta, cfg.nu, seed)
+    rng = np.random.default_rng(seed + 1)
+    obs = np.sort(rng.choice(xy.shape[0], size=m, replace=False)).astype(np.int64)
+    y = field_[obs] + tau * rng.standard_normal(m)
+    return PosteriorInputs(cfg, xy, np.zeros(xy.shape[0]), obs, y, tau)
