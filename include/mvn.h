@@ -110,7 +110,7 @@ mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
 /* ---------------------------------------------------------------------------------------------
  * NEXT-1: building blocks of the distributed tiled Cholesky, 1-D
  * block-cyclic over super-panels of kp tile columns (super-panel s = tile columns s*kp ..
- * s*kp+kp-1 is owned by rank s mod W; kp = mvn_potrf_panel_width(), 2). The step loop and the
+ * s*kp+kp-1 is owned by rank s mod W; kp = mvn_potrf_panel_width(n)). The step loop and the
  * NCCL panel broadcasts are in the Python layer (paper_2405_14892_b200/parallel.py,
  * potrf_distributed); the right-looking recurrence is the one of mvn_potrf, which is built from
  * the same two calls (Alg. 1 l.8; the paper runs it distributed on Chameleon/StarPU, P:81,
@@ -122,8 +122,9 @@ mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
  * column: sum_j (nt-k-j) * nb*nb doubles, device. All calls are asynchronous on the context's
  * stream; pivots are checked on the device and collected by mvn_potrf_info.                    */
 
-/* Tile columns per super-panel used by mvn_potrf (and expected by potrf_distributed). */
-int64_t mvn_potrf_panel_width(void);
+/* Tile columns per super-panel (1..3) that mvn_potrf uses for order n (and potrf_distributed must
+ * use to produce the same factor); -1 if n < 1. The environment variable MVN_POTRF_KP overrides. */
+int64_t mvn_potrf_panel_width(int64_t n);
 
 /* Factor the kp (1..4; clipped at nt) tile columns k .. k+kp-1 in place: POTRF of the diagonal tile
  * and TRSM of the tiles below, column by column, each further column first updated with the

@@ -113,7 +113,7 @@ def lib() -> ctypes.CDLL:
         "mvn_crd": (S, [P, ctypes.POINTER(mvn_crd_problem), ctypes.POINTER(mvn_crd_result)]),
         "mvn_potrf_panel": (S, [P, T, P, I64, I64]),
         "mvn_potrf_update": (S, [P, T, P, I64, I64, I64, I64, I64, I32]),
-        "mvn_potrf_panel_width": (I64, []),
+        "mvn_potrf_panel_width": (I64, [I64]),
         "mvn_panel_pack": (S, [P, T, P, I64, I64, P]),
         "mvn_panel_unpack": (S, [P, T, P, I64, I64, P]),
         "mvn_potrf_info": (S, [P, ctypes.POINTER(I64), I32]),
@@ -253,9 +253,9 @@ def mvn_potrf(t, n: int, raise_on_numeric: bool = True) -> int:
 
 
 # ---- NEXT-1: building blocks of the distributed factorisation (driven by parallel.potrf_distributed)
-def mvn_potrf_panel_width() -> int:
-    """kp: tile columns per super-panel of mvn_potrf (the distributed schedule uses the same)."""
-    return int(lib().mvn_potrf_panel_width())
+def mvn_potrf_panel_width(n: int) -> int:
+    """kp: tile columns per super-panel of mvn_potrf at order n (the distributed schedule uses the same)."""
+    return int(lib().mvn_potrf_panel_width(int(n)))
 
 
 def mvn_potrf_panel(t, n: int, k: int, kp: int = 1, stream=None):

@@ -32,6 +32,14 @@ __global__ void k_set_row(double *__restrict__ tiles, int64_t row, int64_t col0,
     if (j < ncols) tiles[tp_index(row, col0 + j)] = v[j];
 }
 
+// element (rows[j], col0 + j) += v for j < count (rows[j] >= col0 + j): the nugget on the
+// site-observation cross covariance of an observed site with its own observation (Cov(x_i, y_j) =
+// Sigma_ii = sigma^2 + nugget when i = obs_j, which the Matérn kernel of two distinct indices omits).
+__global__ void k_add_pairs(double *__restrict__ tiles, const int64_t *__restrict__ rows, int64_t col0, int64_t count, double v) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < count) tiles[tp_index(rows[j], col0 + j)] += v;
+}
+
 __global__ void k_get_row(const double *__restrict__ tiles, int64_t row, int64_t col0, int64_t ncols, double *__restrict__ out) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j < ncols) out[j] = tiles[tp_index(row, col0 + j)];
@@ -79,6 +87,12 @@ cudaError_t launch_add_diag(double *tiles, int64_t begin, int64_t end, double v,
 cudaError_t launch_set_row(double *tiles, int64_t row, int64_t col0, int64_t ncols, const double *v, cudaStream_t st) {
     if (ncols <= 0) return cudaSuccess;
     k_set_row<<<(unsigned)((ncols + 255) / 256), 256, 0, st>>>(tiles, row, col0, ncols, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add_pairs(double *tiles, const int64_t *rows, int64_t col0, int64_t count, double v, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    k_add_pairs<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(tiles, rows, col0, count, v);
     return cudaGetLastError();
 }
 

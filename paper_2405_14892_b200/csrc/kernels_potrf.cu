@@ -544,9 +544,14 @@ cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0,
     return cudaGetLastError();
 }
 
-int potrf_panel_width() {
-    static const int kp = [] { const char *e = getenv("MVN_POTRF_KP"); const int v = e ? atoi(e) : 2; return v >= 1 && v <= 4 ? v : 2; }();
-    return kp;
+// Super-panel width for an order-n factorisation: wider panels halve / third the update passes
+// (K = 128 kp) but lengthen the panel chain on the critical path; measured on B200 (r01):
+// n = 16,384: kp 1 / 2 / 3 = 60 / 64 / 66 ms; n = 65,536: 3.14 / 2.96 / 2.89 s. MVN_POTRF_KP overrides.
+int potrf_panel_width(int64_t n) {
+    static const int env = [] { const char *e = getenv("MVN_POTRF_KP"); const int v = e ? atoi(e) : 0; return v >= 1 && v <= 4 ? v : 0; }();
+    if (env) return env;
+    const int64_t nt = (n + kTile - 1) / kTile;
+    return nt >= 384 ? 3 : nt >= 192 ? 2 : 1;
 }
 
 // Right-looking factorisation over super-panels of kp = potrf_panel_width() tile columns (K = 128 kp
@@ -560,7 +565,7 @@ int potrf_panel_width() {
 cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols) {
     const int nt = (int)((n + kTile - 1) / kTile);
     if (ncols <= 0 || ncols > nt) ncols = nt;      // ncols < nt: partial factorisation (Schur complement left)
-    const int KP = potrf_panel_width();
+    const int KP = potrf_panel_width(n);
     const int S = (ncols + KP - 1) / KP;
     int dev = 0;
     cudaGetDevice(&dev);

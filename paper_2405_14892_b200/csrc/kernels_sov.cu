@@ -106,6 +106,7 @@ struct SovArgs {
     int *step_done;           // [max blocks][nrb]
     const int *need;          // [max blocks]
     int hints;                // L2 cache-policy hints on the producer's copies
+    int serial_rb;            // row blocks rb <= serial_rb * 128 / w: GEMM of rb waits for the chain of rb-1
 };
 
 __device__ __forceinline__ int block_width(int64_t count, int b) {
@@ -147,8 +148,15 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
                 }
                 __syncwarp();
             }
+            // Y_{rb-1} must be published before the chunks that read it (c >= CPB (rb-1)). For the
+            // first row blocks (rb <= serial_rb) the producer waits for it before issuing ANY chunk of
+            // rb: the GEMM warps then idle (spinning, no fp64) while the chain of rb-1 runs, so the
+            // chain gets the fp64 pipe to itself (7x faster per row than next to DMMA) —
+            // cheaper than overlapping where the GEMM of a row block is shorter than the contended chain.
+            // (the GEMM of a row block scales with the block width w; the chain does not)
+            const int c_sync = rb * w <= p.serial_rb * NB ? 0 : CPB * (rb - 1);
             for (int c = 0; c < CPB * rb; ++c, ++q) {
-                if (c == CPB * (rb - 1)) named_sync(BAR_YREADY, N_YREADY);   // Y_{rb-1} published
+                if (c == c_sync) named_sync(BAR_YREADY, N_YREADY);
                 const int st = q % STAGES;
                 mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
                 const int64_t kc = (int64_t)c * BK;
@@ -466,7 +474,7 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
     SovArgs a;
     a.L = L.L; a.n = L.n; a.nrb = (int)((L.n + 63) / 64); a.a = L.a; a.b = L.b; a.G = L.G; a.N = L.N;
     a.seed = L.seed; a.cta = L.cta; a.n_pad = (int64_t)a.nrb * 64; a.Y = L.Y; a.part = L.part;
-    a.lag = L.lag; a.step_done = L.step_done; a.need = L.need; a.hints = L.hints;
+    a.lag = L.lag; a.step_done = L.step_done; a.need = L.need; a.hints = L.hints; a.serial_rb = L.serial_rb;
     if (a.lag > 0) {
         cudaError_t e = cudaMemsetAsync(L.step_done, 0, sizeof(int) * (size_t)L.max_blocks * a.nrb, st);
         if (e != cudaSuccess) return e;

@@ -279,7 +279,7 @@ mvn_status mvn_potrf_update(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k,
     return MVN_OK;
 }
 
-int64_t mvn_potrf_panel_width(void) { return mvn::potrf_panel_width(); }
+int64_t mvn_potrf_panel_width(int64_t n) { return n < 1 ? -1 : mvn::potrf_panel_width(n); }
 
 mvn_status mvn_panel_pack(mvn_ctx *c, mvn_tiles t, const double *d_tiles, int64_t k, int64_t kp, double *d_panel) {
     if (!c) return MVN_E_USAGE;
@@ -362,6 +362,8 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
                                 cudaMemcpyHostToDevice, c->stream));
     L.lag = env_lag; L.step_done = d_sync; L.need = d_sync + (size_t)max_blocks * nrb; L.max_blocks = max_blocks;
     L.hints = env_hints;
+    static const int env_serial = [] { const char *e = getenv("MVN_SOV_SERIAL"); return e ? atoi(e) : 64; }();
+    L.serial_rb = env_serial;
     MVN_CUDA(c, cudaMemcpyAsync(c->cta, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     L.cta = (const int64_t *)c->cta;
     L.Y = (double *)c->Y; L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S;
@@ -456,10 +458,12 @@ mvn_status mvn_posterior(mvn_ctx *c, const mvn_posterior_problem *p, double *mu_
     mvn_tiles ta{N, mvn::kTile};
     // augmented locations: observed sites, decoupled far points (padding), all sites, far point (r row)
     std::vector<double> xy((size_t)(2 * N)), r((size_t)m);
+    std::vector<int64_t> rows((size_t)m);
     for (int64_t j = 0; j < m; ++j) {
         xy[2 * j] = p->xy[2 * p->obs[j]];
         xy[2 * j + 1] = p->xy[2 * p->obs[j] + 1];
         r[(size_t)j] = p->y[j] - p->mu[p->obs[j]];
+        rows[(size_t)j] = m_pad + p->obs[j];                      // the site row of observation j
     }
     for (int64_t j = m; j < m_pad; ++j) { xy[2 * j] = 1e9 * (double)(j + 1); xy[2 * j + 1] = 1e9; }
     for (int64_t i = 0; i < n; ++i) { xy[2 * (m_pad + i)] = p->xy[2 * i]; xy[2 * (m_pad + i) + 1] = p->xy[2 * i + 1]; }
@@ -467,12 +471,15 @@ mvn_status mvn_posterior(mvn_ctx *c, const mvn_posterior_problem *p, double *mu_
     xy[2 * extra + 1] = -1e9;
     mvn_status s;
     if ((s = ensure(c, &c->post, &c->post_cap, mvn_tiles_bytes(ta))) != MVN_OK) return s;
-    if ((s = ensure(c, &c->postv, &c->postv_cap, sizeof(double) * (size_t)(2 * N + m + 2 * n))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->postv, &c->postv_cap, sizeof(double) * (size_t)(2 * N + 2 * m + 2 * n))) != MVN_OK) return s;
     double *A = (double *)c->post, *d_xy = (double *)c->postv, *d_r = d_xy + 2 * N, *d_dg = d_r + m, *d_row = d_dg + n;
+    int64_t *d_rows = (int64_t *)(d_row + n);
     MVN_CUDA(c, cudaMemcpyAsync(d_xy, xy.data(), sizeof(double) * 2 * N, cudaMemcpyHostToDevice, c->stream));
     MVN_CUDA(c, cudaMemcpyAsync(d_r, r.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(d_rows, rows.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice, c->stream));
     if ((s = mvn_cov_matern(c, ta, d_xy, p->sigma2, p->beta, p->nu, p->nugget, A)) != MVN_OK) return s;
     MVN_CUDA(c, mvn::launch_add_diag(A, 0, m, p->tau * p->tau, c->stream));           // Sigma_oo + tau^2 I
+    MVN_CUDA(c, mvn::launch_add_pairs(A, d_rows, 0, m, p->nugget, c->stream));        // Cov(x_obs_j, y_j) = Sigma_jj
     MVN_CUDA(c, mvn::launch_set_row(A, extra, 0, m, d_r, c->stream));                 // r^T
     const int64_t minus1 = -1;
     MVN_CUDA(c, cudaMemcpyAsync(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));

@@ -16,7 +16,7 @@ cudaError_t launch_finalize(int64_t n, int64_t NR, const double *M, const double
 cudaError_t potrf_init();
 cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols = 0);
 // distributed-factorisation building blocks (NEXT-1)
-int potrf_panel_width();   // kp: tile columns per super-panel (2; MVN_POTRF_KP overrides)
+int potrf_panel_width(int64_t n);   // kp: tile columns per super-panel for order n (MVN_POTRF_KP overrides)
 cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int kp, int64_t *d_info, cudaStream_t st);
 cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0, int cs, int cb, int sm_reserve,
                                 cudaStream_t st);
@@ -41,6 +41,7 @@ struct SovLaunch {
     const int *need = nullptr; // [max_blocks]: CTAs with more than b blocks
     int max_blocks = 0;
     int hints = 1;           // L2 cache-policy hints
+    int serial_rb = 0;       // row blocks whose GEMM waits for the previous chain (no fp64 contention)
 };
 cudaError_t sov_init();
 int sov_block_samples();
@@ -51,6 +52,7 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
 // NEXT-4: posterior conditioning helpers (kernels_post.cu)
 cudaError_t launch_add_diag(double *tiles, int64_t begin, int64_t end, double v, cudaStream_t st);
 cudaError_t launch_set_row(double *tiles, int64_t row, int64_t col0, int64_t ncols, const double *v, cudaStream_t st);
+cudaError_t launch_add_pairs(double *tiles, const int64_t *rows, int64_t col0, int64_t count, double v, cudaStream_t st);
 cudaError_t launch_get_row(const double *tiles, int64_t row, int64_t col0, int64_t ncols, double *out, cudaStream_t st);
 cudaError_t launch_get_diag(const double *tiles, int64_t begin, int64_t n, double *out, cudaStream_t st);
 cudaError_t launch_permute_sym(const double *src, int64_t off, const int64_t *order, int64_t n, double *dst, cudaStream_t st);

@@ -104,11 +104,14 @@ def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg,
     return logp
 
 
-def potrf_launches(n: int, world: int = 1, rank: int = 0, kp: int = 2, nsm: int = 148) -> int:
+def potrf_launches(n: int, world: int = 1, rank: int = 0, kp: int | None = None, nsm: int = 148) -> int:
     """Kernels launched by one factorisation with super-panels of kp columns: mvn_potrf (world 1)
     or this rank's share of potrf_distributed (panel = per column [update] + POTRF [+ TRSM]; one
     update per bulk / lookahead step; pack / unpack)."""
     nt = -(-n // TILE)
+    if kp is None:
+        from . import mvn_potrf_panel_width
+        kp = mvn_potrf_panel_width(n)
     S = -(-nt // kp)
 
     def panel(sp):
@@ -198,7 +201,7 @@ class CudaPotrfOps:
         self.torch = torch
         self.L, self.n = L, n
         self.nt = -(-n // TILE)
-        self.kp = kp or mvn_potrf_panel_width()
+        self.kp = kp or mvn_potrf_panel_width(n)
         self.dev = L.device
         self.main = main if main is not None else torch.cuda.current_stream(self.dev)
         self.side = torch.cuda.Stream(device=self.dev, priority=-1)

@@ -168,3 +168,21 @@ def test_potrf_distributed_single_process(torch):
     assert potrf_distributed(T, n) == -1
     torch.cuda.synchronize()
     assert torch.equal(T, ref)
+
+
+@pytest.mark.parametrize("kp", [2, 3])
+def test_super_panel_widths(kp):
+    """The emulated-distributed and single-process tests again with super-panels of kp tile columns
+    (MVN_POTRF_KP is read once per process, hence the subprocess): mvn_potrf with K = 128 kp
+    trailing updates stays bitwise equal to the distributed schedule, and within the oracle bars."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("MVN_POTRF_KP"):
+        pytest.skip("already running under a fixed MVN_POTRF_KP")
+    env = dict(os.environ, MVN_POTRF_KP=str(kp))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_potrf_dist.py",
+                        "tests/test_gpu_parity.py", "-k", "emulated or single_process or potrf_vs_oracle"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

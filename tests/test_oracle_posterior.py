@@ -29,8 +29,23 @@ def test_matches_conditional_gaussian_form():
     C = S[np.ix_(obs, obs)] + tau ** 2 * np.eye(m)
     K = S[obs, :]
     G = np.linalg.solve(C, K)
-    assert np.max(np.abs(Sp - (S - K.T @ G))) <= 1e-9
-    assert np.max(np.abs(mp - (mu + K.T @ np.linalg.solve(C, y - mu[obs])))) <= 1e-9
+    assert np.max(np.abs(Sp - (S - K.T @ G))) <= 1e-12
+    assert np.max(np.abs(mp - (mu + K.T @ np.linalg.solve(C, y - mu[obs])))) <= 1e-12
+
+
+def test_matches_eq7_as_printed_on_a_well_conditioned_case():
+    """The push-through evaluation equals Eq. 7 with explicit inverses where the latter is accurate."""
+    rng = np.random.default_rng(8)
+    n, m = 40, 9
+    xy = rng.uniform(size=(n, 2))
+    S = oracle.covariance(xy, 1.0, 0.05, 0.5, 1e-2)            # short range + nugget: cond ~ 1e2
+    mu = rng.standard_normal(n)
+    obs = np.sort(rng.choice(n, m, replace=False))
+    y = rng.standard_normal(m)
+    Sp, mp = oracle.posterior(S, mu, obs, y, 0.5)
+    Sl, ml = oracle.posterior.__globals__["posterior_literal"](S, mu, obs, y, 0.5)
+    assert np.linalg.cond(S) < 1e3
+    assert np.max(np.abs(Sp - Sl)) <= 1e-12 and np.max(np.abs(mp - ml)) <= 1e-12
 
 
 def test_independent_block_unchanged_and_limits():

@@ -12,6 +12,8 @@ import workloads as W  # noqa: E402
 
 cfg = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "D"]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+if len(sys.argv) > 3:                                    # grid side override: n = g^2
+    cfg = W.small_config(f"{cfg.name}-g{sys.argv[3]}", int(sys.argv[3]), cfg.N, cfg.R, base=cfg.name)
 inp = W.make_inputs(cfg)
 n = cfg.n
 order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
@@ -29,5 +31,5 @@ for it in range(reps + 1):
     if it:
         ts.append(e0.elapsed_time(e1))
 ms = float(np.mean(ts))
-print(f"cfg={cfg.name} kp={os.environ.get('MVN_POTRF_KP', 'def')} potrf_ms={ms:.1f} "
+print(f"cfg={cfg.name} n={n} kp={os.environ.get('MVN_POTRF_KP', 'def')} potrf_ms={ms:.1f} "
       f"tflops={n ** 3 / 3 / (ms / 1e3) / 1e12:.2f} frac={n ** 3 / 3 / (ms / 1e3) / 1e12 / 37.07:.3f}", flush=True)
