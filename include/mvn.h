@@ -122,7 +122,7 @@ mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
  * column: sum_j (nt-k-j) * nb*nb doubles, device. All calls are asynchronous on the context's
  * stream; pivots are checked on the device and collected by mvn_potrf_info.                    */
 
-/* Tile columns per super-panel (1..3) that mvn_potrf uses for order n (and potrf_distributed must
+/* Tile columns per super-panel (1..4) that mvn_potrf uses for order n (and potrf_distributed must
  * use to produce the same factor); -1 if n < 1. The environment variable MVN_POTRF_KP overrides. */
 int64_t mvn_potrf_panel_width(int64_t n);
 

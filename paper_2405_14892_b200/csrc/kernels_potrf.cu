@@ -544,14 +544,18 @@ cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0,
     return cudaGetLastError();
 }
 
-// Super-panel width for an order-n factorisation: wider panels halve / third the update passes
-// (K = 128 kp) but lengthen the panel chain on the critical path; measured on B200 (r01):
-// n = 16,384: kp 1 / 2 / 3 = 60 / 64 / 66 ms; n = 65,536: 3.14 / 2.96 / 2.89 s. MVN_POTRF_KP overrides.
+// Super-panel width for an order-n factorisation: wider panels cut the update passes (K = 128 kp
+// per pass) but lengthen the panel chain on the critical path. Measured on B200 (r01, CUDA events):
+//   n = 16,384  kp 1 / 2 / 3      = 60 / 64 / 66 ms
+//   n = 32,761  kp 1 / 2 / 3      = 409 / 390 / 384 ms
+//   n = 65,536  kp 1 / 2 / 3 / 4  = 3.14 / 2.96 / 2.89 / 2.86 s
+//   n = 102,400 kp 2 / 3 / 4      = 11.21 / 10.96 / 10.83 s
+// MVN_POTRF_KP overrides.
 int potrf_panel_width(int64_t n) {
     static const int env = [] { const char *e = getenv("MVN_POTRF_KP"); const int v = e ? atoi(e) : 0; return v >= 1 && v <= 4 ? v : 0; }();
     if (env) return env;
     const int64_t nt = (n + kTile - 1) / kTile;
-    return nt >= 384 ? 3 : nt >= 192 ? 2 : 1;
+    return nt >= 384 ? 4 : nt >= 192 ? 3 : 1;
 }
 
 // Right-looking factorisation over super-panels of kp = potrf_panel_width() tile columns (K = 128 kp

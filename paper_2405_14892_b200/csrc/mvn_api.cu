@@ -362,7 +362,7 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
                                 cudaMemcpyHostToDevice, c->stream));
     L.lag = env_lag; L.step_done = d_sync; L.need = d_sync + (size_t)max_blocks * nrb; L.max_blocks = max_blocks;
     L.hints = env_hints;
-    static const int env_serial = [] { const char *e = getenv("MVN_SOV_SERIAL"); return e ? atoi(e) : 64; }();
+    static const int env_serial = [] { const char *e = getenv("MVN_SOV_SERIAL"); return e ? atoi(e) : 0; }();   // off: measured no gain (r01)
     L.serial_rb = env_serial;
     MVN_CUDA(c, cudaMemcpyAsync(c->cta, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     L.cta = (const int64_t *)c->cta;

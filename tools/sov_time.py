@@ -13,6 +13,9 @@ import workloads as W  # noqa: E402
 
 cfg = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C"]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+if len(sys.argv) > 4:                                    # reduced variant: grid side g, total samples N*R
+    g, NR = int(sys.argv[3]), int(sys.argv[4])
+    cfg = W.small_config(f"{cfg.name}-g{g}", g, NR // cfg.R, cfg.R, base=cfg.name)
 inp = W.make_inputs(cfg)
 n = cfg.n
 order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
@@ -30,7 +33,7 @@ for it in range(reps + 1):
     if it:
         ts.append(e0.elapsed_time(e1))
 lp = mvn.mvn_prefix_finalize(M, S, cfg.NR).cpu().numpy()
-ms = float(np.mean(ts))
+ms = float(np.mean(ts)) if ts else float("nan")
 fr = n * (n - 1) * cfg.NR / (ms / 1e3) / 1e12 / 37.07
 print(f"cfg={cfg.name} lag={os.environ.get('MVN_SOV_LAG', 'def')} hints={os.environ.get('MVN_SOV_HINTS', 'def')} "
       f"sov_ms={ms:.1f} frac={fr:.3f} logP[-1]={lp[-1]:.12f} logP[100]={lp[min(100, n - 1)]:.15f}", flush=True)
