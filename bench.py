@@ -261,6 +261,90 @@ def run_mc(args, cfg):
     return 0
 
 
+# --------------------------------------------------------------------------------- NEXT-4 / NEXT-1 workloads
+def run_posterior(args):
+    """Posterior conditioning (Eq. 7-8) at the paper's synthetic size: n = 40,000 sites
+    (200 x 200 jittered grid, config-B kernel), m = 6,250 noisy observations (tau = 0.5). Timed:
+    mvn_posterior (augmented Matérn, partial DMMA Cholesky, extraction) + marginal order +
+    mvn_posterior_tiles (permutation into sorted order). Algorithmic flops: m^3/3 + m^2 n + n^2 m."""
+    import torch
+    import paper_2405_14892_b200 as mvn
+    torch.cuda.set_device(0)
+    cfg = W.small_config("posterior-40K", 200, 10_000, 8, base="B")
+    m = 6_250
+    P = W.make_posterior_inputs(cfg, m)
+    n = cfg.n
+    out = mvn.alloc_tiles(n)
+
+    def once():
+        mp, vp = mvn.mvn_posterior(P.xy, P.mu, P.obs, P.y, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, P.tau)
+        order, a, _ = mvn.mvn_marginal_order(mp, vp, cfg.u)
+        mvn.mvn_posterior_tiles(order, out=out)
+        return order
+
+    for _ in range(max(1, args.warmup)):
+        once()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        once()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    mp_ = -(-m // 128) * 128
+    flops = mp_ ** 3 / 3 + mp_ ** 2 * n + float(n) ** 2 * mp_
+    line = {"metric": "posterior conditioning time (NEXT-4)", "value": t * 1e3, "unit": "ms", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{n} sites (200x200 jittered grid, Matern s2=1, beta=0.1, nu=0.5), "
+                                   f"{m} observations, tau=0.5 (P:369)", "n": n, "m": m},
+            "roofline": {"bound": "tensor", "achieved": flops / t / 1e12, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
+                         "frac": flops / t / 1e12 / PEAK_FP64_TFLOPS,
+                         "algorithmic": "m^3/3 + m^2 n + n^2 m (C factor, TRSM, SYRK of the Schur complement); "
+                                        "host-timed incl. H2D/D2H of n-vectors and the permutation"}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_potrf_dist(args, cfg):
+    """NEXT-1 on one GPU: the distributed schedule (parallel.potrf_distributed, W = 1, one generator
+    driven from Python, one ABI call per building block) against mvn_potrf (the same kernels driven
+    from C++): the cost of the Python step loop and of the generic schedule."""
+    import torch
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200 import parallel
+    torch.cuda.set_device(0)
+    inp = W.make_inputs(cfg)
+    n = cfg.n
+    order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
+    d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+    L = mvn.alloc_tiles(n)
+    res = {}
+    for name, fn in [("mvn_potrf", lambda: mvn.mvn_potrf(L, n)), ("potrf_distributed_w1", lambda: parallel.potrf_distributed(L, n))]:
+        ts = []
+        for it in range(args.steps + 1):
+            mvn.mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, out=L)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            assert fn() == -1
+            e1.record()
+            torch.cuda.synchronize()
+            if it:
+                ts.append(e0.elapsed_time(e1))
+        res[name] = float(np.mean(ts))
+    flops = n ** 3 / 3
+    line = {"metric": "Cholesky fp64 TFLOP/s, distributed schedule at W = 1 (NEXT-1)",
+            "value": flops / (res["potrf_distributed_w1"] / 1e3) / 1e12, "unit": "TFLOP/s", "n_gpus": 1,
+            "steps": args.steps, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {cfg.name}: n={n}", "n": n,
+                       "kp": mvn.mvn_potrf_panel_width(n)},
+            "ms": res, "mvn_potrf_tflops": flops / (res["mvn_potrf"] / 1e3) / 1e12,
+            "launches_per_rank_w8": [parallel.potrf_launches(n, 8, r) for r in range(8)]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # --------------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -273,8 +357,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--potrf", default="auto", choices=["auto", "rank0", "dist"],
                     help="N>1: factor on rank 0 + broadcast L, or distributed (NEXT-1); auto = dist")
-    ap.add_argument("--workload", default="crd", choices=["crd", "mc"],
-                    help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions")
+    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist"],
+                    help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
+                         "posterior: NEXT-4 conditioning (paper size: 200x200 sites, 6,250 observations); "
+                         "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU")
     ap.add_argument("--mc-samples", type=int, default=50_000, help="--workload mc: draws (paper: N = 50,000, P:595)")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
@@ -282,6 +368,10 @@ def main():
         return run_reference(args, cfg)
     if args.workload == "mc":
         return run_mc(args, cfg)
+    if args.workload == "posterior":
+        return run_posterior(args)
+    if args.workload == "potrf-dist":
+        return run_potrf_dist(args, cfg)
 
     import torch
     import torch.distributed as dist

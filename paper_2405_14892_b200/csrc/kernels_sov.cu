@@ -109,10 +109,20 @@ struct SovArgs {
     int serial_rb;            // row blocks rb <= serial_rb * 128 / w: GEMM of rb waits for the chain of rb-1
 };
 
-__device__ __forceinline__ int block_width(int64_t count, int b) {
-    const int64_t rem = count - (int64_t)b * sovk::NB;
-    const int cnt = rem < sovk::NB ? (int)rem : sovk::NB;
-    return cnt;
+// Sample blocks of a CTA: its `count` samples are split into nblk = ceil(count / 128) blocks whose
+// widths are multiples of 32 spread as evenly as possible (540 -> 128, 128, 96, 96, 96), so no block
+// degenerates to a 32-wide sliver whose GEMM is too short to hide the chain. Block b starts at sample
+// offset off and holds cnt <= w samples (only the last block can have cnt < w).
+struct BlockGeom { int64_t off; int cnt, w; };
+__device__ __forceinline__ BlockGeom block_geom(int64_t count, int b) {
+    const int64_t units = (count + 31) / 32, nblk = (count + sovk::NB - 1) / sovk::NB;
+    const int64_t q = units / nblk, r = units % nblk;
+    BlockGeom g;
+    g.w = (int)(32 * (q + (b < r ? 1 : 0)));
+    g.off = 32 * ((int64_t)b * q + (b < r ? b : r));
+    const int64_t left = count - g.off;
+    g.cnt = (int)(left < g.w ? left : g.w);
+    return g;
 }
 
 // ------------------------------------------------------------------------------------ producer
@@ -128,7 +138,7 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
     uint32_t q = 0;
     const uint64_t pol_L = policy_evict_last(), pol_Y = policy_evict_first();
     for (int b = 0; b < nblk; ++b) {
-        const int w = (block_width(count, b) + 31) & ~31;
+        const int w = block_geom(count, b).w;
         if (p.lag > 0 && lane == 0) atomicAdd(p.step_done + (int64_t)b * p.nrb, 1);   // row block 0: no GEMM
         for (int rb = 1; rb < p.nrb; ++rb) {
             const int64_t row0 = (int64_t)rb * M;
@@ -369,7 +379,7 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
         // ============================================================ GEMM warps
         uint32_t q = 0;
         for (int b = 0; b < nblk; ++b) {
-            const int w = (block_width(count, b) + 31) & ~31;
+            const int w = block_geom(count, b).w;
             for (int rb = 1; rb < p.nrb; ++rb) {
                 switch (w >> 5) {
                     case 1: sov_gemm_rowblock<1>(sm, rb, tid, q); break;
@@ -384,9 +394,10 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
         // ============================================================ chain warps
         const int j = tid - NGEMM;
         for (int b = 0; b < nblk; ++b) {
-            const int64_t g0 = g_first + (int64_t)b * NB;
-            const int cnt = block_width(count, b);
-            const int w = (cnt + 31) & ~31;
+            const BlockGeom bg = block_geom(count, b);
+            const int64_t g0 = g_first + bg.off;
+            const int cnt = bg.cnt;
+            const int w = bg.w;
             const uint64_t g = (uint64_t)(g0 + (j < cnt ? j : 0));
             const uint64_t r = g / (uint64_t)p.N;
             const uint64_t jl = g - r * (uint64_t)p.N + 1ull;    // 1-based lattice index
