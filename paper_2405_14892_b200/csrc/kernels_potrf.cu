@@ -483,7 +483,11 @@ cudaError_t potrf_init() {
 
 // Streams and events of the single-GPU lookahead schedule (launch_potrf).
 namespace {
-constexpr int kPanelSMs = 8;
+// SMs left to the panel stream beside the persistent update (MVN_POTRF_PANEL_SMS overrides).
+int panel_sms() {
+    static const int v = [] { const char *e = getenv("MVN_POTRF_PANEL_SMS"); const int x = e ? atoi(e) : 8; return x >= 0 && x < 64 ? x : 8; }();
+    return v;
+}
 struct PotrfStreams {
     int dev = -1;
     cudaStream_t sp = nullptr;
@@ -564,7 +568,7 @@ int potrf_panel_width(int64_t n) {
 //   panel stream (high priority): update of the next super-panel's columns with super-panel s, then
 //                                 its factorisation (launch_potrf_panel);
 //   main stream                 : persistent update of the columns after the next super-panel, on
-//                                 all but kPanelSMs SMs, so the panel work runs beside it.
+//                                 all but panel_sms() SMs, so the panel work runs beside it.
 // Events order the two (panel s before update s; update s-1 before the panel-stream update of s).
 cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols) {
     const int nt = (int)((n + kTile - 1) / kTile);
@@ -592,7 +596,7 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
         }
         const int wn = std::min(KP, ncols - kn);
         // main stream: columns >= kn + wn with super-panel s
-        if ((e = launch_potrf_update(n, tiles, k, w, kn + wn, 1, 1, kPanelSMs, st))) return e;
+        if ((e = launch_potrf_update(n, tiles, k, w, kn + wn, 1, 1, panel_sms(), st))) return e;
         if ((e = cudaEventRecord(g_ps.ev_rest[s & 1], st))) return e;
         // panel stream: columns kn .. kn+wn-1 with super-panel s, then factor super-panel s+1
         if (s >= 1 && (e = cudaStreamWaitEvent(sp, g_ps.ev_rest[(s - 1) & 1], 0))) return e;
