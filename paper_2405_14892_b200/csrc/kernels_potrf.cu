@@ -484,8 +484,9 @@ cudaError_t potrf_init() {
 // Streams and events of the single-GPU lookahead schedule (launch_potrf).
 namespace {
 // SMs left to the panel stream beside the persistent update (MVN_POTRF_PANEL_SMS overrides).
+// Measured at D (r01): 4 / 6 / 8 / 12 SMs -> 2.814 / 2.825 / 2.845 / 2.925 s.
 int panel_sms() {
-    static const int v = [] { const char *e = getenv("MVN_POTRF_PANEL_SMS"); const int x = e ? atoi(e) : 8; return x >= 0 && x < 64 ? x : 8; }();
+    static const int v = [] { const char *e = getenv("MVN_POTRF_PANEL_SMS"); const int x = e ? atoi(e) : 4; return x >= 0 && x < 64 ? x : 4; }();
     return v;
 }
 struct PotrfStreams {
