@@ -193,7 +193,7 @@ class CudaPotrfOps:
     """libmvn building blocks for potrf_dist_schedule on one device: the bulk updates on `main`
     (default: torch's current stream), the panel chain on a high-priority side stream."""
 
-    SIDE_SMS = 8                                 # SMs left free for the panel chain (cf. kPanelSMs)
+    SIDE_SMS = 4                                 # SMs left free for the panel chain (as mvn_potrf, panel_sms())
 
     def __init__(self, L, n: int, main=None, kp: int | None = None):
         import torch
