@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 import workloads as W  # noqa: E402
 
 PEAK_FP64_TFLOPS = 37.07          # measured DMMA peak on this pool (profiles/r01_fp64_calibration.md)
+INT8_PEAK_POPS = 4.75             # tcgen05 kind::i8 dense, measured 8,174 MAC/clk/SM at 1,965 MHz (tools/umma_i8_test.cu)
 METRIC = "SOV-QMC n·N sample-dims/s"
 UNIT = "sample-dims/s"
 
@@ -212,7 +213,7 @@ def run_mc(args, cfg):
     count = torch.zeros(n + 1, dtype=torch.uint64, device="cuda")
     for _ in range(args.warmup):
         count.zero_()
-        mvn.mvn_mc_validate(L, n, d_a, 777, b, e, count=count)
+        mvn.mvn_mc_validate(L, n, d_a, 777, b, e, count=count, method=args.mc_method)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
@@ -224,7 +225,7 @@ def run_mc(args, cfg):
     for _ in range(args.steps):
         count.zero_()
         ev0.record()
-        mvn.mvn_mc_validate(L, n, d_a, 777, b, e, count=count)
+        mvn.mvn_mc_validate(L, n, d_a, 777, b, e, count=count, method=args.mc_method)
         ev1.record()
         torch.cuda.synchronize()
         ms.append(ev0.elapsed_time(ev1))
@@ -245,10 +246,16 @@ def run_mc(args, cfg):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config {cfg.name}: MC validation, {Ns} draws of mu + L z", "n": n, "draws": Ns},
-            "roofline": {"kernel": "k_mc_trmm (X = L Z on DMMA + first-failure epilogue)", "bound": "tensor",
-                         "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
-                         "algorithmic": f"n(n+1) flops per draw x {e - b} draws"},
+            "roofline": ({"kernel": "k_mc_trmm (X = L Z on DMMA + first-failure epilogue)", "bound": "tensor",
+                          "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
+                          "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
+                          "algorithmic": f"n(n+1) flops per draw x {e - b} draws"} if args.mc_method == 0 else
+                         {"kernel": "k_oz_trmm (X = L Z as 36 exact int8 GEMMs per 32-K chunk on tcgen05, TMEM)",
+                          "bound": "tensor", "achieved": achieved * 36 / 1e3, "peak": INT8_PEAK_POPS, "unit": "POP/s (int8 MAC x2)",
+                          "frac": achieved * 36 / 1e3 / INT8_PEAK_POPS, "traffic": None,
+                          "fp64_equivalent_tflops": achieved,
+                          "algorithmic": f"n(n+1) fp64-equivalent flops per draw x {e - b} draws; 36 int8 products each"}),
+            "mc_method": args.mc_method,
             "levels": [float(c) for c in cfg.conf], "k_star": [int(k) for k in k_star],
             "p_hat": [float(p) for p in p_hat],
             "one_minus_alpha_minus_p_hat": [float(c - p) for c, p in zip(cfg.conf, p_hat)],
@@ -362,6 +369,8 @@ def main():
                          "posterior: NEXT-4 conditioning (paper size: 200x200 sites, 6,250 observations); "
                          "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU")
     ap.add_argument("--mc-samples", type=int, default=50_000, help="--workload mc: draws (paper: N = 50,000, P:595)")
+    ap.add_argument("--mc-method", type=int, default=0, choices=[0, 1],
+                    help="--workload mc: 0 = fp64 DMMA, 1 = int8 tensor cores (tcgen05 Ozaki emulation)")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":

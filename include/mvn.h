@@ -216,6 +216,10 @@ typedef struct {
     uint64_t seed;         /* z-generator seed */
     int64_t sample_begin;  /* global sample range [begin, end) of this call (a rank's shard) */
     int64_t sample_end;
+    int32_t method;        /* 0: X = L Z on the fp64 tensor path (DMMA); 1: the same product emulated
+                              exactly-per-slice on the int8 tensor cores (tcgen05.mma kind::i8, TMEM
+                              accumulators; Ozaki split into 8 signed 7-bit slices, absolute error
+                              <= ~1e-12 relative to max|L_k.| max|z|, reading R22) */
 } mvn_mc;
 
 /* d_L: tile-packed L (mvn_potrf), d_a: n device doubles (the limits a_k of the sweep).

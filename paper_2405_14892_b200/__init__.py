@@ -53,7 +53,8 @@ class mvn_qmc(ctypes.Structure):
 
 
 class mvn_mc(ctypes.Structure):
-    _fields_ = [("seed", ctypes.c_uint64), ("sample_begin", ctypes.c_int64), ("sample_end", ctypes.c_int64)]
+    _fields_ = [("seed", ctypes.c_uint64), ("sample_begin", ctypes.c_int64), ("sample_end", ctypes.c_int64),
+                ("method", ctypes.c_int32)]
 
 
 class mvn_posterior_problem(ctypes.Structure):
@@ -353,15 +354,16 @@ def mvn_confidence_region(logP: np.ndarray, conf):
 
 
 # ---- NEXT-2: Monte-Carlo validation of the regions
-def mvn_mc_validate(L, n: int, a, seed: int, begin: int, end: int, count=None, first=None):
+def mvn_mc_validate(L, n: int, a, seed: int, begin: int, end: int, count=None, first=None, method: int = 0):
     """Draws samples [begin, end) of mu + L z (reading R20) and accumulates the histogram of their
     first failing rows into `count` (CUDA uint64, n+1; created zeroed if None). `first`: optional
-    CUDA int32 of end-begin, receives f_s. Returns count."""
+    CUDA int32 of end-begin, receives f_s. method 0: X = L Z on fp64 DMMA; 1: on the int8 tensor
+    cores (tcgen05, Ozaki split, R22). Returns count."""
     import torch
     c = Context.get(L.device.index)
     if count is None:
         count = torch.zeros(n + 1, dtype=torch.uint64, device=L.device)
-    m = mvn_mc(int(seed), int(begin), int(end))
+    m = mvn_mc(int(seed), int(begin), int(end), int(method))
     c.check(lib().mvn_mc_validate(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64), ctypes.byref(m),
                                   _dev_ptr(count, torch.uint64), None if first is None else _dev_ptr(first, torch.int32)),
             "mvn_mc_validate")

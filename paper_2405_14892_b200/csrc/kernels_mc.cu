@@ -186,6 +186,16 @@ __global__ void k_mc_count(const int *__restrict__ first, int64_t ns, unsigned l
     if (s < ns) atomicAdd(count + first[s], 1ull);
 }
 
+cudaError_t launch_mc_first_init(int *first, int64_t ns, int n, cudaStream_t st) {
+    k_mc_init<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(first, ns, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mc_count(const int *first, int64_t ns, unsigned long long *count, cudaStream_t st) {
+    k_mc_count<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(first, ns, count);
+    return cudaGetLastError();
+}
+
 cudaError_t mc_init() {
     return cudaFuncSetAttribute(k_mc_trmm, cudaFuncAttributeMaxDynamicSharedMemorySize, mck::SMEM);
 }

@@ -62,5 +62,15 @@ cudaError_t mc_init();
 int64_t mc_z_doubles(int64_t n, int64_t ns);
 cudaError_t launch_mc_chunk(int64_t n, const double *tiles, const double *a, uint64_t seed, int64_t s0, int64_t ns,
                             double *Z, int *first, unsigned long long *count, int nsm, cudaStream_t st);
+cudaError_t launch_mc_first_init(int *first, int64_t ns, int n, cudaStream_t st);
+cudaError_t launch_mc_count(const int *first, int64_t ns, unsigned long long *count, cudaStream_t st);
+// NEXT-2 on the int8 tensor cores (kernels_mc_oz.cu): Ozaki-split X = L Z with tcgen05.mma kind::i8
+cudaError_t mc_oz_init();
+int64_t mc_oz_la_bytes(int64_t n);
+int64_t mc_oz_zb_bytes(int64_t n, int64_t ns);
+cudaError_t launch_mc_oz_prepare(int64_t n, const double *tiles, double *rowscale, int8_t *LA, cudaStream_t st);
+cudaError_t launch_mc_oz_chunk(int64_t n, const int8_t *LA, const double *rowscale, const double *a, uint64_t seed,
+                               int64_t s0, int64_t ns, int8_t *ZB, int *first, unsigned long long *count, int nsm,
+                               cudaStream_t st);
 
 }  // namespace mvn

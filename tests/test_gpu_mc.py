@@ -44,10 +44,10 @@ def factor(torch, cfg):
     return T, a
 
 
-def gpu_first(torch, T, n, a, seed, begin, end):
+def gpu_first(torch, T, n, a, seed, begin, end, method=0):
     d_a = torch.from_numpy(np.ascontiguousarray(a)).cuda()
     first = torch.empty(end - begin, dtype=torch.int32, device="cuda")
-    count = mvn().mvn_mc_validate(T, n, d_a, seed, begin, end, first=first)
+    count = mvn().mvn_mc_validate(T, n, d_a, seed, begin, end, first=first, method=method)
     return first.cpu().numpy(), count.cpu().numpy().astype(np.int64)
 
 
@@ -58,28 +58,58 @@ def check_against_oracle(fg, L, a, seed, begin, end):
     return fo, int(diff.sum())
 
 
+@pytest.mark.parametrize("method", [0, 1])
 @pytest.mark.parametrize("g,base,begin,end", [(20, "A", 0, 4096), (9, "A", 5, 700), (23, "C", 1000, 3333),
                                               (11, "A", 0, 129)])
-def test_mc_first_vs_oracle(torch, g, base, begin, end):
+def test_mc_first_vs_oracle(torch, g, base, begin, end, method):
+    """method 0: X = L Z on fp64 DMMA; method 1: on the int8 tensor cores (tcgen05 Ozaki split)."""
     cfg = W.small_config(f"mc{g}", g, 100, 1, base=base)
     T, a = factor(torch, cfg)
     n = cfg.n
-    fg, count = gpu_first(torch, T, n, a, 1234, begin, end)
+    fg, count = gpu_first(torch, T, n, a, 1234, begin, end, method)
     assert np.array_equal(count, np.bincount(fg, minlength=n + 1))
     fo, nd = check_against_oracle(fg, dense(T, n), a, 1234, begin, end)
     assert nd <= max(1, (end - begin) // 1000)
 
 
-def test_mc_multiple_row_tiles_and_far_rows(torch):
-    """n = 1,000 (8 row tiles, ragged last) with limits pushed low so that draws survive deep into
+@pytest.mark.parametrize("method", [0, 1])
+def test_mc_multiple_row_tiles_and_far_rows(torch, method):
+    """n = 961 (8 row tiles, ragged last) with limits pushed low so that draws survive deep into
     the sweep and the later row tiles decide."""
     cfg = W.small_config("mc-deep", 31, 100, 1, base="A")   # n = 961
     T, a = factor(torch, cfg)
     n = cfg.n
     a = a - 3.5
-    fg, count = gpu_first(torch, T, n, a, 77, 0, 2000)
+    fg, count = gpu_first(torch, T, n, a, 77, 0, 2000, method)
     assert fg.max() > 600                                   # the deep tiles were exercised
     check_against_oracle(fg, dense(T, n), a, 77, 0, 2000)
+
+
+def test_mc_int8_emulation_matches_fp64_path(torch):
+    """The two products decide identically except where |x_k - a_k| is at rounding level; at
+    n = 4,900 (config B geometry, 39 row tiles incl. a ragged one) over 10,000 draws."""
+    cfg = W.small_config("mc-oz", 70, 100, 1, base="B")
+    T, a = factor(torch, cfg)
+    n = cfg.n
+    f0, c0 = gpu_first(torch, T, n, a, 9, 0, 10_000, 0)
+    f1, c1 = gpu_first(torch, T, n, a, 9, 0, 10_000, 1)
+    assert np.mean(f0 != f1) <= 1e-3
+    assert np.array_equal(c1, np.bincount(f1, minlength=n + 1))
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_mc_identity_closed_form_both_methods(torch, method):
+    n, N = 300, 50_000
+    T = mvn().mvn_pack_lower(torch.from_numpy(np.eye(n)).cuda(), n)
+    a = np.full(n, -2.5)
+    a[:3] = [-0.5, 0.0, -1.0]
+    cnt = mvn().mvn_mc_validate(T, n, torch.from_numpy(a).cuda(), 3, 0, N, method=method).cpu().numpy()
+    from scipy.special import ndtr
+    ks = [1, 2, 3, 10, 100, 300]
+    ph = mvn().mvn_mc_levels(cnt, N, ks)
+    for k, p_hat in zip(ks, ph):
+        p = float(np.prod(1 - ndtr(a[:k])))
+        assert abs(p_hat - p) <= 4 * math.sqrt(p * (1 - p) / N) + 1e-12, (k, p_hat, p)
 
 
 def test_mc_chunks_accumulate_and_split(torch):
