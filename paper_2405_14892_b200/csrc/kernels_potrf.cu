@@ -1,9 +1,10 @@
 // K2-K4 — right-looking tiled Cholesky Sigma = L L^T (Alg. 1 line 8; box (a) of P:319).
 //
-// Per step k (nt steps, 128x128 tiles, lower tile-packed storage):
-//   K2 k_potrf_diag : A_kk = L_kk L_kk^T in shared memory (one CTA), pivot check -> info
-//   K3 k_trsm       : L_ik = A_ik L_kk^{-T}, i > k (one CTA per tile, one thread per row)
-//   K4 k_update     : A_ij -= L_ik L_jk^T, i >= j > k (DMMA GEMM, two 64x128 CTAs per tile)
+// Per super-panel of kp tile columns (128x128 tiles, lower tile-packed storage):
+//   K2 k_potrf_diag2 : A_kk = L_kk L_kk^T in shared memory (one CTA, blocked, DMMA), pivot check -> info
+//   K3 k_trsm2       : L_ik = A_ik L_kk^{-T}, i > k (two CTAs per tile, blocked, DMMA)
+//   K4 k_update2 / k_update : A_ij -= sum_c L_ic L_jc^T over the super-panel (persistent DMMA GEMM /
+//                      two 64x128 CTAs per tile for small counts)
 // The paper's StarPU task DAG becomes stream order; the K4 GEMM carries
 // n^3/3 of the n^3/3 + O(n^2 nb) flops.
 #include <algorithm>
@@ -14,80 +15,6 @@
 #include "mvn_internal.h"
 
 namespace mvn {
-
-// ------------------------------------------------------------------------------------------ K2
-// Unblocked right-looking Cholesky of one 128x128 tile held in shared memory (column-major).
-// The first non-positive (or NaN) pivot writes its global row to *info (only if no earlier step
-// failed) and stops the factorisation of this tile.
-__global__ void __launch_bounds__(512) k_potrf_diag(double *__restrict__ tiles, int k, int64_t *__restrict__ info) {
-    extern __shared__ double A[];  // 128 x 128, column-major
-    __shared__ int failed;
-    double *T = tiles + tile_offset(k, k);
-    const int tid = threadIdx.x, nth = blockDim.x;
-    for (int e = tid; e < kTile * kTile / 2; e += nth)
-        reinterpret_cast<double2 *>(A)[e] = reinterpret_cast<const double2 *>(T)[e];
-    if (tid == 0) failed = (*info >= 0);  // an earlier step already failed: leave tiles as they are
-    __syncthreads();
-    if (failed) return;
-    const int warp = tid >> 5, lane = tid & 31, nwarp = nth >> 5;
-    for (int c = 0; c < kTile; ++c) {
-        if (tid == 0) {
-            const double d = A[c * kTile + c];
-            if (!(d > 0.0)) {
-                failed = 1;
-                *info = (int64_t)k * kTile + c;
-            } else {
-                A[c * kTile + c] = sqrt(d);
-            }
-        }
-        __syncthreads();
-        if (failed) return;
-        const double piv = A[c * kTile + c];
-        for (int i = c + 1 + tid; i < kTile; i += nth) A[c * kTile + i] /= piv;
-        __syncthreads();
-        // trailing update of the lower triangle: column j handled by warp (j - c - 1) % nwarp
-        for (int j = c + 1 + warp; j < kTile; j += nwarp) {
-            const double ljc = A[c * kTile + j];
-            for (int i = j + lane; i < kTile; i += 32) A[j * kTile + i] -= A[c * kTile + i] * ljc;
-        }
-        __syncthreads();
-    }
-    // write back L_kk with the strict upper triangle zeroed
-    for (int e = tid; e < kTile * kTile; e += nth) {
-        const int col = e >> 7, row = e & 127;
-        T[e] = (row >= col) ? A[e] : 0.0;
-    }
-}
-
-// ------------------------------------------------------------------------------------------ K3
-// L_ik = A_ik L_kk^{-T}: row r of the tile solves x L_kk^T = a by forward substitution,
-// x_j = (a_j - sum_{t<j} x_t L_kk(j,t)) / L_kk(j,j). Thread r owns row r; its x lives in a
-// column-major shared copy of the tile (conflict-free), L_kk(j,t) is a warp-uniform broadcast.
-__global__ void __launch_bounds__(128) k_trsm(double *__restrict__ tiles, int k, int nt) {
-    extern __shared__ double X[];  // 128 x 128 column-major: X[col*128 + row]
-    const int i = k + 1 + blockIdx.x;
-    double *T = tiles + tile_offset(i, k);
-    const double *__restrict__ Lkk = tiles + tile_offset(k, k);
-    const int r = threadIdx.x;
-    for (int e = r; e < kTile * kTile / 2; e += 128)
-        reinterpret_cast<double2 *>(X)[e] = reinterpret_cast<const double2 *>(T)[e];
-    __syncthreads();
-    for (int j = 0; j < kTile; ++j) {
-        double s0 = X[j * kTile + r], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int t = 0;
-        for (; t + 4 <= j; t += 4) {
-            s0 -= X[(t + 0) * kTile + r] * __ldg(Lkk + (t + 0) * kTile + j);
-            s1 -= X[(t + 1) * kTile + r] * __ldg(Lkk + (t + 1) * kTile + j);
-            s2 -= X[(t + 2) * kTile + r] * __ldg(Lkk + (t + 2) * kTile + j);
-            s3 -= X[(t + 3) * kTile + r] * __ldg(Lkk + (t + 3) * kTile + j);
-        }
-        for (; t < j; ++t) s0 -= X[t * kTile + r] * __ldg(Lkk + t * kTile + j);
-        X[j * kTile + r] = ((s0 + s1) + (s2 + s3)) / __ldg(Lkk + j * kTile + j);
-    }
-    __syncthreads();
-    for (int e = r; e < kTile * kTile / 2; e += 128)
-        reinterpret_cast<double2 *>(T)[e] = reinterpret_cast<const double2 *>(X)[e];
-}
 
 // ------------------------------------------------------------------------------------------ K2/K3
 // Blocked versions (32-column blocks) of the diagonal POTRF and the panel TRSM. Shared-memory
@@ -472,8 +399,6 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
 
 cudaError_t potrf_init() {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * kTile * 8))) return e;
-    if ((e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * kTile * 8))) return e;
     if ((e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, upd::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, upd2::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(k_potrf_diag2, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * blk::SP * 8))) return e;
