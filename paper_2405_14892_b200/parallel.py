@@ -30,9 +30,12 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < rem else 0)
 
 
-def combine_prefix(M: torch.Tensor, S: torch.Tensor, group=None, rescale=None) -> tuple[torch.Tensor, torch.Tensor]:
+def combine_prefix(M: torch.Tensor, S: torch.Tensor, group=None, rescale=None,
+                   force_collectives: bool = False) -> tuple[torch.Tensor, torch.Tensor]:
     """In place: M <- max over ranks, S <- sum over ranks of S_g exp(M_g - Mglob). Returns (M, S)."""
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+    if not (dist.is_available() and dist.is_initialized()):
+        return M, S
+    if dist.get_world_size(group) == 1 and not force_collectives:
         return M, S
     Mg = M.clone()
     dist.all_reduce(Mg, op=dist.ReduceOp.MAX, group=group)
@@ -254,13 +257,16 @@ class CudaPotrfOps:
         self.main.wait_stream(self.side)
 
 
-def potrf_distributed(L, n: int, group=None, ops=None) -> int:
+def potrf_distributed(L, n: int, group=None, ops=None, force_collectives: bool = False) -> int:
     """Distributed tiled Cholesky of the tile-packed Sigma in `L` (every rank holds the full buffer
     with the same Sigma); on return every rank's `L` holds all of L. Returns info (-1 = SPD, else
     the first failing 0-based row, agreed over the ranks). With one rank this is the lookahead
-    schedule of mvn_potrf driven from Python."""
-    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
-    rank = dist.get_rank(group) if world > 1 else 0
+    schedule of mvn_potrf driven from Python; force_collectives issues the NCCL broadcasts and the
+    info all_reduce even then (a one-rank communicator exercises the exact multi-GPU plumbing)."""
+    initialized = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if initialized else 1
+    rank = dist.get_rank(group) if initialized else 0
+    use_comm = initialized and (world > 1 or force_collectives)
     if ops is None:
         _cuda_info(L)                            # reset the device pivot flag (synchronises)
         ops = CudaPotrfOps(L, n)
@@ -269,7 +275,7 @@ def potrf_distributed(L, n: int, group=None, ops=None) -> int:
     while req is not None:
         _, k, src = req
         h = None
-        if world == 1:
+        if not use_comm:
             h = ops.record("side")               # the panel chain ran on the side stream
         else:
             buf = ops.panel_buf(k)
@@ -284,7 +290,7 @@ def potrf_distributed(L, n: int, group=None, ops=None) -> int:
         except StopIteration:
             req = None
     info = ops.info() if hasattr(ops, "info") else _cuda_info(L)
-    if world > 1:
+    if use_comm:
         big = 1 << 62
         t = torch.tensor([info if info >= 0 else big], dtype=torch.int64, device=getattr(ops, "dev", "cpu"))
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)

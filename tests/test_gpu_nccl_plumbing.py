@@ -1,0 +1,66 @@
+"""The multi-GPU plumbing on a real NCCL communicator, on the one GPU this pool provides: a one-rank
+NCCL process group drives potrf_distributed with its broadcasts forced (async NCCL broadcast issued
+from the side stream, Work.wait on the main stream, info all_reduce) and combine_prefix with its
+all_reduces forced. Results must equal the single-GPU calls bit for bit. No ranks wait on each
+other (world size 1): this checks the stream / event / NCCL ordering the 8-GPU run relies on."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def nccl(cuda_device):
+    import torch
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+def test_potrf_distributed_with_nccl_broadcasts(nccl):
+    import torch
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200.parallel import potrf_distributed
+    for n in (900, 40 * 128 + 77):
+        xy = np.random.default_rng(n).uniform(size=(n, 2))
+        T = mvn.mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, 0.1, 0.5, 1e-8)
+        ref = T.clone()
+        assert mvn.mvn_potrf(ref, n) == -1
+        assert potrf_distributed(T, n, force_collectives=True) == -1
+        torch.cuda.synchronize()
+        assert torch.equal(T, ref)
+
+
+def test_combine_prefix_with_nccl_allreduce(nccl):
+    import torch
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200.parallel import combine_prefix
+    import workloads as W
+    cfg = W.small_config("nccl", 15, 500, 2)
+    inp = W.make_inputs(cfg)
+    n = cfg.n
+    order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
+    T = mvn.mvn_cov_matern(torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda(), cfg.sigma2, cfg.beta, cfg.nu,
+                           cfg.nugget)
+    mvn.mvn_potrf(T, n)
+    d_a = torch.from_numpy(a).cuda()
+    M, S = mvn.mvn_sov_prefix(T, n, d_a, cfg.N, cfg.R, cfg.seed_lattice)
+    M2, S2 = M.clone(), S.clone()
+    combine_prefix(M2, S2, force_collectives=True)
+    torch.cuda.synchronize()
+    assert torch.equal(M2, M) and torch.equal(S2, S)
