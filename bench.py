@@ -364,6 +364,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--potrf", default="auto", choices=["auto", "rank0", "dist"],
                     help="N>1: factor on rank 0 + broadcast L, or distributed (NEXT-1); auto = dist")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="testing: run the multi-GPU code path (NCCL process group, distributed Cholesky, "
+                         "all_reduce combine, pinned-buffer e2e) even with one rank")
     ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist"],
                     help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
                          "posterior: NEXT-4 conditioning (paper size: 200x200 sites, 6,250 observations); "
@@ -391,7 +394,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    multi = world > 1 or args.force_dist                 # the multi-GPU code path
+    if multi:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+            parallel.FORCE_COLLECTIVES = True
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
 
@@ -417,7 +427,7 @@ def main():
 
     clocks = ClockSampler(local)
     clocks.start()
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     step_ms, stage = [], {}
@@ -434,12 +444,12 @@ def main():
         stage.setdefault("region", []).append(ev[-1][1].elapsed_time(e_end))
         step_ms.append(ev[0][1].elapsed_time(e_end))
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     clk = clocks.stop()
 
     total_ms = float(np.sum(step_ms))
-    if world > 1:
+    if multi:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -455,7 +465,7 @@ def main():
     # host, H2D of sorted locations and limits, a2..a8, D2H of log P, a10). N > 1: the same steps
     # through parallel.crd_step on every rank from pinned host buffers, max over ranks.
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not multi:
         ts = []
         for it in range(2):                      # one warm-up call (allocations), one timed
             t0 = time.perf_counter()
@@ -467,7 +477,7 @@ def main():
         e2e = {"value": n * NR / float(np.mean(ts)), "unit": UNIT, "h2d_bytes_per_step": 24 * n,
                "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)), "api": "mvn_crd (C ABI)",
                "k_star_matches_device_path": bool(np.array_equal(out.k_star, k))}
-    elif not args.no_e2e:
+    elif not args.no_e2e and multi:
         import torch as _t
         h_xy = _t.empty((n, 2), dtype=_t.float64).pin_memory()
         h_a = _t.empty(n, dtype=_t.float64).pin_memory()
@@ -497,12 +507,12 @@ def main():
     my_samples = my_end - my_begin
     sov_flops = float(n) * (n - 1) * my_samples       # algorithmic: sum_k 2(k-1) per sample (a6 + in-block dot)
     achieved = sov_flops / (sov_ms / 1e3) / 1e12
-    mode = ("dist" if world > 1 else "rank0") if args.potrf == "auto" else args.potrf
+    mode = ("dist" if multi else "rank0") if args.potrf == "auto" else args.potrf
     if mode == "dist":
         n_potrf = parallel.potrf_launches(n, world, rank)
     else:
         n_potrf = parallel.potrf_launches(n) if rank == 0 else 0
-    launches = (1 if (mode == "dist" or rank == 0) else 0) + n_potrf + 2 + 1 + (1 if world > 1 else 0)
+    launches = (1 if (mode == "dist" or rank == 0) else 0) + n_potrf + 2 + 1 + (1 if multi else 0)
     potrf_ms = stage_mean["potrf"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -547,7 +557,7 @@ def main():
                                 "measured": det}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
     return 0
 

@@ -20,6 +20,10 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
+# Testing aid: issue the collectives of the multi-GPU path even on a one-rank process group
+# (bench.py --force-dist), so the NCCL plumbing runs on a single GPU.
+FORCE_COLLECTIVES = False
+
 
 def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     """Balanced contiguous split of [0, total) into `world` ranges; rank's [begin, end)."""
@@ -35,7 +39,7 @@ def combine_prefix(M: torch.Tensor, S: torch.Tensor, group=None, rescale=None,
     """In place: M <- max over ranks, S <- sum over ranks of S_g exp(M_g - Mglob). Returns (M, S)."""
     if not (dist.is_available() and dist.is_initialized()):
         return M, S
-    if dist.get_world_size(group) == 1 and not force_collectives:
+    if dist.get_world_size(group) == 1 and not (force_collectives or FORCE_COLLECTIVES):
         return M, S
     Mg = M.clone()
     dist.all_reduce(Mg, op=dist.ReduceOp.MAX, group=group)
@@ -65,7 +69,7 @@ def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg,
     n = d_a.numel()
     world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
     rank = dist.get_rank(group) if world > 1 else 0
-    mode = ("dist" if world > 1 else "rank0") if potrf == "auto" else potrf
+    mode = ("dist" if (world > 1 or FORCE_COLLECTIVES) else "rank0") if potrf == "auto" else potrf
 
     def mark(name):
         if events is None:
@@ -266,7 +270,7 @@ def potrf_distributed(L, n: int, group=None, ops=None, force_collectives: bool =
     initialized = dist.is_available() and dist.is_initialized()
     world = dist.get_world_size(group) if initialized else 1
     rank = dist.get_rank(group) if initialized else 0
-    use_comm = initialized and (world > 1 or force_collectives)
+    use_comm = initialized and (world > 1 or force_collectives or FORCE_COLLECTIVES)
     if ops is None:
         _cuda_info(L)                            # reset the device pivot flag (synchronises)
         ops = CudaPotrfOps(L, n)
