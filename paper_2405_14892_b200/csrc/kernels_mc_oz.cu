@@ -134,6 +134,21 @@ __global__ void k_oz_zgen(int8_t *__restrict__ ZB, int64_t n, int nchunk, int64_
 
 __device__ __forceinline__ void oz_mbar_wait(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
 
+// CL = 2: the two CTAs of a cluster work on the same row tile (draw blocks 2b, 2b+1) in lockstep
+// and each fetches half of the shared L-slice chunk with a multicast bulk copy into BOTH CTAs'
+// rings (L2 -> SM traffic for A halved); each CTA's MMA completion is committed to both CTAs'
+// `empty` barriers, so a slot is refilled only when both have consumed it.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int CL>
 __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict__ LA, const int8_t *__restrict__ ZB, int64_t n,
                                                       int nt, int nblk, int64_t ns, const double *__restrict__ rowscale,
                                                       const double *__restrict__ a, int *__restrict__ first) {
@@ -147,9 +162,12 @@ __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict_
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nchunk_all = nt * 4;              // chunks of 32 rows over n_pad (B layout)
-    const int64_t nitems = (int64_t)nt * nblk;
+    // items: (row tile, group of CL draw blocks); this CTA takes block CL * g + crank of the group
+    const int crank = CL > 1 ? (int)cluster_rank() : 0;
+    const int64_t nitems = (int64_t)nt * (nblk / CL);
+    const int64_t item0 = blockIdx.x / CL, istep = gridDim.x / CL;
     if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL); }
         mbar_init(tfull, 1);
         mbar_init(tempty, 4);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -160,15 +178,17 @@ __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict_
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
+    if (CL > 1) cluster_sync_all();             // the peer's barriers exist before any multicast / remote arrive
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem = *tmem_slot;
+    const int nbg = nblk / CL;
 
     if (warp == 4) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             uint32_t q = 0;
-            for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-                const int i = nt - 1 - (int)(item / nblk), blk = (int)(item % nblk);
+            for (int64_t item = item0; item < nitems; item += istep) {
+                const int i = nt - 1 - (int)(item / nbg), blk = (int)(item % nbg) * CL + crank;
                 const int nch = 4 * (i + 1);
                 const int8_t *Ai = LA + 2ll * i * (i + 1) * A_BYTES;
                 const int8_t *Bb = ZB + (int64_t)blk * nchunk_all * B_BYTES;
@@ -177,7 +197,15 @@ __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict_
                     oz_mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
                     uint8_t *dst = ring + st * STAGE;
                     mbar_arrive_expect_tx(&full[st], STAGE);
-                    bulk_g2s(dst, Ai + (int64_t)c * A_BYTES, A_BYTES, &full[st]);
+                    if (CL == 1) {
+                        bulk_g2s(dst, Ai + (int64_t)c * A_BYTES, A_BYTES, &full[st]);
+                    } else {                             // my half of the A chunk, into both CTAs
+                        constexpr int H = A_BYTES / CL;
+                        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+                                     " [%0], [%1], %2, [%3], %4;\n"
+                                     ::"r"(smem_u32(dst + crank * H)), "l"(Ai + (int64_t)c * A_BYTES + crank * H), "r"(H),
+                                       "r"(smem_u32(&full[st])), "h"((uint16_t)((1u << CL) - 1)) : "memory");
+                    }
                     bulk_g2s(dst + A_BYTES, Bb + (int64_t)c * B_BYTES, B_BYTES, &full[st]);
                 }
             }
@@ -186,8 +214,8 @@ __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict_
         // ------------------------------------------------------------ MMA issuer
         uint32_t q = 0, flush = 0;
         constexpr uint32_t idesc = oz_idesc();
-        for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-            const int i = nt - 1 - (int)(item / nblk);
+        for (int64_t item = item0; item < nitems; item += istep) {
+            const int i = nt - 1 - (int)(item / nbg);
             const int nch = 4 * (i + 1);
             for (int c = 0; c < nch; ++c, ++q) {
                 const bool fresh = (c % FLUSH) == 0;          // first chunk after a flush: overwrite TMEM
@@ -212,8 +240,12 @@ __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict_
                                          ::"r"(tmem + (uint32_t)(d * NS)), "l"(da), "l"(db), "r"(idesc), "r"(acc));
                         }
                     }
-                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-                                 ::"r"(smem_u32(&empty[st])) : "memory");
+                    if (CL == 1)
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                                     ::"r"(smem_u32(&empty[st])) : "memory");
+                    else                                 // the slot is free only when both CTAs consumed it
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                                     " [%0], %1;\n" ::"r"(smem_u32(&empty[st])), "h"((uint16_t)((1u << CL) - 1)) : "memory");
                     if ((c + 1) % FLUSH == 0 || c + 1 == nch)
                         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
                                      ::"r"(smem_u32(tfull)) : "memory");
@@ -225,8 +257,8 @@ __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict_
     } else if (warp < 4) {
         // ------------------------------------------------------------ epilogue (row = tid)
         uint32_t flush = 0;
-        for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-            const int i = nt - 1 - (int)(item / nblk), blk = (int)(item % nblk);
+        for (int64_t item = item0; item < nitems; item += istep) {
+            const int i = nt - 1 - (int)(item / nbg), blk = (int)(item % nbg) * CL + crank;
             const int nch = 4 * (i + 1);
             double acc[NS];
 #pragma unroll
@@ -271,18 +303,34 @@ __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict_
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
+    if (CL > 1) cluster_sync_all();             // no CTA leaves while its peer may still write into it
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(oz::TMEM_COLS));
 }
 
-cudaError_t mc_oz_init() { return cudaFuncSetAttribute(k_oz_trmm, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM); }
+cudaError_t mc_oz_init() {
+    cudaError_t e = cudaFuncSetAttribute(k_oz_trmm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_oz_trmm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM);
+}
+
+// Cluster size of k_oz_trmm (MVN_MC_CLUSTER: 1 or 2). Measured at D (r01): 53.35 (1) vs 53.25 (2)
+// fp64-equivalent TFLOP/s — the shared-operand traffic is not the limiter; the MMA shape is:
+// tcgen05 kind::i8 runs M128 N64 (and M64 N128) at half the M128 N128 rate (3,890 vs 7,381
+// MAC/clk/SM, tools/umma_i8_test.cu, tools/umma_i8_m64.cu), and 8 level accumulators of 128
+// columns do not fit the 512 TMEM columns. Default 1.
+int mc_oz_cluster() {
+    static const int v = [] { const char *e = getenv("MVN_MC_CLUSTER"); const int x = e ? atoi(e) : 1; return x == 2 ? 2 : 1; }();
+    return v;
+}
 
 int64_t mc_oz_la_bytes(int64_t n) {
     const int64_t nt = (n + kTile - 1) / kTile;
     return 2 * nt * (nt + 1) * oz::A_BYTES;
 }
-int64_t mc_oz_zb_bytes(int64_t n, int64_t ns) {
+int64_t mc_oz_zb_bytes(int64_t n, int64_t ns) {        // draw blocks rounded up to a multiple of 2
     const int64_t nt = (n + kTile - 1) / kTile;
-    return (ns + oz::NS - 1) / oz::NS * nt * 4 * oz::B_BYTES;
+    const int64_t nblk = ((ns + oz::NS - 1) / oz::NS + 1) / 2 * 2;
+    return nblk * nt * 4 * oz::B_BYTES;
 }
 
 cudaError_t launch_mc_oz_prepare(int64_t n, const double *tiles, double *rowscale, int8_t *LA, cudaStream_t st) {
@@ -298,14 +346,48 @@ cudaError_t launch_mc_oz_chunk(int64_t n, const int8_t *LA, const double *rowsca
                                int64_t s0, int64_t ns, int8_t *ZB, int *first, unsigned long long *count, int nsm,
                                cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
-    const int nblk = (int)((ns + oz::NS - 1) / oz::NS);
+    const int CL = mc_oz_cluster();
+    const int nblk = (int)(((ns + oz::NS - 1) / oz::NS + CL - 1) / CL * CL);   // padded draws are zero
     const int64_t total = (int64_t)nblk * nt * 4 * oz::KC * oz::NS;
     k_oz_zgen<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(ZB, n, nt * 4, s0, ns, seed, total);
     cudaError_t e = launch_mc_first_init(first, ns, (int)n, st);
     if (e != cudaSuccess) return e;
-    const int64_t items = (int64_t)nt * nblk;
-    const int grid = (int)std::min<int64_t>(items, nsm);
-    k_oz_trmm<<<grid, oz::NT, oz::SMEM, st>>>(LA, ZB, n, nt, nblk, ns, rowscale, a, first);
+    const int64_t items = (int64_t)nt * (nblk / CL);
+    const int grid = (int)std::min<int64_t>(items, nsm / CL) * CL;
+    if (CL == 1) {
+        k_oz_trmm<1><<<grid, oz::NT, oz::SMEM, st>>>(LA, ZB, n, nt, nblk, ns, rowscale, a, first);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        // co-resident clusters of 2 (a GPC with an odd SM count leaves one SM out): persistent grid
+        static int max_clusters = 0;
+        if (!max_clusters) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(2);
+            q.blockDim = dim3(oz::NT);
+            q.dynamicSmemBytes = oz::SMEM;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = 2; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&max_clusters, k_oz_trmm<2>, &q) != cudaSuccess || max_clusters < 1)
+                max_clusters = nsm / 2;
+        }
+        cfg.gridDim = dim3((unsigned)(std::min<int64_t>(items, max_clusters) * 2));
+        cfg.blockDim = dim3(oz::NT);
+        cfg.dynamicSmemBytes = oz::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e2 = cudaLaunchKernelEx(&cfg, k_oz_trmm<2>, LA, ZB, n, nt, nblk, ns, rowscale, a, first);
+        if (e2 != cudaSuccess) return e2;
+    }
     return launch_mc_count(first, ns, count, st);
 }
 

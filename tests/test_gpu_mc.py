@@ -164,3 +164,18 @@ def test_mc_full_config_D_sampled(torch):
     bad = decided & (fg != fo) & (gap > GAP)
     assert not np.any(bad)
     assert np.all(fg[~decided] >= m)
+
+
+def test_mc_int8_cluster_variant():
+    """The 2-CTA cluster variant of the int8 kernel (multicast of the shared L slices;
+    MVN_MC_CLUSTER=2, read once per process, hence the subprocess) passes the same oracle tests."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("MVN_MC_CLUSTER"):
+        pytest.skip("already running under a fixed MVN_MC_CLUSTER")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu and not slow", "tests/test_gpu_mc.py",
+                        "-k", "method and not cluster_variant"], cwd=root, env=dict(os.environ, MVN_MC_CLUSTER="2"),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

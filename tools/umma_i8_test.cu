@@ -144,5 +144,6 @@ int main() {
     fails += run<256>(256, 1);
     fails += run<128>(512, 64);     // rate: operands resident in smem
     fails += run<256>(256, 128);
+    fails += run<64>(1024, 64);     // rate at N = 64 (the MC emulation's shape)
     return fails;
 }
