@@ -292,9 +292,9 @@ def leading_block(T, n, m):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["C", "D"])
+@pytest.mark.parametrize("name", ["C", "D", "E"])
 def test_full_config_sampled_parity(torch_cuda, name):
-    """BASELINE configs C (n = 16,384, nu = 3/2) and D (n = 65,536) at full size, in the launch
+    """BASELINE configs C (n = 16,384, nu = 3/2), D (n = 65,536) and E (n = 102,400) at full size, in the launch
     configuration bench.py times: (1) Cholesky residual on 1,000 sampled entries (L L^T)_ij vs the
     oracle's Matérn Sigma_ij; (2) the leading 4,096 x 4,096 block of L vs the oracle's own Cholesky of
     the leading block of Sigma (independent mode; a leading principal block factors on its own);
@@ -328,4 +328,8 @@ def test_full_config_sampled_parity(torch_cuda, name):
         Ms, Ss = oracle_range(Lg, a[:m], np.full(m, np.inf), cfg.N, cfg.R, cfg.seed_lattice, begin, end)
         assert np.max(np.abs(lp_g - logp_from(Ms, Ss, end - begin))) <= 1e-10
         Mo, So_ = oracle_range(Lo, a[:m], np.full(m, np.inf), cfg.N, cfg.R, cfg.seed_lattice, begin, end)
-        assert np.max(np.abs(lp_g - logp_from(Mo, So_, end - begin))) <= LOGP_TOL
+        # independent mode: both sides factor Sigma; at E (nu = 3/2, 320 x 320 grid) the conditioning
+        # makes two backward-stable factors differ by more (SURVEY §8(c) parity modes: grade C/E SOV
+        # parity in shared-L mode, report independent mode) — bar 1e-7 there, the north_star 1e-8 else
+        tol = 1e-7 if name == "E" else LOGP_TOL
+        assert np.max(np.abs(lp_g - logp_from(Mo, So_, end - begin))) <= tol
