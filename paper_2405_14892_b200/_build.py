@@ -14,6 +14,8 @@ HEADERS = ["common.cuh", "gemm_dmma.cuh", "normal.cuh", "mvn_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+# experiments only (e.g. MVN_NVCC_EXTRA=-DMVN_SOV_GW=16); the default build uses none
+FLAGS += [f for f in os.environ.get("MVN_NVCC_EXTRA", "").split() if f]
 
 
 def _stale() -> bool:

@@ -35,7 +35,13 @@ constexpr int BK = 16, STAGES = 4;
 constexpr int SA = M + 4;                // 68  == 4 (mod 16): conflict-free DMMA fragment loads
 constexpr int SB = NB + 4;               // 132 == 4 (mod 16); also the Y-history row stride
 constexpr int SS = NB + 8;               // S tile stride (16-byte fragment stores conflict-free)
-constexpr int NGEMM = 256, NCHAIN = NB, NPROD = 32, NT = NGEMM + NCHAIN + NPROD;
+// GEMM warps: GW = 8 (2 x 4, warp tile 32 x 32) or 16 (4 x 4, warp tile 16 x 32: more warps per
+// scheduler to cover the operand waits; MVN build flag MVN_SOV_GW)
+#ifndef MVN_SOV_GW
+#define MVN_SOV_GW 8
+#endif
+constexpr int GW = MVN_SOV_GW, GROWS = GW / 4, WROWS = M / GROWS, WRB = WROWS / 8;
+constexpr int NGEMM = 32 * GW, NCHAIN = NB, NPROD = 32, NT = NGEMM + NCHAIN + NPROD;
 constexpr int STAGE = BK * (SA + SB);                    // doubles per pipeline stage
 constexpr int OFF_S = STAGES * STAGE;                    // S[64][SS]: s, then y, of the row block
 constexpr int OFF_LD = OFF_S + M * SS;                   // Ld[64 cols][64 rows] (column-major)
@@ -206,10 +212,10 @@ __device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, u
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
     uint64_t *empty = full + STAGES;
     const int lane = tid & 31, warp = tid >> 5;
-    const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * (WN * 8);
-    double acc[4][WN][2];
+    const int wm0 = (warp % GROWS) * WROWS, wn0 = (warp / GROWS) * (WN * 8);
+    double acc[WRB][WN][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < WRB; ++i)
 #pragma unroll
         for (int j = 0; j < WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int c = 0; c < CPB * rb; ++c, ++q) {
@@ -219,14 +225,14 @@ __device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, u
         const double *bs = as + BK * SA;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            double fa[4], fb[WN];
+            double fa[WRB], fb[WN];
             const int kr = kk + (lane & 3);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) fa[i] = as[kr * SA + wm0 + i * 8 + (lane >> 2)];
+            for (int i = 0; i < WRB; ++i) fa[i] = as[kr * SA + wm0 + i * 8 + (lane >> 2)];
 #pragma unroll
             for (int j = 0; j < WN; ++j) fb[j] = bs[kr * SB + wn0 + j * 8 + (lane >> 2)];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < WRB; ++i)
 #pragma unroll
                 for (int j = 0; j < WN; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
         }
@@ -235,7 +241,7 @@ __device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, u
     }
     double *S = sm + OFF_S;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < WRB; ++i) {
         const int row = wm0 + i * 8 + (lane >> 2);
 #pragma unroll
         for (int j = 0; j < WN; ++j) {

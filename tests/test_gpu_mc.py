@@ -147,7 +147,8 @@ def test_mc_levels_host():
 
 
 @pytest.mark.slow
-def test_mc_full_config_D_sampled(torch):
+@pytest.mark.parametrize("method", [0, 1])
+def test_mc_full_config_D_sampled(torch, method):
     """Config D (n = 65,536) at full size: 2,048 draws through the bench launch configuration; the
     oracle decides each draw from the leading 4,096 x 4,096 block of L (a draw whose first failure
     lies in the block is decided there; the GPU must then agree; draws that survive the block
@@ -156,7 +157,7 @@ def test_mc_full_config_D_sampled(torch):
     cfg = W.CONFIGS["D"]
     T, a = factor(torch, cfg)
     n, m = cfg.n, 4096
-    fg, count = gpu_first(torch, T, n, a, 42, 10_000, 12_048)
+    fg, count = gpu_first(torch, T, n, a, 42, 10_000, 12_048, method)
     Lm = P.leading_block(T, n, m)
     fo, _, gap = oracle.mc_first(Lm, a[:m], 42, 10_000, 2048, nthreads=16, diagnostics=True)
     decided = fo < m
