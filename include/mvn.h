@@ -179,7 +179,8 @@ typedef struct {
  * device (fixed sample blocking, fixed combine order).
  * d_L: tile-packed L from mvn_potrf. d_a: n device doubles (-inf allowed). d_b: n device doubles
  * or NULL for b = +inf (every BASELINE config). MVN_E_USAGE if the range is empty/out of bounds,
- * or n, N, R < 1.                                                                              */
+ * n, N, R < 1, or any limit is NaN or a_k > b_k (checked on the device; the call synchronises the
+ * stream once for that check before enqueuing the sweep).                                      */
 mvn_status mvn_sov_prefix(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_a,
                           const double *d_b, const mvn_qmc *q, double *d_M, double *d_S);
 

@@ -135,6 +135,22 @@ __global__ void k_finalize(int64_t n, double lognr, const double *__restrict__ M
     logP[k] = (s > 0.0) ? M[k] + log(s) - lognr : -CUDART_INF;
 }
 
+// Limits check for mvn_sov_prefix: flag = 1 if any a_k or b_k is NaN or a_k > b_k (b = NULL: +inf).
+__global__ void k_check_limits(int64_t n, const double *__restrict__ a, const double *__restrict__ b, int *__restrict__ flag) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double ak = a[k];
+    const double bk = b ? b[k] : CUDART_INF;
+    if (isnan(ak) || isnan(bk) || ak > bk) atomicOr(flag, 1);
+}
+
+cudaError_t launch_check_limits(int64_t n, const double *a, const double *b, int *flag, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    k_check_limits<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, a, b, flag);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rescale(int64_t n, const double *Mg, double *M, double *S, cudaStream_t st) {
     k_rescale<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, Mg, M, S);
     return cudaGetLastError();

@@ -152,7 +152,7 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
     c->stream = (cudaStream_t)cuda_stream;
     if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess || mvn::mc_init() != cudaSuccess ||
         mvn::mc_oz_init() != cudaSuccess ||
-        cudaMalloc(&c->d_info, sizeof(int64_t)) != cudaSuccess) {
+        cudaMalloc(&c->d_info, 2 * sizeof(int64_t)) != cudaSuccess) {
         delete c;
         return MVN_E_CUDA;
     }
@@ -336,6 +336,14 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
         return fail(c, MVN_E_USAGE, "mvn_sov_prefix: bad arguments (need nb=128, 0 <= begin < end <= N*R)");
     mvn_status s;
     if ((s = ensure_generators(c, t.n)) != MVN_OK) return s;
+    {   // NaN limits or a_k > b_k: MVN_E_USAGE (synchronises on a 4-byte flag before the sweep)
+        int *d_flag = reinterpret_cast<int *>(c->d_info) + 2;      // spare bytes after the pivot flag
+        int h_flag = 0;
+        MVN_CUDA(c, mvn::launch_check_limits(t.n, d_a, d_b, d_flag, c->stream));
+        MVN_CUDA(c, cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (h_flag) return fail(c, MVN_E_USAGE, "mvn_sov_prefix: a limit is NaN or a_k > b_k");
+    }
     const int64_t nsamp = q->sample_end - q->sample_begin;
     mvn::SovLaunch L;
     L.L = d_L; L.n = t.n; L.a = d_a; L.b = d_b; L.G = c->G; L.N = q->N; L.seed = q->seed;

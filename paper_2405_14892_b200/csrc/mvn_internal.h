@@ -11,6 +11,7 @@ cudaError_t launch_cov_matern(int64_t n, const double *xy, double sigma2, double
                               double *tiles, cudaStream_t st);
 cudaError_t launch_pack(int64_t n, const double *dense, int64_t ld, double *tiles, bool to_tiles, cudaStream_t st);
 cudaError_t launch_rescale(int64_t n, const double *Mg, double *M, double *S, cudaStream_t st);
+cudaError_t launch_check_limits(int64_t n, const double *a, const double *b, int *flag, cudaStream_t st);
 cudaError_t launch_finalize(int64_t n, int64_t NR, const double *M, const double *S, double *logP, cudaStream_t st);
 
 cudaError_t potrf_init();
