@@ -49,7 +49,8 @@ constexpr int OFF_PS = OFF_LD + M * M;                   // per-row, per-chain-w
 constexpr int OFF_AG = OFF_PS + M * 4 * 2;               // [3][64]: a, b, G (as double bits)
 constexpr int OFF_DINV = OFF_AG + 3 * M;                 // [64]: 1 / L_kk of the row block
 constexpr int OFF_ELL8 = OFF_DINV + M;                   // [8][NB]: log weights of the current 8-row sub-block
-constexpr int OFF_BAR = OFF_ELL8 + 8 * NB;               // full[STAGES], empty[STAGES] mbarriers
+constexpr int OFF_P8 = OFF_ELL8 + 8 * NB;                // [8][NB]: exp(ell - c_w) of the sub-block (b = +inf path)
+constexpr int OFF_BAR = OFF_P8 + 8 * NB;                 // full[STAGES], empty[STAGES] mbarriers
 constexpr int SMEM = (OFF_BAR + 2 * STAGES) * 8;
 constexpr int CPB = M / BK;                              // K-chunks per row block
 enum : int { BAR_SFULL = 1, BAR_YREADY = 2, BAR_CHAIN = 3 };
@@ -309,6 +310,19 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
         if (left <= 0) break;                             // uniform: padded rows need no y
         const int nrows = left < 8 ? (int)left : 8;
         double s = S[rb0 * SS + j];                       // row rb0: GEMM part + earlier sub-blocks
+        // b = +inf path: the per-row log-sum-exp of this sub-block uses ONE warp reference c_w (the
+        // warp max of ell at the sub-block start; ell never increases, so every term is <= 1) and
+        // the running product pw = exp(ell - c_w) * prod q instead of 8 exps and 8 max trees; a warp
+        // that meets a q < 1e-250 (far tail: pw could underflow) takes the exact path below.
+        double c_w = -CUDART_INF, pw = 0.0;
+        bool tiny = false;
+        if (!HAS_B) {
+            c_w = valid ? ell : -CUDART_INF;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) c_w = fmax(c_w, __shfl_xor_sync(0xffffffffu, c_w, o));
+            pw = (valid && c_w != -CUDART_INF) ? exp(ell - c_w) : 0.0;
+        }
+        double *P8 = sm + OFF_P8;
 #pragma unroll 1
         for (int i = 0; i < nrows; ++i) {
             const int li = rb0 + i;
@@ -318,8 +332,15 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
             const double ap = (a_s[li] - s) * dinv[li];
             const double wq = lattice_w(jl, G_s[li], lattice_shift(p.seed, r, (uint64_t)k));
             double lq, y;
-            if (HAS_B) sov_step(ap, (b_s[li] - s) * dinv[li], wq, lq, y);
-            else sov_step_upper(ap, wq, lq, y);
+            if (HAS_B) {
+                sov_step(ap, (b_s[li] - s) * dinv[li], wq, lq, y);
+            } else {
+                double q;
+                sov_step_upper(ap, wq, lq, y, q);
+                pw *= q;
+                tiny |= !(q >= 1e-250);
+                P8[i * NB + j] = pw;
+            }
             ell += lq;
             S[li * SS + j] = y;
             ELL8[i * NB + j] = ell;
@@ -331,14 +352,22 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
         }
         // per-row log-sum-exp over this warp's samples, 8 rows at once
         double m[8], e[8];
+        if (!HAS_B && !__any_sync(0xffffffffu, tiny)) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) m[i] = (valid && i < nrows) ? ELL8[i * NB + j] : -CUDART_INF;
+            for (int i = 0; i < 8; ++i) {
+                m[i] = c_w;
+                e[i] = (valid && i < nrows && c_w != -CUDART_INF) ? P8[i * NB + j] : 0.0;
+            }
+        } else {
 #pragma unroll
-        for (int o = 16; o; o >>= 1)
+            for (int i = 0; i < 8; ++i) m[i] = (valid && i < nrows) ? ELL8[i * NB + j] : -CUDART_INF;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) m[i] = fmax(m[i], __shfl_xor_sync(0xffffffffu, m[i], o));
+            for (int o = 16; o; o >>= 1)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) e[i] = (valid && i < nrows && m[i] != -CUDART_INF) ? exp(ELL8[i * NB + j] - m[i]) : 0.0;
+                for (int i = 0; i < 8; ++i) m[i] = fmax(m[i], __shfl_xor_sync(0xffffffffu, m[i], o));
+#pragma unroll
+            for (int i = 0; i < 8; ++i) e[i] = (valid && i < nrows && m[i] != -CUDART_INF) ? exp(ELL8[i * NB + j] - m[i]) : 0.0;
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1)
 #pragma unroll

@@ -151,8 +151,8 @@ __device__ __forceinline__ double Phi_inv_lower_nb(double p) {
 // log1p(-t) is formed as log(v) - delta (2 - v) with v = fl(1 - t) in [1/2, 1) and
 // delta = (v - 1) + t the exact rounding error of 1 - t (first-order correction; error <= 2^-55
 // absolute), so both signs share one log.
-__device__ __forceinline__ void sov_step_upper(double ap, double w, double &logq, double &y) {
-    if (ap >= kFarTail) { sov_step_far_upper(ap, CUDART_INF, w, logq, y); return; }
+__device__ __forceinline__ void sov_step_upper(double ap, double w, double &logq, double &y, double &q) {
+    if (ap >= kFarTail) { sov_step_far_upper(ap, CUDART_INF, w, logq, y); q = exp(logq); return; }
     const bool pos = ap >= 0.0;
     const double t = isinf(ap) ? 0.0 : 0.5 * erfc(fabs(ap) * kRsqrt2);
     const double v = pos ? t : 1.0 - t;                  // q
@@ -163,6 +163,7 @@ __device__ __forceinline__ void sov_step_upper(double ap, double w, double &logq
     const bool lower = plo < phi;
     const double r = Phi_inv_lower_nb(lower ? plo : phi);
     y = lower ? r : -r;
+    q = v;
 }
 
 }  // namespace mvn

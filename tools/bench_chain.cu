@@ -25,7 +25,8 @@ __global__ void k_chain(int rows, int nchain, int ndmma, long long *cyc, double 
             const uint64_t X = (uint64_t)(threadIdx.x + 1) * G + mix(0x1234ull + k);
             const double w = ((double)(X >> 12) + 0.5) * 0x1p-52;
             double lq, y;
-            sov_step_upper(ap, w, lq, y);
+            double qq;
+            sov_step_upper(ap, w, lq, y, qq);
             ell += lq;
             s = 0.5 * s + 0.3 * y;           // next row depends on this y (like the in-block dot)
         }
