@@ -11,6 +11,15 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running (large configs)")
+    # make sure libmvn.so (and the C oracle) exist and are not older than their sources: nvcc
+    # cross-compiles for sm_100a without a GPU, so this works on the CPU box too
+    try:
+        from paper_2405_14892_b200 import _build
+        _build.build()
+        import oracle
+        oracle.build()
+    except Exception as e:  # pragma: no cover - reported by the tests that need the library
+        sys.stderr.write(f"conftest: library build skipped: {e}\n")
 
 
 @pytest.fixture(scope="session")
