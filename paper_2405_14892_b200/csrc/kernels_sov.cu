@@ -31,7 +31,12 @@ namespace mvn {
 namespace sovk {
 constexpr int M = 64;                    // SOV row block
 constexpr int NB = 128;                  // max samples per block (= chain threads)
-constexpr int BK = 16, STAGES = 4;
+// K-chunk rows per pipeline stage and stages (same bytes in flight: BK * STAGES = 64); compile-time
+// MVN_SOV_BK for experiments (16 x 4 or 8 x 8)
+#ifndef MVN_SOV_BK
+#define MVN_SOV_BK 16
+#endif
+constexpr int BK = MVN_SOV_BK, STAGES = 64 / MVN_SOV_BK;
 constexpr int SA = M + 4;                // 68  == 4 (mod 16): conflict-free DMMA fragment loads
 constexpr int SB = NB + 4;               // 132 == 4 (mod 16); also the Y-history row stride
 constexpr int SS = NB + 8;               // S tile stride (16-byte fragment stores conflict-free)
