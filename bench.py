@@ -250,7 +250,9 @@ def run_mc(args, cfg):
                           "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
                           "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
                           "algorithmic": f"n(n+1) flops per draw x {e - b} draws"} if args.mc_method == 0 else
-                         {"kernel": "k_oz_trmm (X = L Z as 36 exact int8 GEMMs per 32-K chunk on tcgen05, TMEM)",
+                         {"kernel": ("k_oz_trmm (X = L Z as 36 exact int8 GEMMs per 32-K chunk on tcgen05, TMEM)"
+                                     if args.mc_method == 1 else
+                                     "k_oz2_trmm (36 exact int8 GEMMs per 32-K chunk split by level over a 2-CTA cluster, M128 N128)"),
                           "bound": "tensor", "achieved": achieved * 36 / 1e3, "peak": INT8_PEAK_POPS, "unit": "POP/s (int8 MAC x2)",
                           "frac": achieved * 36 / 1e3 / INT8_PEAK_POPS, "traffic": None,
                           "fp64_equivalent_tflops": achieved,
@@ -372,8 +374,9 @@ def main():
                          "posterior: NEXT-4 conditioning (paper size: 200x200 sites, 6,250 observations); "
                          "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU")
     ap.add_argument("--mc-samples", type=int, default=50_000, help="--workload mc: draws (paper: N = 50,000, P:595)")
-    ap.add_argument("--mc-method", type=int, default=0, choices=[0, 1],
-                    help="--workload mc: 0 = fp64 DMMA, 1 = int8 tensor cores (tcgen05 Ozaki emulation)")
+    ap.add_argument("--mc-method", type=int, default=0, choices=[0, 1, 2],
+                    help="--workload mc: 0 = fp64 DMMA, 1 = int8 tensor cores (tcgen05 Ozaki emulation, M128 N64), "
+                         "2 = the same at M128 N128 with the products split by level over a 2-CTA cluster")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":

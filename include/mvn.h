@@ -220,7 +220,9 @@ typedef struct {
     int32_t method;        /* 0: X = L Z on the fp64 tensor path (DMMA); 1: the same product emulated
                               exactly-per-slice on the int8 tensor cores (tcgen05.mma kind::i8, TMEM
                               accumulators; Ozaki split into 8 signed 7-bit slices, absolute error
-                              <= ~1e-12 relative to max|L_k.| max|z|, reading R22) */
+                              <= ~1e-12 relative to max|L_k.| max|z|, reading R22), M128 N64 per CTA;
+                              2: the same arithmetic at the full-rate M128 N128 shape, the 36 products
+                              split by level over a 2-CTA cluster (multicast operands, L2 exchange) */
 } mvn_mc;
 
 /* d_L: tile-packed L (mvn_potrf), d_a: n device doubles (the limits a_k of the sweep).

@@ -37,6 +37,7 @@ struct mvn_ctx {
     void *mcZ = nullptr; size_t mcZ_cap = 0;
     void *mcLA = nullptr; size_t mcLA_cap = 0;     // int8 slices of L (method 1)
     void *mcRS = nullptr; size_t mcRS_cap = 0;     // per-row scales
+    void *mcX = nullptr; size_t mcX_cap = 0;       // method 2: cluster exchange scratch
     void *mcF = nullptr; size_t mcF_cap = 0;
 };
 
@@ -170,7 +171,7 @@ void mvn_destroy(mvn_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF,
-                    c->post, c->postv, c->mcLA, c->mcRS})
+                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX})
         if (p) cudaFree(p);
     delete c;
 }
@@ -186,10 +187,10 @@ const char *mvn_last_error(const mvn_ctx *c) { return c ? c->err.c_str() : "null
 mvn_status mvn_trim(mvn_ctx *c) {
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX})
         if (*p) { cudaFree(*p); *p = nullptr; }
     c->Y_cap = c->part_cap = c->cta_cap = c->sync_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
-    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = 0;
+    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = 0;
     c->post_n = c->post_off = 0;
     return MVN_OK;
 }
@@ -422,27 +423,36 @@ mvn_status mvn_mc_validate(mvn_ctx *c, mvn_tiles t, const double *d_L, const dou
     if (!tiles_ok(t) || !d_L || !d_a || !m || !d_count || m->sample_begin < 0 || m->sample_end <= m->sample_begin)
         return fail(c, MVN_E_USAGE, "mvn_mc_validate: bad arguments (need nb=128, 0 <= begin < end)");
     const int64_t total = m->sample_end - m->sample_begin;
-    if (m->method == 1) {
+    if (m->method == 1 || m->method == 2) {
         // int8 tensor-core emulation: slice L once, then chunks of draws (Z slices <= ~8 GB)
         const int64_t nt = (t.n + t.nb - 1) / t.nb;
         mvn_status s;
         if ((s = ensure(c, &c->mcLA, &c->mcLA_cap, (size_t)mvn::mc_oz_la_bytes(t.n))) != MVN_OK) return s;
         if ((s = ensure(c, &c->mcRS, &c->mcRS_cap, sizeof(double) * (size_t)(nt * t.nb))) != MVN_OK) return s;
         MVN_CUDA(c, mvn::launch_mc_oz_prepare(t.n, d_L, (double *)c->mcRS, (int8_t *)c->mcLA, c->stream));
-        const int64_t per64 = mvn::mc_oz_zb_bytes(t.n, 64);
-        const int64_t chunk = std::min<int64_t>(total, std::max<int64_t>(1, (int64_t)(8ll << 30) / per64) * 64);
-        if ((s = ensure(c, &c->mcZ, &c->mcZ_cap, (size_t)mvn::mc_oz_zb_bytes(t.n, chunk))) != MVN_OK) return s;
+        const int blk = m->method == 1 ? 64 : 128;
+        const int64_t perblk = m->method == 1 ? mvn::mc_oz_zb_bytes(t.n, blk) : mvn::mc_oz2_zb_bytes(t.n, blk);
+        const int64_t chunk = std::min<int64_t>(total, std::max<int64_t>(1, (int64_t)(8ll << 30) / perblk) * blk);
+        const int64_t zb = m->method == 1 ? mvn::mc_oz_zb_bytes(t.n, chunk) : mvn::mc_oz2_zb_bytes(t.n, chunk);
+        if ((s = ensure(c, &c->mcZ, &c->mcZ_cap, (size_t)zb)) != MVN_OK) return s;
+        if (m->method == 2 && (s = ensure(c, &c->mcX, &c->mcX_cap, (size_t)mvn::mc_oz2_xch_bytes(c->nsm))) != MVN_OK) return s;
         if (!d_first && (s = ensure(c, &c->mcF, &c->mcF_cap, (size_t)chunk * sizeof(int32_t))) != MVN_OK) return s;
         for (int64_t s0 = 0; s0 < total; s0 += chunk) {
             const int64_t ns = std::min(chunk, total - s0);
             int *first = d_first ? (int *)d_first + s0 : (int *)c->mcF;
-            MVN_CUDA(c, mvn::launch_mc_oz_chunk(t.n, (const int8_t *)c->mcLA, (const double *)c->mcRS, d_a, m->seed,
-                                                m->sample_begin + s0, ns, (int8_t *)c->mcZ, first,
-                                                (unsigned long long *)d_count, c->nsm, c->stream));
+            if (m->method == 1)
+                MVN_CUDA(c, mvn::launch_mc_oz_chunk(t.n, (const int8_t *)c->mcLA, (const double *)c->mcRS, d_a, m->seed,
+                                                    m->sample_begin + s0, ns, (int8_t *)c->mcZ, first,
+                                                    (unsigned long long *)d_count, c->nsm, c->stream));
+            else
+                MVN_CUDA(c, mvn::launch_mc_oz2_chunk(t.n, (const int8_t *)c->mcLA, (const double *)c->mcRS, d_a, m->seed,
+                                                     m->sample_begin + s0, ns, (int8_t *)c->mcZ, (double *)c->mcX, first,
+                                                     (unsigned long long *)d_count, c->nsm, c->stream));
         }
         return MVN_OK;
     }
-    if (m->method != 0) return fail(c, MVN_E_USAGE, "mvn_mc_validate: method must be 0 (fp64 DMMA) or 1 (int8 tensor cores)");
+    if (m->method != 0)
+        return fail(c, MVN_E_USAGE, "mvn_mc_validate: method must be 0 (fp64 DMMA), 1 or 2 (int8 tensor cores)");
     const int64_t n_pad = (t.n + t.nb - 1) / t.nb * t.nb;
     // chunk: as many 128-sample blocks as fit ~8 GB of Z, at least one
     const int64_t per_blk = mvn::mc_z_doubles(t.n, 128) * (int64_t)sizeof(double);

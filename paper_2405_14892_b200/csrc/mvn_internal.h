@@ -70,6 +70,11 @@ cudaError_t mc_oz_init();
 int64_t mc_oz_la_bytes(int64_t n);
 int64_t mc_oz_zb_bytes(int64_t n, int64_t ns);
 cudaError_t launch_mc_oz_prepare(int64_t n, const double *tiles, double *rowscale, int8_t *LA, cudaStream_t st);
+int64_t mc_oz2_zb_bytes(int64_t n, int64_t ns);
+int64_t mc_oz2_xch_bytes(int nsm);
+cudaError_t launch_mc_oz2_chunk(int64_t n, const int8_t *LA, const double *rowscale, const double *a, uint64_t seed,
+                                int64_t s0, int64_t ns, int8_t *ZB, double *xch, int *first, unsigned long long *count,
+                                int nsm, cudaStream_t st);
 cudaError_t launch_mc_oz_chunk(int64_t n, const int8_t *LA, const double *rowscale, const double *a, uint64_t seed,
                                int64_t s0, int64_t ns, int8_t *ZB, int *first, unsigned long long *count, int nsm,
                                cudaStream_t st);

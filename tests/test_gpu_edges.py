@@ -43,7 +43,7 @@ def test_sov_edge_sizes(torch, n, begin, end):
     assert np.max(np.abs(logp(M, S, end - begin) - logp(Mo, So, end - begin))) <= 1e-11
 
 
-@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("method", [0, 1, 2])
 def test_mc_single_site(torch, method):
     T = mvn().mvn_pack_lower(torch.from_numpy(np.array([[2.0]])).cuda(), 1)
     mvn().mvn_potrf(T, 1)

@@ -58,7 +58,7 @@ def check_against_oracle(fg, L, a, seed, begin, end):
     return fo, int(diff.sum())
 
 
-@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("method", [0, 1, 2])
 @pytest.mark.parametrize("g,base,begin,end", [(20, "A", 0, 4096), (9, "A", 5, 700), (23, "C", 1000, 3333),
                                               (11, "A", 0, 129)])
 def test_mc_first_vs_oracle(torch, g, base, begin, end, method):
@@ -72,7 +72,7 @@ def test_mc_first_vs_oracle(torch, g, base, begin, end, method):
     assert nd <= max(1, (end - begin) // 1000)
 
 
-@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("method", [0, 1, 2])
 def test_mc_multiple_row_tiles_and_far_rows(torch, method):
     """n = 961 (8 row tiles, ragged last) with limits pushed low so that draws survive deep into
     the sweep and the later row tiles decide."""
@@ -93,11 +93,13 @@ def test_mc_int8_emulation_matches_fp64_path(torch):
     n = cfg.n
     f0, c0 = gpu_first(torch, T, n, a, 9, 0, 10_000, 0)
     f1, c1 = gpu_first(torch, T, n, a, 9, 0, 10_000, 1)
-    assert np.mean(f0 != f1) <= 1e-3
+    f2, c2 = gpu_first(torch, T, n, a, 9, 0, 10_000, 2)
+    assert np.mean(f0 != f1) <= 1e-3 and np.mean(f0 != f2) <= 1e-3
     assert np.array_equal(c1, np.bincount(f1, minlength=n + 1))
+    assert np.array_equal(f1, f2)            # same slices, same products: identical exact integer sums
 
 
-@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("method", [0, 1, 2])
 def test_mc_identity_closed_form_both_methods(torch, method):
     n, N = 300, 50_000
     T = mvn().mvn_pack_lower(torch.from_numpy(np.eye(n)).cuda(), n)
@@ -147,7 +149,7 @@ def test_mc_levels_host():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("method", [0, 1, 2])
 def test_mc_full_config_D_sampled(torch, method):
     """Config D (n = 65,536) at full size: 2,048 draws through the bench launch configuration; the
     oracle decides each draw from the leading 4,096 x 4,096 block of L (a draw whose first failure
