@@ -414,24 +414,31 @@ int panel_sms() {
     static const int v = [] { const char *e = getenv("MVN_POTRF_PANEL_SMS"); const int x = e ? atoi(e) : 4; return x >= 0 && x < 64 ? x : 4; }();
     return v;
 }
+// One panel stream and its events per device (created on first use, kept for the process; a
+// process may drive several devices).
 struct PotrfStreams {
-    int dev = -1;
+    bool ready = false;
     cudaStream_t sp = nullptr;
     cudaEvent_t ev_panel[2] = {}, ev_rest[2] = {}, ev_start = nullptr;
 };
-PotrfStreams g_ps;
+constexpr int kMaxDevices = 64;
+PotrfStreams g_ps_dev[kMaxDevices];
+PotrfStreams *g_cur = nullptr;
 cudaError_t potrf_streams(int dev) {
-    if (g_ps.dev == dev) return cudaSuccess;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    PotrfStreams &ps = g_ps_dev[dev];
+    g_cur = &ps;
+    if (ps.ready) return cudaSuccess;
     int lo = 0, hi = 0;
     cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (e != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithPriority(&g_ps.sp, cudaStreamNonBlocking, hi))) return e;
+    if ((e = cudaStreamCreateWithPriority(&ps.sp, cudaStreamNonBlocking, hi))) return e;
     for (int i = 0; i < 2; ++i) {
-        if ((e = cudaEventCreateWithFlags(&g_ps.ev_panel[i], cudaEventDisableTiming))) return e;
-        if ((e = cudaEventCreateWithFlags(&g_ps.ev_rest[i], cudaEventDisableTiming))) return e;
+        if ((e = cudaEventCreateWithFlags(&ps.ev_panel[i], cudaEventDisableTiming))) return e;
+        if ((e = cudaEventCreateWithFlags(&ps.ev_rest[i], cudaEventDisableTiming))) return e;
     }
-    if ((e = cudaEventCreateWithFlags(&g_ps.ev_start, cudaEventDisableTiming))) return e;
-    g_ps.dev = dev;
+    if ((e = cudaEventCreateWithFlags(&ps.ev_start, cudaEventDisableTiming))) return e;
+    ps.ready = true;
     return cudaSuccess;
 }
 }  // namespace
@@ -505,16 +512,17 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
     cudaGetDevice(&dev);
     cudaError_t e = potrf_streams(dev);
     if (e != cudaSuccess) return e;
-    cudaStream_t sp = g_ps.sp;
+    PotrfStreams &ps = *g_cur;
+    cudaStream_t sp = ps.sp;
     // the panel stream starts after everything already queued on the main stream (Sigma)
-    if ((e = cudaEventRecord(g_ps.ev_start, st))) return e;
-    if ((e = cudaStreamWaitEvent(sp, g_ps.ev_start, 0))) return e;
+    if ((e = cudaEventRecord(ps.ev_start, st))) return e;
+    if ((e = cudaStreamWaitEvent(sp, ps.ev_start, 0))) return e;
     if ((e = launch_potrf_panel(n, tiles, 0, std::min(KP, ncols), d_info, sp))) return e;
-    if ((e = cudaEventRecord(g_ps.ev_panel[0], sp))) return e;
+    if ((e = cudaEventRecord(ps.ev_panel[0], sp))) return e;
     for (int s = 0; s < S; ++s) {
         const int k = s * KP, w = std::min(KP, ncols - k);
         const int kn = k + w;
-        if ((e = cudaStreamWaitEvent(st, g_ps.ev_panel[s & 1], 0))) return e;
+        if ((e = cudaStreamWaitEvent(st, ps.ev_panel[s & 1], 0))) return e;
         if (s + 1 == S) {
             // last super-panel: the trailing (Schur complement) block of a partial factorisation
             if (kn < nt && (e = launch_potrf_update(n, tiles, k, w, kn, 1, 1, 0, st))) return e;
@@ -523,12 +531,12 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
         const int wn = std::min(KP, ncols - kn);
         // main stream: columns >= kn + wn with super-panel s
         if ((e = launch_potrf_update(n, tiles, k, w, kn + wn, 1, 1, panel_sms(), st))) return e;
-        if ((e = cudaEventRecord(g_ps.ev_rest[s & 1], st))) return e;
+        if ((e = cudaEventRecord(ps.ev_rest[s & 1], st))) return e;
         // panel stream: columns kn .. kn+wn-1 with super-panel s, then factor super-panel s+1
-        if (s >= 1 && (e = cudaStreamWaitEvent(sp, g_ps.ev_rest[(s - 1) & 1], 0))) return e;
+        if (s >= 1 && (e = cudaStreamWaitEvent(sp, ps.ev_rest[(s - 1) & 1], 0))) return e;
         if ((e = launch_potrf_update(n, tiles, k, w, kn, nt, wn, 0, sp))) return e;
         if ((e = launch_potrf_panel(n, tiles, kn, wn, d_info, sp))) return e;
-        if ((e = cudaEventRecord(g_ps.ev_panel[(s + 1) & 1], sp))) return e;
+        if ((e = cudaEventRecord(ps.ev_panel[(s + 1) & 1], sp))) return e;
     }
     return cudaGetLastError();
 }
