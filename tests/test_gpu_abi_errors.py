@@ -65,7 +65,7 @@ def test_mc_and_posterior_and_matern_reject_bad_arguments(torch):
     n = 200
     T = small_L(torch, n)
     d_a = torch.zeros(n, dtype=torch.float64, device="cuda")
-    usage(mvn().mvn_mc_validate, T, n, d_a, 1, 0, 100, method=2)
+    usage(mvn().mvn_mc_validate, T, n, d_a, 1, 0, 100, method=3)
     usage(mvn().mvn_mc_validate, T, n, d_a, 1, 50, 50)
     xy = np.random.default_rng(1).uniform(size=(60, 2))
     mvn().mvn_posterior(xy, np.zeros(60), np.array([1, 5]), np.zeros(2), 1.0, 0.1, 0.5, 1e-8, 0.5)
