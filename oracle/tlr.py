@@ -1,0 +1,53 @@
+"""ORACLE (test infrastructure only) — NEXT-3 (part), Tile Low-Rank compression at a fixed accuracy.
+
+PAPER.md §II-C: TLR "is based on the separate approximation of each tile using the
+Singular Value Decomposition (SVD) ... the ranks of the tiles correspond to the most significant
+singular values"; Alg. 1 l.7: pmvn_init "encompasses the compression of the covariance
+matrix Sigma into the TLR format". Reading R23: the matrix is cut into nb x nb tiles
+(nb = 128, the last tile zero-padded); the diagonal tiles stay dense; every off-diagonal tile A keeps
+its singular triplets with sigma_i >= eps (absolute threshold) and is replaced by U_k S_k V_k^T.
+One library SVD (numpy.linalg.svd, LAPACK gesdd) per tile, fp64. Pinned in tests/test_oracle_tlr.py
+against Eckart-Young (spectral error = sigma_{k+1} < eps, Frobenius error^2 = sum of the dropped
+sigma_i^2), exact-rank tiles, eps = 0 (identity), and singular values from an independent route
+(eigenvalues of A^T A).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+NB = 128
+
+
+def tile_svd(A: np.ndarray):
+    """Singular values (descending) and factors of one tile."""
+    U, s, Vt = np.linalg.svd(A)
+    return U, s, Vt
+
+
+def compress_tile(A: np.ndarray, eps: float):
+    """(A_tilde, k, s): rank-k truncation keeping sigma_i >= eps (R23)."""
+    U, s, Vt = tile_svd(A)
+    k = int(np.count_nonzero((s >= eps) & (s > 0.0)))
+    return (U[:, :k] * s[:k]) @ Vt[:k, :], k, s
+
+
+def tlr_compress(S: np.ndarray, eps: float, nb: int = NB):
+    """Symmetric S (n x n) -> (S_tilde, ranks, sigmas). ranks[I(I-1)/2 + J] for tile (I, J), I > J;
+    S_tilde is symmetric, diagonal tiles equal to S's."""
+    S = np.asarray(S, dtype=np.float64)
+    n = S.shape[0]
+    nt = -(-n // nb)
+    P = np.zeros((nt * nb, nt * nb))
+    P[:n, :n] = S
+    out = P.copy()
+    ranks = np.zeros(max(nt * (nt - 1) // 2, 0), dtype=np.int64)
+    sig = np.zeros((len(ranks), nb))
+    for I in range(1, nt):
+        for J in range(I):
+            A = P[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb]
+            At, k, s = compress_tile(A, eps)
+            t = I * (I - 1) // 2 + J
+            ranks[t], sig[t] = k, s
+            out[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb] = At
+            out[J * nb:(J + 1) * nb, I * nb:(I + 1) * nb] = At.T
+    return out[:n, :n], ranks, sig

@@ -33,7 +33,7 @@ ABI_SYMBOLS = [
     "mvn_lattice_shifts", "mvn_sov_prefix", "mvn_prefix_rescale", "mvn_prefix_finalize",
     "mvn_confidence_region", "mvn_crd", "mvn_potrf_panel", "mvn_potrf_update", "mvn_panel_pack",
     "mvn_panel_unpack", "mvn_potrf_info", "mvn_mc_validate", "mvn_mc_levels", "mvn_potrf_panel_width",
-    "mvn_posterior", "mvn_posterior_tiles",
+    "mvn_posterior", "mvn_posterior_tiles", "mvn_tlr_compress",
 ]
 
 
@@ -122,6 +122,7 @@ def lib() -> ctypes.CDLL:
         "mvn_mc_levels": (S, [I64, P, I64, P, I64, P]),
         "mvn_posterior": (S, [P, ctypes.POINTER(mvn_posterior_problem), P, P, ctypes.POINTER(I64)]),
         "mvn_posterior_tiles": (S, [P, T, P, P]),
+        "mvn_tlr_compress": (S, [P, T, P, D, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -423,6 +424,19 @@ def crd_posterior(xy, mu, obs, y, sigma2, beta, nu, nugget, tau, u, N, R, seed, 
     logp = mvn_prefix_finalize(M, S, N * R).cpu().numpy()
     k, tie = mvn_confidence_region(logp, conf)
     return CrdOutput(order, logp, k, tie, info, ()), mp, vp, T
+
+
+# ---- NEXT-3 (part): fixed-accuracy TLR compression
+def mvn_tlr_compress(t, n: int, eps: float, ranks=None):
+    """Replaces every off-diagonal tile of the tile-packed `t` by its truncated SVD (sigma_i >= eps),
+    in place. Returns the CUDA int32 ranks, tile (I, J) at I(I-1)/2 + J."""
+    import torch
+    c = Context.get(t.device.index)
+    nt = -(-n // TILE)
+    ranks = torch.empty(max(nt * (nt - 1) // 2, 1), dtype=torch.int32, device=t.device) if ranks is None else ranks
+    c.check(lib().mvn_tlr_compress(c.h, tiles(n), _dev_ptr(t, torch.float64), float(eps), _dev_ptr(ranks, torch.int32)),
+            "mvn_tlr_compress")
+    return ranks
 
 
 @dataclass

@@ -152,7 +152,7 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
     c->nsm = prop.multiProcessorCount;
     c->stream = (cudaStream_t)cuda_stream;
     if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess || mvn::mc_init() != cudaSuccess ||
-        mvn::mc_oz_init() != cudaSuccess ||
+        mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess ||
         cudaMalloc(&c->d_info, 2 * sizeof(int64_t)) != cudaSuccess) {
         delete c;
         return MVN_E_CUDA;
@@ -557,6 +557,14 @@ mvn_status mvn_posterior_tiles(mvn_ctx *c, mvn_tiles t, const int64_t *order, do
     MVN_CUDA(c, cudaMemcpyAsync(c->cta, order, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
     MVN_CUDA(c, mvn::launch_permute_sym((const double *)c->post, c->post_off, (const int64_t *)c->cta, n, d_tiles, c->stream));
     MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_tlr_compress(mvn_ctx *c, mvn_tiles t, double *d_tiles, double eps, int32_t *d_ranks) {
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !d_tiles || !d_ranks || !(eps >= 0.0))
+        return fail(c, MVN_E_USAGE, "mvn_tlr_compress: bad arguments (need nb=128, eps >= 0)");
+    MVN_CUDA(c, mvn::launch_tlr_compress(t.n, d_tiles, eps, d_ranks, c->stream));
     return MVN_OK;
 }
 

@@ -58,6 +58,10 @@ cudaError_t launch_get_row(const double *tiles, int64_t row, int64_t col0, int64
 cudaError_t launch_get_diag(const double *tiles, int64_t begin, int64_t n, double *out, cudaStream_t st);
 cudaError_t launch_permute_sym(const double *src, int64_t off, const int64_t *order, int64_t n, double *dst, cudaStream_t st);
 
+// NEXT-3 (part): fixed-accuracy TLR compression of the off-diagonal tiles (kernels_tlr.cu)
+cudaError_t tlr_init();
+cudaError_t launch_tlr_compress(int64_t n, double *tiles, double eps, int *ranks, cudaStream_t st);
+
 // NEXT-2: Monte-Carlo validation
 cudaError_t mc_init();
 int64_t mc_z_doubles(int64_t n, int64_t ns);

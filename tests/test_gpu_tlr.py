@@ -1,0 +1,149 @@
+"""NEXT-3 (part) on the GPU: fixed-accuracy TLR compression (mvn_tlr_compress, reading R23) against
+the oracle (oracle/tlr.py: one LAPACK SVD per tile). Ranks must agree except where an oracle
+singular value lies within 1e-12 of eps (a near tie, decided by rounding); the compressed tiles
+agree to 1e-12 + 1e-13 sigma_1 (1 + sigma_1 / gap) (the Jacobi and gesdd subspaces of the same tile
+differ by rounding / gap, gap = sigma_k - sigma_k+1); and the
+GPU result satisfies Eckart-Young itself (||A - A_k||_2 = sigma_{k+1} < eps). The compressed matrix
+then runs through POTRF + SOV and matches the oracle pipeline on the oracle's compressed matrix."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+NB = 128
+
+
+@pytest.fixture(scope="module")
+def torch(cuda_device):
+    import torch as t
+    return t
+
+
+def mvn():
+    import paper_2405_14892_b200 as m
+    return m
+
+
+def dense_sym(T, n):
+    L = mvn().mvn_unpack_lower(T, n).T.contiguous().cpu().numpy()
+    return np.tril(L) + np.tril(L, -1).T
+
+
+def sorted_cov(torch, cfg):
+    import test_gpu_parity as P
+    inp, order, a = P.sorted_inputs(cfg)
+    xs = inp.xy[order]
+    T = P.gpu_cov(torch, xs, cfg)
+    S = oracle.covariance(xs, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    return T, S, a
+
+
+def check_vs_oracle(T, S, ranks_gpu, eps, n):
+    St, ro, sig = oracle.tlr_compress(S, eps)
+    G = dense_sym(T, n)
+    nt = -(-n // NB)
+    t = 0
+    for I in range(1, nt):
+        for J in range(I):
+            k, ko = int(ranks_gpu[t]), int(ro[t])
+            if k != ko:      # only a near tie at the threshold may differ
+                lo, hi = min(k, ko), max(k, ko)
+                assert np.all(np.abs(sig[t][lo:hi] - eps) <= 1e-12), (I, J, k, ko, sig[t][lo:hi])
+            rs, cs = slice(I * NB, min((I + 1) * NB, n)), slice(J * NB, (J + 1) * NB)
+            E = S[rs, cs] - G[rs, cs]
+            e2 = np.linalg.norm(E, 2)
+            assert (e2 < eps + 1e-12) if eps > 0 else np.max(np.abs(E)) < 1e-13, (I, J, k, ko, e2, sig[t][max(k - 2, 0):k + 2])
+            if k == ko:
+                # the kept subspace of a tile moves by (rounding perturbation) / (sigma_k - sigma_k+1)
+                sg = sig[t]
+                gap = sg[k - 1] - sg[k] if 0 < k < NB else np.inf
+                tol = 1e-12 + 1e-13 * sg[0] * (1.0 + sg[0] / gap)
+                assert np.max(np.abs(G[rs, cs] - St[rs, cs])) <= tol, (I, J, k, gap)
+            t += 1
+    for I in range(nt):                       # diagonal tiles untouched
+        rs = slice(I * NB, min((I + 1) * NB, n))
+        assert np.array_equal(G[rs, rs], dense_sym(T, n)[rs, rs])
+    return St, ro
+
+
+@pytest.mark.parametrize("base,g", [("B", 23), ("C", 30), ("B", 17)])
+@pytest.mark.parametrize("eps", [1e-1, 1e-3, 1e-6])
+def test_tlr_compress_vs_oracle(torch, base, g, eps):
+    cfg = W.small_config(f"tlr{g}", g, 100, 1, base=base)
+    T, S, _ = sorted_cov(torch, cfg)
+    T0 = T.clone()
+    n = cfg.n
+    ranks = mvn().mvn_tlr_compress(T, n, eps).cpu().numpy()
+    nt = -(-n // NB)
+    assert ranks.shape[0] == nt * (nt - 1) // 2 and ranks.min() >= 0 and ranks.max() <= NB
+    check_vs_oracle(T, S, ranks, eps, n)
+    G0 = dense_sym(T0, n)
+    G = dense_sym(T, n)
+    for I in range(nt):
+        rs = slice(I * NB, min((I + 1) * NB, n))
+        assert np.array_equal(G[rs, rs], G0[rs, rs])
+
+
+def test_tlr_exact_rank(torch):
+    rng = np.random.default_rng(11)
+    n = 300
+    X = rng.standard_normal((n, 5))
+    S = X @ X.T + np.diag(rng.uniform(1, 2, n))
+    T = mvn().mvn_pack_lower(torch.from_numpy(S).cuda(), n)
+    ranks = mvn().mvn_tlr_compress(T, n, 1e-9).cpu().numpy()
+    assert list(ranks) == [5, 5, 5]
+    assert np.max(np.abs(dense_sym(T, n) - S)) <= 1e-12 * np.max(np.abs(S))
+    T = mvn().mvn_pack_lower(torch.from_numpy(S).cuda(), n)
+    assert list(mvn().mvn_tlr_compress(T, n, 1e6).cpu().numpy()) == [0, 0, 0]
+    G = dense_sym(T, n)
+    assert not G[NB:2 * NB, :NB].any() and not G[2 * NB:, :2 * NB].any()
+
+
+def test_tlr_eps_zero_full_rank(torch):
+    rng = np.random.default_rng(12)
+    n = 256
+    A = rng.standard_normal((n, n))
+    S = A @ A.T / n + np.eye(n)
+    T = mvn().mvn_pack_lower(torch.from_numpy(S).cuda(), n)
+    ranks = mvn().mvn_tlr_compress(T, n, 0.0).cpu().numpy()
+    assert list(ranks) == [128]
+    assert np.max(np.abs(dense_sym(T, n) - S)) <= 1e-13
+
+
+def test_tlr_single_tile_is_noop(torch):
+    n = 100
+    rng = np.random.default_rng(13)
+    xy = rng.uniform(size=(n, 2))
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, 0.1, 0.5, 1e-8)
+    T0 = T.clone()
+    mvn().mvn_tlr_compress(T, n, 1e-2)
+    assert torch.equal(T, T0)
+
+
+def test_tlr_bad_args(torch):
+    T = mvn().alloc_tiles(300, "cuda")
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_tlr_compress(T, 300, -1.0)
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-5])
+def test_tlr_pipeline_vs_oracle(torch, eps):
+    """Compressed Sigma -> POTRF -> SOV -> log P_k, against the oracle pipeline on its own compressed
+    Sigma (shared sample range; the two compressed matrices differ at rounding level)."""
+    import test_gpu_parity as P
+    cfg = W.small_config("tlrp", 23, 300, 2, base="B")
+    T, S, a = sorted_cov(torch, cfg)
+    n = cfg.n
+    ranks = mvn().mvn_tlr_compress(T, n, eps).cpu().numpy()
+    St, ro = check_vs_oracle(T, S, ranks, eps, n)
+    info = mvn().mvn_potrf(T, n, raise_on_numeric=False)
+    Lo, info_o = oracle.cholesky(St)
+    assert (info == -1) == (info_o < 0)
+    if info != -1:
+        pytest.skip("compressed Sigma not SPD at this eps")
+    M, Sg = P.gpu_sov(torch, T, n, a, cfg.N, cfg.R, 5)
+    Mo, So = P.oracle_range(Lo, a, np.full(n, np.inf), cfg.N, cfg.R, 5, 0, cfg.NR)
+    lg, lo = P.logp_from(M, Sg, cfg.NR), P.logp_from(Mo, So, cfg.NR)
+    assert np.max(np.abs(lg - lo)) <= 1e-9

@@ -1,0 +1,73 @@
+"""Pins for oracle/tlr.py (NEXT-3 part, reading R23) against what the mathematics fixes:
+Eckart-Young optimality of the truncated SVD, exact-rank tiles, eps = 0, and singular values
+computed by an independent route (eigenvalues of A^T A, LAPACK syevd instead of gesdd)."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.filterwarnings("ignore")
+
+
+def test_exact_rank_tiles():
+    rng = np.random.default_rng(3)
+    n, nb = 300, 128                            # 3 tile rows, ragged last tile
+    X = rng.standard_normal((n, 5))
+    S = X @ X.T + np.diag(rng.uniform(1, 2, n))  # off-diagonal blocks have rank <= 5
+    St, ranks, _ = oracle.tlr_compress(S, 1e-10)
+    assert list(ranks) == [5, 5, 5]
+    assert np.max(np.abs(St - S)) < 1e-12
+    St0, r0, _ = oracle.tlr_compress(S, 1e3)   # above every singular value: off-diagonal tiles vanish
+    assert list(r0) == [0, 0, 0]
+    for I in range(3):
+        sl = slice(I * nb, min((I + 1) * nb, n))
+        assert np.array_equal(St0[sl, sl], S[sl, sl])
+    St0[:nb, :nb] = 0; St0[nb:2 * nb, nb:2 * nb] = 0; St0[2 * nb:, 2 * nb:] = 0
+    assert not St0.any()
+
+
+def test_eps_zero_is_identity():
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((260, 260))
+    S = A @ A.T
+    St, ranks, _ = oracle.tlr_compress(S, 0.0)
+    assert ranks[0] == 128
+    assert np.max(np.abs(St - S)) < 1e-10 * np.max(np.abs(S))
+
+
+@pytest.mark.parametrize("eps", [1e-1, 1e-3, 1e-6])
+def test_eckart_young(eps):
+    cfg = W.small_config("tlr", 16, 10, 1, base="B")
+    inp = W.make_inputs(cfg)
+    S = oracle.covariance(inp.xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    St, ranks, sig = oracle.tlr_compress(S, eps)
+    nb, t = 128, 0
+    for I in range(1, 2):
+        for J in range(I):
+            A = S[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb]
+            E = A - St[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb]
+            k = ranks[t]
+            # independent singular values: eig(A^T A) = sigma^2, each within eps_mach * sigma_1^2
+            ev = np.linalg.eigvalsh(A.T @ A)[::-1]
+            assert np.allclose(ev, sig[t] ** 2, rtol=1e-10, atol=1e-13 * sig[t][0] ** 2)
+            s2 = np.linalg.norm(E, 2)
+            tail = sig[t][k] if k < nb else 0.0
+            assert abs(s2 - tail) <= 1e-12 + 1e-10 * tail and s2 < eps
+            assert abs(np.linalg.norm(E) ** 2 - np.sum(sig[t][k:] ** 2)) <= 1e-12 * max(1.0, np.sum(sig[t] ** 2))
+            assert k == 0 or sig[t][k - 1] >= eps
+            t += 1
+    assert np.allclose(St, St.T, atol=0, rtol=0)
+
+
+def test_rank_monotone_in_eps():
+    cfg = W.small_config("tlr", 20, 10, 1, base="B")
+    inp = W.make_inputs(cfg)
+    S = oracle.covariance(inp.xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    prev = None
+    for eps in [1e-1, 1e-2, 1e-4, 1e-8]:
+        _, r, _ = oracle.tlr_compress(S, eps)
+        if prev is not None:
+            assert np.all(r >= prev)
+        prev = r
+    assert prev.max() <= 128
