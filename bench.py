@@ -354,6 +354,61 @@ def run_potrf_dist(args, cfg):
     return 0
 
 
+# --------------------------------------------------------------------------------- NEXT-3 workload
+def run_tlr(args):
+    """TLR compression (NEXT-3 part, R23) at the paper's accuracy setting: n = 40,000 sites
+    (200 x 200 jittered grid), exponential kernel, sigma^2 = 1, beta = 0.1 (medium correlation),
+    Sigma in the sorted order, eps = --tlr-eps. Timed on the device (CUDA events around
+    mvn_tlr_compress on its stream): the compression of all 48,828 off-diagonal tiles; the copy of the
+    dense Sigma into the working buffer before each step is outside the events. Algorithmic flops
+    per tile: 12 nb^3 (the Golub-Van Loan count of an nb x nb SVD with Sigma and V) + 4 nb^2 k (the
+    projection A V_k V_k^T), nb = 128."""
+    import torch
+    import paper_2405_14892_b200 as mvn
+    torch.cuda.set_device(0)
+    cfg = W.small_config("tlr-40K", 200, 10_000, 8, base="B")
+    inp = W.make_inputs(cfg)
+    n = cfg.n
+    order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
+    d_xs = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+    base = mvn.mvn_cov_matern(d_xs, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    T = torch.empty_like(base)
+    nt = -(-n // 128)
+    ntiles = nt * (nt - 1) // 2
+    ranks = torch.empty(ntiles, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream()
+    ts = []
+    for it in range(args.warmup + args.steps):
+        T.copy_(base)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        mvn.mvn_tlr_compress(T, n, args.tlr_eps, ranks)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            ts.append(e0.elapsed_time(e1))
+    ms = float(np.mean(ts))
+    r = ranks.cpu().numpy()
+    flops = ntiles * 12.0 * 128 ** 3 + 4.0 * 128 ** 2 * float(r.sum())
+    achieved = flops / (ms / 1e3) / 1e12
+    info = mvn.mvn_potrf(T, n, raise_on_numeric=False)
+    line = {"metric": "TLR compression time (NEXT-3)", "value": ms, "unit": "ms", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{n} sites (200x200 jittered grid, exponential kernel s2=1, beta=0.1), sorted order, "
+                                   f"128-wide tiles, eps={args.tlr_eps:g} (P:368, P:439)", "n": n, "tiles": ntiles,
+                       "eps": args.tlr_eps},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
+                         "algorithmic": "12 nb^3 (SVD with Sigma and V, Golub-Van Loan) + 4 nb^2 k per tile; peak = the "
+                                        "fp64 pipe (64 FMA/clk/SM x 148 x 1.965 GHz = 37.2 TF nominal, shared with DMMA, "
+                                        "measured 37.07)"},
+            "ranks": {"mean": float(r.mean()), "p90": float(np.percentile(r, 90)), "max": int(r.max())},
+            "potrf_info_after": int(info), "gpu_launches": args.steps}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # --------------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -369,10 +424,12 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: run the multi-GPU code path (NCCL process group, distributed Cholesky, "
                          "all_reduce combine, pinned-buffer e2e) even with one rank")
-    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist"],
+    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr"],
                     help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
                          "posterior: NEXT-4 conditioning (paper size: 200x200 sites, 6,250 observations); "
-                         "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU")
+                         "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU; "
+                         "tlr: NEXT-3 TLR compression at the paper's 40K-site accuracy setting")
+    ap.add_argument("--tlr-eps", type=float, default=1e-3, help="--workload tlr: accuracy eps (R23)")
     ap.add_argument("--mc-samples", type=int, default=50_000, help="--workload mc: draws (paper: N = 50,000, P:595)")
     ap.add_argument("--mc-method", type=int, default=0, choices=[0, 1, 2],
                     help="--workload mc: 0 = fp64 DMMA, 1 = int8 tensor cores (tcgen05 Ozaki emulation, M128 N64), "
@@ -383,6 +440,8 @@ def main():
         return run_reference(args, cfg)
     if args.workload == "mc":
         return run_mc(args, cfg)
+    if args.workload == "tlr":
+        return run_tlr(args)
     if args.workload == "posterior":
         return run_posterior(args)
     if args.workload == "potrf-dist":

@@ -24,8 +24,10 @@
 
 namespace mvn {
 namespace tlr {
-// LD odd: a warp reading one row across 32 columns is conflict-free (phase 3)
-constexpr int NB = kTile, LD = kTile + 1, NT = 512, NW = NT / 32, MAX_SWEEPS = 30;
+// LD even (16-byte aligned columns): the Jacobi steps move columns as double2, an 8-lane group
+// covering 128 contiguous bytes per access, so a warp request is exactly 4 wavefronts whatever the
+// 4 columns are; strided phases (transpose, phase 3) use a skewed index order instead
+constexpr int NB = kTile, LD = kTile + 2, NT = 512, NW = NT / 32, MAX_SWEEPS = 30;
 constexpr int SMEM = (NB * LD + 2 * NW * NB + 2 * NB) * 8 + NB * 4;
 }  // namespace tlr
 
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
     }
     // X = R^T (lower triangular)
     for (int e = tid; e < NB * NB; e += NT) {
-        const int i = e >> 7, c = e & 127;
+        const int c = e & 127, i = ((e >> 7) + c) & 127;   // skewed: lanes hit distinct banks
         if (i > c) {
             X[c * LD + i] = X[i * LD + c];
             X[i * LD + c] = 0.0;
@@ -179,15 +181,15 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
         for (int s = 0; s < NB - 1; ++s) {
             const int p = warp + NW * grp;
             double *ai = X + rr_col(p, s) * LD, *aj = X + rr_col(NB - 1 - p, s) * LD;
-            double x[NB / 8], y[NB / 8];
+            double2 x[NB / 16], y[NB / 16];       // elements 2 l8 + 16 m (+1)
             double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-            for (int m = 0; m < NB / 8; ++m) {
-                x[m] = ai[l8 + 8 * m];
-                y[m] = aj[l8 + 8 * m];
-                al = fma(x[m], x[m], al);
-                be = fma(y[m], y[m], be);
-                ga = fma(x[m], y[m], ga);
+            for (int m = 0; m < NB / 16; ++m) {
+                x[m] = *reinterpret_cast<const double2 *>(ai + 2 * l8 + 16 * m);
+                y[m] = *reinterpret_cast<const double2 *>(aj + 2 * l8 + 16 * m);
+                al = fma(x[m].x, x[m].x, fma(x[m].y, x[m].y, al));
+                be = fma(y[m].x, y[m].x, fma(y[m].y, y[m].y, be));
+                ga = fma(x[m].x, y[m].x, fma(x[m].y, y[m].y, ga));
             }
 #pragma unroll
             for (int o = 4; o; o >>= 1) {
@@ -200,9 +202,9 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
                 const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
 #pragma unroll
-                for (int m = 0; m < NB / 8; ++m) {
-                    ai[l8 + 8 * m] = c * x[m] - sn * y[m];
-                    aj[l8 + 8 * m] = sn * x[m] + c * y[m];
+                for (int m = 0; m < NB / 16; ++m) {
+                    *reinterpret_cast<double2 *>(ai + 2 * l8 + 16 * m) = make_double2(c * x[m].x - sn * y[m].x, c * x[m].y - sn * y[m].y);
+                    *reinterpret_cast<double2 *>(aj + 2 * l8 + 16 * m) = make_double2(sn * x[m].x + c * y[m].x, sn * x[m].y + c * y[m].y);
                 }
                 if (l8 == 0) chg = 1;
             }
@@ -244,7 +246,10 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
         for (int q = lane; q < k; q += 32) {      // w_q = u_q^T a
             const double *u = X + sel[q] * LD;
             double d = 0.0;
-            for (int r = 0; r < NB; ++r) d = fma(u[r], wa[r], d);
+            for (int r0 = 0; r0 < NB; ++r0) {     // skewed start: the 32 lanes read 32 columns in distinct banks
+                const int r = (r0 + q) & (NB - 1);
+                d = fma(u[r], wa[r], d);
+            }
             ww[q] = d;
         }
         __syncwarp();
