@@ -75,6 +75,21 @@ mvn_status ensure(mvn_ctx *c, void **buf, size_t *cap, size_t bytes) {
     return MVN_OK;
 }
 
+// Every entry point runs on the context's device (the caller's current device is restored on
+// return), so one process may drive several GPUs through several contexts.
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(const mvn_ctx *c) {
+        int cur = -1;
+        if (c && cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess) prev = cur;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DevGuard(const DevGuard &) = delete;
+    DevGuard &operator=(const DevGuard &) = delete;
+};
+
 bool tiles_ok(mvn_tiles t) { return t.n >= 1 && t.nb == mvn::kTile; }
 
 // ----------------------------------------------------------------------------- lattice (R8)
@@ -159,6 +174,7 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
     }
     const int64_t minus1 = -1;
     if (cudaMemcpy(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(c->d_info);
         delete c;
         return MVN_E_CUDA;
     }
@@ -185,6 +201,7 @@ mvn_status mvn_set_stream(mvn_ctx *c, void *s) {
 const char *mvn_last_error(const mvn_ctx *c) { return c ? c->err.c_str() : "null context"; }
 
 mvn_status mvn_trim(mvn_ctx *c) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
     for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX})
@@ -207,12 +224,14 @@ size_t mvn_tiles_bytes(mvn_tiles t) {
 }
 
 mvn_status mvn_pack_lower(mvn_ctx *c, mvn_tiles t, const double *d_dense, int64_t ld, double *d_tiles) {
+    DevGuard dev_guard(c);
     if (!c || !tiles_ok(t) || !d_dense || !d_tiles || ld < t.n) return fail(c, MVN_E_USAGE, "mvn_pack_lower: bad arguments");
     MVN_CUDA(c, mvn::launch_pack(t.n, d_dense, ld, d_tiles, true, c->stream));
     return MVN_OK;
 }
 
 mvn_status mvn_unpack_lower(mvn_ctx *c, mvn_tiles t, const double *d_tiles, double *d_dense, int64_t ld) {
+    DevGuard dev_guard(c);
     if (!c || !tiles_ok(t) || !d_dense || !d_tiles || ld < t.n) return fail(c, MVN_E_USAGE, "mvn_unpack_lower: bad arguments");
     MVN_CUDA(c, mvn::launch_pack(t.n, d_dense, ld, const_cast<double *>(d_tiles), false, c->stream));
     return MVN_OK;
@@ -240,6 +259,7 @@ mvn_status mvn_marginal_order(int64_t n, const double *mu, const double *var, do
 
 mvn_status mvn_cov_matern(mvn_ctx *c, mvn_tiles t, const double *d_xy, double sigma2, double beta, double nu,
                           double nugget, double *d_tiles) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!tiles_ok(t) || !d_xy || !d_tiles || !(sigma2 > 0) || !(beta > 0) || !(nugget >= 0) ||
         !(nu == 0.5 || nu == 1.5 || nu == 2.5))
@@ -249,6 +269,7 @@ mvn_status mvn_cov_matern(mvn_ctx *c, mvn_tiles t, const double *d_xy, double si
 }
 
 mvn_status mvn_potrf(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t *info) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!tiles_ok(t) || !d_tiles || !info) return fail(c, MVN_E_USAGE, "mvn_potrf: bad arguments");
     const int64_t minus1 = -1;
@@ -263,6 +284,7 @@ mvn_status mvn_potrf(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t *info) {
 }
 
 mvn_status mvn_potrf_panel(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k, int64_t kp) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
     if (!nt || !d_tiles || k < 0 || k >= nt || kp < 1 || kp > 4) return fail(c, MVN_E_USAGE, "mvn_potrf_panel: bad arguments");
@@ -272,6 +294,7 @@ mvn_status mvn_potrf_panel(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k, 
 
 mvn_status mvn_potrf_update(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k, int64_t kp, int64_t col_first,
                             int64_t col_stride, int64_t col_block, int32_t sm_reserve) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
     if (!nt || !d_tiles || k < 0 || kp < 1 || kp > 4 || col_first < std::min(k + kp, nt) || col_stride < 1 ||
@@ -286,6 +309,7 @@ mvn_status mvn_potrf_update(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k,
 int64_t mvn_potrf_panel_width(int64_t n) { return n < 1 ? -1 : mvn::potrf_panel_width(n); }
 
 mvn_status mvn_panel_pack(mvn_ctx *c, mvn_tiles t, const double *d_tiles, int64_t k, int64_t kp, double *d_panel) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
     if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 4)
@@ -295,6 +319,7 @@ mvn_status mvn_panel_pack(mvn_ctx *c, mvn_tiles t, const double *d_tiles, int64_
 }
 
 mvn_status mvn_panel_unpack(mvn_ctx *c, mvn_tiles t, const double *d_panel, int64_t k, int64_t kp, double *d_tiles) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
     if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 4)
@@ -304,6 +329,7 @@ mvn_status mvn_panel_unpack(mvn_ctx *c, mvn_tiles t, const double *d_panel, int6
 }
 
 mvn_status mvn_potrf_info(mvn_ctx *c, int64_t *info, int32_t reset) {
+    DevGuard dev_guard(c);
     if (!c || !info) return fail(c, MVN_E_USAGE, "mvn_potrf_info: bad arguments");
     MVN_CUDA(c, cudaMemcpyAsync(info, c->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     if (reset) {
@@ -331,6 +357,7 @@ mvn_status mvn_lattice_shifts(uint64_t seed, int32_t R, int64_t n, uint64_t *D) 
 
 mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
                           const mvn_qmc *q, double *d_M, double *d_S) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!tiles_ok(t) || !d_L || !d_a || !q || !d_M || !d_S || q->N < 1 || q->R < 1 || q->sample_begin < 0 ||
         q->sample_end <= q->sample_begin || q->sample_end > q->N * (int64_t)q->R)
@@ -384,12 +411,14 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
 }
 
 mvn_status mvn_prefix_rescale(mvn_ctx *c, int64_t n, const double *d_Mglob, double *d_M, double *d_S) {
+    DevGuard dev_guard(c);
     if (!c || n < 1 || !d_Mglob || !d_M || !d_S) return fail(c, MVN_E_USAGE, "mvn_prefix_rescale: bad arguments");
     MVN_CUDA(c, mvn::launch_rescale(n, d_Mglob, d_M, d_S, c->stream));
     return MVN_OK;
 }
 
 mvn_status mvn_prefix_finalize(mvn_ctx *c, int64_t n, int64_t NR, const double *d_M, const double *d_S, double *d_logP) {
+    DevGuard dev_guard(c);
     if (!c || n < 1 || NR < 1 || !d_M || !d_S || !d_logP) return fail(c, MVN_E_USAGE, "mvn_prefix_finalize: bad arguments");
     MVN_CUDA(c, mvn::launch_finalize(n, NR, d_M, d_S, d_logP, c->stream));
     return MVN_OK;
@@ -419,6 +448,7 @@ mvn_status mvn_confidence_region(int64_t n, const double *logP, const double *co
 
 mvn_status mvn_mc_validate(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const mvn_mc *m,
                            uint64_t *d_count, int32_t *d_first) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!tiles_ok(t) || !d_L || !d_a || !m || !d_count || m->sample_begin < 0 || m->sample_end <= m->sample_begin)
         return fail(c, MVN_E_USAGE, "mvn_mc_validate: bad arguments (need nb=128, 0 <= begin < end)");
@@ -484,6 +514,7 @@ mvn_status mvn_mc_levels(int64_t n, const uint64_t *count, int64_t N_total, cons
 }
 
 mvn_status mvn_posterior(mvn_ctx *c, const mvn_posterior_problem *p, double *mu_post, double *var_post, int64_t *info) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!p || !mu_post || !var_post || !info || p->n < 1 || p->m < 1 || !p->xy || !p->mu || !p->obs || !p->y ||
         !(p->tau > 0) || !(p->sigma2 > 0) || !(p->beta > 0) || !(p->nugget >= 0) || !(p->nu == 0.5 || p->nu == 1.5 || p->nu == 2.5))
@@ -543,6 +574,7 @@ mvn_status mvn_posterior(mvn_ctx *c, const mvn_posterior_problem *p, double *mu_
 }
 
 mvn_status mvn_posterior_tiles(mvn_ctx *c, mvn_tiles t, const int64_t *order, double *d_tiles) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!tiles_ok(t) || !order || !d_tiles || c->post_n != t.n || !c->post)
         return fail(c, MVN_E_USAGE, "mvn_posterior_tiles: call mvn_posterior first (same n)");
@@ -561,6 +593,7 @@ mvn_status mvn_posterior_tiles(mvn_ctx *c, mvn_tiles t, const int64_t *order, do
 }
 
 mvn_status mvn_tlr_compress(mvn_ctx *c, mvn_tiles t, double *d_tiles, double eps, int32_t *d_ranks) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!tiles_ok(t) || !d_tiles || !d_ranks || !(eps >= 0.0))
         return fail(c, MVN_E_USAGE, "mvn_tlr_compress: bad arguments (need nb=128, eps >= 0)");
@@ -569,6 +602,7 @@ mvn_status mvn_tlr_compress(mvn_ctx *c, mvn_tiles t, double *d_tiles, double eps
 }
 
 mvn_status mvn_crd(mvn_ctx *c, const mvn_crd_problem *p, mvn_crd_result *out) {
+    DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!p || !out || p->n < 1 || !p->xy || !p->mu || !out->order || !out->logP || (p->nconf > 0 && !out->k_star))
         return fail(c, MVN_E_USAGE, "mvn_crd: bad arguments");
