@@ -382,7 +382,7 @@ def run_tlr(args):
         T.copy_(base)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        mvn.mvn_tlr_compress(T, n, args.tlr_eps, ranks)
+        mvn.mvn_tlr_compress(T, n, args.tlr_eps, ranks, mode=args.tlr_mode)
         e1.record(st)
         torch.cuda.synchronize()
         if it >= args.warmup:
@@ -397,7 +397,7 @@ def run_tlr(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{n} sites (200x200 jittered grid, exponential kernel s2=1, beta=0.1), sorted order, "
                                    f"128-wide tiles, eps={args.tlr_eps:g} (P:368, P:439)", "n": n, "tiles": ntiles,
-                       "eps": args.tlr_eps},
+                       "eps": args.tlr_eps, "mode": args.tlr_mode},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
                          "algorithmic": "12 nb^3 (SVD with Sigma and V, Golub-Van Loan) + 4 nb^2 k per tile; peak = the "
@@ -430,6 +430,8 @@ def main():
                          "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU; "
                          "tlr: NEXT-3 TLR compression at the paper's 40K-site accuracy setting")
     ap.add_argument("--tlr-eps", type=float, default=1e-3, help="--workload tlr: accuracy eps (R23)")
+    ap.add_argument("--tlr-mode", type=int, default=0, choices=[0, 1],
+                    help="--workload tlr: 0 = keep sigma_i >= eps, 1 = relative Frobenius error <= eps per tile")
     ap.add_argument("--mc-samples", type=int, default=50_000, help="--workload mc: draws (paper: N = 50,000, P:595)")
     ap.add_argument("--mc-method", type=int, default=0, choices=[0, 1, 2],
                     help="--workload mc: 0 = fp64 DMMA, 1 = int8 tensor cores (tcgen05 Ozaki emulation, M128 N64), "

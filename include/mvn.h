@@ -276,12 +276,15 @@ mvn_status mvn_posterior_tiles(mvn_ctx *ctx, mvn_tiles t, const int64_t *order, 
  * NEXT-3 (part): Tile Low-Rank compression at a fixed accuracy (§II-C,
  * P:175-176; Alg. 1 l.7 "pmvn_init() also encompasses the compression of the covariance matrix into
  * the TLR format"). Reading R23: every off-diagonal tile (I, J), I > J, of the tile-packed
- * d_tiles is replaced IN PLACE by its rank-k truncated SVD U_k S_k V_k^T, k = #{sigma_i >= eps}
- * (absolute threshold; diagonal tiles stay dense); the dense POTRF / SOV then run on the
- * compressed covariance unchanged (the TLR arithmetic of the Cholesky is not built: this gives the
- * paper's accuracy study of TLR vs dense, not its speedup). d_ranks: device int32 array of
- * nt(nt-1)/2 ranks, tile (I, J) at I(I-1)/2 + J. Asynchronous.                               */
-mvn_status mvn_tlr_compress(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, double eps, int32_t *d_ranks);
+ * d_tiles is replaced IN PLACE by its rank-k truncated SVD U_k S_k V_k^T; diagonal tiles stay dense.
+ * k follows the accuracy eps: mode MVN_TLR_ABS (0): k = #{sigma_i >= eps}; mode MVN_TLR_REL_FRO (1):
+ * the smallest k with ||A - A_k||_F <= eps ||A||_F for that tile (0 <= eps <= 1). The paper does not
+ * state its convention; both are offered. The dense POTRF / SOV then run on the compressed
+ * covariance unchanged (the TLR arithmetic of the Cholesky is not built: this gives the paper's
+ * accuracy study of TLR vs dense, not its speedup). d_ranks: device int32 array of nt(nt-1)/2
+ * ranks, tile (I, J) at I(I-1)/2 + J. Asynchronous. USAGE on a bad mode or eps.               */
+enum { MVN_TLR_ABS = 0, MVN_TLR_REL_FRO = 1 };
+mvn_status mvn_tlr_compress(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, double eps, int32_t mode, int32_t *d_ranks);
 
 /* ---------------------------------------------------------------------------------------------
  * End-to-end CRD (Alg. 1) on one GPU with HOST buffers: upload, a1..a10, download.

@@ -5,7 +5,9 @@ Singular Value Decomposition (SVD) ... the ranks of the tiles correspond to the 
 singular values"; Alg. 1 l.7: pmvn_init "encompasses the compression of the covariance
 matrix Sigma into the TLR format". Reading R23: the matrix is cut into nb x nb tiles
 (nb = 128, the last tile zero-padded); the diagonal tiles stay dense; every off-diagonal tile A keeps
-its singular triplets with sigma_i >= eps (absolute threshold) and is replaced by U_k S_k V_k^T.
+its k largest singular triplets and is replaced by U_k S_k V_k^T, k from the accuracy eps:
+mode "abs": k = #{sigma_i >= eps}; mode "fro": the smallest k with ||A - A_k||_F <= eps ||A||_F
+(relative per tile; the paper does not state its convention, both are offered).
 One library SVD (numpy.linalg.svd, LAPACK gesdd) per tile, fp64. Pinned in tests/test_oracle_tlr.py
 against Eckart-Young (spectral error = sigma_{k+1} < eps, Frobenius error^2 = sum of the dropped
 sigma_i^2), exact-rank tiles, eps = 0 (identity), and singular values from an independent route
@@ -24,14 +26,27 @@ def tile_svd(A: np.ndarray):
     return U, s, Vt
 
 
-def compress_tile(A: np.ndarray, eps: float):
-    """(A_tilde, k, s): rank-k truncation keeping sigma_i >= eps (R23)."""
+def rank_for(s: np.ndarray, eps: float, mode: str = "abs") -> int:
+    """k from the singular values s (descending) and the accuracy eps (R23)."""
+    if mode == "abs":
+        return int(np.count_nonzero((s >= eps) & (s > 0.0)))
+    tot = float(np.sum(s ** 2))
+    k = len(s)
+    tail = 0.0
+    while k > 0 and tail + s[k - 1] ** 2 <= eps * eps * tot:   # drop the smallest while within budget
+        tail += s[k - 1] ** 2
+        k -= 1
+    return k
+
+
+def compress_tile(A: np.ndarray, eps: float, mode: str = "abs"):
+    """(A_tilde, k, s): rank-k truncation (R23)."""
     U, s, Vt = tile_svd(A)
-    k = int(np.count_nonzero((s >= eps) & (s > 0.0)))
+    k = rank_for(s, eps, mode)
     return (U[:, :k] * s[:k]) @ Vt[:k, :], k, s
 
 
-def tlr_compress(S: np.ndarray, eps: float, nb: int = NB):
+def tlr_compress(S: np.ndarray, eps: float, nb: int = NB, mode: str = "abs"):
     """Symmetric S (n x n) -> (S_tilde, ranks, sigmas). ranks[I(I-1)/2 + J] for tile (I, J), I > J;
     S_tilde is symmetric, diagonal tiles equal to S's."""
     S = np.asarray(S, dtype=np.float64)
@@ -45,7 +60,7 @@ def tlr_compress(S: np.ndarray, eps: float, nb: int = NB):
     for I in range(1, nt):
         for J in range(I):
             A = P[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb]
-            At, k, s = compress_tile(A, eps)
+            At, k, s = compress_tile(A, eps, mode)
             t = I * (I - 1) // 2 + J
             ranks[t], sig[t] = k, s
             out[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb] = At

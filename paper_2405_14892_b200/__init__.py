@@ -122,7 +122,7 @@ def lib() -> ctypes.CDLL:
         "mvn_mc_levels": (S, [I64, P, I64, P, I64, P]),
         "mvn_posterior": (S, [P, ctypes.POINTER(mvn_posterior_problem), P, P, ctypes.POINTER(I64)]),
         "mvn_posterior_tiles": (S, [P, T, P, P]),
-        "mvn_tlr_compress": (S, [P, T, P, D, P]),
+        "mvn_tlr_compress": (S, [P, T, P, D, I32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -427,14 +427,19 @@ def crd_posterior(xy, mu, obs, y, sigma2, beta, nu, nugget, tau, u, N, R, seed, 
 
 
 # ---- NEXT-3 (part): fixed-accuracy TLR compression
-def mvn_tlr_compress(t, n: int, eps: float, ranks=None):
-    """Replaces every off-diagonal tile of the tile-packed `t` by its truncated SVD (sigma_i >= eps),
-    in place. Returns the CUDA int32 ranks, tile (I, J) at I(I-1)/2 + J."""
+TLR_ABS, TLR_REL_FRO = 0, 1
+
+
+def mvn_tlr_compress(t, n: int, eps: float, ranks=None, mode: int = TLR_ABS):
+    """Replaces every off-diagonal tile of the tile-packed `t` by its truncated SVD, in place: mode
+    TLR_ABS keeps sigma_i >= eps, TLR_REL_FRO the smallest rank with ||A - A_k||_F <= eps ||A||_F.
+    Returns the CUDA int32 ranks, tile (I, J) at I(I-1)/2 + J."""
     import torch
     c = Context.get(t.device.index)
     nt = -(-n // TILE)
     ranks = torch.empty(max(nt * (nt - 1) // 2, 1), dtype=torch.int32, device=t.device) if ranks is None else ranks
-    c.check(lib().mvn_tlr_compress(c.h, tiles(n), _dev_ptr(t, torch.float64), float(eps), _dev_ptr(ranks, torch.int32)),
+    c.check(lib().mvn_tlr_compress(c.h, tiles(n), _dev_ptr(t, torch.float64), float(eps), int(mode),
+                                   _dev_ptr(ranks, torch.int32)),
             "mvn_tlr_compress")
     return ranks
 

@@ -2,9 +2,9 @@
 // "the separate approximation of each tile using the Singular Value Decomposition ...
 // the ranks of the tiles correspond to the most significant singular values"; Alg. 1 l.7, P:248:
 // pmvn_init "encompasses the compression of the covariance matrix Sigma into the TLR format").
-// Reading R23: an off-diagonal 128 x 128 tile keeps the singular triplets with
-// sigma_i >= eps (absolute threshold on a unit-variance Sigma, HiCMA's fixed-accuracy mode); the
-// diagonal tiles stay dense.
+// Reading R23: an off-diagonal 128 x 128 tile keeps its k largest singular triplets,
+// k set by the accuracy eps: mode 0, sigma_i >= eps (absolute, on a unit-variance Sigma); mode 1,
+// the smallest k with ||A - A_k||_F <= eps ||A||_F (relative per tile). Diagonal tiles stay dense.
 //
 // One CTA per off-diagonal tile, the tile (column-major) in shared memory:
 //  1. column-pivoted Householder QR, A P = Q R (Q is not kept);
@@ -14,7 +14,7 @@
 //     Matérn tiles and is what makes the iteration converge within its sweep cap there
 //     (tools/tlr_jacobi_sweeps.py). X's columns are then u_i sigma_i with R^T = U_x Sigma W^T, so
 //     the right singular vectors of A are v_i = P u_i;
-//  3. k = #{sigma_i >= eps}; each row of A (re-read from global memory) is projected onto
+//  3. k from eps (mode above); each row of A (re-read from global memory) is projected onto
 //     span(v_1..v_k): A~ = A V_k V_k^T = U_k Sigma_k V_k^T, written back in place (the compressed
 //     tile in reconstructed form, which the dense POTRF / SOV consume unchanged); k is recorded.
 // Work is O(sweeps * 128^3) per tile on the fp64 ALU; used for the accuracy study, not on the
@@ -41,7 +41,7 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-__global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict__ tiles, int nt, double eps,
+__global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict__ tiles, int nt, double eps, int mode,
                                                             int *__restrict__ ranks) {
     using namespace tlr;
     extern __shared__ double sh[];
@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
     int *perm = reinterpret_cast<int *>(cn + NB); // column pivots: (A P)(:, r) = A(:, perm[r])
     __shared__ int chgf[2], k_sel, piv;
     __shared__ double vtv_s;
-    __shared__ double sig[NB];
-    __shared__ int sel[NB];
+    __shared__ double sig[NB], srt[NB];
+    __shared__ int sel[NB], pos[NB];
     (void)nt;
     // off-diagonal tile index -> (I, J), I > J
     const int64_t t = blockIdx.x;
@@ -220,13 +220,37 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
         sig[tid] = sqrt(s2);
     }
     __syncthreads();
+    if (tid < NB) {                               // position in descending order (ties: lower index first)
+        const double v = sig[tid];
+        int p = 0;
+#pragma unroll 4
+        for (int j = 0; j < NB; ++j) p += (sig[j] > v) || (sig[j] == v && j < tid);
+        pos[tid] = p;
+        srt[p] = v;
+    }
+    __syncthreads();
     if (tid == 0) {
         int k = 0;
-        for (int i = 0; i < NB; ++i)
-            if (sig[i] >= eps && sig[i] > 0.0) sel[k++] = i;
+        if (mode == 0) {                          // absolute: sigma_i >= eps
+#pragma unroll 1
+            while (k < NB && srt[k] >= eps && srt[k] > 0.0) ++k;
+        } else {                                  // relative Frobenius: ||A - A_k||_F <= eps ||A||_F
+            double tot = 0.0;
+#pragma unroll 1
+            for (int i = NB - 1; i >= 0; --i) tot = fma(srt[i], srt[i], tot);
+            const double budget = eps * eps * tot;
+            double tail = 0.0;
+            k = NB;
+            while (k > 0 && tail + srt[k - 1] * srt[k - 1] <= budget) {
+                tail = fma(srt[k - 1], srt[k - 1], tail);
+                --k;
+            }
+        }
         k_sel = k;
         ranks[t] = k;
     }
+    __syncthreads();
+    if (tid < NB && pos[tid] < k_sel) sel[pos[tid]] = tid;
     __syncthreads();
     const int k = k_sel;
     for (int e = tid; e < k * NB; e += NT) {
@@ -270,11 +294,11 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
 
 cudaError_t tlr_init() { return cudaFuncSetAttribute(k_tlr_compress, cudaFuncAttributeMaxDynamicSharedMemorySize, tlr::SMEM); }
 
-cudaError_t launch_tlr_compress(int64_t n, double *tiles, double eps, int *ranks, cudaStream_t st) {
+cudaError_t launch_tlr_compress(int64_t n, double *tiles, double eps, int mode, int *ranks, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
     const int64_t noff = (int64_t)nt * (nt - 1) / 2;
     if (noff == 0) return cudaSuccess;
-    k_tlr_compress<<<(unsigned)noff, tlr::NT, tlr::SMEM, st>>>(tiles, nt, eps, ranks);
+    k_tlr_compress<<<(unsigned)noff, tlr::NT, tlr::SMEM, st>>>(tiles, nt, eps, mode, ranks);
     return cudaGetLastError();
 }
 

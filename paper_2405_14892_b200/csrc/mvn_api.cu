@@ -592,12 +592,13 @@ mvn_status mvn_posterior_tiles(mvn_ctx *c, mvn_tiles t, const int64_t *order, do
     return MVN_OK;
 }
 
-mvn_status mvn_tlr_compress(mvn_ctx *c, mvn_tiles t, double *d_tiles, double eps, int32_t *d_ranks) {
+mvn_status mvn_tlr_compress(mvn_ctx *c, mvn_tiles t, double *d_tiles, double eps, int32_t mode, int32_t *d_ranks) {
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
-    if (!tiles_ok(t) || !d_tiles || !d_ranks || !(eps >= 0.0))
-        return fail(c, MVN_E_USAGE, "mvn_tlr_compress: bad arguments (need nb=128, eps >= 0)");
-    MVN_CUDA(c, mvn::launch_tlr_compress(t.n, d_tiles, eps, d_ranks, c->stream));
+    if (!tiles_ok(t) || !d_tiles || !d_ranks || !(eps >= 0.0) || (mode != MVN_TLR_ABS && mode != MVN_TLR_REL_FRO) ||
+        (mode == MVN_TLR_REL_FRO && !(eps <= 1.0)))
+        return fail(c, MVN_E_USAGE, "mvn_tlr_compress: bad arguments (need nb=128, eps >= 0, mode 0 or 1, eps <= 1 for mode 1)");
+    MVN_CUDA(c, mvn::launch_tlr_compress(t.n, d_tiles, eps, mode, d_ranks, c->stream));
     return MVN_OK;
 }
 

@@ -60,7 +60,7 @@ cudaError_t launch_permute_sym(const double *src, int64_t off, const int64_t *or
 
 // NEXT-3 (part): fixed-accuracy TLR compression of the off-diagonal tiles (kernels_tlr.cu)
 cudaError_t tlr_init();
-cudaError_t launch_tlr_compress(int64_t n, double *tiles, double eps, int *ranks, cudaStream_t st);
+cudaError_t launch_tlr_compress(int64_t n, double *tiles, double eps, int mode, int *ranks, cudaStream_t st);
 
 // NEXT-2: Monte-Carlo validation
 cudaError_t mc_init();

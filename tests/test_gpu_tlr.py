@@ -40,8 +40,8 @@ def sorted_cov(torch, cfg):
     return T, S, a
 
 
-def check_vs_oracle(T, S, ranks_gpu, eps, n):
-    St, ro, sig = oracle.tlr_compress(S, eps)
+def check_vs_oracle(T, S, ranks_gpu, eps, n, mode="abs"):
+    St, ro, sig = oracle.tlr_compress(S, eps, mode=mode)
     G = dense_sym(T, n)
     nt = -(-n // NB)
     t = 0
@@ -50,11 +50,19 @@ def check_vs_oracle(T, S, ranks_gpu, eps, n):
             k, ko = int(ranks_gpu[t]), int(ro[t])
             if k != ko:      # only a near tie at the threshold may differ
                 lo, hi = min(k, ko), max(k, ko)
-                assert np.all(np.abs(sig[t][lo:hi] - eps) <= 1e-12), (I, J, k, ko, sig[t][lo:hi])
+                if mode == "abs":
+                    assert np.all(np.abs(sig[t][lo:hi] - eps) <= 1e-12), (I, J, k, ko, sig[t][lo:hi])
+                else:            # the smaller rank is feasible up to rounding of the tail sum
+                    tot = np.sum(sig[t] ** 2)
+                    assert np.sum(sig[t][lo:] ** 2) <= eps * eps * tot * (1 + 1e-9) + 1e-28, (I, J, k, ko)
             rs, cs = slice(I * NB, min((I + 1) * NB, n)), slice(J * NB, (J + 1) * NB)
             E = S[rs, cs] - G[rs, cs]
-            e2 = np.linalg.norm(E, 2)
-            assert (e2 < eps + 1e-12) if eps > 0 else np.max(np.abs(E)) < 1e-13, (I, J, k, ko, e2, sig[t][max(k - 2, 0):k + 2])
+            if mode == "abs":
+                e2 = np.linalg.norm(E, 2)
+                assert (e2 < eps + 1e-12) if eps > 0 else np.max(np.abs(E)) < 1e-13, (I, J, k, ko, e2, sig[t][max(k - 2, 0):k + 2])
+            else:
+                ef, af = np.linalg.norm(E), np.linalg.norm(S[rs, cs])
+                assert ef <= eps * af * (1 + 1e-9) + 1e-13, (I, J, k, ko, ef, af)
             if k == ko:
                 # the kept subspace of a tile moves by (rounding perturbation) / (sigma_k - sigma_k+1)
                 sg = sig[t]
@@ -69,16 +77,17 @@ def check_vs_oracle(T, S, ranks_gpu, eps, n):
 
 
 @pytest.mark.parametrize("base,g", [("B", 23), ("C", 30), ("B", 17)])
-@pytest.mark.parametrize("eps", [1e-1, 1e-3, 1e-6])
-def test_tlr_compress_vs_oracle(torch, base, g, eps):
+@pytest.mark.parametrize("eps,mode", [(1e-1, "abs"), (1e-3, "abs"), (1e-6, "abs"), (1e-1, "fro"), (1e-4, "fro"),
+                                      (1e-8, "fro")])
+def test_tlr_compress_vs_oracle(torch, base, g, eps, mode):
     cfg = W.small_config(f"tlr{g}", g, 100, 1, base=base)
     T, S, _ = sorted_cov(torch, cfg)
     T0 = T.clone()
     n = cfg.n
-    ranks = mvn().mvn_tlr_compress(T, n, eps).cpu().numpy()
+    ranks = mvn().mvn_tlr_compress(T, n, eps, mode=0 if mode == "abs" else 1).cpu().numpy()
     nt = -(-n // NB)
     assert ranks.shape[0] == nt * (nt - 1) // 2 and ranks.min() >= 0 and ranks.max() <= NB
-    check_vs_oracle(T, S, ranks, eps, n)
+    check_vs_oracle(T, S, ranks, eps, n, mode)
     G0 = dense_sym(T0, n)
     G = dense_sym(T, n)
     for I in range(nt):
@@ -124,8 +133,9 @@ def test_tlr_single_tile_is_noop(torch):
 
 def test_tlr_bad_args(torch):
     T = mvn().alloc_tiles(300, "cuda")
-    with pytest.raises(mvn().MvnError):
-        mvn().mvn_tlr_compress(T, 300, -1.0)
+    for eps, mode in [(-1.0, 0), (1e-3, 2), (1.5, 1), (float("nan"), 0)]:
+        with pytest.raises(mvn().MvnError):
+            mvn().mvn_tlr_compress(T, 300, eps, mode=mode)
 
 
 @pytest.mark.parametrize("eps", [1e-2, 1e-5])

@@ -71,3 +71,23 @@ def test_rank_monotone_in_eps():
             assert np.all(r >= prev)
         prev = r
     assert prev.max() <= 128
+
+
+@pytest.mark.parametrize("eps", [0.3, 1e-2, 1e-4])
+def test_relative_frobenius_mode(eps):
+    """mode "fro": ||A - A_k||_F <= eps ||A||_F, and k is minimal (rank k - 1 violates it) —
+    Eckart-Young in the Frobenius norm, with the error from the matrix itself, not from s."""
+    cfg = W.small_config("tlr", 16, 10, 1, base="B")
+    inp = W.make_inputs(cfg)
+    S = oracle.covariance(inp.xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    St, ranks, sig = oracle.tlr_compress(S, eps, mode="fro")
+    A = S[128:256, :128]
+    E = A - St[128:256, :128]
+    k = int(ranks[0])
+    assert np.linalg.norm(E) <= eps * np.linalg.norm(A) * (1 + 1e-12)
+    if k > 0:
+        U, s, Vt = np.linalg.svd(A)
+        Ak1 = (U[:, :k - 1] * s[:k - 1]) @ Vt[:k - 1]
+        assert np.linalg.norm(A - Ak1) > eps * np.linalg.norm(A)
+    _, r_abs, _ = oracle.tlr_compress(S, eps * np.linalg.norm(A), mode="abs")
+    assert 0 <= k <= 128 and r_abs[0] >= 0

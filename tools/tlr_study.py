@@ -43,6 +43,7 @@ def main():
     N, R = int(os.environ.get("TLR_N", "10000")), int(os.environ.get("TLR_R", "8"))
     betas = [float(b) for b in os.environ.get("TLR_BETAS", "0.033,0.1,0.234").split(",")]
     epss = [float(e) for e in os.environ.get("TLR_EPS", "1e-1,1e-2,1e-3,1e-4").split(",")]
+    mode = int(os.environ.get("TLR_MODE", "0"))          # 0: sigma_i >= eps, 1: relative Frobenius per tile
     out = []
     for beta in betas:
         cfg = W.small_config(f"tlr_b{beta}", g, N, R, base="B", beta=beta)
@@ -65,18 +66,18 @@ def main():
         d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy)).cuda()
         for eps in epss:
             Tg = mvn.mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
-            rg = mvn.mvn_tlr_compress(Tg, n, eps).cpu().numpy()
+            rg = mvn.mvn_tlr_compress(Tg, n, eps, mode=mode).cpu().numpy()
             del Tg
             T.copy_(base)
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record()
-            ranks = mvn.mvn_tlr_compress(T, n, eps)
+            ranks = mvn.mvn_tlr_compress(T, n, eps, mode=mode)
             ev1.record()
             torch.cuda.synchronize()
             ms = ev0.elapsed_time(ev1)
             ranks = ranks.cpu().numpy()
             info, lp = run(T, n, a, N, R, cfg.seed_lattice)
-            rec = {"beta": beta, "n": n, "eps": eps, "compress_ms": ms, "info": info,
+            rec = {"beta": beta, "n": n, "eps": eps, "mode": mode, "compress_ms": ms, "info": info,
                    "ranks_sorted_order": rank_stats(ranks), "ranks_spatial_order": rank_stats(rg)}
             if lp is not None:
                 k = mvn.mvn_confidence_region(lp, CONF)[0]
@@ -90,7 +91,7 @@ def main():
         del T, base
         torch.cuda.empty_cache()
     os.makedirs("gpurun_out", exist_ok=True)
-    with open("gpurun_out/tlr_study.json", "w") as f:
+    with open(f"gpurun_out/tlr_study_mode{mode}.json", "w") as f:
         json.dump(out, f, indent=1)
 
 
