@@ -333,3 +333,36 @@ def test_full_config_sampled_parity(torch_cuda, name):
         # parity in shared-L mode, report independent mode) — bar 1e-7 there, the north_star 1e-8 else
         tol = 1e-7 if name == "E" else LOGP_TOL
         assert np.max(np.abs(lp_g - logp_from(Mo, So_, end - begin))) <= tol
+
+
+@pytest.mark.slow
+def test_max_size_sampled_parity(torch_cuda):
+    """The largest problem one B200 holds with this layout: n = 386^2 = 148,996 sites
+    (config-D kernel), tile-packed L = 89 GB plus the per-SM Y histories. Sampled checks as in
+    test_full_config_sampled_parity: (L L^T)_ij vs the oracle's Matérn on 500 entries, and log P_k
+    of the first 2,048 prefixes over 96 samples in shared-L mode (the oracle runs the SOV on the GPU's
+    leading block of L) within 1e-10."""
+    torch = torch_cuda
+    free, _ = torch.cuda.mem_get_info()
+    cfg = W.small_config("max", 386, 10_000, 8, base="D")
+    n = cfg.n
+    need = mvn().mvn_tiles_bytes(n) + 148 * (-(-n // 64) * 64) * 132 * 8 + (8 << 30)
+    if free < need:
+        pytest.skip(f"needs {need / 2**30:.0f} GiB free, {free / 2**30:.0f} GiB available")
+    inp, order, a = sorted_inputs(cfg)
+    xy = inp.xy[order]
+    T = gpu_cov(torch, xy, cfg)
+    assert mvn().mvn_potrf(T, n) == -1
+    rng = np.random.default_rng(6)
+    ii = np.sort(rng.integers(0, n, 500))
+    jj = np.array([rng.integers(0, i + 1) for i in ii])
+    got = np.einsum("ij,ij->i", tile_rows(T, n, ii, n), tile_rows(T, n, jj, n))
+    h = np.sqrt(((xy[ii] - xy[jj]) ** 2).sum(1))
+    want = oracle.matern(h, cfg.sigma2, cfg.beta, cfg.nu) + np.where(ii == jj, cfg.nugget, 0.0)
+    assert np.max(np.abs(got - want)) <= 1e-12 * (cfg.sigma2 + cfg.nugget)
+    m = 2048
+    Lg = leading_block(T, n, m)
+    begin, end = cfg.N - 48, cfg.N + 48
+    M, S = gpu_sov(torch, T, n, a, cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+    Ms, Ss = oracle_range(Lg, a[:m], np.full(m, np.inf), cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+    assert np.max(np.abs(logp_from(M, S, end - begin)[:m] - logp_from(Ms, Ss, end - begin))) <= 1e-10
