@@ -12,6 +12,7 @@ host arguments are numpy arrays.
 from __future__ import annotations
 
 import ctypes
+import threading
 import math
 import os
 from dataclasses import dataclass
@@ -149,9 +150,11 @@ def _dev_ptr(t, dtype=None) -> int:
 
 
 class Context:
-    """An mvn_ctx bound to one CUDA device; follows torch's current stream on every call."""
+    """An mvn_ctx bound to one CUDA device; follows torch's current stream on every call. One
+    context per (thread, device): the stream is context state (mvn_set_stream), so threads must
+    not share a context."""
 
-    _by_device: dict[int, "Context"] = {}
+    _tls = threading.local()
 
     def __init__(self, device: int = 0):
         import torch
@@ -169,9 +172,12 @@ class Context:
         import torch
         if device is None:
             device = torch.cuda.current_device()
-        if device not in cls._by_device:
-            cls._by_device[device] = Context(device)
-        c = cls._by_device[device]
+        by_device = getattr(cls._tls, "by_device", None)
+        if by_device is None:
+            by_device = cls._tls.by_device = {}
+        if device not in by_device:
+            by_device[device] = Context(device)
+        c = by_device[device]
         st = stream if stream is not None else torch.cuda.current_stream(device)
         lib().mvn_set_stream(c.h, ctypes.c_void_p(st.cuda_stream))
         return c

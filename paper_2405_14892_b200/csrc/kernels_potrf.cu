@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "gemm_dmma.cuh"
 #include "mvn_internal.h"
@@ -415,19 +417,19 @@ int panel_sms() {
     return v;
 }
 // One panel stream and its events per device (created on first use, kept for the process; a
-// process may drive several devices).
+// process may drive several devices). The per-device mutex makes the enqueue of one factorisation
+// atomic with respect to other host threads using the same device: the events are re-recorded by
+// every call, and a stream-wait captures the latest record at enqueue time.
 struct PotrfStreams {
     bool ready = false;
     cudaStream_t sp = nullptr;
     cudaEvent_t ev_panel[2] = {}, ev_rest[2] = {}, ev_start = nullptr;
+    std::mutex mu;
 };
 constexpr int kMaxDevices = 64;
 PotrfStreams g_ps_dev[kMaxDevices];
-PotrfStreams *g_cur = nullptr;
-cudaError_t potrf_streams(int dev) {
-    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
-    PotrfStreams &ps = g_ps_dev[dev];
-    g_cur = &ps;
+// caller holds ps.mu
+cudaError_t potrf_streams(PotrfStreams &ps) {
     if (ps.ready) return cudaSuccess;
     int lo = 0, hi = 0;
     cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -510,9 +512,11 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
     const int S = (ncols + KP - 1) / KP;
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaError_t e = potrf_streams(dev);
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    PotrfStreams &ps = g_ps_dev[dev];
+    std::lock_guard<std::mutex> lock(ps.mu);
+    cudaError_t e = potrf_streams(ps);
     if (e != cudaSuccess) return e;
-    PotrfStreams &ps = *g_cur;
     cudaStream_t sp = ps.sp;
     // the panel stream starts after everything already queued on the main stream (Sigma)
     if ((e = cudaEventRecord(ps.ev_start, st))) return e;
