@@ -276,8 +276,14 @@ __global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, i
 //                      layout and ONE TMA bulk reduction (cp.reduce.async.bulk .add.f64) adds it
 //                      to C in L2 — no global loads, nothing to wait for before the next tile.
 // The producer runs ahead across tiles, so the next tile's operands stream in during the epilogue.
+// K-columns per ring stage and stages of k_update2 (same bytes in flight, BK * STAGES = 32);
+// compile-time MVN_UPD2_BK for experiments: 16 x 2 measured 1.1 % slower than 8 x 4 at D and E
+// (tools/upd2_bk_ab.sh), unlike the SOV ring where fewer, larger chunks won
+#ifndef MVN_UPD2_BK
+#define MVN_UPD2_BK 8
+#endif
 namespace upd2 {
-constexpr int BK = 8, STAGES = 4;
+constexpr int BK = MVN_UPD2_BK, STAGES = 32 / MVN_UPD2_BK;
 constexpr int SP = kTile + 4;                       // 132 == 4 (mod 16)
 constexpr int STAGE = 2 * BK * SP;                  // A and B chunks
 constexpr int NCONS = 256, NT = NCONS + 32;
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
                 mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
                 double *as = sm + st * STAGE;
                 double *bs = as + BK * SP;
-                // 8 columns of L_ik and of L_jk (1 KB each) into padded rows: cp.async, 16 B per lane
+                // BK columns of L_ik and of L_jk (1 KB each) into padded rows: cp.async, 16 B per lane
                 const double *a0 = Lik + (int64_t)c * BK * kTile + lane * 2;
                 const double *b0 = Ljk + (int64_t)c * BK * kTile + lane * 2;
 #pragma unroll

@@ -7,9 +7,9 @@
 //     samples (the last block of a CTA is narrowed to a multiple of 32, so no CTA idles in a tail
 //     wave). Each block sweeps all n rows in row blocks of 64.
 //   * Warp specialisation (416 threads):
-//       warp 12    (producer): streams 16-column K-chunks of the L row panel (from L2 — all CTAs
-//                  sweep the same rows) and 16-row chunks of the Y history (this CTA's HBM scratch)
-//                  into a 4-stage shared-memory ring with TMA bulk copies (cp.async.bulk, mbarrier
+//       warp 12    (producer): streams 32-column K-chunks of the L row panel (from L2 — all CTAs
+//                  sweep the same rows) and 32-row chunks of the Y history (this CTA's HBM scratch)
+//                  into a 2-stage shared-memory ring with TMA bulk copies (cp.async.bulk, mbarrier
 //                  complete_tx); full/empty mbarriers, no CTA-wide barrier in the main loop.
 //       warps 0-7  (GEMM): (a6) S_r = L[rows r, 0:64r] * Y[0:64r, block] on fp64 DMMA. The part
 //                  of S_{r+1} that only needs Y[0:64r] is computed WHILE the chain warps run row
@@ -32,9 +32,10 @@ namespace sovk {
 constexpr int M = 64;                    // SOV row block
 constexpr int NB = 128;                  // max samples per block (= chain threads)
 // K-chunk rows per pipeline stage and stages (same bytes in flight: BK * STAGES = 64); compile-time
-// MVN_SOV_BK for experiments (16 x 4 or 8 x 8)
+// MVN_SOV_BK for experiments. 32 x 2 (default): half the ring handshakes of 16 x 4, measured 3.9 %
+// faster at D and 2.4 % at E, equal at B / C (tools/sov_bk32_ab.sh); 8 x 8 is slower.
 #ifndef MVN_SOV_BK
-#define MVN_SOV_BK 16
+#define MVN_SOV_BK 32
 #endif
 constexpr int BK = MVN_SOV_BK, STAGES = 64 / MVN_SOV_BK;
 constexpr int SA = M + 4;                // 68  == 4 (mod 16): conflict-free DMMA fragment loads
@@ -138,9 +139,9 @@ __device__ __forceinline__ BlockGeom block_geom(int64_t count, int b) {
 }
 
 // ------------------------------------------------------------------------------------ producer
-// One warp streams K-chunks (16 columns of the L row panel + 16 rows of the Y history) into the
-// STAGES-deep ring with TMA bulk copies: lanes 0-15 copy one 512-byte L column segment each,
-// lanes 16-31 one Y row (w samples) each. The chunk of row block r whose Y rows come from row
+// One warp streams K-chunks (BK columns of the L row panel + BK rows of the Y history) into the
+// STAGES-deep ring: the L columns by cp.async (one 16-byte piece per lane per column), the Y rows by
+// one TMA bulk copy. The chunk of row block r whose Y rows come from row
 // block r-1 is only issued after the chain warps have published Y_{r-1} (barrier Y_READY).
 __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const double *Yslot, int64_t count, int nblk,
                                              int lane) {
@@ -184,7 +185,7 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
                 const int64_t kc = (int64_t)c * BK;
                 double *as = sm + st * STAGE;
                 double *bs = as + BK * SA;
-                // A: 16 L columns x 64 rows (512 B each, 1 KB apart) by cp.async, one 16 B piece per lane
+                // A: BK L columns x 64 rows (512 B each, 1 KB apart) by cp.async, one 16 B piece per lane
                 const int T = (int)(kc / kTile), cc = (int)(kc % kTile);
                 const double *Lsrc = p.L + tile_offset(R, T) + (int64_t)cc * kTile + hh + lane * 2;
                 if (p.hints) {
@@ -196,7 +197,7 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
                 }
                 cp_async_mbar_arrive(&full[st]);
                 __syncwarp();
-                // B: 16 Y-history rows, contiguous thanks to the padded row stride SB: one TMA bulk copy
+                // B: BK Y-history rows, contiguous thanks to the padded row stride SB: one TMA bulk copy
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[st], BK * SB * 8);
                     if (p.hints) bulk_g2s_hint(bs, Yslot + kc * SB, BK * SB * 8, &full[st], pol_Y);
