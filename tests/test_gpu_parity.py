@@ -342,7 +342,11 @@ def test_max_size_sampled_parity(torch_cuda):
     test_full_config_sampled_parity: (L L^T)_ij vs the oracle's Matérn on 500 entries, and log P_k
     of the first 2,048 prefixes over 96 samples in shared-L mode (the oracle runs the SOV on the GPU's
     leading block of L) within 1e-10."""
+    import gc
     torch = torch_cuda
+    gc.collect()
+    mvn().Context.get(0).trim()                  # workspace of earlier tests (Y histories, MC buffers)
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     cfg = W.small_config("max", 386, 10_000, 8, base="D")
     n = cfg.n
