@@ -50,6 +50,8 @@ typedef struct mvn_ctx mvn_ctx;
  * the legacy default stream). Fails with MVN_E_CUDA unless the device is compute capability 10.0
  * (B200, sm_100a — the only architecture this library is built for). */
 mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out);
+/* Free the context and its workspace. Waits for all outstanding work on the context's device (the
+ * bound stream itself is not touched: its owner may have destroyed it already). */
 void mvn_destroy(mvn_ctx *ctx);
 mvn_status mvn_set_stream(mvn_ctx *ctx, void *cuda_stream);
 const char *mvn_last_error(const mvn_ctx *ctx);

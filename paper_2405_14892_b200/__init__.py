@@ -11,6 +11,7 @@ host arguments are numpy arrays.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import threading
 import math
@@ -149,6 +150,17 @@ def _dev_ptr(t, dtype=None) -> int:
     return t.data_ptr()
 
 
+_exiting = False
+
+
+def _at_exit():
+    global _exiting
+    _exiting = True                  # process teardown: leave the contexts to the driver
+
+
+atexit.register(_at_exit)
+
+
 class Context:
     """An mvn_ctx bound to one CUDA device; follows torch's current stream on every call. One
     context per (thread, device): the stream is context state (mvn_set_stream), so threads must
@@ -181,6 +193,16 @@ class Context:
         st = stream if stream is not None else torch.cuda.current_stream(device)
         lib().mvn_set_stream(c.h, ctypes.c_void_p(st.cuda_stream))
         return c
+
+    def __del__(self):
+        # a thread's contexts are collected with its thread-local dict; free their workspace
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None and not _exiting:
+            try:
+                _lib.mvn_destroy(h)
+            except Exception:
+                pass
+            self.h = None
 
     def check(self, st: int, what: str):
         if st != MVN_OK:

@@ -184,12 +184,17 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
 
 void mvn_destroy(mvn_ctx *c) {
     if (!c) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    cudaStreamSynchronize(c->stream);
+    // no stream synchronise: the bound stream may already be destroyed by its owner; cudaFree
+    // waits for the device's outstanding work itself
+    cudaDeviceSynchronize();
     for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF,
                     c->post, c->postv, c->mcLA, c->mcRS, c->mcX})
         if (p) cudaFree(p);
     delete c;
+    if (prev >= 0) cudaSetDevice(prev);
 }
 
 mvn_status mvn_set_stream(mvn_ctx *c, void *s) {

@@ -57,3 +57,29 @@ def test_two_threads_bitwise_equal_to_alone(torch):
         for x, y in zip(out[g][1:], ref[g][1:]):
             assert np.array_equal(x, y)
     assert torch.cuda.current_device() == 0
+
+
+def test_thread_contexts_are_freed(torch):
+    """A thread's contexts go with its thread-local storage (mvn_destroy frees their workspace)."""
+    import gc
+    import paper_2405_14892_b200 as mvn
+    gc.collect()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    seen = []
+
+    def worker():
+        c = mvn.Context.get(0)
+        seen.append(c.h.value)
+        run_one(torch, 47, 7, torch.cuda.Stream())
+
+    for _ in range(3):
+        t = threading.Thread(target=worker)
+        t.start()
+        t.join()
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    free1, _ = torch.cuda.mem_get_info()
+    assert len(seen) == 3
+    assert free0 - free1 < (256 << 20), (free0, free1)    # no per-thread workspace left behind
