@@ -128,7 +128,7 @@ mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
  * use to produce the same factor); -1 if n < 1. The environment variable MVN_POTRF_KP overrides. */
 int64_t mvn_potrf_panel_width(int64_t n);
 
-/* Factor the kp (1..4; clipped at nt) tile columns k .. k+kp-1 in place: POTRF of the diagonal tile
+/* Factor the kp (1..8; clipped at nt) tile columns k .. k+kp-1 in place: POTRF of the diagonal tile
  * and TRSM of the tiles below, column by column, each further column first updated with the
  * previous columns of the super-panel. All updates from columns < k must have been applied. A
  * non-positive pivot records its 0-based global row in the context's device info (first failure

@@ -495,12 +495,16 @@ cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0,
 //   n = 32,761  kp 1 / 2 / 3      = 409 / 390 / 384 ms
 //   n = 65,536  kp 1 / 2 / 3 / 4  = 3.14 / 2.96 / 2.89 / 2.86 s
 //   n = 102,400 kp 2 / 3 / 4      = 11.21 / 10.96 / 10.83 s
-// MVN_POTRF_KP overrides.
+// and with the final kernels (r01, tools/potrf_kp_ab.sh, one box):
+//   n = 25,600  kp 3 / 6 / 8      = 199 / 201 / 203 ms
+//   n = 65,536  kp 4 / 6 / 8      = 2.822 / 2.805 / 2.791 s
+//   n = 102,400 kp 4 / 6 / 8      = 10.57 / 10.46 / 10.39 s
+// MVN_POTRF_KP (1..8) overrides.
 int potrf_panel_width(int64_t n) {
-    static const int env = [] { const char *e = getenv("MVN_POTRF_KP"); const int v = e ? atoi(e) : 0; return v >= 1 && v <= 4 ? v : 0; }();
+    static const int env = [] { const char *e = getenv("MVN_POTRF_KP"); const int v = e ? atoi(e) : 0; return v >= 1 && v <= 8 ? v : 0; }();
     if (env) return env;
     const int64_t nt = (n + kTile - 1) / kTile;
-    return nt >= 384 ? 4 : nt >= 192 ? 3 : 1;
+    return nt >= 384 ? 8 : nt >= 192 ? 3 : 1;
 }
 
 // Right-looking factorisation over super-panels of kp = potrf_panel_width() tile columns (K = 128 kp

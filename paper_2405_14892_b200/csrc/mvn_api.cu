@@ -292,7 +292,7 @@ mvn_status mvn_potrf_panel(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k, 
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
-    if (!nt || !d_tiles || k < 0 || k >= nt || kp < 1 || kp > 4) return fail(c, MVN_E_USAGE, "mvn_potrf_panel: bad arguments");
+    if (!nt || !d_tiles || k < 0 || k >= nt || kp < 1 || kp > 8) return fail(c, MVN_E_USAGE, "mvn_potrf_panel: bad arguments");
     MVN_CUDA(c, mvn::launch_potrf_panel(t.n, d_tiles, (int)k, (int)kp, c->d_info, c->stream));
     return MVN_OK;
 }
@@ -302,7 +302,7 @@ mvn_status mvn_potrf_update(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t k,
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
-    if (!nt || !d_tiles || k < 0 || kp < 1 || kp > 4 || col_first < std::min(k + kp, nt) || col_stride < 1 ||
+    if (!nt || !d_tiles || k < 0 || kp < 1 || kp > 8 || col_first < std::min(k + kp, nt) || col_stride < 1 ||
         col_block < 1 || col_block > col_stride || sm_reserve < 0 || sm_reserve >= c->nsm)
         return fail(c, MVN_E_USAGE, "mvn_potrf_update: bad arguments (need k + kp <= col_first, 1 <= col_block <= col_stride)");
     if (col_first >= nt) return MVN_OK;
@@ -317,7 +317,7 @@ mvn_status mvn_panel_pack(mvn_ctx *c, mvn_tiles t, const double *d_tiles, int64_
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
-    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 4)
+    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 8)
         return fail(c, MVN_E_USAGE, "mvn_panel_pack: bad arguments");
     MVN_CUDA(c, mvn::launch_panel_copy(t.n, const_cast<double *>(d_tiles), (int)k, (int)kp, d_panel, true, c->stream));
     return MVN_OK;
@@ -327,7 +327,7 @@ mvn_status mvn_panel_unpack(mvn_ctx *c, mvn_tiles t, const double *d_panel, int6
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     const int64_t nt = tiles_ok(t) ? (t.n + t.nb - 1) / t.nb : 0;
-    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 4)
+    if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 8)
         return fail(c, MVN_E_USAGE, "mvn_panel_unpack: bad arguments");
     MVN_CUDA(c, mvn::launch_panel_copy(t.n, d_tiles, (int)k, (int)kp, const_cast<double *>(d_panel), false, c->stream));
     return MVN_OK;

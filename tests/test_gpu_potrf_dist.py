@@ -81,7 +81,7 @@ def emulate(torch, tiles, n):
     return mvn().mvn_potrf_info(0, reset=True)
 
 
-@pytest.mark.parametrize("kp", [1, 2, 3])
+@pytest.mark.parametrize("kp", [1, 2, 3, 8])
 def test_panel_pack_unpack(torch, kp):
     n = 5 * NB + 3
     T, _ = sigma(torch, n)
@@ -170,7 +170,7 @@ def test_potrf_distributed_single_process(torch):
     assert torch.equal(T, ref)
 
 
-@pytest.mark.parametrize("kp", [2, 3])
+@pytest.mark.parametrize("kp", [2, 3, 8])
 def test_super_panel_widths(kp):
     """The emulated-distributed and single-process tests again with super-panels of kp tile columns
     (MVN_POTRF_KP is read once per process, hence the subprocess): mvn_potrf with K = 128 kp
