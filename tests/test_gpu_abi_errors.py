@@ -55,7 +55,7 @@ def test_potrf_building_blocks_reject_bad_arguments(torch):
     T = small_L(torch, n)
     usage(mvn().mvn_potrf_update, T, n, 2, 1, 2)          # col_first < k + kp
     usage(mvn().mvn_potrf_update, T, n, 0, 1, 1, 2, 3)    # col_block > col_stride
-    usage(mvn().mvn_potrf_update, T, n, 0, 5, 6)          # kp > 4
+    usage(mvn().mvn_potrf_update, T, n, 0, 9, 10)         # kp > 8
     usage(mvn().mvn_potrf_panel, T, n, 5)                 # k >= nt
     buf = torch.empty(mvn().panel_numel(n, 0, 1), dtype=torch.float64, device="cuda")
     usage(mvn().mvn_panel_pack, T, n, 7, 1, buf)
