@@ -417,7 +417,8 @@ cudaError_t potrf_init() {
 // Streams and events of the single-GPU lookahead schedule (launch_potrf).
 namespace {
 // SMs left to the panel stream beside the persistent update (MVN_POTRF_PANEL_SMS overrides).
-// Measured at D (r01): 4 / 6 / 8 / 12 SMs -> 2.814 / 2.825 / 2.845 / 2.925 s.
+// Measured at D (r01, kp = 4): 4 / 6 / 8 / 12 SMs -> 2.814 / 2.825 / 2.845 / 2.925 s; with kp = 8
+// (tools/panel_sms_ab.sh): 2 / 4 / 6 / 8 SMs -> 2.805 / 2.786 / 2.778 / 2.792 s (4 kept: within 0.3 %).
 int panel_sms() {
     static const int v = [] { const char *e = getenv("MVN_POTRF_PANEL_SMS"); const int x = e ? atoi(e) : 4; return x >= 0 && x < 64 ? x : 4; }();
     return v;
