@@ -6,8 +6,14 @@ Run: PYTHONPATH=. python tools/tlr_jacobi_sweeps.py"""
 import numpy as np
 import scipy.linalg as sl
 
-import oracle
 import workloads as W
+
+
+def covariance(xy, sigma2, beta, nu, nugget):
+    """Eq. 6 for nu = 3/2 (config C's kernel), dense fp64 (study tool; does not use oracle/)."""
+    assert nu == 1.5
+    h = np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1)) / beta
+    return sigma2 * (1.0 + h) * np.exp(-h) + nugget * np.eye(len(xy))
 
 NB = 128
 
@@ -46,8 +52,8 @@ def jacobi(X, eps, max_sweeps):
 def main(eps=1e-6, max_sweeps=60):
     cfg = W.small_config("tlr30", 30, 100, 1, base="C")
     inp = W.make_inputs(cfg)
-    order, _, _ = oracle.marginal_order(inp.mu, np.full(cfg.n, cfg.sigma2 + cfg.nugget), cfg.u)
-    S = oracle.covariance(inp.xy[order], cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    order = np.argsort(-(inp.mu - cfg.u), kind="stable")          # R13 sort key (equal variances)
+    S = covariance(inp.xy[order], cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
     for (I, J) in [(1, 0), (2, 0), (3, 1), (4, 0), (6, 5)]:
         A = S[I * NB:(I + 1) * NB, J * NB:(J + 1) * NB]
         s = np.linalg.svd(A, compute_uv=False)

@@ -3,14 +3,25 @@
 marginal-probability order (R1). For n = g^2 sites (exponential kernel, the three correlation
 levels of P:368) this prints the mean / max rank of the off-diagonal tiles at eps = 1e-3 relative
 to the tile width, in the sorted order and in the spatial (grid row-major) order.
-Run: PYTHONPATH=. python tools/tlr_rank_vs_tile.py [g]"""
+Run: PYTHONPATH=. python tools/tlr_rank_vs_tile.py [g]
+(Study tool: its own few lines of Eq. 6 and the sort key; it does not use oracle/.)"""
 import sys
 
 import numpy as np
 
 import workloads as W
-from oracle.matern import covariance   # plain Eq. 6, fp64
-from oracle.pipeline import marginal_order
+
+
+def covariance(xy, sigma2, beta, nu, nugget):
+    """Eq. 6 for nu = 1/2 (the exponential kernel of these settings), dense fp64 (study tool)."""
+    assert nu == 0.5
+    h = np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1))
+    return sigma2 * np.exp(-h / beta) + nugget * np.eye(len(xy))
+
+
+def marginal_order(mu, var, u):
+    """Descending marginal exceedance probability = descending (mu - u) / sqrt(var), stable (R13)."""
+    return np.argsort(-(mu - u) / np.sqrt(var), kind="stable"), None, None
 
 
 def ranks(S, nb, eps):
