@@ -10,7 +10,7 @@
 //  1. column-pivoted Householder QR, A P = Q R (Q is not kept);
 //  2. X = R^T, orthogonalised by one-sided Jacobi (Hestenes) rotations in round-robin column pairs
 //     until every pair is orthogonal to 1e-15 relative (pairs of columns both below 1e-3 eps
-//     excepted). The QR preconditioning (Drmac-Veselic) cuts the sweeps from 24-32 to 8-12 on the
+//     excepted). The QR preconditioning (Drmac-Veselic) cuts the sweeps from 24-37 to 8-12 on the
 //     Matérn tiles and is what makes the iteration converge within its sweep cap there
 //     (tools/tlr_jacobi_sweeps.py). X's columns are then u_i sigma_i with R^T = U_x Sigma W^T, so
 //     the right singular vectors of A are v_i = P u_i;
