@@ -157,3 +157,21 @@ def test_tlr_pipeline_vs_oracle(torch, eps):
     Mo, So = P.oracle_range(Lo, a, np.full(n, np.inf), cfg.N, cfg.R, 5, 0, cfg.NR)
     lg, lo = P.logp_from(M, Sg, cfg.NR), P.logp_from(Mo, So, cfg.NR)
     assert np.max(np.abs(lg - lo)) <= 1e-9
+
+
+def test_tlr_relative_mode_limits(torch):
+    """Mode 1 (relative Frobenius) at its ends: eps = 1 drops every off-diagonal tile (k = 0 meets
+    ||A - 0||_F <= ||A||_F), eps = 0 keeps every nonzero singular value (the tile is unchanged up to
+    rounding); n a multiple of 128 (no ragged tile)."""
+    rng = np.random.default_rng(21)
+    n = 256
+    A = rng.standard_normal((n, n))
+    S = A @ A.T / n + np.eye(n)
+    T = mvn().mvn_pack_lower(torch.from_numpy(S).cuda(), n)
+    assert list(mvn().mvn_tlr_compress(T, n, 1.0, mode=1).cpu().numpy()) == [0]
+    G = dense_sym(T, n)
+    assert not G[128:, :128].any()
+    assert np.array_equal(G[:128, :128], S[:128, :128]) and np.array_equal(G[128:, 128:], S[128:, 128:])
+    T = mvn().mvn_pack_lower(torch.from_numpy(S).cuda(), n)
+    assert list(mvn().mvn_tlr_compress(T, n, 0.0, mode=1).cpu().numpy()) == [128]
+    assert np.max(np.abs(dense_sym(T, n) - S)) <= 1e-13
