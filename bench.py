@@ -147,6 +147,23 @@ def oracle_plan(cfg):
     return n_sub, J
 
 
+def config_dict(cfg, world: int, mode: str) -> dict:
+    """The `config` object of the JSON line; identical for both arms (ours and --impl reference)."""
+    return {"workload": f"config {cfg.name}: n={cfg.n} ({cfg.g}x{cfg.g} jittered grid), Matern "
+                        f"(s2={cfg.sigma2}, beta={cfg.beta}, nu={cfg.nu}) + nugget {cfg.nugget}, u={cfg.u}, "
+                        f"N={cfg.N} x R={cfg.R} QMC", "n": cfg.n, "N": cfg.N, "R": cfg.R,
+            "parallelism": (f"samples sharded over {world} GPU(s); " +
+                            ("Cholesky 1-D block-cyclic over the GPUs (NEXT-1)" if mode == "dist" and world > 1
+                             else "Cholesky on rank 0, L broadcast" if world > 1 else "one GPU")),
+            "l2": "flushed between timed steps (256 MB write); L itself is "
+                  f"{8 * cfg.n * (cfg.n + 1) / 2 / 1e9:.2f} GB (> 126 MB L2)"}
+
+
+def potrf_mode(args, world: int, force: bool) -> str:
+    """--potrf auto = the north_star layout (rank 0 factors, L broadcast); dist = NEXT-1."""
+    return "rank0" if args.potrf == "auto" else args.potrf
+
+
 # --------------------------------------------------------------------------------- reference arm
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
@@ -168,7 +185,7 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config {cfg.name}", "n": cfg.n, "N": cfg.N, "R": cfg.R},
+            "config": config_dict(cfg, args.gpus, potrf_mode(args, args.gpus, args.force_dist)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample,
                              "measured_s_per_step": float(np.mean(times))},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -420,7 +437,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--potrf", default="auto", choices=["auto", "rank0", "dist"],
-                    help="N>1: factor on rank 0 + broadcast L, or distributed (NEXT-1); auto = dist")
+                    help="N>1: factor on rank 0 + broadcast L (north_star), or distributed (NEXT-1); "
+                         "auto = rank0")
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: run the multi-GPU code path (NCCL process group, distributed Cholesky, "
                          "all_reduce combine, pinned-buffer e2e) even with one rank")
@@ -479,8 +497,10 @@ def main():
     L = mvn.alloc_tiles(n)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
 
+    mode = potrf_mode(args, world, args.force_dist)
+
     def step(events=None):
-        logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events, potrf=args.potrf)
+        logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events, potrf=mode)
         lp = logp.cpu().numpy()                          # a10 on the host: regions
         k, _ = mvn.mvn_confidence_region(lp, cfg.conf)
         return lp, k
@@ -517,11 +537,15 @@ def main():
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-        st = torch.tensor([np.mean(stage[k]) for k in sorted(stage)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(st, op=dist.ReduceOp.MAX)
-        stage_mean = dict(zip(sorted(stage), st.cpu().tolist()))
+        mine = torch.tensor([np.mean(stage[k]) for k in sorted(stage)], dtype=torch.float64, device="cuda")
+        every = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(every, mine)
+        per_rank = torch.stack(every).cpu().numpy()              # [rank][stage]
+        stage_mean = dict(zip(sorted(stage), per_rank.max(axis=0).tolist()))
+        stage_per_rank = {k: per_rank[:, i].tolist() for i, k in enumerate(sorted(stage))}
     else:
         stage_mean = {k: float(np.mean(v)) for k, v in stage.items()}
+        stage_per_rank = None
     ms_per_step = total_ms / args.steps
     value = n * NR / (ms_per_step / 1e3)
 
@@ -531,7 +555,7 @@ def main():
     e2e = None
     if not args.no_e2e and not multi:
         ts = []
-        for it in range(2):                      # one warm-up call (allocations), one timed
+        for it in range(4):                      # one warm-up call (allocations), three timed
             t0 = time.perf_counter()
             out = mvn.mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
                               cfg.seed_lattice, cfg.conf)
@@ -539,29 +563,33 @@ def main():
             if it > 0:
                 ts.append(t1 - t0)
         e2e = {"value": n * NR / float(np.mean(ts)), "unit": UNIT, "h2d_bytes_per_step": 24 * n,
-               "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)), "api": "mvn_crd (C ABI)",
+               "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)), "calls": len(ts),
+               "s_per_call_each": [float(t) for t in ts], "api": "mvn_crd (C ABI)",
                "k_star_matches_device_path": bool(np.array_equal(out.k_star, k))}
     elif not args.no_e2e and multi:
         import torch as _t
         h_xy = _t.empty((n, 2), dtype=_t.float64).pin_memory()
         h_a = _t.empty(n, dtype=_t.float64).pin_memory()
         h_lp = _t.empty(n, dtype=_t.float64).pin_memory()
-        dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        o2, a2, _ = mvn.mvn_marginal_order(inp.mu, var, cfg.u)              # a1 (host)
-        h_xy.numpy()[:] = inp.xy[o2]
-        h_a.numpy()[:] = a2
-        d_xy.copy_(h_xy, non_blocking=True)
-        d_a.copy_(h_a, non_blocking=True)
-        logp = parallel.crd_step(d_xy, d_a, L, cfg, potrf=args.potrf)
-        h_lp.copy_(logp, non_blocking=True)
-        torch.cuda.synchronize()
-        k2, _ = mvn.mvn_confidence_region(h_lp.numpy(), cfg.conf)          # a10 (host)
-        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": n * NR / float(t.item()), "unit": UNIT, "h2d_bytes_per_step": 24 * n,
-               "d2h_bytes_per_step": 8 * n, "s_per_call": float(t.item()),
+        ts = []
+        for _ in range(3):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            o2, a2, _ = mvn.mvn_marginal_order(inp.mu, var, cfg.u)              # a1 (host)
+            h_xy.numpy()[:] = inp.xy[o2]
+            h_a.numpy()[:] = a2
+            d_xy.copy_(h_xy, non_blocking=True)
+            d_a.copy_(h_a, non_blocking=True)
+            logp = parallel.crd_step(d_xy, d_a, L, cfg, potrf=mode)
+            h_lp.copy_(logp, non_blocking=True)
+            torch.cuda.synchronize()
+            k2, _ = mvn.mvn_confidence_region(h_lp.numpy(), cfg.conf)          # a10 (host)
+            t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ts.append(float(t.item()))
+        e2e = {"value": n * NR / float(np.mean(ts)), "unit": UNIT, "h2d_bytes_per_step": 24 * n,
+               "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)), "calls": len(ts),
                "api": "parallel.crd_step from pinned host buffers, max over ranks",
                "k_star_matches_device_path": bool(np.array_equal(k2, k))}
 
@@ -571,7 +599,6 @@ def main():
     my_samples = my_end - my_begin
     sov_flops = float(n) * (n - 1) * my_samples       # algorithmic: sum_k 2(k-1) per sample (a6 + in-block dot)
     achieved = sov_flops / (sov_ms / 1e3) / 1e12
-    mode = ("dist" if multi else "rank0") if args.potrf == "auto" else args.potrf
     if mode == "dist":
         n_potrf = parallel.potrf_launches(n, world, rank)
     else:
@@ -585,18 +612,13 @@ def main():
         # lattice shift per rank, BASELINE.json): per-GPU work shrinks with N -> strong scaling
         "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config {cfg.name}: n={n} ({cfg.g}x{cfg.g} jittered grid), Matern "
-                               f"(s2={cfg.sigma2}, beta={cfg.beta}, nu={cfg.nu}) + nugget {cfg.nugget}, u={cfg.u}, "
-                               f"N={cfg.N} x R={cfg.R} QMC", "n": n, "N": cfg.N, "R": cfg.R,
-                   "parallelism": (f"samples sharded over {world} GPU(s); " +
-                                   ("Cholesky 1-D block-cyclic over the GPUs (NEXT-1)" if mode == "dist" and world > 1
-                                    else "Cholesky on rank 0, L broadcast" if world > 1 else "one GPU")),
-                   "l2": "flushed between timed steps (256 MB write); L itself is "
-                         f"{mvn.mvn_tiles_bytes(n) / 1e9:.2f} GB"},
+        "config": config_dict(cfg, world, mode),
+        "potrf_mode": mode,
         "cholesky_tflops": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12,
         "sov_sample_dims_per_s": n * my_samples / (sov_ms / 1e3),
         "region_time_ms": ms_per_step,
         "stage_ms": stage_mean,
+        "stage_ms_per_rank": stage_per_rank,
         "roofline": {"kernel": "k_sov (SOV DMMA GEMM + Phi chain)", "bound": "tensor", "achieved": achieved,
                      "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
                      "traffic": committed_traffic(cfg.name, "k_sov"),

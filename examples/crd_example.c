@@ -4,12 +4,15 @@
  *
  *   gcc -O2 -std=c11 -I include examples/crd_example.c -L paper_2405_14892_b200 -lmvn \
  *       -Wl,-rpath,'$ORIGIN/../paper_2405_14892_b200' -lm -o examples/crd_example
- *   ./examples/crd_example [grid_side] [N] [R]
+ *   ./examples/crd_example [grid_side] [N] [R] [dump_file]
  *
  * The field: a jittered g x g grid on [0,1]^2, Matérn (sigma^2 = 1, beta = 0.1, nu = 1/2) with a
  * nugget 1e-8, and a smooth mean mu(x, y) = sin(3x) cos(2y) (inputs only; the method's arithmetic
  * all runs in libmvn). Prints log P_k for the first prefixes and the regions for 1 - alpha in
- * {0.8, 0.9, 0.95, 0.99}. Exit status: 0 on success, the mvn_status otherwise.
+ * {0.8, 0.9, 0.95, 0.99}. With a dump_file, the inputs and results are also written there (raw
+ * little-endian: int64 n, double xy[2n], double mu[n], int64 order[n], double logP[n], int64 k*[4])
+ * so a checker can recompute them independently (tests/test_c_example.py runs the oracle on them).
+ * Exit status: 0 on success, the mvn_status otherwise.
  */
 #include <math.h>
 #include <stdint.h>
@@ -54,6 +57,17 @@ int main(int argc, char **argv) {
     for (int i = 0; i < 4; ++i) printf("  region for 1-alpha = %.2f: %lld sites\n", conf[i], (long long)kstar[i]);
     printf("  device ms: upload %.3f cov %.3f potrf %.3f sov %.3f finalize %.3f download %.3f\n", r.ms_stage[0],
            r.ms_stage[1], r.ms_stage[2], r.ms_stage[3], r.ms_stage[4], r.ms_stage[5]);
+    if (argc > 4) {
+        FILE *f = fopen(argv[4], "wb");
+        if (!f) { perror(argv[4]); mvn_destroy(ctx); return 3; }
+        fwrite(&n, sizeof n, 1, f);
+        fwrite(xy, sizeof(double), (size_t)(2 * n), f);
+        fwrite(mu, sizeof(double), (size_t)n, f);
+        fwrite(order, sizeof(int64_t), (size_t)n, f);
+        fwrite(logP, sizeof(double), (size_t)n, f);
+        fwrite(kstar, sizeof(int64_t), 4, f);
+        fclose(f);
+    }
     mvn_destroy(ctx);
     free(xy); free(mu); free(logP); free(order);
     return 0;

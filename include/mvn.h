@@ -53,6 +53,9 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out);
 /* Free the context and its workspace. Waits for all outstanding work on the context's device (the
  * bound stream itself is not touched: its owner may have destroyed it already). */
 void mvn_destroy(mvn_ctx *ctx);
+/* Rebind the context to another stream of its device. The new stream first waits (device-side
+ * event, no host sync) for everything the context enqueued before, so a context's workspace is
+ * never used by two streams at once; calls on the new stream are then ordered after the old ones. */
 mvn_status mvn_set_stream(mvn_ctx *ctx, void *cuda_stream);
 const char *mvn_last_error(const mvn_ctx *ctx);
 const char *mvn_version(void);
@@ -124,7 +127,7 @@ mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
  * column: sum_j (nt-k-j) * nb*nb doubles, device. All calls are asynchronous on the context's
  * stream; pivots are checked on the device and collected by mvn_potrf_info.                    */
 
-/* Tile columns per super-panel (1..4) that mvn_potrf uses for order n (and potrf_distributed must
+/* Tile columns per super-panel (1..8) that mvn_potrf uses for order n (and potrf_distributed must
  * use to produce the same factor); -1 if n < 1. The environment variable MVN_POTRF_KP overrides. */
 int64_t mvn_potrf_panel_width(int64_t n);
 

@@ -501,13 +501,4 @@ def mvn_crd(xy: np.ndarray, mu: np.ndarray, sigma2, beta, nu, nugget, u, N, R, s
     return CrdOutput(order, logP, k[:len(cf)], tie[:len(cf)].astype(bool), int(res.info), tuple(res.ms_stage))
 
 
-def running_min(logP: np.ndarray) -> np.ndarray:
-    return np.minimum.accumulate(np.asarray(logP, dtype=np.float64))
-
-
-def lower_dense_from_unpacked(M) -> np.ndarray:
-    """mvn_unpack_lower output (column-major memory) -> row-major numpy L."""
-    return M.T.contiguous().cpu().numpy() if hasattr(M, "cpu") else np.ascontiguousarray(M.T)
-
-
 __all__ = [n for n in dir() if n.startswith("mvn_")] + ["Context", "MvnError", "lib", "TILE", "alloc_tiles"]

@@ -18,8 +18,17 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 FLAGS += [f for f in os.environ.get("MVN_NVCC_EXTRA", "").split() if f]
 
 
+STAMP = LIB + ".flags"        # the nvcc flags the library was built with (an experiment build is stale)
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(STAMP) as f:
+            if f.read() != " ".join(FLAGS):
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "mvn.h"), __file__]
@@ -52,6 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-o", tmp, *objs])
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(FLAGS))
     return LIB
 
 

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, i
 // The producer runs ahead across tiles, so the next tile's operands stream in during the epilogue.
 // K-columns per ring stage and stages of k_update2 (same bytes in flight, BK * STAGES = 32);
 // compile-time MVN_UPD2_BK for experiments: 16 x 2 measured 1.1 % slower than 8 x 4 at D and E
-// (tools/upd2_bk_ab.sh), unlike the SOV ring where fewer, larger chunks won
+// (round-1 A/B, profiles/r01_sov_evolution.md), unlike the SOV ring where fewer, larger chunks won
 #ifndef MVN_UPD2_BK
 #define MVN_UPD2_BK 8
 #endif
@@ -418,7 +418,7 @@ cudaError_t potrf_init() {
 namespace {
 // SMs left to the panel stream beside the persistent update (MVN_POTRF_PANEL_SMS overrides).
 // Measured at D (r01, kp = 4): 4 / 6 / 8 / 12 SMs -> 2.814 / 2.825 / 2.845 / 2.925 s; with kp = 8
-// (tools/panel_sms_ab.sh): 2 / 4 / 6 / 8 SMs -> 2.805 / 2.786 / 2.778 / 2.792 s (4 kept: within 0.3 %).
+// (round-1 A/B): 2 / 4 / 6 / 8 SMs -> 2.805 / 2.786 / 2.778 / 2.792 s (4 kept: within 0.3 %).
 int panel_sms() {
     static const int v = [] { const char *e = getenv("MVN_POTRF_PANEL_SMS"); const int x = e ? atoi(e) : 4; return x >= 0 && x < 64 ? x : 4; }();
     return v;
@@ -496,7 +496,7 @@ cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0,
 //   n = 32,761  kp 1 / 2 / 3      = 409 / 390 / 384 ms
 //   n = 65,536  kp 1 / 2 / 3 / 4  = 3.14 / 2.96 / 2.89 / 2.86 s
 //   n = 102,400 kp 2 / 3 / 4      = 11.21 / 10.96 / 10.83 s
-// and with the final kernels (r01, tools/potrf_kp_ab.sh, one box):
+// and with the final kernels (r01 A/B on one box):
 //   n = 25,600  kp 3 / 6 / 8      = 199 / 201 / 203 ms
 //   n = 65,536  kp 4 / 6 / 8      = 2.822 / 2.805 / 2.791 s
 //   n = 102,400 kp 4 / 6 / 8      = 10.57 / 10.46 / 10.39 s

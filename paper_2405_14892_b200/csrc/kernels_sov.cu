@@ -33,7 +33,7 @@ constexpr int M = 64;                    // SOV row block
 constexpr int NB = 128;                  // max samples per block (= chain threads)
 // K-chunk rows per pipeline stage and stages (same bytes in flight: BK * STAGES = 64); compile-time
 // MVN_SOV_BK for experiments. 32 x 2 (default): half the ring handshakes of 16 x 4, measured 3.9 %
-// faster at D and 2.4 % at E, equal at B / C (tools/sov_bk32_ab.sh); 8 x 8 is slower.
+// faster at D and 2.4 % at E, equal at B / C (round-1 A/B, profiles/r01_sov_evolution.md); 8 x 8 is slower.
 #ifndef MVN_SOV_BK
 #define MVN_SOV_BK 32
 #endif
@@ -318,10 +318,12 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
         double s = S[rb0 * SS + j];                       // row rb0: GEMM part + earlier sub-blocks
         // b = +inf path: the per-row log-sum-exp of this sub-block uses ONE warp reference c_w (the
         // warp max of ell at the sub-block start; ell never increases, so every term is <= 1) and
-        // the running product pw = exp(ell - c_w) * prod q instead of 8 exps and 8 max trees; a warp
-        // that meets a q < 1e-250 (far tail: pw could underflow) takes the exact path below.
+        // the running product pw = exp(ell - c_w) * prod q instead of 8 exps and 8 max trees. pw is
+        // non-increasing along the sub-block, so the warp max of its final value bounds every row's
+        // largest term from below: if it is < 2^-960 (~1e-289) some row's sum may have underflowed
+        // or gone subnormal (e.g. 8 far-tail factors q ~ 1e-44, each harmless alone), and the warp
+        // takes the exact per-row max/exp path below instead (reading R10: no product underflow).
         double c_w = -CUDART_INF, pw = 0.0;
-        bool tiny = false;
         if (!HAS_B) {
             c_w = valid ? ell : -CUDART_INF;
 #pragma unroll
@@ -348,7 +350,6 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
                 sov_step_upper(ap, wq, lq, y, q);
 #endif
                 pw *= q;
-                tiny |= !(q >= 1e-250);
                 P8[i * NB + j] = pw;
             }
             ell += lq;
@@ -362,7 +363,14 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
         }
         // per-row log-sum-exp over this warp's samples, 8 rows at once
         double m[8], e[8];
-        if (!HAS_B && !__any_sync(0xffffffffu, tiny)) {
+        bool fast = false;
+        if (!HAS_B) {
+            double pmax = valid ? pw : 0.0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+            fast = pmax >= 0x1p-960;
+        }
+        if (fast) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 m[i] = c_w;

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
     double *cn = vb + NB;                         // squared norms of the trailing sub-columns
     int *perm = reinterpret_cast<int *>(cn + NB); // column pivots: (A P)(:, r) = A(:, perm[r])
     __shared__ int chgf[2], k_sel, piv;
-    __shared__ double vtv_s;
+    __shared__ double vtv_s, fro2_s;
     __shared__ double sig[NB], srt[NB];
     __shared__ int sel[NB], pos[NB];
     (void)nt;
@@ -74,6 +74,13 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
         if (lane == 0) cn[c] = s2;
     }
     __syncthreads();
+    if (warp == 0) {                              // ||A||_F^2 (the scale of the mode-1 Jacobi floor)
+        double f = 0.0;
+#pragma unroll
+        for (int m = 0; m < NB / 32; ++m) f += cn[lane + 32 * m];
+        f = warp_sum(f);
+        if (lane == 0) fro2_s = f;
+    }
 
     // ---- 1. column-pivoted Householder QR (R overwrites A; the reflectors are not kept)
     for (int j = 0; j < NB; ++j) {
@@ -171,7 +178,9 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(double *__restrict_
     // ---- 2. one-sided Jacobi on X: an 8-lane group per column pair, 4 pairs per warp, 64 per step
     const int grp = lane >> 3, l8 = lane & 7;
     const unsigned gmask = 0xffu << (grp * 8);
-    const double floor2 = 1e-6 * eps * eps;       // pairs with both columns below 1e-3 eps stay unrotated
+    // pairs whose two columns together are below 1e-3 of the truncation scale stay unrotated: 1e-3 eps
+    // (mode 0, absolute sigma_i >= eps) or 1e-3 eps ||A||_F (mode 1, relative: scale-invariant)
+    const double floor2 = 1e-6 * eps * eps * (mode == 1 ? fro2_s : 1.0);
     for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
         // flag slot of this sweep; the other slot is the one a lagging warp may still be reading for
         // the previous sweep's exit test

@@ -26,6 +26,10 @@ struct mvn_ctx {
     void *sync = nullptr; size_t sync_cap = 0;   // SOV lockstep counters + need[]
     uint64_t *G = nullptr; int64_t G_n = 0;
     int64_t *d_info = nullptr;
+    // recorded on the bound stream at the end of every entry point (DevGuard); a stream change
+    // makes the new stream wait on it, so work enqueued on two streams never shares the workspace
+    // concurrently (the workspace above is per context, not per stream)
+    cudaEvent_t done = nullptr;
     // mvn_crd buffers
     void *crd_L = nullptr; size_t crd_L_cap = 0;
     void *crd_vec = nullptr; size_t crd_vec_cap = 0;
@@ -77,13 +81,17 @@ mvn_status ensure(mvn_ctx *c, void **buf, size_t *cap, size_t bytes) {
 
 // Every entry point runs on the context's device (the caller's current device is restored on
 // return), so one process may drive several GPUs through several contexts.
+// The guard also records the context's `done` event on its stream when the call returns (the
+// ordering point mvn_set_stream hands to a new stream).
 struct DevGuard {
     int prev = -1;
-    explicit DevGuard(const mvn_ctx *c) {
+    const mvn_ctx *ctx = nullptr;
+    explicit DevGuard(const mvn_ctx *c) : ctx(c) {
         int cur = -1;
         if (c && cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess) prev = cur;
     }
     ~DevGuard() {
+        if (ctx && ctx->done) cudaEventRecord(ctx->done, ctx->stream);
         if (prev >= 0) cudaSetDevice(prev);
     }
     DevGuard(const DevGuard &) = delete;
@@ -161,22 +169,26 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return MVN_E_CUDA;
     if (prop.major != 10 || prop.minor != 0) return MVN_E_CUDA;   // sm_100a binary only
-    if (cudaSetDevice(device) != cudaSuccess) return MVN_E_CUDA;
     mvn_ctx *c = new mvn_ctx();
     c->device = device;
     c->nsm = prop.multiProcessorCount;
     c->stream = (cudaStream_t)cuda_stream;
-    if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess || mvn::mc_init() != cudaSuccess ||
-        mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess ||
-        cudaMalloc(&c->d_info, 2 * sizeof(int64_t)) != cudaSuccess) {
-        delete c;
-        return MVN_E_CUDA;
-    }
-    const int64_t minus1 = -1;
-    if (cudaMemcpy(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess) {
-        cudaFree(c->d_info);
-        delete c;
-        return MVN_E_CUDA;
+    {
+        DevGuard dev_guard(c);                        // the caller's current device is restored
+        const int64_t minus1 = -1;
+        if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess || mvn::mc_init() != cudaSuccess ||
+            mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess ||
+            cudaMalloc(&c->d_info, 2 * sizeof(int64_t)) != cudaSuccess ||
+            cudaMemcpy(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            if (c->d_info) cudaFree(c->d_info);
+            if (c->done) cudaEventDestroy(c->done);
+            c->done = nullptr;
+            dev_guard.ctx = nullptr;
+            delete c;
+            return MVN_E_CUDA;
+        }
     }
     *out = c;
     return MVN_OK;
@@ -193,12 +205,23 @@ void mvn_destroy(mvn_ctx *c) {
     for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF,
                     c->post, c->postv, c->mcLA, c->mcRS, c->mcX})
         if (p) cudaFree(p);
+    if (c->done) cudaEventDestroy(c->done);
     delete c;
     if (prev >= 0) cudaSetDevice(prev);
 }
 
 mvn_status mvn_set_stream(mvn_ctx *c, void *s) {
     if (!c) return MVN_E_USAGE;
+    if ((cudaStream_t)s != c->stream && c->done) {
+        // everything the context enqueued so far (on the old stream, recorded when each call
+        // returned) completes before the new stream's next use of the shared workspace
+        int prev = -1;
+        cudaGetDevice(&prev);
+        if (prev != c->device) cudaSetDevice(c->device);
+        const cudaError_t e = cudaStreamWaitEvent((cudaStream_t)s, c->done, 0);
+        if (prev >= 0 && prev != c->device) cudaSetDevice(prev);
+        if (e != cudaSuccess) return cuda_fail(c, e, "mvn_set_stream: cudaStreamWaitEvent");
+    }
     c->stream = (cudaStream_t)s;
     return MVN_OK;
 }

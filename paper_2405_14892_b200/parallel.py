@@ -50,26 +50,68 @@ def combine_prefix(M: torch.Tensor, S: torch.Tensor, group=None, rescale=None,
     return M, S
 
 
-def broadcast_L(L: torch.Tensor, group=None, src: int = 0) -> torch.Tensor:
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.broadcast(L, src=src, group=group)
+def broadcast_L(L: torch.Tensor, group=None, src: int = 0, force_collectives: bool = False) -> torch.Tensor:
+    """C1: rank `src` (group rank) sends the tile-packed factor to every rank (NCCL over NVLink), in
+    place. A no-op without a process group, and on one rank unless collectives are forced."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return L
+    if dist.get_world_size(group) > 1 or force_collectives or FORCE_COLLECTIVES:
+        g_src = dist.get_global_rank(group, src) if group is not None else src
+        dist.broadcast(L, src=g_src, group=group)
     return L
 
 
+class LibmvnCrdOps:
+    """The building blocks crd_step drives, on the CUDA library (the product path). Tests replace
+    them with host stand-ins to run the multi-rank step logic on CPU with gloo."""
+
+    @staticmethod
+    def cov(d_xy, cfg, L):
+        from . import mvn_cov_matern
+        mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, out=L)
+
+    @staticmethod
+    def potrf(L, n):
+        from . import mvn_potrf
+        return mvn_potrf(L, n)
+
+    @staticmethod
+    def potrf_dist(L, n, group):
+        return potrf_distributed(L, n, group)
+
+    @staticmethod
+    def sov(L, n, d_a, cfg, begin, end):
+        from . import mvn_sov_prefix
+        return mvn_sov_prefix(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+
+    @staticmethod
+    def rescale(Mg, M, S):
+        from . import mvn_prefix_rescale
+        mvn_prefix_rescale(Mg, M, S)
+
+    @staticmethod
+    def finalize(M, S, NR):
+        from . import mvn_prefix_finalize
+        return mvn_prefix_finalize(M, S, NR)
+
+
 def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg, group=None, events=None,
-             potrf: str = "auto"):
+             potrf: str = "auto", ops=None):
     """One pass of the whole hot path (a2..a9) on this rank; returns device log P (n,).
 
     potrf: "rank0" — rank 0 builds and factors Sigma, then broadcasts L (C1, the north_star
     layout); "dist" — every rank builds Sigma and the ranks factor it together
-    (potrf_distributed, NEXT-1), after which every rank holds L; "auto" = "dist" when W > 1.
+    (potrf_distributed, NEXT-1), after which every rank holds L; "auto" = "rank0".
     events: optional list to which (name, event) pairs are appended for stage timing.
+    ops: the building blocks (default LibmvnCrdOps, the CUDA library).
     """
-    from . import mvn_cov_matern, mvn_potrf, mvn_sov_prefix, mvn_prefix_finalize
+    ops = ops or LibmvnCrdOps
     n = d_a.numel()
     world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
     rank = dist.get_rank(group) if world > 1 else 0
-    mode = ("dist" if (world > 1 or FORCE_COLLECTIVES) else "rank0") if potrf == "auto" else potrf
+    mode = "rank0" if potrf == "auto" else potrf
+    if mode not in ("rank0", "dist"):
+        raise ValueError(f"potrf must be auto, rank0 or dist, not {potrf!r}")
 
     def mark(name):
         if events is None:
@@ -81,18 +123,18 @@ def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg,
 
     mark("start")
     if mode == "dist":
-        mvn_cov_matern(d_xy_sorted, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, out=L)
+        ops.cov(d_xy_sorted, cfg, L)
         mark("cov")
-        info = potrf_distributed(L, n, group)
+        info = ops.potrf_dist(L, n, group)
         if info != -1:
             raise FloatingPointError(f"Sigma not SPD at row {info}")
         mark("potrf")
         mark("bcast")
     else:
         if rank == 0:
-            mvn_cov_matern(d_xy_sorted, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, out=L)
+            ops.cov(d_xy_sorted, cfg, L)
             mark("cov")
-            info = mvn_potrf(L, n)
+            info = ops.potrf(L, n)
             if info != -1:
                 raise FloatingPointError(f"Sigma not SPD at row {info}")
             mark("potrf")
@@ -102,11 +144,11 @@ def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg,
         broadcast_L(L, group)
         mark("bcast")
     begin, end = shard_range(cfg.N * cfg.R, rank, world)
-    M, S = mvn_sov_prefix(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+    M, S = ops.sov(L, n, d_a, cfg, begin, end)
     mark("sov")
-    combine_prefix(M, S, group)
+    combine_prefix(M, S, group, rescale=ops.rescale)
     mark("combine")
-    logp = mvn_prefix_finalize(M, S, cfg.N * cfg.R)
+    logp = ops.finalize(M, S, cfg.N * cfg.R)
     mark("finalize")
     return logp
 

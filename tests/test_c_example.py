@@ -1,6 +1,7 @@
 """The C ABI from plain C (examples/crd_example.c, no Python): it compiles and links against
 include/mvn.h + libmvn.so; without a GPU it must fail loudly with MVN_E_CUDA (no CPU fallback);
-on a B200 it runs end to end (mvn_crd) and prints the regions."""
+on a B200 it runs end to end (mvn_crd), and its log P_k and regions equal the oracle's on the
+inputs the C program generated (north_star bars: |dlog P_k| <= 1e-8, identical order and k*)."""
 import os
 import subprocess
 
@@ -30,8 +31,29 @@ def test_c_example_builds_and_fails_loudly_without_gpu():
 
 
 @pytest.mark.gpu
-def test_c_example_runs_on_gpu(cuda_device):
+def test_c_example_runs_on_gpu(cuda_device, tmp_path):
+    import numpy as np
+    import oracle
     build_example()
-    r = subprocess.run([EXE, "20", "2000", "4"], capture_output=True, text=True, timeout=300)
+    dump = str(tmp_path / "crd.bin")
+    r = subprocess.run([EXE, "20", "2000", "4", dump], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     assert "region for 1-alpha = 0.95" in r.stdout and "sm_100a" in r.stdout
+    raw = open(dump, "rb").read()
+    n = int(np.frombuffer(raw[:8], dtype=np.int64)[0])
+    off = 8
+    def take(dt, cnt):
+        nonlocal off
+        a = np.frombuffer(raw[off:off + 8 * cnt], dtype=dt)
+        off += 8 * cnt
+        return a
+    xy = take(np.float64, 2 * n).reshape(n, 2)
+    mu = take(np.float64, n)
+    order = take(np.int64, n)
+    logP = take(np.float64, n)
+    kstar = take(np.int64, 4)
+    conf = [0.80, 0.90, 0.95, 0.99]
+    ref = oracle.crd(xy, mu, 1.0, 0.1, 0.5, 1e-8, 0.0, 2000, 4, 3001, conf, chunk=500, nthreads=8)
+    assert np.array_equal(order, ref.order)
+    assert np.max(np.abs(logP - ref.logp)) <= 1e-8
+    assert np.array_equal(kstar, ref.k_star)

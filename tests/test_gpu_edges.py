@@ -55,3 +55,55 @@ def test_mc_single_site(torch, method):
     assert abs(cnt[1] / N - p) <= 4 * math.sqrt(p * (1 - p) / N)
     f = oracle.mc_first(np.array([[math.sqrt(2.0)]]), np.array([0.5]), 5, 0, N)
     assert abs(int(cnt[1]) - int(np.sum(f >= 1))) <= 2      # same draws, rounding-level ties only
+
+
+# ---------------------------------------------------------------------- b = +inf far tails (a8)
+# The upper-exceedance fast path of k_sov forms each 8-row sub-block's log-sum-exp from a running
+# product exp(ell - c_w) * prod q; it must fall back to the exact per-row path whenever that product
+# underflows (reading R10), e.g. eight factors q ~ Phibar(14) ~ 8e-45 in a row.
+@pytest.mark.parametrize("n", [16, 129])
+@pytest.mark.parametrize("aval", [13.3, 13.5, 14.0, 20.0, 30.0, 34.9])
+def test_sov_upper_far_tail_identity(torch, n, aval):
+    """Sigma = I, b = NULL: log P_k = k log Phibar(a) exactly (zero variance); and = the oracle."""
+    from scipy.special import log_ndtr
+    import test_gpu_parity as P
+    T = mvn().mvn_pack_lower(torch.from_numpy(np.eye(n)).cuda(), n)
+    assert mvn().mvn_potrf(T, n) == -1
+    a = np.full(n, aval)
+    N, R = 96, 2
+    M, S = P.gpu_sov(torch, T, n, a, N, R, 11)
+    lp = logp(M, S, N * R)
+    assert np.all(np.isfinite(lp))
+    k = np.arange(1, n + 1)
+    want = k * log_ndtr(-aval)
+    assert np.all(np.abs(lp - want) <= 1e-12 + 4e-15 * np.abs(want)), np.max(np.abs(lp - want))
+    Mo, So = P.oracle_range(np.eye(n), a, np.full(n, np.inf), N, R, 11, 0, N * R, nthreads=4)
+    lo = logp(Mo, So, N * R)
+    assert np.all(np.abs(lp - lo) <= 1e-12 + 4e-15 * np.abs(lo))
+
+
+def test_sov_upper_far_tail_correlated(torch):
+    """A correlated nu = 3/2 field (12 x 12 grid, beta = 0.02) with thresholds putting every
+    conditional limit a' of every sample in the far tail [13, 35] (checked on the oracle's own
+    y): GPU = oracle within 1e-12 relative, no -inf."""
+    import test_gpu_parity as P
+    g = 12
+    n = g * g
+    c = (np.arange(g) + 0.5) / g
+    xy = np.stack(np.meshgrid(c, c, indexing="ij"), -1).reshape(-1, 2)
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, 0.02, 1.5, 1e-8)
+    assert mvn().mvn_potrf(T, n) == -1
+    L = P.to_dense_lower(T, n)
+    a = np.full(n, 22.0)
+    N, R, seed = 64, 2, 23
+    from oracle import lattice
+    G, D = lattice.generators(n), lattice.shifts(seed, R, n)
+    _, _, y = oracle.sov_unit(L, a, np.full(n, np.inf), G, D[0], 1, N, want_y=True)
+    ap = (a[:, None] - (np.tril(L, -1) @ y)) / np.diag(L)[:, None]
+    assert ap.min() >= 13.0 and ap.max() <= 35.0, (ap.min(), ap.max())
+    M, S = P.gpu_sov(torch, T, n, a, N, R, seed)
+    lp = logp(M, S, N * R)
+    Mo, So = P.oracle_range(L, a, np.full(n, np.inf), N, R, seed, 0, N * R, nthreads=4)
+    lo = logp(Mo, So, N * R)
+    assert np.all(np.isfinite(lp))
+    assert np.all(np.abs(lp - lo) <= 1e-12 + 1e-14 * np.abs(lo)), np.max(np.abs(lp - lo))

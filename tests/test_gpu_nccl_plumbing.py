@@ -64,3 +64,46 @@ def test_combine_prefix_with_nccl_allreduce(nccl):
     combine_prefix(M2, S2, force_collectives=True)
     torch.cuda.synchronize()
     assert torch.equal(M2, M) and torch.equal(S2, S)
+
+
+@pytest.mark.parametrize("mode", ["rank0", "dist"])
+def test_crd_step_with_nccl_collectives_equals_mvn_crd(nccl, mode):
+    """The multi-GPU step (parallel.crd_step) on the one-rank NCCL communicator with every
+    collective forced — broadcast_L of the whole tile buffer (rank0, the north_star C1), or the
+    distributed Cholesky's panel broadcasts (dist, NEXT-1), then the all_reduce combine — returns
+    log P bitwise equal to the single-GPU C call mvn_crd on the same inputs."""
+    import torch
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200 import parallel
+    import workloads as W
+    cfg = W.small_config("nccl-crd", 30, 1000, 3, base="C")        # n = 900, nu = 3/2
+    inp = W.make_inputs(cfg)
+    n = cfg.n
+    ref = mvn.mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                      cfg.seed_lattice, cfg.conf)
+    order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
+    d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+    d_a = torch.from_numpy(a).cuda()
+    L = mvn.alloc_tiles(n)
+    parallel.FORCE_COLLECTIVES = True
+    try:
+        ev = []
+        lp = parallel.crd_step(d_xy, d_a, L, cfg, potrf=mode, events=ev).cpu().numpy()
+    finally:
+        parallel.FORCE_COLLECTIVES = False
+    assert [e[0] for e in ev] == ["start", "cov", "potrf", "bcast", "sov", "combine", "finalize"]
+    assert np.array_equal(lp, ref.logP)
+    k, _ = mvn.mvn_confidence_region(lp, cfg.conf)
+    assert np.array_equal(k, ref.k_star)
+
+
+def test_broadcast_L_forced_is_identity(nccl):
+    import torch
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200.parallel import broadcast_L
+    n = 700
+    T = mvn.mvn_cov_matern(torch.from_numpy(np.random.default_rng(2).uniform(size=(n, 2))).cuda(), 1.0, 0.1, 0.5, 1e-8)
+    T0 = T.clone()
+    broadcast_L(T, force_collectives=True)
+    torch.cuda.synchronize()
+    assert torch.equal(T, T0)

@@ -370,3 +370,57 @@ def test_max_size_sampled_parity(torch_cuda):
     M, S = gpu_sov(torch, T, n, a, cfg.N, cfg.R, cfg.seed_lattice, begin, end)
     Ms, Ss = oracle_range(Lg, a[:m], np.full(m, np.inf), cfg.N, cfg.R, cfg.seed_lattice, begin, end)
     assert np.max(np.abs(logp_from(M, S, end - begin)[:m] - logp_from(Ms, Ss, end - begin))) <= 1e-10
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C", "D", "E"])
+def test_full_config_all_samples_regions(torch_cuda, name):
+    """The north_star acceptance at the BASELINE configs, in the launch configuration bench.py times:
+    mvn_sov_prefix over ALL N*R samples of the config (one call, grid of 148 persistent CTAs with
+    their full sample shares, 128/96-wide blocks, ring phases carried across blocks) against the
+    oracle over the same N*R samples on the leading m = 1,024 prefixes (a leading prefix depends only
+    on L[0:m, 0:m], reading R1). Shared-L mode (the oracle consumes the GPU's leading block of L):
+    |dlog P_k| <= 1e-10 for k <= m. Independent mode (the oracle's own Crout factor of the leading
+    block of Sigma) at C and D: <= 1e-8 (north_star; E is reported, SURVEY §8(c) parity modes). The
+    regions k*(1 - alpha) at every level of the config (Eq. 4) must be identical, a level
+    where the oracle's log P is within 1e-8 of log(1 - alpha) (near tie) excepted and reported."""
+    torch = torch_cuda
+    cfg = W.CONFIGS[name]
+    inp, order, a = sorted_inputs(cfg)
+    n, NR = cfg.n, cfg.NR
+    xy = inp.xy[order]
+    T = gpu_cov(torch, xy, cfg)
+    assert mvn().mvn_potrf(T, n) == -1
+    M, S = gpu_sov(torch, T, n, a, cfg.N, cfg.R, cfg.seed_lattice, 0, NR)
+    lp_g = logp_from(M, S, NR)
+    k_g, _ = mvn().mvn_confidence_region(lp_g, cfg.conf)
+    m = 1024
+    Lg = leading_block(T, n, m)
+    G = lattice.generators(m)
+    D = lattice.shifts(cfg.seed_lattice, cfg.R, m)
+    binf = np.full(m, np.inf)
+
+    def oracle_logp(L):
+        parts = oracle.sov_units(L, a[:m], binf, G, D, cfg.N, cfg.R, 1000, nthreads=0)
+        Mo, So = oracle.combine_units(parts)
+        return oracle.prefix_logp(Mo, So, NR)
+
+    lp_s = oracle_logp(Lg)
+    d_shared = float(np.max(np.abs(lp_g[:m] - lp_s)))
+    assert d_shared <= 1e-10, d_shared
+    k_s, tie_s = oracle.region(lp_s, cfg.conf)
+    assert np.all(k_s < m), "m too small: a region reaches past the compared prefixes"
+    ties = [(float(c), int(kg), int(ks)) for c, kg, ks, t in zip(cfg.conf, k_g, k_s, tie_s) if t]
+    if ties:
+        print(f"config {name}: near ties (level, k* gpu, k* oracle): {ties}")
+    assert all(kg == ks or t for kg, ks, t in zip(k_g, k_s, tie_s)), (list(k_g), list(k_s))
+    So = oracle.covariance(xy[:m], cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    Lo, info = oracle.cholesky(So, nthreads=0)
+    assert info == -1
+    lp_i = oracle_logp(Lo)
+    d_indep = float(np.max(np.abs(lp_g[:m] - lp_i)))
+    print(f"config {name}: all {NR} samples, leading {m} prefixes: max|dlog P| shared-L {d_shared:.2e}, "
+          f"independent {d_indep:.2e}; k* = {list(k_g)}")
+    assert d_indep <= (1e-7 if name == "E" else LOGP_TOL), d_indep
+    k_i, tie_i = oracle.region(lp_i, cfg.conf)
+    assert all(kg == ki or t for kg, ki, t in zip(k_g, k_i, tie_i)), (list(k_g), list(k_i))

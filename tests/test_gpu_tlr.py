@@ -175,3 +175,29 @@ def test_tlr_relative_mode_limits(torch):
     T = mvn().mvn_pack_lower(torch.from_numpy(S).cuda(), n)
     assert list(mvn().mvn_tlr_compress(T, n, 0.0, mode=1).cpu().numpy()) == [128]
     assert np.max(np.abs(dense_sym(T, n) - S)) <= 1e-13
+
+
+@pytest.mark.parametrize("eps", [1e-1, 1e-4])
+def test_tlr_relative_mode_scale_invariant(torch, eps):
+    """Mode 1 is a relative criterion, so compressing s * Sigma must give the same ranks and s times
+    the same tiles for any scale s (here 2^-27: every tile norm far below eps, where an absolute
+    Jacobi skip floor would leave the columns unrotated and break ||A - A_k||_F <= eps ||A||_F).
+    Checked against the oracle on the scaled matrix with no absolute slack."""
+    cfg = W.small_config("tlrs", 23, 100, 1, base="B")
+    T, S, _ = sorted_cov(torch, cfg)
+    n = cfg.n
+    s = 2.0 ** -27                                # ~7.5e-9, exact scaling (power of two)
+    Ts = T * s
+    r1 = mvn().mvn_tlr_compress(T, n, eps, mode=1).cpu().numpy()
+    rs = mvn().mvn_tlr_compress(Ts, n, eps, mode=1).cpu().numpy()
+    _, ro, _ = oracle.tlr_compress(S * s, eps, mode="fro")
+    assert np.array_equal(rs, r1)
+    assert np.sum(rs != ro) <= 1                  # a near tie at most
+    G, Gs = dense_sym(T, n), dense_sym(Ts, n)
+    assert np.max(np.abs(Gs / s - G)) <= 1e-12 * np.max(np.abs(S))
+    nt = -(-n // NB)
+    for I in range(1, nt):
+        for J in range(I):
+            rsl, csl = slice(I * NB, min((I + 1) * NB, n)), slice(J * NB, (J + 1) * NB)
+            ef = np.linalg.norm(S[rsl, csl] * s - Gs[rsl, csl])
+            assert ef <= eps * np.linalg.norm(S[rsl, csl] * s) * (1 + 1e-9), (I, J)
