@@ -371,6 +371,57 @@ def run_potrf_dist(args, cfg):
     return 0
 
 
+def run_shard(args, cfg):
+    """Per-rank shard efficiency on one GPU: the SOV sweep (k_sov + k_reduce_blocks, through
+    mvn_sov_prefix) over rank 0's 1/W share of the config's N*R samples, the exact range rank 0
+    sweeps at W GPUs (parallel.shard_range), for each W in --shard. Cov + Cholesky untimed; each
+    range timed --steps times with CUDA events after --warmup sweeps. Roofline: n(n-1) flops per
+    sample against the fp64 DMMA peak."""
+    import torch
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200 import parallel
+    torch.cuda.set_device(0)
+    inp = W.make_inputs(cfg)
+    n, NR = cfg.n, cfg.NR
+    order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
+    d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+    d_a = torch.from_numpy(a).cuda()
+    L = mvn.mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    assert mvn.mvn_potrf(L, n) == -1
+    shards = {}
+    clocks = ClockSampler(0)
+    clocks.start()
+    for w in [int(x) for x in args.shard.split(",")]:
+        b, e = parallel.shard_range(NR, 0, w)
+        for _ in range(args.warmup):
+            mvn.mvn_sov_prefix(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, b, e)
+        ts = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            mvn.mvn_sov_prefix(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, b, e)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = float(np.mean(ts))
+        per_cta = (e - b) / min(e - b, 148)
+        tf = float(n) * (n - 1) * (e - b) / (ms / 1e3) / 1e12
+        cnt = math.ceil(per_cta)                             # the largest CTA share (k_sov block_geom)
+        nblk, units = -(-cnt // 128), -(-cnt // 8)
+        shards[str(w)] = {"samples": e - b, "samples_per_cta": per_cta, "blocks_per_cta": nblk,
+                          "widest_block": 8 * -(-units // nblk), "padding": 8 * units / cnt - 1,
+                          "sov_ms": ms, "tflops": tf, "frac": tf / PEAK_FP64_TFLOPS, "ms_each": ts}
+    clk = clocks.stop()
+    line = {"metric": "SOV per-rank shard efficiency (fraction of the fp64 DMMA peak)", "unit": "frac",
+            "value": min(v["frac"] for v in shards.values()), "higher_is_better": True, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {cfg.name}: rank 0's share of N*R = {NR} samples at W GPUs", "n": n,
+                       "N": cfg.N, "R": cfg.R},
+            "shards": shards, "peak": PEAK_FP64_TFLOPS, "clocks": clk}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # --------------------------------------------------------------------------------- NEXT-3 workload
 def run_tlr(args):
     """TLR compression (NEXT-3 part, R23) at the paper's accuracy setting: n = 40,000 sites
@@ -442,11 +493,13 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: run the multi-GPU code path (NCCL process group, distributed Cholesky, "
                          "all_reduce combine, pinned-buffer e2e) even with one rank")
-    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr"],
+    ap.add_argument("--shard", default="1,2,4,8", help="--workload shard: the world sizes W whose rank-0 share is timed")
+    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr", "shard"],
                     help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
                          "posterior: NEXT-4 conditioning (paper size: 200x200 sites, 6,250 observations); "
                          "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU; "
-                         "tlr: NEXT-3 TLR compression at the paper's 40K-site accuracy setting")
+                         "tlr: NEXT-3 TLR compression at the paper's 40K-site accuracy setting; "
+                         "shard: the SOV over rank 0's 1/W sample share for each W in --shard (one GPU)")
     ap.add_argument("--tlr-eps", type=float, default=1e-3, help="--workload tlr: accuracy eps (R23)")
     ap.add_argument("--tlr-mode", type=int, default=0, choices=[0, 1],
                     help="--workload tlr: 0 = keep sigma_i >= eps, 1 = relative Frobenius error <= eps per tile")
@@ -466,6 +519,8 @@ def main():
         return run_posterior(args)
     if args.workload == "potrf-dist":
         return run_potrf_dist(args, cfg)
+    if args.workload == "shard":
+        return run_shard(args, cfg)
 
     import torch
     import torch.distributed as dist

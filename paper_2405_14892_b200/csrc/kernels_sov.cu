@@ -41,12 +41,8 @@ constexpr int BK = MVN_SOV_BK, STAGES = 64 / MVN_SOV_BK;
 constexpr int SA = M + 4;                // 68  == 4 (mod 16): conflict-free DMMA fragment loads
 constexpr int SB = NB + 4;               // 132 == 4 (mod 16); also the Y-history row stride
 constexpr int SS = NB + 8;               // S tile stride (16-byte fragment stores conflict-free)
-// GEMM warps: GW = 8 (2 x 4, warp tile 32 x 32) or 16 (4 x 4, warp tile 16 x 32: more warps per
-// scheduler to cover the operand waits; MVN build flag MVN_SOV_GW)
-#ifndef MVN_SOV_GW
-#define MVN_SOV_GW 8
-#endif
-constexpr int GW = MVN_SOV_GW, GROWS = GW / 4, WROWS = M / GROWS, WRB = WROWS / 8;
+// GEMM warps (8; 16 warps of 16 x 32 tiles were measured slower in round 1)
+constexpr int GW = 8;
 constexpr int NGEMM = 32 * GW, NCHAIN = NB, NPROD = 32, NT = NGEMM + NCHAIN + NPROD;
 constexpr int STAGE = BK * (SA + SB);                    // doubles per pipeline stage
 constexpr int OFF_S = STAGES * STAGE;                    // S[64][SS]: s, then y, of the row block
@@ -123,16 +119,19 @@ struct SovArgs {
 };
 
 // Sample blocks of a CTA: its `count` samples are split into nblk = ceil(count / 128) blocks whose
-// widths are multiples of 32 spread as evenly as possible (540 -> 128, 128, 96, 96, 96), so no block
-// degenerates to a 32-wide sliver whose GEMM is too short to hide the chain. Block b starts at sample
-// offset off and holds cnt <= w samples (only the last block can have cnt < w).
+// widths are multiples of 8 (the DMMA n-dimension) spread as evenly as possible (540 -> 112, 112,
+// 112, 104, 104), so no block degenerates to a sliver whose GEMM is too short to hide the chain,
+// and a small per-CTA share is padded by < 8 samples (a rank's 1/8 of config D: 67.6 samples per
+// CTA -> one 72-wide block; with 32-wide granularity it was 96, 29 % of the DMMA work padding).
+// Block b starts at sample offset off and holds cnt <= w samples (only the last block can have
+// cnt < w).
 struct BlockGeom { int64_t off; int cnt, w; };
 __device__ __forceinline__ BlockGeom block_geom(int64_t count, int b) {
-    const int64_t units = (count + 31) / 32, nblk = (count + sovk::NB - 1) / sovk::NB;
+    const int64_t units = (count + 7) / 8, nblk = (count + sovk::NB - 1) / sovk::NB;
     const int64_t q = units / nblk, r = units % nblk;
     BlockGeom g;
-    g.w = (int)(32 * (q + (b < r ? 1 : 0)));
-    g.off = 32 * ((int64_t)b * q + (b < r ? b : r));
+    g.w = (int)(8 * (q + (b < r ? 1 : 0)));
+    g.off = 8 * ((int64_t)b * q + (b < r ? b : r));
     const int64_t left = count - g.off;
     g.cnt = (int)(left < g.w ? left : g.w);
     return g;
@@ -211,16 +210,24 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
 }
 
 // ------------------------------------------------------------------------------------ GEMM warps
-// S_r (64 x w) = L[rows r, 0:64r] * Y[0:64r, block]: 8 warps as 2 (rows) x 4 (columns), warp tile
-// 32 x 8*WN, fp64 DMMA.8x8x4 from conflict-free shared-memory fragments.
-template <int WN>
-__device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, uint32_t &q) {
+// S_r (64 x w) = L[rows r, 0:64r] * Y[0:64r, block], fp64 DMMA.8x8x4 from conflict-free shared-memory
+// fragments, w = 8u. Two warp layouts:
+//   u = 4, 8, 12, 16 (w a multiple of 32): 2 (rows) x 4 (columns), warp tile 32 x 8*(u/4);
+//   other u: 4 (rows) x 2 (column halves), warp tile 16 x 8*ceil(u/2) or 16 x 8*floor(u/2). Warp w
+//     sits on scheduler w % 4 and takes row group w % 4, so each scheduler holds both halves of one
+//     row group: the 2u DMMAs per k-step are the same on every scheduler for any u.
+// Template arguments: LROWS = rows per warp (32 or 16), WN = 8-column fragments of this warp (0 for
+// the empty half at u = 1: it still releases the ring stages).
+template <int LROWS, int WN>
+__device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, int wn0, uint32_t &q) {
     using namespace sovk;
+    constexpr int WRB = LROWS / 8;
+    constexpr int GR = M / LROWS;                         // row groups
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
     uint64_t *empty = full + STAGES;
     const int lane = tid & 31, warp = tid >> 5;
-    const int wm0 = (warp % GROWS) * WROWS, wn0 = (warp / GROWS) * (WN * 8);
-    double acc[WRB][WN][2];
+    const int wm0 = (warp % GR) * LROWS;
+    double acc[WRB][WN > 0 ? WN : 1][2];
 #pragma unroll
     for (int i = 0; i < WRB; ++i)
 #pragma unroll
@@ -232,7 +239,7 @@ __device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, u
         const double *bs = as + BK * SA;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            double fa[WRB], fb[WN];
+            double fa[WRB], fb[WN > 0 ? WN : 1];
             const int kr = kk + (lane & 3);
 #pragma unroll
             for (int i = 0; i < WRB; ++i) fa[i] = as[kr * SA + wm0 + i * 8 + (lane >> 2)];
@@ -294,7 +301,7 @@ __device__ __forceinline__ void chain_load(const SovArgs &p, double *sm, int rb,
 // weights for the 8 rows at once (8 independent shuffle trees) into ps[row][warp].
 template <bool HAS_B>
 __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, double *Yslot, int rb, int j, int cnt,
-                                               uint64_t r, uint64_t jl, double &ell) {
+                                               int w, uint64_t r, uint64_t jl, double &ell) {
     using namespace sovk;
     const int64_t row0 = (int64_t)rb * M;
     double *S = sm + OFF_S;
@@ -307,7 +314,10 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
     double *ELL8 = sm + OFF_ELL8;
     const int lane = j & 31, cw = j >> 5;
     const bool valid = j < cnt;
-    if (rb == 0)                                          // S_0 = 0: no GEMM for the first row block
+    // S_0 = 0 (no GEMM for the first row block); columns j >= w of a block whose width is not a
+    // multiple of 32 are outside the GEMM tile: their lanes run as invalid samples (warp-wide
+    // shuffles need whole warps) on s = 0, never feeding a reduction
+    if (rb == 0 || j >= w)
         for (int li = 0; li < M; ++li) S[li * SS + j] = 0.0;
 #pragma unroll 1
     for (int sb = 0; sb < M / 8; ++sb) {
@@ -431,15 +441,25 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
     if (tid < NGEMM) {
         // ============================================================ GEMM warps
         uint32_t q = 0;
+        const int warp = tid >> 5;
         for (int b = 0; b < nblk; ++b) {
-            const int w = block_geom(count, b).w;
+            const int u = block_geom(count, b).w >> 3;          // 8-column fragments of the block
+            // layout 2 x 4 (u % 4 == 0): column group warp / 2; layout 4 x 2: half warp / 4
+            const int half = warp >> 2, u0 = (u + 1) >> 1;
+            const int wn0 = (u & 3) == 0 ? (warp >> 1) * 2 * u : half * 8 * u0;
             for (int rb = 1; rb < p.nrb; ++rb) {
-                switch (w >> 5) {
-                    case 1: sov_gemm_rowblock<1>(sm, rb, tid, q); break;
-                    case 2: sov_gemm_rowblock<2>(sm, rb, tid, q); break;
-                    case 3: sov_gemm_rowblock<3>(sm, rb, tid, q); break;
-                    default: sov_gemm_rowblock<4>(sm, rb, tid, q); break;
+#define MVN_G2(U) case U: if (half == 0) sov_gemm_rowblock<16, (U + 1) / 2>(sm, rb, tid, wn0, q); \
+                          else sov_gemm_rowblock<16, U / 2>(sm, rb, tid, wn0, q); break;
+                switch (u) {
+                    case 4: sov_gemm_rowblock<32, 1>(sm, rb, tid, wn0, q); break;
+                    case 8: sov_gemm_rowblock<32, 2>(sm, rb, tid, wn0, q); break;
+                    case 12: sov_gemm_rowblock<32, 3>(sm, rb, tid, wn0, q); break;
+                    case 16: sov_gemm_rowblock<32, 4>(sm, rb, tid, wn0, q); break;
+                    MVN_G2(1) MVN_G2(2) MVN_G2(3) MVN_G2(5) MVN_G2(6) MVN_G2(7) MVN_G2(9) MVN_G2(10) MVN_G2(11)
+                    MVN_G2(13) MVN_G2(14) MVN_G2(15)
+                    default: break;
                 }
+#undef MVN_G2
                 named_arrive(BAR_SFULL, N_SFULL);
             }
         }
@@ -464,7 +484,7 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
                 named_sync(BAR_CHAIN, NCHAIN);
                 if (j < M) sm[OFF_DINV + j] = 1.0 / sm[OFF_LD + j * M + j];
                 named_sync(BAR_CHAIN, NCHAIN);
-                if (j < w) chain_rowblock<HAS_B>(p, sm, Yslot, rb, j, cnt, r, jl, ell);
+                if (j < ((w + 31) & ~31)) chain_rowblock<HAS_B>(p, sm, Yslot, rb, j, cnt, w, r, jl, ell);
                 __threadfence();                                  // Y_rb: generic-proxy writes ...
                 asm volatile("fence.proxy.async.global;\n" ::: "memory");   // ... visible to the TMA reads
                 named_arrive(BAR_YREADY, N_YREADY);
@@ -473,7 +493,7 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
                     const int64_t k = (int64_t)rb * M + j;
                     if (k < p.n) {
                         const double *ps = sm + OFF_PS + j * 8;
-                        const int nw = w >> 5;
+                        const int nw = (w + 31) >> 5;
                         double mm = -CUDART_INF;
                         for (int qq = 0; qq < nw; ++qq) mm = fmax(mm, ps[2 * qq]);
                         double ss = 0.0;

@@ -107,3 +107,30 @@ def test_sov_upper_far_tail_correlated(torch):
     lo = logp(Mo, So, N * R)
     assert np.all(np.isfinite(lp))
     assert np.all(np.abs(lp - lo) <= 1e-12 + 1e-14 * np.abs(lo)), np.max(np.abs(lp - lo))
+
+
+# ---------------------------------------------------------------------- sample-block widths
+@pytest.mark.parametrize("per_cta", [9, 17, 45, 67, 70, 100, 121, 128, 300, 541])
+def test_sov_block_widths(torch, per_cta):
+    """Every sample-block width k_sov can pick (multiples of 8 up to 128; both GEMM warp layouts:
+    2 x 4 for widths that are multiples of 32, 4 x 2 column halves otherwise, including the empty
+    half at width 8) against the oracle in shared-L mode: 148 * per_cta samples give every
+    persistent CTA per_cta samples (one block of 8 ceil(per_cta / 8), or several blocks of
+    near-equal widths), across shift boundaries, n = 263 (five row blocks, a ragged tail)."""
+    import test_gpu_parity as P
+    n = 263
+    rng = np.random.default_rng(77)
+    xy = rng.uniform(size=(n, 2))
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, 0.12, 1.5, 1e-8)
+    assert mvn().mvn_potrf(T, n) == -1
+    a = np.sort(rng.uniform(-2.0, 0.3, n))
+    total = 148 * per_cta
+    R = 3
+    N = -(-total // R) + 5
+    begin = 3
+    end = begin + total
+    M, S = P.gpu_sov(torch, T, n, a, N, R, 41, begin, end)
+    L = P.to_dense_lower(T, n)
+    Mo, So = P.oracle_range(L, a, np.full(n, np.inf), N, R, 41, begin, end, nthreads=8)
+    d = np.max(np.abs(logp(M, S, total) - logp(Mo, So, total)))
+    assert d <= 1e-11, d
