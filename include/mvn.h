@@ -123,8 +123,8 @@ mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
  *   owner(s):  mvn_potrf_panel(k, kp)  -> mvn_panel_pack(k, kp)  -> broadcast
  *   others:    receive                 -> mvn_panel_unpack(k, kp)
  *   all:       mvn_potrf_update(k, kp, own columns >= k+kp)
- * A panel of (k, kp) is the tiles (k+j .. nt-1, k+j), j < kp, stored contiguously column after
- * column: sum_j (nt-k-j) * nb*nb doubles, device. All calls are asynchronous on the context's
+ * A panel of (k, kp) is the tiles (k+j .. nt-1, k+j), j < kp, stored contiguously (layout at
+ * mvn_panel_pack): sum_j (nt-k-j) * nb*nb doubles, device. All calls are asynchronous on the context's
  * stream; pivots are checked on the device and collected by mvn_potrf_info.                    */
 
 /* Tile columns per super-panel (1..8) that mvn_potrf uses for order n (and potrf_distributed must
@@ -146,13 +146,53 @@ mvn_status mvn_potrf_panel(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t k
 mvn_status mvn_potrf_update(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t k, int64_t kp, int64_t col_first,
                             int64_t col_stride, int64_t col_block, int32_t sm_reserve);
 
-/* Super-panel (k, kp) <-> contiguous panel buffer (device, caller-owned, size above). */
+/* Super-panel (k, kp) <-> contiguous panel buffer (device, caller-owned, size above); the buffer
+ * holds the super-panel's tiles row after row: tile (i, k+j) at ((m <= kp ? m(m+1)/2 : kp(kp+1)/2 +
+ * (m-kp) kp) + j) nb^2 doubles, m = i - k (kp clipped at nt - k), so a row (i, k .. k+kp-1) is
+ * contiguous — the operand layout of the trailing update. */
 mvn_status mvn_panel_pack(mvn_ctx *ctx, mvn_tiles t, const double *d_tiles, int64_t k, int64_t kp, double *d_panel);
 mvn_status mvn_panel_unpack(mvn_ctx *ctx, mvn_tiles t, const double *d_panel, int64_t k, int64_t kp, double *d_tiles);
 
 /* Reads (synchronising the stream) the device info of mvn_potrf_panel: -1 if every pivot so far
  * was positive, else the first failing 0-based row. reset != 0 sets it back to -1 afterwards.  */
 mvn_status mvn_potrf_info(mvn_ctx *ctx, int64_t *info, int32_t reset);
+
+/* ---------------------------------------------------------------------------------------------
+ * NEXT-1 distributed STORAGE (P:81, P:609-645 — the paper's dense runs keep
+ * the tiles distributed over the nodes): a rank holds only the tile columns it owns under the 1-D
+ * block-cyclic map (super-panel s = tile columns s*kp .. s*kp+kp-1 owned by rank s mod world), so
+ * its memory is ~1/world of the 8 n^2/2 bytes. Local layout: the owned tiles, row after row —
+ * tile (i, j), i >= j, j owned, at (owned tiles in rows < i + owned columns < j) * nb*nb doubles.
+ * The same recurrence as mvn_potrf (bit-identical factor): per super-step s, owner(s) factors
+ * super-panel s in its storage (mvn_dpotrf_panel) and packs it (mvn_dpanel_pack, layout at
+ * mvn_panel_pack); the buffer is broadcast (torch.distributed / NCCL, above the ABI); every rank
+ * updates its own columns from the BUFFER (mvn_dpotrf_update: no unpack, no full copy).
+ * Synchronisation, streams and errors as the calls above; pivots go to the context's device info
+ * (mvn_potrf_info). kp = 1..8 (normally mvn_potrf_panel_width(n)).                               */
+typedef struct {
+    int64_t n, nb;          /* order, tile size (128) */
+    int32_t world, rank;    /* ranks, this rank (0 <= rank < world) */
+    int32_t kp;             /* tile columns per super-panel */
+} mvn_dtiles;
+
+/* Bytes of the rank's local storage (0 for invalid d). */
+size_t mvn_dtiles_bytes(mvn_dtiles d);
+/* Doubles in the broadcast buffer of super-panel s (-1 for invalid arguments). */
+int64_t mvn_dpanel_numel(mvn_dtiles d, int64_t s);
+/* a2 on the owned tiles only (arguments as mvn_cov_matern; d_xy holds all n sorted locations). */
+mvn_status mvn_dcov_matern(mvn_ctx *ctx, mvn_dtiles d, const double *d_xy, double sigma2, double beta, double nu,
+                           double nugget, double *d_local);
+/* Factor the owned super-panel s in place (as mvn_potrf_panel; MVN_E_USAGE unless s % world == rank). */
+mvn_status mvn_dpotrf_panel(mvn_ctx *ctx, mvn_dtiles d, double *d_local, int64_t s);
+/* Owned super-panel s -> broadcast buffer d_panel (mvn_dpanel_numel(d, s) doubles). */
+mvn_status mvn_dpanel_pack(mvn_ctx *ctx, mvn_dtiles d, const double *d_local, int64_t s, double *d_panel);
+/* A_ij -= sum_{c in super-panel s} L_ic L_jc^T, operands read from super-panel s's buffer, for every
+ * owned tile column j of the super-panels >= sp_first (just_one != 0: super-panel sp_first only,
+ * which must then be owned) and every i >= j. Requires sp_first > s. sm_reserve as mvn_potrf_update. */
+mvn_status mvn_dpotrf_update(mvn_ctx *ctx, mvn_dtiles d, double *d_local, int64_t s, const double *d_panel,
+                             int64_t sp_first, int32_t just_one, int32_t sm_reserve);
+/* Copy the owned tiles into their places in a full tile-packed buffer (other tiles untouched). */
+mvn_status mvn_dgather(mvn_ctx *ctx, mvn_dtiles d, const double *d_local, double *d_tiles);
 
 /* ---------------------------------------------------------------------------------------------
  * a5. QMC point set (reading R8). The global sample index g in [0, N*R) maps to shift r = g / N

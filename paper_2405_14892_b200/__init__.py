@@ -36,6 +36,8 @@ ABI_SYMBOLS = [
     "mvn_confidence_region", "mvn_crd", "mvn_potrf_panel", "mvn_potrf_update", "mvn_panel_pack",
     "mvn_panel_unpack", "mvn_potrf_info", "mvn_mc_validate", "mvn_mc_levels", "mvn_potrf_panel_width",
     "mvn_posterior", "mvn_posterior_tiles", "mvn_tlr_compress",
+    "mvn_dtiles_bytes", "mvn_dpanel_numel", "mvn_dcov_matern", "mvn_dpotrf_panel", "mvn_dpanel_pack",
+    "mvn_dpotrf_update", "mvn_dgather",
 ]
 
 
@@ -47,6 +49,11 @@ class MvnError(RuntimeError):
 
 class mvn_tiles(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("nb", ctypes.c_int64)]
+
+
+class mvn_dtiles(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nb", ctypes.c_int64), ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("kp", ctypes.c_int32)]
 
 
 class mvn_qmc(ctypes.Structure):
@@ -125,6 +132,13 @@ def lib() -> ctypes.CDLL:
         "mvn_posterior": (S, [P, ctypes.POINTER(mvn_posterior_problem), P, P, ctypes.POINTER(I64)]),
         "mvn_posterior_tiles": (S, [P, T, P, P]),
         "mvn_tlr_compress": (S, [P, T, P, D, I32, P]),
+        "mvn_dtiles_bytes": (ctypes.c_size_t, [mvn_dtiles]),
+        "mvn_dpanel_numel": (I64, [mvn_dtiles, I64]),
+        "mvn_dcov_matern": (S, [P, mvn_dtiles, P, D, D, D, D, P]),
+        "mvn_dpotrf_panel": (S, [P, mvn_dtiles, P, I64]),
+        "mvn_dpanel_pack": (S, [P, mvn_dtiles, P, I64, P]),
+        "mvn_dpotrf_update": (S, [P, mvn_dtiles, P, I64, P, I64, I32, I32]),
+        "mvn_dgather": (S, [P, mvn_dtiles, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -318,6 +332,53 @@ def mvn_panel_unpack(panel, n: int, k: int, kp: int, t, stream=None):
     c.check(lib().mvn_panel_unpack(c.h, tiles(n), _dev_ptr(panel), int(k), int(kp), _dev_ptr(t)), "mvn_panel_unpack")
 
 
+# ---- NEXT-1 distributed storage: a rank's owned tile columns only (include/mvn.h, mvn_dtiles)
+def dtiles(n: int, world: int, rank: int, kp: int) -> mvn_dtiles:
+    return mvn_dtiles(int(n), TILE, int(world), int(rank), int(kp))
+
+
+def mvn_dtiles_bytes(n: int, world: int, rank: int, kp: int) -> int:
+    return int(lib().mvn_dtiles_bytes(dtiles(n, world, rank, kp)))
+
+
+def mvn_dpanel_numel(n: int, world: int, rank: int, kp: int, s: int) -> int:
+    return int(lib().mvn_dpanel_numel(dtiles(n, world, rank, kp), int(s)))
+
+
+def alloc_dtiles(n: int, world: int, rank: int, kp: int, device=None):
+    import torch
+    return torch.empty(max(mvn_dtiles_bytes(n, world, rank, kp) // 8, 1), dtype=torch.float64, device=device or "cuda")
+
+
+def mvn_dcov_matern(xy_sorted, d: mvn_dtiles, sigma2, beta, nu, nugget, local, stream=None):
+    import torch
+    c = Context.get(local.device.index, stream)
+    c.check(lib().mvn_dcov_matern(c.h, d, _dev_ptr(xy_sorted, torch.float64), float(sigma2), float(beta), float(nu),
+                                  float(nugget), _dev_ptr(local, torch.float64)), "mvn_dcov_matern")
+
+
+def mvn_dpotrf_panel(local, d: mvn_dtiles, s: int, stream=None):
+    c = Context.get(local.device.index, stream)
+    c.check(lib().mvn_dpotrf_panel(c.h, d, _dev_ptr(local), int(s)), "mvn_dpotrf_panel")
+
+
+def mvn_dpanel_pack(local, d: mvn_dtiles, s: int, panel, stream=None):
+    c = Context.get(local.device.index, stream)
+    c.check(lib().mvn_dpanel_pack(c.h, d, _dev_ptr(local), int(s), _dev_ptr(panel)), "mvn_dpanel_pack")
+
+
+def mvn_dpotrf_update(local, d: mvn_dtiles, s: int, panel, sp_first: int, just_one: bool = False, sm_reserve: int = 0,
+                      stream=None):
+    c = Context.get(local.device.index, stream)
+    c.check(lib().mvn_dpotrf_update(c.h, d, _dev_ptr(local), int(s), _dev_ptr(panel), int(sp_first),
+                                    1 if just_one else 0, int(sm_reserve)), "mvn_dpotrf_update")
+
+
+def mvn_dgather(local, d: mvn_dtiles, full, stream=None):
+    c = Context.get(local.device.index, stream)
+    c.check(lib().mvn_dgather(c.h, d, _dev_ptr(local), _dev_ptr(full)), "mvn_dgather")
+
+
 def mvn_potrf_info(device: int = 0, reset: bool = True, stream=None) -> int:
     c = Context.get(device, stream)
     info = ctypes.c_int64(-1)
@@ -501,4 +562,5 @@ def mvn_crd(xy: np.ndarray, mu: np.ndarray, sigma2, beta, nu, nugget, u, N, R, s
     return CrdOutput(order, logP, k[:len(cf)], tie[:len(cf)].astype(bool), int(res.info), tuple(res.ms_stage))
 
 
-__all__ = [n for n in dir() if n.startswith("mvn_")] + ["Context", "MvnError", "lib", "TILE", "alloc_tiles"]
+__all__ = [n for n in dir() if n.startswith("mvn_")] + ["Context", "MvnError", "lib", "TILE", "alloc_tiles", "dtiles",
+                                                      "alloc_dtiles"]

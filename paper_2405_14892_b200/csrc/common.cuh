@@ -19,6 +19,46 @@ __host__ __device__ inline int64_t tile_offset(int64_t i, int64_t j) {
     return ((i * (i + 1)) / 2 + j) * (int64_t)kTile * kTile;
 }
 
+// Where tile (i, j), i >= j, of a lower tile-packed matrix lives (128 x 128 column-major tiles):
+//   kFull : every lower tile, row after row — tile_offset(i, j);
+//   kDist : only the tile columns a rank owns under the 1-D block-cyclic map of super-panels of kp
+//           columns over W ranks (super-panel s = columns s kp .. s kp + kp - 1, owned by rank
+//           s mod W), row after row: (owned tiles in rows < i) + (owned columns < j). A rank's
+//           memory is ~1/W of the matrix (NEXT-1 distributed storage);
+//   kPanel: the tiles (i, k .. min(i, k + kp - 1)), i >= k, of the super-panel (k, kp), row after
+//           row (the broadcast buffer of the distributed factorisation).
+// In every mode the tiles (i, c .. c + m) of one super-panel row are consecutive in memory.
+struct TileMap {
+    enum : int { kFull = 0, kDist = 1, kPanel = 2 };
+    double *base = nullptr;
+    int mode = kFull, W = 1, g = 0, kp = 1, k = 0;
+
+    // owned columns in [0, x) (kDist)
+    __host__ __device__ int64_t owned_below(int64_t x) const {
+        const int64_t P = (int64_t)kp * W, r = x % P - (int64_t)g * kp;
+        return (x / P) * kp + (r < 0 ? 0 : r > kp ? kp : r);
+    }
+    // owned tiles in tile rows < i = sum_{x=1..i} owned_below(x) (kDist), closed form
+    __host__ __device__ int64_t owned_rows_below(int64_t i) const {
+        const int64_t P = (int64_t)kp * W, T = i + 1, Q = T / P, R = T % P, K = kp;
+        const int64_t H = K * (K - 1) / 2 + K * (P - (int64_t)(g + 1) * K);
+        const int64_t u = R - (int64_t)g * K;
+        const int64_t Hp = u <= 0 ? 0 : u <= K ? u * (u - 1) / 2 : K * (K - 1) / 2 + K * (u - K);
+        return P * K * Q * (Q - 1) / 2 + Q * H + R * Q * K + Hp;
+    }
+    __host__ __device__ int64_t index(int64_t i, int64_t j) const {
+        if (mode == kFull) return (i * (i + 1)) / 2 + j;
+        if (mode == kDist) return owned_rows_below(i) + owned_below(j);
+        const int64_t m = i - k;
+        return (m <= kp ? m * (m + 1) / 2 : (int64_t)kp * (kp + 1) / 2 + (m - kp) * kp) + (j - k);
+    }
+    __host__ __device__ double *tile(int64_t i, int64_t j) const { return base + index(i, j) * (int64_t)kTile * kTile; }
+    __host__ __device__ bool owns_col(int64_t j) const { return mode != kDist || (j / kp) % W == g; }
+    static TileMap full(double *b) { TileMap m; m.base = b; return m; }
+    static TileMap dist(double *b, int W_, int g_, int kp_) { TileMap m; m.base = b; m.mode = kDist; m.W = W_; m.g = g_; m.kp = kp_; return m; }
+    static TileMap panel(double *b, int k_, int kp_) { TileMap m; m.base = b; m.mode = kPanel; m.k = k_; m.kp = kp_; return m; }
+};
+
 // C(8x8) += A(8x4, row) * B(4x8, col). Fragment ownership (lane l):
 //   a = A[l/4][l%4], b = B[l%4][l/4], c = {C[l/4][2(l%4)], C[l/4][2(l%4)+1]}
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {

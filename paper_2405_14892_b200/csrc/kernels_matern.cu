@@ -2,13 +2,12 @@
 // tile-layout helpers (pack / unpack) plus the small prefix kernels (rescale, finalize).
 //
 // Layout: lower tile-packed, tile (i,j) i>=j is a 128x128 column-major block at tile_offset(i,j).
-// One CTA (256 threads) writes one tile; each thread owns pairs of consecutive rows of a column
-// and writes them with one 16-byte store, so a warp writes 512 contiguous bytes per instruction
-// (fully coalesced). Locations of the tile's 128 rows and 128 columns are staged in shared memory.
+// One CTA (256 threads) writes one tile (layout in k_cov_matern's header); every store is part of
+// a warp-wide 1 KB contiguous column write.
 // Bound: HBM stores (8 B per element, 6.4 TB/s -> ~23 fp64-pipe instructions per element at 64
 // DFMA/clk/SM) vs the fp64 arithmetic per element: distance (3), sqrt, x = h / beta as a product
 // with the host's 1/beta (1; a division costs ~10 plus a slow-path call), exp(-x) with sigma2
-// folded in (11, exp_neg_scaled), the nu = 3/2, 5/2 factor (1-2).
+// folded in (10, exp_neg_scaled), the nu = 3/2, 5/2 factor (1-2).
 #include <math_constants.h>
 
 #include "common.cuh"
@@ -16,114 +15,147 @@
 
 namespace mvn {
 
-// exp(-x) for 0 <= x <= 700 in 11 fp64-pipe instructions (CUDA's exp: ~18 plus branches), with
-// the factor sigma2 folded into the table: x = k ln2/32 + r, |r| <= ln2/64, k = round(32 x / ln2)
-// (magic-constant rounding), exp(-x) = 2^-(k >> 5) * 2^-((k & 31)/32) * exp(-r); exp(-r) by its
-// Taylor polynomial of degree 6 (truncation <= r^7/7! = 3.4e-18 relative), the 32 values
-// sigma2 * 2^-(j/32) from a host table (long double, correctly rounded), and 2^-(k >> 5) applied
-// to the exponent field with an integer subtract (INT pipe). Error <= ~3 ulp (vs ~1 for exp()).
+// exp(-x) for 0 <= x <= 700 in 10 fp64-pipe instructions (CUDA's exp: ~18 plus branches), with
+// the factor sigma2 folded into the table: x = k ln2/128 + r, |r| <= ln2/256, k = round(128 x / ln2)
+// (magic-constant rounding), exp(-x) = 2^-(k >> 7) * 2^-((k & 127)/128) * exp(-r); exp(-r) by its
+// Taylor polynomial of degree 5 (truncation <= r^6/6! = 5.4e-19 relative), the 128 values
+// sigma2 * 2^-(j/128) from a host table (long double, correctly rounded, in shared memory), and
+// 2^-(k >> 7) applied to the exponent field with an integer subtract. Error <= ~3 ulp.
 struct MaternArgs {
     int64_t n;
     const double *xy;
     double sigma2, inv_beta, nugget;
-    double *tiles;
-    double tab[32];      // sigma2 * 2^(-j/32), j = 0..31
+    TileMap tm;          // destination storage (the full buffer, or a rank's owned tile columns)
+    int libm;            // sigma2 so small or large that the scaled result could leave the normal range
+    double tab[128];     // sigma2 * 2^(-j/128), j = 0..127
 };
 
 __device__ __forceinline__ double exp_neg_scaled(double x, const double *tb) {
     constexpr double kMagic = 0x1.8p52;                   // 1.5 * 2^52: fma(.., .., kMagic) rounds to an integer
-    constexpr double k32ln2 = 46.166241308446828384;      // 32 / ln 2
-    constexpr double kLn2hi = 0x1.62e42fefa3800p-6;       // ln2/32, high part (exact product with k < 2^20)
-    constexpr double kLn2lo = 0x1.ef35793c76730p-50;      // ln2/32 - kLn2hi (rounded)
-    const double kd = fma(x, k32ln2, kMagic);
+    constexpr double k128ln2 = 184.6649652337873;         // 128 / ln 2
+    constexpr double kLn2hi = 0x1.62e42fefa2000p-8;       // ln2/128, high part (40 bits)
+    constexpr double kLn2lo = 0x1.9ef35793c7673p-48;      // ln2/128 - kLn2hi (rounded)
+    const double kd = fma(x, k128ln2, kMagic);
     const int k = __double2loint(kd);
     const double kf = kd - kMagic;
     double r = fma(-kf, kLn2hi, x);
     r = fma(-kf, kLn2lo, r);
-    double p = 1.0 / 720.0;                               // exp(-r) = sum (-r)^i / i!
-    p = fma(p, r, -1.0 / 120.0);
+    double p = -1.0 / 120.0;                              // exp(-r) = sum (-r)^i / i!
     p = fma(p, r, 1.0 / 24.0);
     p = fma(p, r, -1.0 / 6.0);
     p = fma(p, r, 0.5);
     p = fma(p, r, -1.0);
     p = fma(p, r, 1.0);
-    const double v = tb[k & 31] * p;
-    return __hiloint2double(__double2hiint(v) - ((k >> 5) << 20), __double2loint(v));
+    const double v = tb[k & 127] * p;
+    return __hiloint2double(__double2hiint(v) - ((k >> 7) << 20), __double2loint(v));
 }
 
-static __device__ __noinline__ double exp_neg_far(double x, double sigma2) { return sigma2 * exp(-x); }
-
-template <int NU2>  // 2*nu: 1 -> nu = 1/2, 3 -> nu = 3/2, 5 -> nu = 5/2; returns sigma2 * C(x)
-__device__ __forceinline__ double matern_scaled(double x, double sigma2, const double *tb) {
-    const double e = x <= 700.0 ? exp_neg_scaled(x, tb) : exp_neg_far(x, sigma2);   // far pairs: libm path
+template <int NU2>  // 2*nu: 1 -> nu = 1/2, 3 -> nu = 3/2, 5 -> nu = 5/2; sigma2 * C(x) from e = sigma2 exp(-x)
+__device__ __forceinline__ double matern_poly(double x, double e) {
     if (NU2 == 1) return e;
     if (NU2 == 3) return fma(x, e, e);
     return fma(fma(x, 1.0 / 3.0, 1.0) * x, e, e);
 }
 
+// sqrt(d) for d >= 0 without the special-operand branch of sqrt(): the MUFU reciprocal square-root
+// seed, one Newton step on it, then one on the root (error ~ ulp; d = 0 gives 0 via the clamp).
+__device__ __forceinline__ double sqrt_nonneg(double d) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(fmax(d, 1e-300)));
+    const double c = fma(-(d * y), y, 1.0);               // 1 - d y^2
+    y = fma(0.5 * y, c, y);
+    const double t = d * y;
+    return fma(0.5 * y, fma(-t, t, d), t);
+}
+
+// One CTA (256 threads) per tile. Thread t owns rows 4 (t % 32) .. +3 of the tile (their locations
+// in registers) and the 16 columns t / 32 + 8 m, m < 16: per column one 32-byte store of 4 rows, so a
+// warp writes one whole 1 KB column per step (coalesced), and a column's location is one broadcast
+// shared-memory read for 4 elements.
 template <int NU2>
 __global__ void __launch_bounds__(256) k_cov_matern(const MaternArgs p) {
-    __shared__ double rx[kTile], ry[kTile], cx[kTile], cy[kTile], tb[32];
+    __shared__ double cx[kTile], cy[kTile], tb[128];
     // blockIdx.x -> tile (ti, tj), ti >= tj, row-major enumeration of the lower triangle
     const int64_t id = blockIdx.x;
     int ti = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
     while ((int64_t)ti * (ti + 1) / 2 > id) --ti;
     while ((int64_t)(ti + 1) * (ti + 2) / 2 <= id) ++ti;
     const int tj = (int)(id - (int64_t)ti * (ti + 1) / 2);
+    if (!p.tm.owns_col(tj)) return;                      // distributed storage: another rank's column
     const int tid = threadIdx.x;
     const int64_t n = p.n;
-    if (tid < kTile) {
-        int64_t r = (int64_t)ti * kTile + tid;
-        rx[tid] = r < n ? p.xy[2 * r] : 0.0;
-        ry[tid] = r < n ? p.xy[2 * r + 1] : 0.0;
-    } else {
-        int64_t c = (int64_t)tj * kTile + (tid - kTile);
-        cx[tid - kTile] = c < n ? p.xy[2 * c] : 0.0;
-        cy[tid - kTile] = c < n ? p.xy[2 * c + 1] : 0.0;
-    }
-    if (tid < 32) tb[tid] = p.tab[tid];
-    __syncthreads();
-    double *T = p.tiles + tile_offset(ti, tj);
     const int64_t r0 = (int64_t)ti * kTile, c0 = (int64_t)tj * kTile;
+    if (tid < kTile) {
+        const int64_t c = c0 + tid;
+        cx[tid] = c < n ? p.xy[2 * c] : 0.0;
+        cy[tid] = c < n ? p.xy[2 * c + 1] : 0.0;
+    } else {
+        tb[tid - kTile] = p.tab[tid - kTile];
+    }
+    const int rq = (tid & 31) * 4, cg = tid >> 5;
+    double rx[4], ry[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const int64_t r = r0 + rq + h;
+        rx[h] = r < n ? p.xy[2 * r] : 0.0;
+        ry[h] = r < n ? p.xy[2 * r + 1] : 0.0;
+    }
+    __syncthreads();
+    double *T = p.tm.tile(ti, tj) + rq;
     const bool edge = r0 + kTile > n || ti == tj;         // padding or diagonal elements in this tile
     const double sigma2 = p.sigma2, ib = p.inv_beta, diag = p.sigma2 + p.nugget;
-    // 128 columns x 64 row-pairs = 8192 double2 stores; 256 threads -> 32 each (a warp stores 512
-    // contiguous bytes per instruction)
-#pragma unroll 4
-    for (int it = 0; it < 32; ++it) {
-        const int e = it * 256 + tid;
-        const int col = e >> 6;
-        const int rp = (e & 63) * 2;
-        double v[2];
+    const bool libm = p.libm != 0;
+#pragma unroll 2
+    for (int m = 0; m < kTile / 8; ++m) {
+        const int col = cg + 8 * m;
+        const double xc = cx[col], yc = cy[col];
+        double x[4], v[4];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int row = rp + h;
-            const double dx = rx[row] - cx[col];
-            const double dy = ry[row] - cy[col];
-            double val = matern_scaled<NU2>(sqrt(fma(dx, dx, dy * dy)) * ib, sigma2, tb);
-            if (edge) {
-                const int64_t gr = r0 + row, gc = c0 + col;
-                if (gr >= n || gc >= n) val = (gr == gc) ? 1.0 : 0.0;
-                else if (gr == gc) val = diag;
-            }
-            v[h] = val;
+        for (int h = 0; h < 4; ++h) {
+            const double dx = rx[h] - xc, dy = ry[h] - yc;
+            x[h] = sqrt_nonneg(fma(dx, dx, dy * dy)) * ib;
         }
-        *reinterpret_cast<double2 *>(T + (int64_t)col * kTile + rp) = make_double2(v[0], v[1]);
+        // far pairs (x > 700: sigma2 e^-x near the bottom of the normal range) take libm's exp for
+        // the whole warp: one vote per 4 elements instead of a divergent branch per element
+        if (!libm && !__any_sync(0xffffffffu, fmax(fmax(x[0], x[1]), fmax(x[2], x[3])) > 700.0)) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) v[h] = matern_poly<NU2>(x[h], exp_neg_scaled(x[h], tb));
+        } else {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) v[h] = matern_poly<NU2>(x[h], sigma2 * exp(-x[h]));
+        }
+        if (edge) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int64_t gr = r0 + rq + h, gc = c0 + col;
+                if (gr >= n || gc >= n) v[h] = (gr == gc) ? 1.0 : 0.0;
+                else if (gr == gc) v[h] = diag;
+            }
+        }
+        double2 *dst = reinterpret_cast<double2 *>(T + (int64_t)col * kTile);
+        dst[0] = make_double2(v[0], v[1]);
+        dst[1] = make_double2(v[2], v[3]);
     }
 }
 
-cudaError_t launch_cov_matern(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
-                              double *tiles, cudaStream_t st) {
+cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
+                                  const TileMap &tm, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
     const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
     MaternArgs a;
-    a.n = n; a.xy = xy; a.sigma2 = sigma2; a.inv_beta = 1.0 / beta; a.nugget = nugget; a.tiles = tiles;
-    for (int j = 0; j < 32; ++j) a.tab[j] = (double)((long double)sigma2 * exp2l(-(long double)j / 32.0L));
+    a.n = n; a.xy = xy; a.sigma2 = sigma2; a.inv_beta = 1.0 / beta; a.nugget = nugget; a.tm = tm;
+    a.libm = sigma2 < 0x1p-100 || sigma2 > 0x1p100;
+    for (int j = 0; j < 128; ++j) a.tab[j] = (double)((long double)sigma2 * exp2l(-(long double)j / 128.0L));
     dim3 grid((unsigned)ntiles);
     if (nu == 0.5) k_cov_matern<1><<<grid, 256, 0, st>>>(a);
     else if (nu == 1.5) k_cov_matern<3><<<grid, 256, 0, st>>>(a);
     else k_cov_matern<5><<<grid, 256, 0, st>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_cov_matern(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
+                              double *tiles, cudaStream_t st) {
+    return launch_cov_matern_map(n, xy, sigma2, beta, nu, nugget, TileMap::full(tiles), st);
 }
 
 // ------------------------------------------------------------------------------ pack / unpack

@@ -324,7 +324,10 @@ constexpr int A_BYTES = oz::S * kTile * oz::KC;      // 32 KB
 constexpr int B_SLICE = NS * oz::KC;                  // 4 KB
 constexpr int B_BYTES = oz::S * B_SLICE;              // 32 KB
 constexpr int STAGE = A_BYTES + B_BYTES;              // 64 KB
-constexpr int STAGES = 3;
+#ifndef MVN_OZ2_STAGES
+#define MVN_OZ2_STAGES 3
+#endif
+constexpr int STAGES = MVN_OZ2_STAGES;           // (experiment knob: bytes in flight per CTA)
 constexpr int NT = 320;                               // 8 epilogue warps + producer + MMA issuer
 constexpr int SMEM = STAGES * STAGE + 1024;
 }  // namespace oz2

@@ -77,11 +77,11 @@ __device__ __forceinline__ void blk_solve32(double *X, int ldx, int c0, int r, c
 // K2 (blocked): POTRF of the 128 x 128 diagonal tile k in shared memory. Per 32-column block cb:
 // DMMA update of rows >= 32cb by the finished columns, one-warp factorisation of the 32 x 32
 // diagonal block (first non-positive pivot -> *info, global row), substitution of the rows below.
-__global__ void __launch_bounds__(256) k_potrf_diag2(double *__restrict__ tiles, int k, int64_t *__restrict__ info) {
+__global__ void __launch_bounds__(256) k_potrf_diag2(const TileMap tm, int k, int64_t *__restrict__ info) {
     using namespace blk;
     extern __shared__ double A[];          // [128 cols][SP]
     __shared__ int failed;
-    double *T = tiles + tile_offset(k, k);
+    double *T = tm.tile(k, k);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < kTile * kTile / 2; e += 256) {
         const int col = e >> 6, seg = e & 63;
@@ -133,14 +133,14 @@ __global__ void __launch_bounds__(256) k_potrf_diag2(double *__restrict__ tiles,
 }
 
 // K3 (blocked): L_ik = A_ik L_kk^{-T} for one 64-row half of panel tile i (grid: 2 CTAs per tile).
-__global__ void __launch_bounds__(256) k_trsm2(double *__restrict__ tiles, int k) {
+__global__ void __launch_bounds__(256) k_trsm2(const TileMap tm, int k) {
     using namespace blk;
     extern __shared__ double sh[];
     double *X = sh;                        // [128 cols][SPX]: rows h*64 .. h*64+63 of A_ik
     double *Lk = sh + kTile * SPX;         // [128 cols][SP]
     const int i = k + 1 + (blockIdx.x >> 1), h = blockIdx.x & 1;
-    double *Ti = tiles + tile_offset(i, k) + h * 64;
-    const double *Lkk = tiles + tile_offset(k, k);
+    double *Ti = tm.tile(i, k) + h * 64;
+    const double *Lkk = tm.tile(k, k);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < kTile * 32; e += 256) {           // 128 cols x 32 pieces
         const int col = e >> 5, seg = e & 31;
@@ -198,8 +198,10 @@ constexpr int SMEM = STAGES * BK * (SA + SB) * 8;
 
 // Trailing update, one CTA per (tile (i,j), row half h): C(64x128) -= L_ik[h-half] * L_jk^T.
 // 4 warps as 2 (M) x 2 (N), warp tile 32x64 = 4x8 DMMA blocks (64 fp64 accumulators / thread).
-__global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, int k, int kp, int nt, int c0, int cs,
-                                                   int cb) {
+// dst: where C lives; src: where the panel's tiles L_ik, L_jk are read (the same storage, or the
+// broadcast panel buffer of the distributed factorisation).
+__global__ void __launch_bounds__(128, 2) k_update(const TileMap dst, const TileMap src, int k, int kp, int nt, int c0,
+                                                   int cs, int cb) {
     using namespace upd;
     extern __shared__ double sm[];
     double *As = sm;
@@ -211,9 +213,9 @@ __global__ void __launch_bounds__(128, 2) k_update(double *__restrict__ tiles, i
     int ti, tj, col = 0;
     int64_t base = 0;
     upd_item(id, nt, c0, cs, cb, ti, tj, base, col);
-    const double *__restrict__ Lik = tiles + tile_offset(ti, k) + h * BM;   // column stride 128
-    const double *__restrict__ Ljk = tiles + tile_offset(tj, k);
-    double *C = tiles + tile_offset(ti, tj) + h * BM;
+    const double *__restrict__ Lik = src.tile(ti, k) + h * BM;   // column stride 128
+    const double *__restrict__ Ljk = src.tile(tj, k);
+    double *C = dst.tile(ti, tj) + h * BM;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 64;
@@ -304,8 +306,8 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // Updates with panel k the tile columns c0, c0 + cs, ... (c0 > k): c0 = k+2, cs = 1 on one GPU
 // (column k+1 is the lookahead stream's); cs = world size for the 1-D block-cyclic distributed
 // factorisation (mvn_potrf_update).
-__global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ tiles, int k, int kp, int nt, int c0,
-                                                        int cs, int cb, int64_t nitems) {
+__global__ void __launch_bounds__(upd2::NT, 1) k_update2(const TileMap dst, const TileMap src, int k, int kp, int nt,
+                                                        int c0, int cs, int cb, int64_t nitems) {
     using namespace upd2;
     extern __shared__ double sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
@@ -328,8 +330,8 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
             int ti, tj;
             upd_item(item, nt, c0, cs, cb, ti, tj, base, col);
-            const double *Lik = tiles + tile_offset(ti, k);    // kp consecutive tiles (row panels are contiguous)
-            const double *Ljk = tiles + tile_offset(tj, k);
+            const double *Lik = src.tile(ti, k);    // kp consecutive tiles (a super-panel row is contiguous in every TileMap)
+            const double *Ljk = src.tile(tj, k);
             for (int c = 0; c < kp * CHUNKS; ++c, ++q) {
                 const int st = q % STAGES;
                 mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(double *__restrict__ ti
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> async proxy
         __syncwarp();
-        if (lane == 0) bulk_reduce_add_f64(tiles + tile_offset(ti, tj) + (int64_t)wn0 * kTile, stg, 16 * kTile * 8);
+        if (lane == 0) bulk_reduce_add_f64(dst.tile(ti, tj) + (int64_t)wn0 * kTile, stg, 16 * kTile * 8);
     }
     if (lane == 0) bulk_wait_all();
 }
@@ -455,24 +457,27 @@ cudaError_t potrf_streams(PotrfStreams &ps) {
 // ---- building blocks shared by mvn_potrf and the distributed factorisation (identical arithmetic)
 // Factor the kp tile columns k .. k+kp-1 (all updates from columns < k applied): POTRF + TRSM of
 // column k; for each further column k+j: update it with columns k .. k+j-1 (K = 128 j), POTRF, TRSM.
-cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int kp, int64_t *d_info, cudaStream_t st) {
+cudaError_t launch_potrf_panel_map(int64_t n, const TileMap &tm, int k, int kp, int64_t *d_info, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
     kp = std::min(kp, nt - k);
     const size_t sm_diag = kTile * blk::SP * 8, sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
     for (int j = 0; j < kp; ++j) {
         const int c = k + j;
-        if (j > 0) k_update<<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tiles, k, j, nt, c, nt, 1);
-        k_potrf_diag2<<<1, 256, sm_diag, st>>>(tiles, c, d_info);
-        if (nt - c - 1 > 0) k_trsm2<<<2 * (nt - c - 1), 256, sm_trsm, st>>>(tiles, c);
+        if (j > 0) k_update<<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tm, tm, k, j, nt, c, nt, 1);
+        k_potrf_diag2<<<1, 256, sm_diag, st>>>(tm, c, d_info);
+        if (nt - c - 1 > 0) k_trsm2<<<2 * (nt - c - 1), 256, sm_trsm, st>>>(tm, c);
     }
     return cudaGetLastError();
+}
+cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int kp, int64_t *d_info, cudaStream_t st) {
+    return launch_potrf_panel_map(n, TileMap::full(tiles), k, kp, d_info, st);
 }
 
 // A_ij -= sum_{c=k}^{k+kp-1} L_ic L_jc^T for the tile columns j = c0 + m cs + b (0 <= b < cb) and
 // i >= j: the persistent kernel (on nsm - sm_reserve SMs) when there are >= 2 tiles per CTA, else
 // two CTAs per tile.
-cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0, int cs, int cb, int sm_reserve,
-                                cudaStream_t st) {
+cudaError_t launch_potrf_update_map(int64_t n, const TileMap &dst, const TileMap &src, int k, int kp, int c0, int cs,
+                                    int cb, int sm_reserve, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
     if (c0 >= nt) return cudaSuccess;
     kp = std::min(kp, nt - k);
@@ -483,11 +488,16 @@ cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0,
     static const bool use_persistent = [] { const char *e = getenv("MVN_POTRF_PERSISTENT"); return !(e && e[0] == '0'); }();
     const int avail = std::max(1, nsm - sm_reserve);
     if (use_persistent && items >= 2 * avail) {
-        k_update2<<<avail, upd2::NT, upd2::SMEM, st>>>(tiles, k, kp, nt, c0, cs, cb, items);
+        k_update2<<<avail, upd2::NT, upd2::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb, items);
     } else {
-        k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(tiles, k, kp, nt, c0, cs, cb);
+        k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb);
     }
     return cudaGetLastError();
+}
+cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0, int cs, int cb, int sm_reserve,
+                                cudaStream_t st) {
+    const TileMap tm = TileMap::full(tiles);
+    return launch_potrf_update_map(n, tm, tm, k, kp, c0, cs, cb, sm_reserve, st);
 }
 
 // Super-panel width for an order-n factorisation: wider panels cut the update passes (K = 128 kp
@@ -564,31 +574,36 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
 // finished, so each rank ends with all of L. launch_potrf_panel / launch_potrf_update above are the
 // arithmetic; this adds the panel copy.
 
-// Panel copy: tiles (k+j .. nt-1, k+j) for j < kp <-> contiguous panel (column k first, then k+1, ...).
+// Super-panel copy between two storages: the tiles (i, c), k <= c < k + kp, i >= c, from one
+// TileMap to another (full storage or a rank's owned columns <-> the kPanel broadcast buffer, whose
+// tiles run row after row so that a super-panel row (i, k .. k+kp-1) is contiguous).
 // grid (8, tiles of the super-panel): one CTA per (tile, 1/8).
-__global__ void __launch_bounds__(256) k_panel_copy(double *__restrict__ tiles, int k, int nt, double *__restrict__ panel,
-                                                   int to_panel) {
+__global__ void __launch_bounds__(256) k_panel_copy(const TileMap from, const TileMap to, int k, int nt) {
     int idx = blockIdx.y, c = k;
     while (idx >= nt - c) { idx -= nt - c; ++c; }
     const int i = c + idx;
-    double2 *t = reinterpret_cast<double2 *>(tiles + tile_offset(i, c));
-    double2 *p = reinterpret_cast<double2 *>(panel + (int64_t)blockIdx.y * kTile * kTile);
+    const double2 *f = reinterpret_cast<const double2 *>(from.tile(i, c));
+    double2 *t = reinterpret_cast<double2 *>(to.tile(i, c));
     constexpr int PER = kTile * kTile / 2 / 8;             // double2 per CTA
     const int e0 = blockIdx.x * PER;
 #pragma unroll 4
-    for (int e = threadIdx.x; e < PER; e += 256) {
-        if (to_panel) p[e0 + e] = t[e0 + e];
-        else t[e0 + e] = p[e0 + e];
-    }
+    for (int e = threadIdx.x; e < PER; e += 256) t[e0 + e] = f[e0 + e];
 }
 
-cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, int kp, double *panel, bool to_panel, cudaStream_t st) {
+cudaError_t launch_panel_copy_map(int64_t n, const TileMap &from, const TileMap &to, int k, int kp, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
     kp = std::min(kp, nt - k);
     int ntiles = 0;
     for (int j = 0; j < kp; ++j) ntiles += nt - k - j;
-    k_panel_copy<<<dim3(8, ntiles), 256, 0, st>>>(tiles, k, nt, panel, to_panel ? 1 : 0);
+    if (ntiles == 0) return cudaSuccess;
+    k_panel_copy<<<dim3(8, ntiles), 256, 0, st>>>(from, to, k, nt);
     return cudaGetLastError();
+}
+
+cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, int kp, double *panel, bool to_panel, cudaStream_t st) {
+    const int nt = (int)((n + kTile - 1) / kTile);
+    const TileMap full = TileMap::full(tiles), pan = TileMap::panel(panel, k, std::min(kp, nt - k));
+    return to_panel ? launch_panel_copy_map(n, full, pan, k, kp, st) : launch_panel_copy_map(n, pan, full, k, kp, st);
 }
 
 }  // namespace mvn

@@ -39,7 +39,8 @@ constexpr int NB = 128;                  // max samples per block (= chain threa
 #endif
 constexpr int BK = MVN_SOV_BK, STAGES = 64 / MVN_SOV_BK;
 constexpr int SA = M + 4;                // 68  == 4 (mod 16): conflict-free DMMA fragment loads
-constexpr int SB = NB + 4;               // 132 == 4 (mod 16); also the Y-history row stride
+constexpr int SB = NB + 4;               // 132 == 4 (mod 16): the widest Y-history row (a block of w samples uses
+                                         // w + 4, == 4 or 12 (mod 16) for w a multiple of 8: conflict-free too)
 constexpr int SS = NB + 8;               // S tile stride (16-byte fragment stores conflict-free)
 // GEMM warps (8; 16 warps of 16 x 32 tiles were measured slower in round 1)
 constexpr int GW = 8;
@@ -107,7 +108,7 @@ struct SovArgs {
     uint64_t seed;
     const int64_t *cta;       // [grid][3]: first global sample, sample count, first block index
     int64_t n_pad;            // Y-history rows per slot (nrb*64)
-    double *Y;                // [grid][n_pad][SB] (row stride SB: padded for conflict-free DMMA loads)
+    double *Y;                // [grid][n_pad * SB]: per block [n_pad][w + 4] (padded for conflict-free DMMA loads)
     double *part;             // [nblk][n_pad][2]
     // soft grid lockstep (L panel reuse in L2): producer of step s = b*nrb + rb waits until every CTA
     // that has step s - lag has issued it; step_done[s] counts issuers, need[b] = CTAs with > b blocks.
@@ -150,7 +151,7 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
     uint32_t q = 0;
     const uint64_t pol_L = policy_evict_last(), pol_Y = policy_evict_first();
     for (int b = 0; b < nblk; ++b) {
-        const int w = block_geom(count, b).w;
+        const int w = block_geom(count, b).w, sbw = w + 4;    // this block's Y-history row stride
         if (p.lag > 0 && lane == 0) atomicAdd(p.step_done + (int64_t)b * p.nrb, 1);   // row block 0: no GEMM
         for (int rb = 1; rb < p.nrb; ++rb) {
             const int64_t row0 = (int64_t)rb * M;
@@ -196,11 +197,12 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
                 }
                 cp_async_mbar_arrive(&full[st]);
                 __syncwarp();
-                // B: BK Y-history rows, contiguous thanks to the padded row stride SB: one TMA bulk copy
+                // B: BK Y-history rows, contiguous at the block's row stride w + 4: one TMA bulk copy
+                // of only the block's columns (+4 padding), so narrow blocks stream fewer bytes
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&full[st], BK * SB * 8);
-                    if (p.hints) bulk_g2s_hint(bs, Yslot + kc * SB, BK * SB * 8, &full[st], pol_Y);
-                    else bulk_g2s(bs, Yslot + kc * SB, BK * SB * 8, &full[st]);
+                    mbar_arrive_expect_tx(&full[st], BK * sbw * 8);
+                    if (p.hints) bulk_g2s_hint(bs, Yslot + kc * sbw, BK * sbw * 8, &full[st], pol_Y);
+                    else bulk_g2s(bs, Yslot + kc * sbw, BK * sbw * 8, &full[st]);
                 }
             }
             if (p.lag > 0 && lane == 0) atomicAdd(p.step_done + (int64_t)b * p.nrb + rb, 1);
@@ -219,7 +221,7 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
 // Template arguments: LROWS = rows per warp (32 or 16), WN = 8-column fragments of this warp (0 for
 // the empty half at u = 1: it still releases the ring stages).
 template <int LROWS, int WN>
-__device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, int wn0, uint32_t &q) {
+__device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, int wn0, int sbw, uint32_t &q) {
     using namespace sovk;
     constexpr int WRB = LROWS / 8;
     constexpr int GR = M / LROWS;                         // row groups
@@ -244,7 +246,7 @@ __device__ __forceinline__ void sov_gemm_rowblock(double *sm, int rb, int tid, i
 #pragma unroll
             for (int i = 0; i < WRB; ++i) fa[i] = as[kr * SA + wm0 + i * 8 + (lane >> 2)];
 #pragma unroll
-            for (int j = 0; j < WN; ++j) fb[j] = bs[kr * SB + wn0 + j * 8 + (lane >> 2)];
+            for (int j = 0; j < WN; ++j) fb[j] = bs[kr * sbw + wn0 + j * 8 + (lane >> 2)];
 #pragma unroll
             for (int i = 0; i < WRB; ++i)
 #pragma unroll
@@ -313,7 +315,8 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
     const double *dinv = sm + OFF_DINV;
     double *ELL8 = sm + OFF_ELL8;
     const int lane = j & 31, cw = j >> 5;
-    const bool valid = j < cnt;
+    const bool valid = j < cnt, incol = j < w;
+    const int sbw = w + 4;
     // S_0 = 0 (no GEMM for the first row block); columns j >= w of a block whose width is not a
     // multiple of 32 are outside the GEMM tile: their lanes run as invalid samples (warp-wide
     // shuffles need whole warps) on s = 0, never feeding a reduction
@@ -347,11 +350,13 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
             const int64_t k = row0 + li;
             // next row's s without the current row's term, read before y exists (off the critical path)
             const double s_next = (i + 1 < 8) ? S[(li + 1) * SS + j] : 0.0;
-            const double ap = (a_s[li] - s) * dinv[li];
+            // lanes past the block's columns run a harmless central step (a' = 0): s = 0 there, and
+            // a' = a / L_kk could sit in the far tail and send the whole warp down the Newton path
+            const double ap = incol ? (a_s[li] - s) * dinv[li] : 0.0;
             const double wq = lattice_w(jl, G_s[li], lattice_shift(p.seed, r, (uint64_t)k));
             double lq, y;
             if (HAS_B) {
-                sov_step(ap, (b_s[li] - s) * dinv[li], wq, lq, y);
+                sov_step(ap, incol ? (b_s[li] - s) * dinv[li] : CUDART_INF, wq, lq, y);
             } else {
                 double q;
 #ifdef MVN_SOV_FAKECHAIN   // timing experiment only: no Phi / Phi^-1 (results are wrong)
@@ -365,7 +370,7 @@ __device__ __forceinline__ void chain_rowblock(const SovArgs &p, double *sm, dou
             ell += lq;
             S[li * SS + j] = y;
             ELL8[i * NB + j] = ell;
-            Yslot[k * SB + j] = y;
+            if (incol) Yslot[k * sbw + j] = y;
             if (i + 1 < 8) s = s_next + Ld[li * M + li + 1] * y;   // row li+1 carried in a register
 #pragma unroll
             for (int d = 2; d < 8; ++d)
@@ -444,17 +449,18 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
         const int warp = tid >> 5;
         for (int b = 0; b < nblk; ++b) {
             const int u = block_geom(count, b).w >> 3;          // 8-column fragments of the block
+            const int sbw = 8 * u + 4;                          // the block's Y-history row stride
             // layout 2 x 4 (u % 4 == 0): column group warp / 2; layout 4 x 2: half warp / 4
             const int half = warp >> 2, u0 = (u + 1) >> 1;
             const int wn0 = (u & 3) == 0 ? (warp >> 1) * 2 * u : half * 8 * u0;
             for (int rb = 1; rb < p.nrb; ++rb) {
-#define MVN_G2(U) case U: if (half == 0) sov_gemm_rowblock<16, (U + 1) / 2>(sm, rb, tid, wn0, q); \
-                          else sov_gemm_rowblock<16, U / 2>(sm, rb, tid, wn0, q); break;
+#define MVN_G2(U) case U: if (half == 0) sov_gemm_rowblock<16, (U + 1) / 2>(sm, rb, tid, wn0, sbw, q); \
+                          else sov_gemm_rowblock<16, U / 2>(sm, rb, tid, wn0, sbw, q); break;
                 switch (u) {
-                    case 4: sov_gemm_rowblock<32, 1>(sm, rb, tid, wn0, q); break;
-                    case 8: sov_gemm_rowblock<32, 2>(sm, rb, tid, wn0, q); break;
-                    case 12: sov_gemm_rowblock<32, 3>(sm, rb, tid, wn0, q); break;
-                    case 16: sov_gemm_rowblock<32, 4>(sm, rb, tid, wn0, q); break;
+                    case 4: sov_gemm_rowblock<32, 1>(sm, rb, tid, wn0, sbw, q); break;
+                    case 8: sov_gemm_rowblock<32, 2>(sm, rb, tid, wn0, sbw, q); break;
+                    case 12: sov_gemm_rowblock<32, 3>(sm, rb, tid, wn0, sbw, q); break;
+                    case 16: sov_gemm_rowblock<32, 4>(sm, rb, tid, wn0, sbw, q); break;
                     MVN_G2(1) MVN_G2(2) MVN_G2(3) MVN_G2(5) MVN_G2(6) MVN_G2(7) MVN_G2(9) MVN_G2(10) MVN_G2(11)
                     MVN_G2(13) MVN_G2(14) MVN_G2(15)
                     default: break;

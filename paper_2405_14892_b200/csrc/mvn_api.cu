@@ -13,6 +13,7 @@
 
 #include "../../include/mvn.h"
 #include "mvn_internal.h"
+#include "common.cuh"
 
 struct mvn_ctx {
     int device = 0;
@@ -353,6 +354,89 @@ mvn_status mvn_panel_unpack(mvn_ctx *c, mvn_tiles t, const double *d_panel, int6
     if (!nt || !d_tiles || !d_panel || k < 0 || k >= nt || kp < 1 || kp > 8)
         return fail(c, MVN_E_USAGE, "mvn_panel_unpack: bad arguments");
     MVN_CUDA(c, mvn::launch_panel_copy(t.n, d_tiles, (int)k, (int)kp, const_cast<double *>(d_panel), false, c->stream));
+    return MVN_OK;
+}
+
+// ---- NEXT-1 distributed storage: a rank holds only the tile columns it owns (TileMap::kDist)
+namespace {
+bool dtiles_ok(const mvn_dtiles &d) {
+    return d.n >= 1 && d.nb == mvn::kTile && d.world >= 1 && d.rank >= 0 && d.rank < d.world && d.kp >= 1 && d.kp <= 8;
+}
+int64_t dtiles_nt(const mvn_dtiles &d) { return (d.n + d.nb - 1) / d.nb; }
+int64_t dtiles_S(const mvn_dtiles &d) { return (dtiles_nt(d) + d.kp - 1) / d.kp; }
+mvn::TileMap dmap(const mvn_dtiles &d, double *local) { return mvn::TileMap::dist(local, d.world, d.rank, d.kp); }
+mvn::TileMap pmap(const mvn_dtiles &d, const double *panel, int64_t s) {
+    const int64_t nt = dtiles_nt(d), k = s * d.kp;
+    return mvn::TileMap::panel(const_cast<double *>(panel), (int)k, (int)std::min<int64_t>(d.kp, nt - k));
+}
+}  // namespace
+
+size_t mvn_dtiles_bytes(mvn_dtiles d) {
+    if (!dtiles_ok(d)) return 0;
+    return (size_t)dmap(d, nullptr).owned_rows_below(dtiles_nt(d)) * (size_t)(d.nb * d.nb) * sizeof(double);
+}
+
+int64_t mvn_dpanel_numel(mvn_dtiles d, int64_t s) {
+    if (!dtiles_ok(d) || s < 0 || s >= dtiles_S(d)) return -1;
+    const int64_t nt = dtiles_nt(d), k = s * d.kp, w = std::min<int64_t>(d.kp, nt - k);
+    int64_t t = 0;
+    for (int64_t j = 0; j < w; ++j) t += nt - k - j;
+    return t * d.nb * d.nb;
+}
+
+mvn_status mvn_dcov_matern(mvn_ctx *c, mvn_dtiles d, const double *d_xy, double sigma2, double beta, double nu,
+                           double nugget, double *d_local) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!dtiles_ok(d) || !d_xy || !d_local || !(sigma2 > 0) || !(beta > 0) || !(nugget >= 0) || !(nu == 0.5 || nu == 1.5 || nu == 2.5))
+        return fail(c, MVN_E_USAGE, "mvn_dcov_matern: bad arguments");
+    MVN_CUDA(c, mvn::launch_cov_matern_map(d.n, d_xy, sigma2, beta, nu, nugget, dmap(d, d_local), c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_dpotrf_panel(mvn_ctx *c, mvn_dtiles d, double *d_local, int64_t s) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!dtiles_ok(d) || !d_local || s < 0 || s >= dtiles_S(d) || s % d.world != d.rank)
+        return fail(c, MVN_E_USAGE, "mvn_dpotrf_panel: bad arguments (super-panel s must be this rank's)");
+    MVN_CUDA(c, mvn::launch_potrf_panel_map(d.n, dmap(d, d_local), (int)(s * d.kp), d.kp, c->d_info, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_dpanel_pack(mvn_ctx *c, mvn_dtiles d, const double *d_local, int64_t s, double *d_panel) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!dtiles_ok(d) || !d_local || !d_panel || s < 0 || s >= dtiles_S(d) || s % d.world != d.rank)
+        return fail(c, MVN_E_USAGE, "mvn_dpanel_pack: bad arguments (super-panel s must be this rank's)");
+    MVN_CUDA(c, mvn::launch_panel_copy_map(d.n, dmap(d, const_cast<double *>(d_local)), pmap(d, d_panel, s),
+                                           (int)(s * d.kp), d.kp, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_dpotrf_update(mvn_ctx *c, mvn_dtiles d, double *d_local, int64_t s, const double *d_panel,
+                             int64_t sp_first, int32_t just_one, int32_t sm_reserve) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    const int64_t S = dtiles_S(d);
+    if (!dtiles_ok(d) || !d_local || !d_panel || s < 0 || s >= S || sp_first <= s || sm_reserve < 0 || sm_reserve >= c->nsm)
+        return fail(c, MVN_E_USAGE, "mvn_dpotrf_update: bad arguments (need 0 <= s < sp_first)");
+    // the first owned super-panel >= sp_first
+    const int64_t sp0 = sp_first + ((d.rank - sp_first % d.world) % d.world + d.world) % d.world;
+    if (sp0 >= S || (just_one && sp0 != sp_first)) return MVN_OK;                 // nothing owned there
+    const int64_t nt = dtiles_nt(d);
+    const int c0 = (int)(sp0 * d.kp), cs = just_one ? (int)nt : d.kp * d.world;
+    MVN_CUDA(c, mvn::launch_potrf_update_map(d.n, dmap(d, d_local), pmap(d, d_panel, s), (int)(s * d.kp),
+                                             d.kp, c0, cs, d.kp, sm_reserve, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_dgather(mvn_ctx *c, mvn_dtiles d, const double *d_local, double *d_tiles) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!dtiles_ok(d) || !d_local || !d_tiles) return fail(c, MVN_E_USAGE, "mvn_dgather: bad arguments");
+    const mvn::TileMap from = dmap(d, const_cast<double *>(d_local)), to = mvn::TileMap::full(d_tiles);
+    for (int64_t s = d.rank; s < dtiles_S(d); s += d.world)
+        MVN_CUDA(c, mvn::launch_panel_copy_map(d.n, from, to, (int)(s * d.kp), d.kp, c->stream));
     return MVN_OK;
 }
 

@@ -11,9 +11,11 @@ The combine is written against an injectable `rescale` so the host logic is test
 gloo (tests/test_parallel_gloo.py); on the GPU path it is the CUDA kernel behind mvn_prefix_rescale.
 
 NEXT-1: `potrf_distributed` factors Sigma across the ranks instead of on
-rank 0 alone — 1-D block-cyclic over super-panels of kp = 2 tile columns (super-panel s owned by
-rank s mod W), one step of lookahead, the finished panel of each step broadcast over NCCL while the ranks update
-their own columns. Every rank ends with all of L, so the broadcast of L (C1) disappears.
+rank 0 alone — 1-D block-cyclic over super-panels of kp tile columns (super-panel s owned by
+rank s mod W), one step of lookahead, the finished panel of each step broadcast over NCCL while the
+ranks update their own columns. With a full buffer per rank (CudaPotrfOps) every rank ends with all
+of L, so the broadcast of L (C1) disappears; with distributed storage (CudaPotrfDistOps,
+potrf_distributed_local) a rank holds only its own columns (~1/W of the memory).
 """
 from __future__ import annotations
 
@@ -301,6 +303,65 @@ class CudaPotrfOps:
 
     def join(self):
         self.main.wait_stream(self.side)
+
+
+class CudaPotrfDistOps(CudaPotrfOps):
+    """potrf_dist_schedule's building blocks on a rank's LOCAL storage (NEXT-1 distributed storage,
+    include/mvn.h mvn_dtiles): `local` holds only the tile columns this rank owns (~1/W of L). The
+    owner factors super-panel s in place and packs it into the broadcast buffer; every rank updates
+    its own columns straight from the buffer (mvn_dpotrf_update), so `unpack` is a no-op and no rank
+    ever holds the whole matrix. Same arithmetic as mvn_potrf: the gathered factor is bit-identical."""
+
+    def __init__(self, local, n: int, world: int, rank: int, main=None, kp: int | None = None):
+        import torch
+        from . import dtiles, mvn_dpanel_numel, mvn_potrf_panel_width
+        self.torch = torch
+        self.L, self.n = local, n
+        self.nt = -(-n // TILE)
+        self.kp = kp or mvn_potrf_panel_width(n)
+        self.world, self.rank = world, rank
+        self.d = dtiles(n, world, rank, self.kp)
+        self.dev = local.device
+        self.main = main if main is not None else torch.cuda.current_stream(self.dev)
+        self.side = torch.cuda.Stream(device=self.dev, priority=-1)
+        self.side.wait_stream(self.main)
+        m = mvn_dpanel_numel(n, world, rank, self.kp, 0)
+        self.bufs = [torch.empty(m, dtype=torch.float64, device=self.dev) for _ in range(2)]
+
+    def panel_buf(self, sp: int):
+        from . import mvn_dpanel_numel
+        return self.bufs[sp & 1][:mvn_dpanel_numel(self.n, self.world, self.rank, self.kp, sp)]
+
+    def panel(self, sp, on):
+        from . import mvn_dpotrf_panel
+        mvn_dpotrf_panel(self.L, self.d, sp, stream=self._st(on))
+
+    def pack(self, sp, on):
+        from . import mvn_dpanel_pack
+        mvn_dpanel_pack(self.L, self.d, sp, self.panel_buf(sp), stream=self._st(on))
+
+    def unpack(self, sp, on):
+        pass                                     # updates read the broadcast buffer directly
+
+    def update(self, sp, c0, cs, cb, on, side_busy=True):
+        from . import mvn_dpotrf_update
+        if c0 < self.nt:
+            reserve = self.SIDE_SMS if (on == "main" and side_busy) else 0
+            # the schedule's two forms: the lookahead (one super-panel, cs = nt) or every owned
+            # super-panel from c0 on (cs = kp * W)
+            mvn_dpotrf_update(self.L, self.d, sp, self.panel_buf(sp), c0 // self.kp, just_one=cs >= self.nt,
+                              sm_reserve=reserve, stream=self._st(on))
+
+
+def potrf_distributed_local(local, n: int, group=None, kp: int | None = None) -> int:
+    """potrf_distributed on distributed storage: `local` is this rank's mvn_dtiles buffer (owned
+    tile columns, Sigma generated there by mvn_dcov_matern); on return it holds this rank's
+    columns of L. Returns info as potrf_distributed."""
+    initialized = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if initialized else 1
+    rank = dist.get_rank(group) if initialized else 0
+    _cuda_info(local)
+    return potrf_distributed(local, n, group, ops=CudaPotrfDistOps(local, n, world, rank, kp=kp))
 
 
 def potrf_distributed(L, n: int, group=None, ops=None, force_collectives: bool = False) -> int:

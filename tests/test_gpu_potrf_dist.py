@@ -42,13 +42,17 @@ def sigma(torch, n, nu=0.5, seed=0):
     return T, oracle.covariance(xy, 1.0, beta, nu, 1e-8)
 
 
-def emulate(torch, tiles, n):
-    """Run potrf_dist_schedule for len(tiles) virtual ranks on one device (see module doc)."""
-    from paper_2405_14892_b200.parallel import CudaPotrfOps, potrf_dist_schedule
+def emulate(torch, tiles, n, local=False):
+    """Run potrf_dist_schedule for len(tiles) virtual ranks on one device (see module doc); local:
+    tiles[r] is rank r's distributed storage (its owned tile columns only, CudaPotrfDistOps)."""
+    from paper_2405_14892_b200.parallel import CudaPotrfDistOps, CudaPotrfOps, potrf_dist_schedule
     W = len(tiles)
     torch.cuda.synchronize()
     mvn().mvn_potrf_info(0, reset=True)
-    ops = [CudaPotrfOps(tiles[r], n, main=torch.cuda.Stream()) for r in range(W)]
+    if local:
+        ops = [CudaPotrfDistOps(tiles[r], n, W, r, main=torch.cuda.Stream()) for r in range(W)]
+    else:
+        ops = [CudaPotrfOps(tiles[r], n, main=torch.cuda.Stream()) for r in range(W)]
     gens = [potrf_dist_schedule(ops[r], r, W) for r in range(W)]
     reqs = [next(g) for g in gens]
     while True:
@@ -93,9 +97,13 @@ def test_panel_pack_unpack(torch, kp):
         T2 = torch.zeros_like(T)
         mvn().mvn_panel_unpack(buf, n, k, kp, T2)
         bh, T2h = buf.cpu().numpy(), T2.cpu().numpy()
+        w = min(kp, nt - k)
         q = 0
-        for c in range(k, min(k + kp, nt)):
-            for i in range(c, nt):
+        for i in range(k, nt):                     # row after row: tiles (i, k .. min(i, k+w-1))
+            m = i - k
+            rowoff = m * (m + 1) // 2 if m <= w else w * (w + 1) // 2 + (m - w) * w
+            for c in range(k, min(i, k + w - 1) + 1):
+                assert rowoff + (c - k) == q
                 off = (i * (i + 1) // 2 + c) * NB * NB
                 assert np.array_equal(bh[q * NB * NB:(q + 1) * NB * NB], Th[off:off + NB * NB])
                 assert np.array_equal(T2h[off:off + NB * NB], Th[off:off + NB * NB])
@@ -148,6 +156,68 @@ def test_emulated_distributed_potrf_matches_single_gpu(torch, n, nu, W):
         assert torch.equal(copies[r], ref), f"rank {r}: max diff {float((copies[r] - ref).abs().max())}"
     res = np.linalg.norm(Lref @ Lref.T - S) / np.linalg.norm(S)
     assert res <= 1e-12
+
+
+@pytest.mark.parametrize("n,nu,W", [(1000, 0.5, 1), (1000, 0.5, 2), (2000, 1.5, 3), (4000, 0.5, 4), (130, 0.5, 3),
+                                    (40 * NB + 77, 0.5, 3), (300, 0.5, 2), (75 * NB, 0.5, 4), (48 * NB + 5, 1.5, 8)])
+def test_emulated_distributed_storage_matches_single_gpu(torch, n, nu, W):
+    """NEXT-1 with distributed storage: each virtual rank holds only its own tile columns (memory
+    ~1/W: mvn_dtiles_bytes), generates its part of Sigma (mvn_dcov_matern), and updates from the
+    broadcast buffers. The ranks' pieces, gathered (mvn_dgather), equal mvn_potrf bit for bit, and the
+    per-rank storage sums to the full tile buffer."""
+    xy = np.random.default_rng(nu + n).uniform(size=(n, 2))
+    beta = 0.1 if nu == 0.5 else 0.05
+    d_xy = torch.from_numpy(xy).cuda()
+    ref = mvn().mvn_cov_matern(d_xy, 1.0, beta, nu, 1e-8)
+    assert mvn().mvn_potrf(ref, n) == -1
+    kp = mvn().mvn_potrf_panel_width(n)
+    locs, total = [], 0
+    for r in range(W):
+        d = mvn().dtiles(n, W, r, kp)
+        loc = mvn().alloc_dtiles(n, W, r, kp)
+        mvn().mvn_dcov_matern(d_xy, d, 1.0, beta, nu, 1e-8, loc)
+        locs.append(loc)
+        total += mvn().mvn_dtiles_bytes(n, W, r, kp)
+    assert total == mvn().mvn_tiles_bytes(n)
+    if W > 1:
+        assert max(mvn().mvn_dtiles_bytes(n, W, r, kp) for r in range(W)) < mvn().mvn_tiles_bytes(n)
+    assert emulate(torch, locs, n, local=True) == -1
+    G = torch.full_like(ref, float("nan"))
+    for r in range(W):
+        mvn().mvn_dgather(locs[r], mvn().dtiles(n, W, r, kp), G)
+    torch.cuda.synchronize()
+    assert torch.equal(G, ref), f"max diff {float((G - ref).abs().max())}"
+
+
+def test_distributed_storage_cov_and_gather_roundtrip(torch):
+    """mvn_dcov_matern writes exactly the owned tiles of mvn_cov_matern's Sigma; gathering every
+    rank's storage rebuilds the full buffer bitwise (W = 3, kp = 2, ragged n)."""
+    n, W, kp = 9 * NB + 17, 3, 2
+    xy = np.random.default_rng(5).uniform(size=(n, 2))
+    d_xy = torch.from_numpy(xy).cuda()
+    full = mvn().mvn_cov_matern(d_xy, 1.0, 0.1, 1.5, 1e-8)
+    G = torch.full_like(full, float("nan"))
+    for r in range(W):
+        d = mvn().dtiles(n, W, r, kp)
+        loc = mvn().alloc_dtiles(n, W, r, kp)
+        mvn().mvn_dcov_matern(d_xy, d, 1.0, 0.1, 1.5, 1e-8, loc)
+        mvn().mvn_dgather(loc, d, G)
+    assert torch.equal(G, full)
+
+
+def test_distributed_storage_bad_args(torch):
+    n, W, kp = 5 * NB, 2, 1
+    loc = mvn().alloc_dtiles(n, W, 0, kp)
+    buf = torch.empty(mvn().mvn_dpanel_numel(n, W, 0, kp, 0), dtype=torch.float64, device="cuda")
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_dpotrf_panel(loc, mvn().dtiles(n, W, 0, kp), 1)          # super-panel 1 is rank 1's
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_dpanel_pack(loc, mvn().dtiles(n, W, 0, kp), 3, buf)
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_dpotrf_update(loc, mvn().dtiles(n, W, 0, kp), 2, buf, 2)  # sp_first must exceed s
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_dpotrf_panel(loc, mvn().dtiles(n, W, 2, kp), 0)          # rank >= world
+    assert mvn().mvn_dtiles_bytes(n, 0, 0, kp) == 0 and mvn().mvn_dpanel_numel(n, W, 0, kp, 5) == -1
 
 
 def test_emulated_distributed_potrf_reports_first_failure(torch):
