@@ -229,6 +229,23 @@ typedef struct {
 mvn_status mvn_sov_prefix(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_a,
                           const double *d_b, const mvn_qmc *q, double *d_M, double *d_S);
 
+/* NEXT-4 ("mixed precision ... tensor core execution"): the same sweep
+ * with a selectable arithmetic for the GEMM update a6 (s of every row from the rows of earlier row
+ * blocks). MVN_SOV_FP64 = mvn_sov_prefix (fp64 DMMA, the default path). MVN_SOV_INT8 = the update
+ * on the int8 tensor cores (tcgen05, TMEM) as an Ozaki-style split, reading R24:
+ * L_kt = 2^{e_k} sum_p a_p 2^{-7p} and y = 2^7 sum_q b_q 2^{-7q} with 8 signed 7-bit digits each,
+ * the 36 products of p + q <= 9 exact in int32, combined in fp64; everything else (in-block part
+ * of s, the Phi / Phi^{-1} chain, log-sum-exp) is the fp64 path's. Same inputs, lattice and
+ * outputs; results agree with the fp64 path to ~1e-12 in log P (not bitwise). Requirements:
+ * d_b == NULL (b = +inf, every BASELINE config) and every sample value |y_k| < 63.5 (|a'| below
+ * ~60); a violation of the latter is detected on the device and returned as MVN_E_NUMERIC. The
+ * int8 call synchronises the stream at its end (that check). Workspace: the 8 slices of L (as
+ * many bytes as L) plus a Y-digit history of ~n KB per pair of SMs.                              */
+#define MVN_SOV_FP64 0
+#define MVN_SOV_INT8 1
+mvn_status mvn_sov_prefix_ex(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_a,
+                             const double *d_b, const mvn_qmc *q, int32_t method, double *d_M, double *d_S);
+
 /* Multi-GPU combine helpers (reading R11): after all_reduce(MAX) of M into d_Mglob,
  *   S <- S * exp(M - Mglob), M <- Mglob  (elementwise, device; S = 0 where M = -inf).
  * Then all_reduce(SUM) of S and mvn_prefix_finalize.                                           */

@@ -37,7 +37,7 @@ ABI_SYMBOLS = [
     "mvn_panel_unpack", "mvn_potrf_info", "mvn_mc_validate", "mvn_mc_levels", "mvn_potrf_panel_width",
     "mvn_posterior", "mvn_posterior_tiles", "mvn_tlr_compress",
     "mvn_dtiles_bytes", "mvn_dpanel_numel", "mvn_dcov_matern", "mvn_dpotrf_panel", "mvn_dpanel_pack",
-    "mvn_dpotrf_update", "mvn_dgather",
+    "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex",
 ]
 
 
@@ -139,6 +139,7 @@ def lib() -> ctypes.CDLL:
         "mvn_dpanel_pack": (S, [P, mvn_dtiles, P, I64, P]),
         "mvn_dpotrf_update": (S, [P, mvn_dtiles, P, I64, P, I64, I32, I32]),
         "mvn_dgather": (S, [P, mvn_dtiles, P, P]),
+        "mvn_sov_prefix_ex": (S, [P, T, P, P, P, ctypes.POINTER(mvn_qmc), I32, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -414,6 +415,25 @@ def mvn_sov_prefix(L, n: int, a, N: int, R: int, seed: int, begin: int = 0, end:
     c.check(lib().mvn_sov_prefix(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64),
                                  None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q),
                                  _dev_ptr(M), _dev_ptr(S)), "mvn_sov_prefix")
+    return M, S
+
+
+SOV_FP64, SOV_INT8 = 0, 1
+
+
+def mvn_sov_prefix_ex(L, n: int, a, N: int, R: int, seed: int, begin: int = 0, end: int | None = None,
+                      b=None, M=None, S=None, method: int = SOV_FP64):
+    """mvn_sov_prefix with a selectable GEMM arithmetic: SOV_FP64 (DMMA, default) or SOV_INT8 (the
+    update on the int8 tensor cores, reading R24; b must be None)."""
+    import torch
+    c = Context.get(L.device.index)
+    end = N * R if end is None else end
+    M = torch.empty(n, dtype=torch.float64, device=L.device) if M is None else M
+    S = torch.empty(n, dtype=torch.float64, device=L.device) if S is None else S
+    q = mvn_qmc(int(N), int(R), int(seed), int(begin), int(end))
+    c.check(lib().mvn_sov_prefix_ex(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64),
+                                    None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q), int(method),
+                                    _dev_ptr(M), _dev_ptr(S)), "mvn_sov_prefix_ex")
     return M, S
 
 

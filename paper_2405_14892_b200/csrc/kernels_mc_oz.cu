@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "mvn_internal.h"
 #include "normal.cuh"
+#include "umma.cuh"
 
 namespace mvn {
 namespace oz {
@@ -43,17 +44,10 @@ constexpr int SMEM = STAGES * STAGE + 1024; // + barriers / bookkeeping
 constexpr uint32_t TMEM_COLS = 512;         // S levels x 64 columns
 }  // namespace oz
 
-__device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
-    // SBO (next 8-row group) = 256 B, LBO (next 16-byte K group) = 128 B, version 1, no swizzle
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) | ((uint64_t)1 << 46);
-}
 constexpr uint32_t oz_idesc() {   // kind::i8: D s32, A/B signed, K-major, N = 64, M = 128
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(oz::NS >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
 }
 
-// Byte offset of element (row, k) (k < 32) inside one slice of a [rows x 32] K-major operand in
-// the canonical core-matrix order [row / 8][k / 16][row % 8][k % 16].
-__device__ __forceinline__ int oz_core(int row, int k) { return ((row >> 3) << 8) + ((k >> 4) << 7) + ((row & 7) << 4) + (k & 15); }
 
 __device__ __forceinline__ void oz_split(double v, int8_t *out, int stride) {
     // v in [-0.53, 0.53]: S signed 7-bit digits, exact (see header)
@@ -139,15 +133,6 @@ __device__ __forceinline__ void oz_mbar_wait(uint64_t *bar, uint32_t parity) { m
 // and each fetches half of the shared L-slice chunk with a multicast bulk copy into BOTH CTAs'
 // rings (L2 -> SM traffic for A halved); each CTA's MMA completion is committed to both CTAs'
 // `empty` barriers, so a slot is refilled only when both have consumed it.
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
 
 template <int CL>
 __global__ void __launch_bounds__(oz::NT, 1) k_oz_trmm(const int8_t *__restrict__ LA, const int8_t *__restrict__ ZB, int64_t n,
@@ -336,18 +321,6 @@ constexpr uint32_t oz2_idesc() {   // kind::i8: D s32, A/B signed, K-major, N = 
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(oz2::NS >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
 }
 
-__device__ __forceinline__ uint32_t mapa_peer(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAITC_%=:\n"
-        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
 
 __global__ void __launch_bounds__(oz2::NT, 1) k_oz2_trmm(const int8_t *__restrict__ LA, const int8_t *__restrict__ ZB,
                                                         int64_t n, int nt, int nblk, int64_t ns,

@@ -200,6 +200,7 @@ constexpr int SMEM = STAGES * BK * (SA + SB) * 8;
 // 4 warps as 2 (M) x 2 (N), warp tile 32x64 = 4x8 DMMA blocks (64 fp64 accumulators / thread).
 // dst: where C lives; src: where the panel's tiles L_ik, L_jk are read (the same storage, or the
 // broadcast panel buffer of the distributed factorisation).
+template <bool MAPPED>   // as k_update2
 __global__ void __launch_bounds__(128, 2) k_update(const TileMap dst, const TileMap src, int k, int kp, int nt, int c0,
                                                    int cs, int cb) {
     using namespace upd;
@@ -213,9 +214,9 @@ __global__ void __launch_bounds__(128, 2) k_update(const TileMap dst, const Tile
     int ti, tj, col = 0;
     int64_t base = 0;
     upd_item(id, nt, c0, cs, cb, ti, tj, base, col);
-    const double *__restrict__ Lik = src.tile(ti, k) + h * BM;   // column stride 128
-    const double *__restrict__ Ljk = src.tile(tj, k);
-    double *C = dst.tile(ti, tj) + h * BM;
+    const double *__restrict__ Lik = (MAPPED ? src.tile(ti, k) : src.base + tile_offset(ti, k)) + h * BM;   // column stride 128
+    const double *__restrict__ Ljk = MAPPED ? src.tile(tj, k) : src.base + tile_offset(tj, k);
+    double *C = (MAPPED ? dst.tile(ti, tj) : dst.base + tile_offset(ti, tj)) + h * BM;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 64;
@@ -306,6 +307,9 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // Updates with panel k the tile columns c0, c0 + cs, ... (c0 > k): c0 = k+2, cs = 1 on one GPU
 // (column k+1 is the lookahead stream's); cs = world size for the 1-D block-cyclic distributed
 // factorisation (mvn_potrf_update).
+// MAPPED = false: the full lower tile-packed buffer (dst.base == src.base, tile_offset addressing —
+// mvn_potrf's hot loop, register-lean); true: explicit TileMaps (NEXT-1 distributed storage).
+template <bool MAPPED>
 __global__ void __launch_bounds__(upd2::NT, 1) k_update2(const TileMap dst, const TileMap src, int k, int kp, int nt,
                                                         int c0, int cs, int cb, int64_t nitems) {
     using namespace upd2;
@@ -330,8 +334,9 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(const TileMap dst, cons
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
             int ti, tj;
             upd_item(item, nt, c0, cs, cb, ti, tj, base, col);
-            const double *Lik = src.tile(ti, k);    // kp consecutive tiles (a super-panel row is contiguous in every TileMap)
-            const double *Ljk = src.tile(tj, k);
+            // kp consecutive tiles (a super-panel row is contiguous in every TileMap)
+            const double *Lik = MAPPED ? src.tile(ti, k) : src.base + tile_offset(ti, k);
+            const double *Ljk = MAPPED ? src.tile(tj, k) : src.base + tile_offset(tj, k);
             for (int c = 0; c < kp * CHUNKS; ++c, ++q) {
                 const int st = q % STAGES;
                 mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
@@ -402,15 +407,19 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(const TileMap dst, cons
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> async proxy
         __syncwarp();
-        if (lane == 0) bulk_reduce_add_f64(dst.tile(ti, tj) + (int64_t)wn0 * kTile, stg, 16 * kTile * 8);
+        if (lane == 0)
+            bulk_reduce_add_f64((MAPPED ? dst.tile(ti, tj) : dst.base + tile_offset(ti, tj)) + (int64_t)wn0 * kTile, stg,
+                                16 * kTile * 8);
     }
     if (lane == 0) bulk_wait_all();
 }
 
 cudaError_t potrf_init() {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, upd::SMEM))) return e;
-    if ((e = cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, upd2::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, upd::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, upd::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_update2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, upd2::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_update2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, upd2::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(k_potrf_diag2, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * blk::SP * 8))) return e;
     if ((e = cudaFuncSetAttribute(k_trsm2, cudaFuncAttributeMaxDynamicSharedMemorySize, kTile * (blk::SP + blk::SPX) * 8))) return e;
     return cudaSuccess;
@@ -463,7 +472,10 @@ cudaError_t launch_potrf_panel_map(int64_t n, const TileMap &tm, int k, int kp, 
     const size_t sm_diag = kTile * blk::SP * 8, sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
     for (int j = 0; j < kp; ++j) {
         const int c = k + j;
-        if (j > 0) k_update<<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tm, tm, k, j, nt, c, nt, 1);
+        if (j > 0) {
+            if (tm.mode == TileMap::kFull) k_update<false><<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tm, tm, k, j, nt, c, nt, 1);
+            else k_update<true><<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tm, tm, k, j, nt, c, nt, 1);
+        }
         k_potrf_diag2<<<1, 256, sm_diag, st>>>(tm, c, d_info);
         if (nt - c - 1 > 0) k_trsm2<<<2 * (nt - c - 1), 256, sm_trsm, st>>>(tm, c);
     }
@@ -487,10 +499,13 @@ cudaError_t launch_potrf_update_map(int64_t n, const TileMap &dst, const TileMap
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     static const bool use_persistent = [] { const char *e = getenv("MVN_POTRF_PERSISTENT"); return !(e && e[0] == '0'); }();
     const int avail = std::max(1, nsm - sm_reserve);
+    const bool mapped = dst.mode != TileMap::kFull || src.mode != TileMap::kFull || dst.base != src.base;
     if (use_persistent && items >= 2 * avail) {
-        k_update2<<<avail, upd2::NT, upd2::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb, items);
+        if (mapped) k_update2<true><<<avail, upd2::NT, upd2::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb, items);
+        else k_update2<false><<<avail, upd2::NT, upd2::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb, items);
     } else {
-        k_update<<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb);
+        if (mapped) k_update<true><<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb);
+        else k_update<false><<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb);
     }
     return cudaGetLastError();
 }

@@ -573,7 +573,12 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
     else k_sov<false><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_reduce_blocks<<<(unsigned)((L.n + 255) / 256), 256, 0, st>>>(L.part, L.nblk, L.n, a.n_pad, L.Mout, L.Sout);
+    return launch_reduce_blocks(L.part, L.nblk, L.n, a.n_pad, L.Mout, L.Sout, st);
+}
+
+cudaError_t launch_reduce_blocks(const double *part, int64_t nblk, int64_t n, int64_t n_pad, double *M, double *S,
+                                 cudaStream_t st) {
+    k_reduce_blocks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nblk, n, n_pad, M, S);
     return cudaGetLastError();
 }
 

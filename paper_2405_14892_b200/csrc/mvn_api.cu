@@ -44,6 +44,7 @@ struct mvn_ctx {
     void *mcRS = nullptr; size_t mcRS_cap = 0;     // per-row scales
     void *mcX = nullptr; size_t mcX_cap = 0;       // method 2: cluster exchange scratch
     void *mcF = nullptr; size_t mcF_cap = 0;
+    void *sozX = nullptr; size_t sozX_cap = 0;     // int8 SOV: cluster exchange scratch
 };
 
 namespace {
@@ -178,7 +179,7 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
         DevGuard dev_guard(c);                        // the caller's current device is restored
         const int64_t minus1 = -1;
         if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess || mvn::mc_init() != cudaSuccess ||
-            mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess ||
+            mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess || mvn::sov_oz_init() != cudaSuccess ||
             cudaMalloc(&c->d_info, 2 * sizeof(int64_t)) != cudaSuccess ||
             cudaMemcpy(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming) != cudaSuccess) {
@@ -204,7 +205,7 @@ void mvn_destroy(mvn_ctx *c) {
     // waits for the device's outstanding work itself
     cudaDeviceSynchronize();
     for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF,
-                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX})
+                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX, c->sozX})
         if (p) cudaFree(p);
     if (c->done) cudaEventDestroy(c->done);
     delete c;
@@ -233,10 +234,10 @@ mvn_status mvn_trim(mvn_ctx *c) {
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX, &c->sozX})
         if (*p) { cudaFree(*p); *p = nullptr; }
     c->Y_cap = c->part_cap = c->cta_cap = c->sync_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
-    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = 0;
+    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = c->sozX_cap = 0;
     c->post_n = c->post_off = 0;
     return MVN_OK;
 }
@@ -519,6 +520,51 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
     L.cta = (const int64_t *)c->cta;
     L.Y = (double *)c->Y; L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S;
     MVN_CUDA(c, mvn::launch_sov(L, c->stream));
+    return MVN_OK;
+}
+
+mvn_status mvn_sov_prefix_ex(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
+                             const mvn_qmc *q, int32_t method, double *d_M, double *d_S) {
+    if (method == MVN_SOV_FP64) return mvn_sov_prefix(c, t, d_L, d_a, d_b, q, d_M, d_S);
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (method != MVN_SOV_INT8) return fail(c, MVN_E_USAGE, "mvn_sov_prefix_ex: method must be MVN_SOV_FP64 or MVN_SOV_INT8");
+    if (!tiles_ok(t) || !d_L || !d_a || d_b || !q || !d_M || !d_S || q->N < 1 || q->R < 1 || q->sample_begin < 0 ||
+        q->sample_end <= q->sample_begin || q->sample_end > q->N * (int64_t)q->R)
+        return fail(c, MVN_E_USAGE, "mvn_sov_prefix_ex (int8): bad arguments (need nb=128, b = NULL (+inf), 0 <= begin < end <= N*R)");
+    mvn_status s;
+    if ((s = ensure_generators(c, t.n)) != MVN_OK) return s;
+    int *d_flag = reinterpret_cast<int *>(c->d_info) + 2;
+    {
+        int h_flag = 0;
+        MVN_CUDA(c, mvn::launch_check_limits(t.n, d_a, nullptr, d_flag, c->stream));
+        MVN_CUDA(c, cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (h_flag) return fail(c, MVN_E_USAGE, "mvn_sov_prefix_ex: a limit is NaN");
+    }
+    // L -> per-row scales and 8 int8 slices in the tcgen05 operand layout (reading R24)
+    const int64_t nt = (t.n + t.nb - 1) / t.nb, n_pad = nt * t.nb;
+    if ((s = ensure(c, &c->mcLA, &c->mcLA_cap, (size_t)mvn::mc_oz_la_bytes(t.n))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->mcRS, &c->mcRS_cap, sizeof(double) * (size_t)n_pad)) != MVN_OK) return s;
+    MVN_CUDA(c, mvn::launch_mc_oz_prepare(t.n, d_L, (double *)c->mcRS, (int8_t *)c->mcLA, c->stream));
+    const int64_t nsamp = q->sample_end - q->sample_begin;
+    mvn::SovOzLaunch L;
+    L.clusters = (int)std::min<int64_t>(mvn::sov_oz_max_clusters(c->nsm), (nsamp + 127) / 128);
+    std::vector<int64_t> cl((size_t)L.clusters * 3);
+    L.nblk = mvn::sov_oz_partition(q->sample_begin, q->sample_end, L.clusters, cl.data());
+    if ((s = ensure(c, &c->Y, &c->Y_cap, (size_t)mvn::sov_oz_ys_bytes(t.n, L.clusters))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->sozX, &c->sozX_cap, (size_t)mvn::sov_oz_xch_bytes(L.clusters))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->part, &c->part_cap, (size_t)(2 * L.nblk) * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->cta, &c->cta_cap, cl.size() * sizeof(int64_t))) != MVN_OK) return s;
+    MVN_CUDA(c, cudaMemcpyAsync(c->cta, cl.data(), cl.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    L.LA = (const int8_t *)c->mcLA; L.rowscale = (const double *)c->mcRS; L.L = d_L; L.n = t.n; L.a = d_a; L.G = c->G;
+    L.N = q->N; L.seed = q->seed; L.cl = (const int64_t *)c->cta; L.YS = (int8_t *)c->Y; L.xch = (double *)c->sozX;
+    L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S; L.flag = d_flag;
+    MVN_CUDA(c, mvn::launch_sov_oz(L, c->stream));
+    int h_big = 0;
+    MVN_CUDA(c, cudaMemcpyAsync(&h_big, d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (h_big) return fail(c, MVN_E_NUMERIC, "mvn_sov_prefix_ex (int8): a sample value |y| >= 63.5 is outside the int8 path's fixed scale; use MVN_SOV_FP64");
     return MVN_OK;
 }
 

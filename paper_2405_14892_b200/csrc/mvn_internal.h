@@ -58,6 +58,34 @@ int sov_block_samples();
 int sov_y_stride();
 int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta);
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
+cudaError_t launch_reduce_blocks(const double *part, int64_t nblk, int64_t n, int64_t n_pad, double *M, double *S,
+                                 cudaStream_t st);
+
+// NEXT-4: the SOV GEMM on the int8 tensor cores (kernels_sov_oz.cu)
+struct SovOzLaunch {
+    const int8_t *LA;        // L slices (launch_mc_oz_prepare)
+    const double *rowscale;
+    const double *L;
+    int64_t n;
+    const double *a;
+    const uint64_t *G;
+    int64_t N;
+    uint64_t seed;
+    const int64_t *cl;       // device [clusters][3] (sov_oz_partition)
+    int clusters;
+    int64_t nblk;            // sample blocks of 128 over all clusters
+    int8_t *YS;              // sov_oz_ys_bytes
+    double *xch;             // sov_oz_xch_bytes
+    double *part;            // [2 nblk][n_pad][2]
+    double *Mout, *Sout;
+    int *flag;               // device int: |y| >= 63.5 seen
+};
+cudaError_t sov_oz_init();
+int sov_oz_max_clusters(int nsm);
+int64_t sov_oz_ys_bytes(int64_t n, int clusters);
+int64_t sov_oz_xch_bytes(int clusters);
+int64_t sov_oz_partition(int64_t g_begin, int64_t g_end, int clusters, int64_t *cl);
+cudaError_t launch_sov_oz(const SovOzLaunch &L, cudaStream_t st);
 
 // NEXT-4: posterior conditioning helpers (kernels_post.cu)
 cudaError_t launch_add_diag(double *tiles, int64_t begin, int64_t end, double v, cudaStream_t st);

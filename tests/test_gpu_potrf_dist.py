@@ -165,7 +165,7 @@ def test_emulated_distributed_storage_matches_single_gpu(torch, n, nu, W):
     ~1/W: mvn_dtiles_bytes), generates its part of Sigma (mvn_dcov_matern), and updates from the
     broadcast buffers. The ranks' pieces, gathered (mvn_dgather), equal mvn_potrf bit for bit, and the
     per-rank storage sums to the full tile buffer."""
-    xy = np.random.default_rng(nu + n).uniform(size=(n, 2))
+    xy = np.random.default_rng(int(2 * nu) + n).uniform(size=(n, 2))
     beta = 0.1 if nu == 0.5 else 0.05
     d_xy = torch.from_numpy(xy).cuda()
     ref = mvn().mvn_cov_matern(d_xy, 1.0, beta, nu, 1e-8)
