@@ -493,6 +493,9 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: run the multi-GPU code path (NCCL process group, distributed Cholesky, "
                          "all_reduce combine, pinned-buffer e2e) even with one rank")
+    ap.add_argument("--sov-method", type=int, default=0, choices=[0, 1],
+                    help="crd: 0 = SOV GEMM on fp64 DMMA (default, the headline); 1 = on the int8 tensor cores "
+                         "(NEXT-4 mixed precision, Ozaki split, reading R24) - its own bench line")
     ap.add_argument("--shard", default="1,2,4,8", help="--workload shard: the world sizes W whose rank-0 share is timed")
     ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr", "shard"],
                     help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
@@ -553,9 +556,10 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
 
     mode = potrf_mode(args, world, args.force_dist)
+    step_ops = parallel.LibmvnCrdOpsInt8 if args.sov_method == 1 else parallel.LibmvnCrdOps
 
     def step(events=None):
-        logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events, potrf=mode)
+        logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events, potrf=mode, ops=step_ops)
         lp = logp.cpu().numpy()                          # a10 on the host: regions
         k, _ = mvn.mvn_confidence_region(lp, cfg.conf)
         return lp, k
@@ -608,7 +612,7 @@ def main():
     # host, H2D of sorted locations and limits, a2..a8, D2H of log P, a10). N > 1: the same steps
     # through parallel.crd_step on every rank from pinned host buffers, max over ranks.
     e2e = None
-    if not args.no_e2e and not multi:
+    if not args.no_e2e and not multi and args.sov_method == 0:
         ts = []
         for it in range(4):                      # one warm-up call (allocations), three timed
             t0 = time.perf_counter()
@@ -636,7 +640,7 @@ def main():
             h_a.numpy()[:] = a2
             d_xy.copy_(h_xy, non_blocking=True)
             d_a.copy_(h_a, non_blocking=True)
-            logp = parallel.crd_step(d_xy, d_a, L, cfg, potrf=mode)
+            logp = parallel.crd_step(d_xy, d_a, L, cfg, potrf=mode, ops=step_ops)
             h_lp.copy_(logp, non_blocking=True)
             torch.cuda.synchronize()
             k2, _ = mvn.mvn_confidence_region(h_lp.numpy(), cfg.conf)          # a10 (host)
@@ -654,11 +658,35 @@ def main():
     my_samples = my_end - my_begin
     sov_flops = float(n) * (n - 1) * my_samples       # algorithmic: sum_k 2(k-1) per sample (a6 + in-block dot)
     achieved = sov_flops / (sov_ms / 1e3) / 1e12
+    if args.sov_method == 1:
+        # int8 work of the emulated GEMM: 36 exact products over the off-diagonal row-block part,
+        # sum_{rb >= 1} 128 rows x 128 rb K per sample
+        nrb = -(-n // 128)
+        i8_ops = 2.0 * 36 * 128 * 128 * (nrb * (nrb - 1) / 2) * my_samples
+        sov_roof = {"kernel": "k_sov_oz (SOV GEMM as 36 exact int8 tcgen05 products per K-chunk, 2-CTA level split; "
+                              "fp64 Phi chain)", "bound": "tensor", "achieved": i8_ops / (sov_ms / 1e3) / 1e15,
+                    "peak": INT8_PEAK_POPS, "unit": "POP/s (int8)",
+                    "frac": i8_ops / (sov_ms / 1e3) / 1e15 / INT8_PEAK_POPS,
+                    "traffic": committed_traffic(cfg.name + "-int8", "k_sov_oz"),
+                    "fp64_equivalent_tflops": achieved, "fp64_equivalent_frac_of_dmma_peak": achieved / PEAK_FP64_TFLOPS,
+                    "peak_source": "int8 tcgen05 dense, measured 8,174 MAC/clk/SM at 1,965 MHz (tools/umma_i8_test.cu)",
+                    "algorithmic": f"2 x 36 x 128^2 x nrb(nrb-1)/2 int8 ops per sample x {my_samples} samples "
+                                   f"(= n(n-1) fp64-equivalent flops per sample)"}
+    else:
+        sov_roof = {"kernel": "k_sov (SOV DMMA GEMM + Phi chain)", "bound": "tensor", "achieved": achieved,
+                    "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
+                    "traffic": committed_traffic(cfg.name, "k_sov"),
+                    "peak_source": "measured fp64 DMMA peak (tools/calib_fp64.cu, profiles/r01_fp64_calibration.md); "
+                                   "MEASURED_PEAKS.json has no fp64 entry",
+                    "algorithmic": f"n(n-1) flops per sample x {my_samples} samples"}
     if mode == "dist":
         n_potrf = parallel.potrf_launches(n, world, rank)
     else:
         n_potrf = parallel.potrf_launches(n) if rank == 0 else 0
-    launches = (1 if (mode == "dist" or rank == 0) else 0) + n_potrf + 2 + 1 + (1 if multi else 0)
+    # cov + potrf + (check_limits, k_sov, k_reduce_blocks) + finalize [+ rescale]; int8: + rowscale,
+    # lslice, k_sov_oz (memset of the flag is a copy-engine op)
+    launches = (1 if (mode == "dist" or rank == 0) else 0) + n_potrf + 3 + 1 + (1 if multi else 0) + \
+        (2 if args.sov_method == 1 else 0)
     potrf_ms = stage_mean["potrf"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -674,12 +702,8 @@ def main():
         "region_time_ms": ms_per_step,
         "stage_ms": stage_mean,
         "stage_ms_per_rank": stage_per_rank,
-        "roofline": {"kernel": "k_sov (SOV DMMA GEMM + Phi chain)", "bound": "tensor", "achieved": achieved,
-                     "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
-                     "traffic": committed_traffic(cfg.name, "k_sov"),
-                     "peak_source": "measured fp64 DMMA peak (tools/calib_fp64.cu, profiles/r01_fp64_calibration.md); "
-                                    "MEASURED_PEAKS.json has no fp64 entry",
-                     "algorithmic": f"n(n-1) flops per sample x {my_samples} samples"},
+        "sov_method": "int8 tensor cores (NEXT-4, R24)" if args.sov_method == 1 else "fp64 DMMA",
+        "roofline": sov_roof,
         "potrf_roofline": {"achieved": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12, "peak": PEAK_FP64_TFLOPS,
                            "frac": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12 / PEAK_FP64_TFLOPS},
         "clocks": clk,

@@ -81,10 +81,12 @@ class LibmvnCrdOps:
     def potrf_dist(L, n, group):
         return potrf_distributed(L, n, group)
 
-    @staticmethod
-    def sov(L, n, d_a, cfg, begin, end):
-        from . import mvn_sov_prefix
-        return mvn_sov_prefix(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+    sov_method = 0           # 0: fp64 DMMA (default), 1: the GEMM on the int8 tensor cores (NEXT-4)
+
+    @classmethod
+    def sov(cls, L, n, d_a, cfg, begin, end):
+        from . import mvn_sov_prefix_ex
+        return mvn_sov_prefix_ex(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, begin, end, method=cls.sov_method)
 
     @staticmethod
     def rescale(Mg, M, S):
@@ -95,6 +97,10 @@ class LibmvnCrdOps:
     def finalize(M, S, NR):
         from . import mvn_prefix_finalize
         return mvn_prefix_finalize(M, S, NR)
+
+
+class LibmvnCrdOpsInt8(LibmvnCrdOps):
+    sov_method = 1
 
 
 def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg, group=None, events=None,
