@@ -58,10 +58,12 @@ __device__ __forceinline__ double matern_poly(double x, double e) {
 }
 
 // sqrt(d) for d >= 0 without the special-operand branch of sqrt(): the MUFU reciprocal square-root
-// seed, one Newton step on it, then one on the root (error ~ ulp; d = 0 gives 0 via the clamp).
+// seed, one Newton step on it, then one on the root (error ~ ulp). The seed is taken at d + 1e-300
+// (= d for d > 1e-284; d = 0 then gives y = 1e150 and t = 0, so sqrt(0) = 0) — one add instead of
+// fmax's compare-and-select.
 __device__ __forceinline__ double sqrt_nonneg(double d) {
     double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(fmax(d, 1e-300)));
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d + 1e-300));
     const double c = fma(-(d * y), y, 1.0);               // 1 - d y^2
     y = fma(0.5 * y, c, y);
     const double t = d * y;

@@ -108,4 +108,6 @@ def test_sov_int8_y_out_of_range(torch):
                                    method=INT8)
     lp = logp(M, S, 256)
     want = np.arange(1, n + 1) * log_ndtr(-30.0)
-    assert np.all(np.abs(lp - want) <= 1e-12 + 4e-15 * np.abs(want))
+    # s = 0 exactly (Sigma = I): what remains is the device log Phibar(30) against scipy's, a fixed
+    # relative bias (measured 4.2e-15) that adds up over the 200 identical rows
+    assert np.all(np.abs(lp - want) <= 1e-12 + 1e-14 * np.abs(want))
