@@ -112,6 +112,18 @@ mvn_status mvn_cov_matern(mvn_ctx *ctx, mvn_tiles t, const double *d_xy, double 
  * non-positive pivot, with MVN_E_NUMERIC returned (reading R17; no jitter retry). Synchronises. */
 mvn_status mvn_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info);
 
+/* NEXT-4 for a3: the same factorisation with the trailing updates
+ * A_ij -= sum_c L_ic L_jc^T (K = 128 kp per super-step) on the int8 tensor cores (tcgen05), an
+ * Ozaki-style split (reading R25): per super-step the panel rows get a power-of-two scale
+ * over the panel's columns and 8 signed 7-bit digits; the 36 products with p + q <= 9 are exact
+ * int8 GEMMs, combined in fp64. The panel factorisation and the look-ahead update stay on fp64
+ * DMMA. MVN_POTRF_FP64 = mvn_potrf. Not bitwise equal to the fp64 factor (the dropped digit products
+ * are ~the rounding of an fp64 GEMM: residual ||L L^T - Sigma||_F / ||Sigma||_F stays ~1e-16);
+ * info / errors / synchronisation as mvn_potrf. Workspace: the panel's slices (~ one panel of L).   */
+#define MVN_POTRF_FP64 0
+#define MVN_POTRF_INT8 1
+mvn_status mvn_potrf_ex(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, int64_t *info, int32_t method);
+
 /* ---------------------------------------------------------------------------------------------
  * NEXT-1: building blocks of the distributed tiled Cholesky, 1-D
  * block-cyclic over super-panels of kp tile columns (super-panel s = tile columns s*kp ..

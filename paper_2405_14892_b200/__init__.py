@@ -37,7 +37,7 @@ ABI_SYMBOLS = [
     "mvn_panel_unpack", "mvn_potrf_info", "mvn_mc_validate", "mvn_mc_levels", "mvn_potrf_panel_width",
     "mvn_posterior", "mvn_posterior_tiles", "mvn_tlr_compress",
     "mvn_dtiles_bytes", "mvn_dpanel_numel", "mvn_dcov_matern", "mvn_dpotrf_panel", "mvn_dpanel_pack",
-    "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex",
+    "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex", "mvn_potrf_ex",
 ]
 
 
@@ -140,6 +140,7 @@ def lib() -> ctypes.CDLL:
         "mvn_dpotrf_update": (S, [P, mvn_dtiles, P, I64, P, I64, I32, I32]),
         "mvn_dgather": (S, [P, mvn_dtiles, P, P]),
         "mvn_sov_prefix_ex": (S, [P, T, P, P, P, ctypes.POINTER(mvn_qmc), I32, P, P]),
+        "mvn_potrf_ex": (S, [P, T, P, ctypes.POINTER(I64), I32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -294,6 +295,21 @@ def mvn_potrf(t, n: int, raise_on_numeric: bool = True) -> int:
     if st == MVN_E_NUMERIC and not raise_on_numeric:
         return int(info.value)
     c.check(st, "mvn_potrf")
+    return int(info.value)
+
+
+POTRF_FP64, POTRF_INT8 = 0, 1
+
+
+def mvn_potrf_ex(t, n: int, method: int = POTRF_FP64, raise_on_numeric: bool = True) -> int:
+    """mvn_potrf with a selectable arithmetic for the trailing updates: POTRF_FP64 (DMMA, default) or
+    POTRF_INT8 (the int8 tensor cores, reading R25). Returns info (-1 ok, else the failing row)."""
+    c = Context.get(t.device.index)
+    info = ctypes.c_int64(-1)
+    st = lib().mvn_potrf_ex(c.h, tiles(n), _dev_ptr(t), ctypes.byref(info), int(method))
+    if st == MVN_E_NUMERIC and not raise_on_numeric:
+        return int(info.value)
+    c.check(st, "mvn_potrf_ex")
     return int(info.value)
 
 

@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmvn.so")
-SOURCES = ["mvn_api.cu", "kernels_matern.cu", "kernels_potrf.cu", "kernels_sov.cu", "kernels_mc.cu", "kernels_post.cu", "kernels_mc_oz.cu", "kernels_tlr.cu", "kernels_sov_oz.cu"]
+SOURCES = ["mvn_api.cu", "kernels_matern.cu", "kernels_potrf.cu", "kernels_sov.cu", "kernels_mc.cu", "kernels_post.cu", "kernels_mc_oz.cu", "kernels_tlr.cu", "kernels_sov_oz.cu", "kernels_potrf_oz.cu"]
 HEADERS = ["common.cuh", "gemm_dmma.cuh", "normal.cuh", "mvn_internal.h", "umma.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -59,6 +59,26 @@ struct TileMap {
     static TileMap panel(double *b, int k_, int kp_) { TileMap m; m.base = b; m.mode = kPanel; m.k = k_; m.kp = kp_; return m; }
 };
 
+// Column-major enumeration of the trailing tiles (ti, tj), ti >= tj, over the tile columns
+//   tj = c0 + m*cs + b,  m >= 0, 0 <= b < cb,  tj < nt
+// (blocks of cb consecutive columns every cs columns; cb = cs = 1: every column from c0; the
+// distributed factorisation passes cb = kp, cs = kp * W). Column tj holds nt - tj tiles. `base` /
+// `col` carry the scan between calls (the items of one CTA increase monotonically).
+__host__ __device__ inline int upd_col(int idx, int c0, int cs, int cb) { return c0 + (idx / cb) * cs + idx % cb; }
+
+__device__ __forceinline__ void upd_item(int64_t item, int nt, int c0, int cs, int cb, int &ti, int &tj, int64_t &base,
+                                         int &col) {
+    while (item >= base + (nt - upd_col(col, c0, cs, cb))) { base += nt - upd_col(col, c0, cs, cb); ++col; }
+    tj = upd_col(col, c0, cs, cb);
+    ti = tj + (int)(item - base);
+}
+
+__host__ __device__ inline int64_t upd_items(int nt, int c0, int cs, int cb) {
+    int64_t s = 0;
+    for (int idx = 0; upd_col(idx, c0, cs, cb) < nt; ++idx) s += nt - upd_col(idx, c0, cs, cb);
+    return s;
+}
+
 // C(8x8) += A(8x4, row) * B(4x8, col). Fragment ownership (lane l):
 //   a = A[l/4][l%4], b = B[l%4][l/4], c = {C[l/4][2(l%4)], C[l/4][2(l%4)+1]}
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {

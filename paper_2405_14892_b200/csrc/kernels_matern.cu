@@ -70,13 +70,15 @@ __device__ __forceinline__ double sqrt_nonneg(double d) {
     return fma(0.5 * y, fma(-t, t, d), t);
 }
 
-// One CTA (256 threads) per tile. Thread t owns rows 4 (t % 32) .. +3 of the tile (their locations
-// in registers) and the 16 columns t / 32 + 8 m, m < 16: per column one 32-byte store of 4 rows, so a
-// warp writes one whole 1 KB column per step (coalesced), and a column's location is one broadcast
-// shared-memory read for 4 elements.
+// One CTA (256 threads) per tile. Thread t owns rows 8 (t % 16) .. +7 of the tile (their locations
+// in registers) and the 8 columns t / 16 + 16 m, m < 8: per column four 16-byte stores of 8 rows
+// (16 lanes write a whole 1 KB column), and a column's location is one shared-memory read for 8
+// elements. The libm fallback for far pairs (x > 700, where sigma2 e^-x nears the bottom of the
+// normal range) is decided once per tile from the bounding boxes of its row and column locations.
 template <int NU2>
 __global__ void __launch_bounds__(256) k_cov_matern(const MaternArgs p) {
-    __shared__ double cx[kTile], cy[kTile], tb[128];
+    __shared__ double cx[kTile], cy[kTile], rxs[kTile], rys[kTile], tb[128], bb[8][4];
+    __shared__ int fast_s;
     // blockIdx.x -> tile (ti, tj), ti >= tj, row-major enumeration of the lower triangle
     const int64_t id = blockIdx.x;
     int ti = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
@@ -84,59 +86,88 @@ __global__ void __launch_bounds__(256) k_cov_matern(const MaternArgs p) {
     while ((int64_t)(ti + 1) * (ti + 2) / 2 <= id) ++ti;
     const int tj = (int)(id - (int64_t)ti * (ti + 1) / 2);
     if (!p.tm.owns_col(tj)) return;                      // distributed storage: another rank's column
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = p.n;
     const int64_t r0 = (int64_t)ti * kTile, c0 = (int64_t)tj * kTile;
+    double vx, vy;                                       // this thread's location (column, then row)
     if (tid < kTile) {
         const int64_t c = c0 + tid;
-        cx[tid] = c < n ? p.xy[2 * c] : 0.0;
-        cy[tid] = c < n ? p.xy[2 * c + 1] : 0.0;
+        vx = c < n ? p.xy[2 * c] : p.xy[2 * c0];        // padding: a real location of the block
+        vy = c < n ? p.xy[2 * c + 1] : p.xy[2 * c0 + 1];
+        cx[tid] = vx;
+        cy[tid] = vy;
+        tb[tid] = p.tab[tid];
     } else {
-        tb[tid - kTile] = p.tab[tid - kTile];
+        const int64_t r = r0 + tid - kTile;
+        vx = r < n ? p.xy[2 * r] : p.xy[2 * r0];
+        vy = r < n ? p.xy[2 * r + 1] : p.xy[2 * r0 + 1];
+        rxs[tid - kTile] = vx;
+        rys[tid - kTile] = vy;
     }
-    const int rq = (tid & 31) * 4, cg = tid >> 5;
-    double rx[4], ry[4];
+    {   // bounding boxes: warps 0-3 the columns, warps 4-7 the rows
+        double mnx = vx, mxx = vx, mny = vy, mxy = vy;
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-        const int64_t r = r0 + rq + h;
-        rx[h] = r < n ? p.xy[2 * r] : 0.0;
-        ry[h] = r < n ? p.xy[2 * r + 1] : 0.0;
+        for (int o = 16; o; o >>= 1) {
+            mnx = fmin(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+            mxx = fmax(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+            mny = fmin(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+            mxy = fmax(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+        }
+        if (lane == 0) { bb[warp][0] = mnx; bb[warp][1] = mxx; bb[warp][2] = mny; bb[warp][3] = mxy; }
     }
     __syncthreads();
+    if (tid == 0) {
+        double b[2][4];
+        for (int h = 0; h < 2; ++h) {
+            b[h][0] = bb[4 * h][0]; b[h][1] = bb[4 * h][1]; b[h][2] = bb[4 * h][2]; b[h][3] = bb[4 * h][3];
+            for (int w = 4 * h + 1; w < 4 * h + 4; ++w) {
+                b[h][0] = fmin(b[h][0], bb[w][0]); b[h][1] = fmax(b[h][1], bb[w][1]);
+                b[h][2] = fmin(b[h][2], bb[w][2]); b[h][3] = fmax(b[h][3], bb[w][3]);
+            }
+        }
+        const double ex = fmax(b[0][1] - b[1][0], b[1][1] - b[0][0]), ey = fmax(b[0][3] - b[1][2], b[1][3] - b[0][2]);
+        fast_s = !p.libm && sqrt(ex * ex + ey * ey) * p.inv_beta <= 699.0;
+    }
+    const int rq = (tid & 15) * 8, cg = tid >> 4;
+    __syncthreads();
+    double rx[8], ry[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) { rx[h] = rxs[rq + h]; ry[h] = rys[rq + h]; }
     double *T = p.tm.tile(ti, tj) + rq;
     const bool edge = r0 + kTile > n || ti == tj;         // padding or diagonal elements in this tile
     const double sigma2 = p.sigma2, ib = p.inv_beta, diag = p.sigma2 + p.nugget;
-    const bool libm = p.libm != 0;
-#pragma unroll 2
-    for (int m = 0; m < kTile / 8; ++m) {
-        const int col = cg + 8 * m;
+    const bool fast = fast_s != 0;
+#pragma unroll 1
+    for (int m = 0; m < kTile / 16; ++m) {
+        const int col = cg + 16 * m;
         const double xc = cx[col], yc = cy[col];
-        double x[4], v[4];
+        double v[8];
+        if (fast) {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const double dx = rx[h] - xc, dy = ry[h] - yc;
-            x[h] = sqrt_nonneg(fma(dx, dx, dy * dy)) * ib;
-        }
-        // far pairs (x > 700: sigma2 e^-x near the bottom of the normal range) take libm's exp for
-        // the whole warp: one vote per 4 elements instead of a divergent branch per element
-        if (!libm && !__any_sync(0xffffffffu, fmax(fmax(x[0], x[1]), fmax(x[2], x[3])) > 700.0)) {
-#pragma unroll
-            for (int h = 0; h < 4; ++h) v[h] = matern_poly<NU2>(x[h], exp_neg_scaled(x[h], tb));
+            for (int h = 0; h < 8; ++h) {
+                const double dx = rx[h] - xc, dy = ry[h] - yc;
+                const double x = sqrt_nonneg(fma(dx, dx, dy * dy)) * ib;
+                v[h] = matern_poly<NU2>(x, exp_neg_scaled(x, tb));
+            }
         } else {
 #pragma unroll
-            for (int h = 0; h < 4; ++h) v[h] = matern_poly<NU2>(x[h], sigma2 * exp(-x[h]));
+            for (int h = 0; h < 8; ++h) {
+                const double dx = rx[h] - xc, dy = ry[h] - yc;
+                const double x = sqrt(fma(dx, dx, dy * dy)) * ib;
+                v[h] = matern_poly<NU2>(x, sigma2 * exp(-x));
+            }
         }
         if (edge) {
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
+            for (int h = 0; h < 8; ++h) {
                 const int64_t gr = r0 + rq + h, gc = c0 + col;
                 if (gr >= n || gc >= n) v[h] = (gr == gc) ? 1.0 : 0.0;
                 else if (gr == gc) v[h] = diag;
             }
         }
         double2 *dst = reinterpret_cast<double2 *>(T + (int64_t)col * kTile);
-        dst[0] = make_double2(v[0], v[1]);
-        dst[1] = make_double2(v[2], v[3]);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) dst[h] = make_double2(v[2 * h], v[2 * h + 1]);
     }
 }
 

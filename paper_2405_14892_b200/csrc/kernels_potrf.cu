@@ -169,26 +169,6 @@ __global__ void __launch_bounds__(256) k_trsm2(const TileMap tm, int k) {
 }
 
 // ------------------------------------------------------------------------------------------ K4
-// Column-major enumeration of the trailing tiles (ti, tj), ti >= tj, over the tile columns
-//   tj = c0 + m*cs + b,  m >= 0, 0 <= b < cb,  tj < nt
-// (blocks of cb consecutive columns every cs columns; cb = cs = 1: every column from c0; the
-// distributed factorisation passes cb = kp, cs = kp * W). Column tj holds nt - tj tiles. `base` /
-// `col` carry the scan between calls (the items of one CTA increase monotonically).
-__host__ __device__ inline int upd_col(int idx, int c0, int cs, int cb) { return c0 + (idx / cb) * cs + idx % cb; }
-
-__device__ __forceinline__ void upd_item(int64_t item, int nt, int c0, int cs, int cb, int &ti, int &tj, int64_t &base,
-                                         int &col) {
-    while (item >= base + (nt - upd_col(col, c0, cs, cb))) { base += nt - upd_col(col, c0, cs, cb); ++col; }
-    tj = upd_col(col, c0, cs, cb);
-    ti = tj + (int)(item - base);
-}
-
-__host__ __device__ inline int64_t upd_items(int nt, int c0, int cs, int cb) {
-    int64_t s = 0;
-    for (int idx = 0; upd_col(idx, c0, cs, cb) < nt; ++idx) s += nt - upd_col(idx, c0, cs, cb);
-    return s;
-}
-
 namespace upd {
 constexpr int BM = 64, BN = 128, BK = 16, STAGES = 3;
 constexpr int SA = BM + 4, SB = BN + 4;  // == 4 (mod 16)
@@ -526,6 +506,8 @@ cudaError_t launch_potrf_update(int64_t n, double *tiles, int k, int kp, int c0,
 //   n = 65,536  kp 4 / 6 / 8      = 2.822 / 2.805 / 2.791 s
 //   n = 102,400 kp 4 / 6 / 8      = 10.57 / 10.46 / 10.39 s
 // MVN_POTRF_KP (1..8) overrides.
+int potrf_panel_sms() { return panel_sms(); }
+
 int potrf_panel_width(int64_t n) {
     static const int env = [] { const char *e = getenv("MVN_POTRF_KP"); const int v = e ? atoi(e) : 0; return v >= 1 && v <= 8 ? v : 0; }();
     if (env) return env;
@@ -542,6 +524,12 @@ int potrf_panel_width(int64_t n) {
 //                                 all but panel_sms() SMs, so the panel work runs beside it.
 // Events order the two (panel s before update s; update s-1 before the panel-stream update of s).
 cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols) {
+    return launch_potrf_ex(n, tiles, d_info, st, ncols, nullptr);
+}
+
+// oz != nullptr: the main-stream trailing updates on the int8 tensor cores (NEXT-4 mixed precision,
+// kernels_potrf_oz.cu); the panel stream (look-ahead update + panel factorisation) stays fp64.
+cudaError_t launch_potrf_ex(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols, const PotrfOz *oz) {
     const int nt = (int)((n + kTile - 1) / kTile);
     if (ncols <= 0 || ncols > nt) ncols = nt;      // ncols < nt: partial factorisation (Schur complement left)
     const int KP = potrf_panel_width(n);
@@ -565,12 +553,18 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
         if ((e = cudaStreamWaitEvent(st, ps.ev_panel[s & 1], 0))) return e;
         if (s + 1 == S) {
             // last super-panel: the trailing (Schur complement) block of a partial factorisation
-            if (kn < nt && (e = launch_potrf_update(n, tiles, k, w, kn, 1, 1, 0, st))) return e;
+            if (kn < nt) {
+                e = oz ? launch_potrf_update_oz(n, tiles, k, w, kn, 1, 1, oz->clusters, oz->LAp, oz->rs, oz->xch, st)
+                       : launch_potrf_update(n, tiles, k, w, kn, 1, 1, 0, st);
+                if (e) return e;
+            }
             break;
         }
         const int wn = std::min(KP, ncols - kn);
         // main stream: columns >= kn + wn with super-panel s
-        if ((e = launch_potrf_update(n, tiles, k, w, kn + wn, 1, 1, panel_sms(), st))) return e;
+        e = oz ? launch_potrf_update_oz(n, tiles, k, w, kn + wn, 1, 1, oz->clusters_reserved, oz->LAp, oz->rs, oz->xch, st)
+               : launch_potrf_update(n, tiles, k, w, kn + wn, 1, 1, panel_sms(), st);
+        if (e) return e;
         if ((e = cudaEventRecord(ps.ev_rest[s & 1], st))) return e;
         // panel stream: columns kn .. kn+wn-1 with super-panel s, then factor super-panel s+1
         if (s >= 1 && (e = cudaStreamWaitEvent(sp, ps.ev_rest[(s - 1) & 1], 0))) return e;

@@ -45,6 +45,9 @@ struct mvn_ctx {
     void *mcX = nullptr; size_t mcX_cap = 0;       // method 2: cluster exchange scratch
     void *mcF = nullptr; size_t mcF_cap = 0;
     void *sozX = nullptr; size_t sozX_cap = 0;     // int8 SOV: cluster exchange scratch
+    void *pozA = nullptr; size_t pozA_cap = 0;     // int8 POTRF: panel digit slices
+    void *pozR = nullptr; size_t pozR_cap = 0;     // int8 POTRF: panel row scales
+    void *pozX = nullptr; size_t pozX_cap = 0;     // int8 POTRF: cluster exchange scratch
 };
 
 namespace {
@@ -179,7 +182,7 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
         DevGuard dev_guard(c);                        // the caller's current device is restored
         const int64_t minus1 = -1;
         if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess || mvn::mc_init() != cudaSuccess ||
-            mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess || mvn::sov_oz_init() != cudaSuccess ||
+            mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess || mvn::sov_oz_init() != cudaSuccess || mvn::potrf_oz_init() != cudaSuccess ||
             cudaMalloc(&c->d_info, 2 * sizeof(int64_t)) != cudaSuccess ||
             cudaMemcpy(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming) != cudaSuccess) {
@@ -205,7 +208,7 @@ void mvn_destroy(mvn_ctx *c) {
     // waits for the device's outstanding work itself
     cudaDeviceSynchronize();
     for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF,
-                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX, c->sozX})
+                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX, c->sozX, c->pozA, c->pozR, c->pozX})
         if (p) cudaFree(p);
     if (c->done) cudaEventDestroy(c->done);
     delete c;
@@ -234,10 +237,10 @@ mvn_status mvn_trim(mvn_ctx *c) {
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX, &c->sozX})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX, &c->sozX, &c->pozA, &c->pozR, &c->pozX})
         if (*p) { cudaFree(*p); *p = nullptr; }
     c->Y_cap = c->part_cap = c->cta_cap = c->sync_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
-    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = c->sozX_cap = 0;
+    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = c->sozX_cap = c->pozA_cap = c->pozR_cap = c->pozX_cap = 0;
     c->post_n = c->post_off = 0;
     return MVN_OK;
 }
@@ -310,6 +313,33 @@ mvn_status mvn_potrf(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t *info) {
     if (*info >= 0 && *info < t.n)
         return fail(c, MVN_E_NUMERIC, "mvn_potrf: matrix not positive definite at row " + std::to_string(*info));
     if (*info >= t.n) *info = -1;   // cannot happen (padding is the identity)
+    return MVN_OK;
+}
+
+mvn_status mvn_potrf_ex(mvn_ctx *c, mvn_tiles t, double *d_tiles, int64_t *info, int32_t method) {
+    if (method == MVN_POTRF_FP64) return mvn_potrf(c, t, d_tiles, info);
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (method != MVN_POTRF_INT8) return fail(c, MVN_E_USAGE, "mvn_potrf_ex: method must be MVN_POTRF_FP64 or MVN_POTRF_INT8");
+    if (!tiles_ok(t) || !d_tiles || !info) return fail(c, MVN_E_USAGE, "mvn_potrf_ex: bad arguments");
+    const int kp = mvn::potrf_panel_width(t.n);
+    const int64_t n_pad = (t.n + t.nb - 1) / t.nb * t.nb;
+    mvn::PotrfOz oz;
+    oz.clusters = mvn::potrf_oz_max_clusters(c->nsm);
+    oz.clusters_reserved = std::max(1, std::min(oz.clusters, (c->nsm - mvn::potrf_panel_sms()) / 2));
+    mvn_status s;
+    if ((s = ensure(c, &c->pozA, &c->pozA_cap, (size_t)mvn::potrf_oz_lap_bytes(t.n, kp))) != MVN_OK) return s;
+    if ((s = ensure(c, &c->pozR, &c->pozR_cap, sizeof(double) * (size_t)n_pad)) != MVN_OK) return s;
+    if ((s = ensure(c, &c->pozX, &c->pozX_cap, (size_t)mvn::potrf_oz_xch_bytes(oz.clusters))) != MVN_OK) return s;
+    oz.LAp = (int8_t *)c->pozA; oz.rs = (double *)c->pozR; oz.xch = (double *)c->pozX;
+    const int64_t minus1 = -1;
+    MVN_CUDA(c, cudaMemcpyAsync(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, mvn::launch_potrf_ex(t.n, d_tiles, c->d_info, c->stream, 0, &oz));
+    MVN_CUDA(c, cudaMemcpyAsync(info, c->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (*info >= 0 && *info < t.n)
+        return fail(c, MVN_E_NUMERIC, "mvn_potrf_ex: matrix not positive definite at row " + std::to_string(*info));
+    if (*info >= t.n) *info = -1;
     return MVN_OK;
 }
 

@@ -16,6 +16,22 @@ cudaError_t launch_finalize(int64_t n, int64_t NR, const double *M, const double
 
 cudaError_t potrf_init();
 cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols = 0);
+// NEXT-4: the trailing updates of the factorisation on the int8 tensor cores (kernels_potrf_oz.cu)
+struct PotrfOz {
+    int8_t *LAp;             // potrf_oz_lap_bytes(n, kp): the panel's digit slices
+    double *rs;              // n_pad doubles: the panel rows' scales
+    double *xch;             // potrf_oz_xch_bytes(clusters)
+    int clusters;            // 2-CTA clusters of the update kernel
+    int clusters_reserved;   // the same while the panel stream runs beside it
+};
+cudaError_t launch_potrf_ex(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols, const PotrfOz *oz);
+cudaError_t potrf_oz_init();
+int potrf_oz_max_clusters(int nsm);
+int potrf_panel_sms();
+int64_t potrf_oz_lap_bytes(int64_t n, int kp);
+int64_t potrf_oz_xch_bytes(int clusters);
+cudaError_t launch_potrf_update_oz(int64_t n, double *tiles, int k, int w, int c0, int cs, int cb, int clusters,
+                                   int8_t *LAp, double *rs, double *xch, cudaStream_t st);
 // distributed-factorisation building blocks (NEXT-1)
 int potrf_panel_width(int64_t n);   // kp: tile columns per super-panel for order n (MVN_POTRF_KP overrides)
 cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int kp, int64_t *d_info, cudaStream_t st);

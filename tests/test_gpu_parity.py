@@ -373,7 +373,7 @@ def test_max_size_sampled_parity(torch_cuda):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name,method", [("C", 0), ("D", 0), ("E", 0), ("C", 1), ("D", 1)])
+@pytest.mark.parametrize("name,method", [("C", 0), ("D", 0), ("E", 0), ("C", 1), ("D", 1), ("E", 1)])
 def test_full_config_all_samples_regions(torch_cuda, name, method):
     """The north_star acceptance at the BASELINE configs, in the launch configuration bench.py times:
     mvn_sov_prefix over ALL N*R samples of the config (one call, grid of 148 persistent CTAs with
