@@ -496,6 +496,8 @@ def main():
     ap.add_argument("--sov-method", type=int, default=0, choices=[0, 1],
                     help="crd: 0 = SOV GEMM on fp64 DMMA (default, the headline); 1 = on the int8 tensor cores "
                          "(NEXT-4 mixed precision, Ozaki split, reading R24) - its own bench line")
+    ap.add_argument("--potrf-method", type=int, default=0, choices=[0, 1],
+                    help="crd: 0 = Cholesky updates on fp64 DMMA (default); 1 = on the int8 tensor cores (NEXT-4, R25)")
     ap.add_argument("--shard", default="1,2,4,8", help="--workload shard: the world sizes W whose rank-0 share is timed")
     ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr", "shard"],
                     help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
@@ -556,7 +558,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
 
     mode = potrf_mode(args, world, args.force_dist)
-    step_ops = parallel.LibmvnCrdOpsInt8 if args.sov_method == 1 else parallel.LibmvnCrdOps
+    step_ops = parallel.crd_ops(args.sov_method, args.potrf_method)
 
     def step(events=None):
         logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events, potrf=mode, ops=step_ops)
@@ -612,7 +614,7 @@ def main():
     # host, H2D of sorted locations and limits, a2..a8, D2H of log P, a10). N > 1: the same steps
     # through parallel.crd_step on every rank from pinned host buffers, max over ranks.
     e2e = None
-    if not args.no_e2e and not multi and args.sov_method == 0:
+    if not args.no_e2e and not multi and args.sov_method == 0 and args.potrf_method == 0:
         ts = []
         for it in range(4):                      # one warm-up call (allocations), three timed
             t0 = time.perf_counter()
@@ -694,7 +696,11 @@ def main():
         # the job (n, N*R of the config) is fixed and split over the GPUs (config D at 8 GPUs: one
         # lattice shift per rank, BASELINE.json): per-GPU work shrinks with N -> strong scaling
         "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None,
+        "dtype": "f64" if (args.sov_method, args.potrf_method) == (0, 0) else
+                 "f64 (" + " and ".join(x for x, on in [("SOV GEMM (R24)", args.sov_method), ("Cholesky updates (R25)",
+                                                        args.potrf_method)] if on) + " as exact int8 tensor-core products)",
+        "data": "synthetic",
         "config": config_dict(cfg, world, mode),
         "potrf_mode": mode,
         "cholesky_tflops": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12,
@@ -703,6 +709,7 @@ def main():
         "stage_ms": stage_mean,
         "stage_ms_per_rank": stage_per_rank,
         "sov_method": "int8 tensor cores (NEXT-4, R24)" if args.sov_method == 1 else "fp64 DMMA",
+        "potrf_method": "int8 tensor cores (NEXT-4, R25)" if args.potrf_method == 1 else "fp64 DMMA",
         "roofline": sov_roof,
         "potrf_roofline": {"achieved": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12, "peak": PEAK_FP64_TFLOPS,
                            "frac": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12 / PEAK_FP64_TFLOPS},

@@ -528,7 +528,18 @@ cudaError_t launch_potrf(int64_t n, double *tiles, int64_t *d_info, cudaStream_t
 }
 
 // oz != nullptr: the main-stream trailing updates on the int8 tensor cores (NEXT-4 mixed precision,
-// kernels_potrf_oz.cu); the panel stream (look-ahead update + panel factorisation) stays fp64.
+// kernels_potrf_oz.cu); the panel stream (look-ahead update + panel factorisation) stays fp64. An
+// int8 update pays only with wide super-panels (K = 128 kp: the per-tile TMEM drain and the per-step
+// slicing are fixed costs) and enough tiles to fill the clusters: below kp = 8 (n < 49,152) or
+// 4 tiles per cluster the update runs on fp64 DMMA (measured at C, kp = 1: 184 ms int8 vs 60 ms).
+// MVN_POTRF_OZ_ALWAYS=1 (read per call; tests) takes the int8 path for every trailing update.
+static bool use_oz(const PotrfOz *oz, int nt, int kp, int c0) {
+    if (!oz) return false;
+    const char *e = getenv("MVN_POTRF_OZ_ALWAYS");
+    if (e && e[0] == '1') return true;
+    return kp >= 8 && upd_items(nt, c0, 1, 1) >= 4ll * oz->clusters;
+}
+
 cudaError_t launch_potrf_ex(int64_t n, double *tiles, int64_t *d_info, cudaStream_t st, int ncols, const PotrfOz *oz) {
     const int nt = (int)((n + kTile - 1) / kTile);
     if (ncols <= 0 || ncols > nt) ncols = nt;      // ncols < nt: partial factorisation (Schur complement left)
@@ -554,7 +565,7 @@ cudaError_t launch_potrf_ex(int64_t n, double *tiles, int64_t *d_info, cudaStrea
         if (s + 1 == S) {
             // last super-panel: the trailing (Schur complement) block of a partial factorisation
             if (kn < nt) {
-                e = oz ? launch_potrf_update_oz(n, tiles, k, w, kn, 1, 1, oz->clusters, oz->LAp, oz->rs, oz->xch, st)
+                e = use_oz(oz, nt, KP, kn) ? launch_potrf_update_oz(n, tiles, k, w, kn, 1, 1, oz->clusters, oz->LAp, oz->rs, oz->xch, st)
                        : launch_potrf_update(n, tiles, k, w, kn, 1, 1, 0, st);
                 if (e) return e;
             }
@@ -562,7 +573,7 @@ cudaError_t launch_potrf_ex(int64_t n, double *tiles, int64_t *d_info, cudaStrea
         }
         const int wn = std::min(KP, ncols - kn);
         // main stream: columns >= kn + wn with super-panel s
-        e = oz ? launch_potrf_update_oz(n, tiles, k, w, kn + wn, 1, 1, oz->clusters_reserved, oz->LAp, oz->rs, oz->xch, st)
+        e = use_oz(oz, nt, KP, kn + wn) ? launch_potrf_update_oz(n, tiles, k, w, kn + wn, 1, 1, oz->clusters_reserved, oz->LAp, oz->rs, oz->xch, st)
                : launch_potrf_update(n, tiles, k, w, kn + wn, 1, 1, panel_sms(), st);
         if (e) return e;
         if ((e = cudaEventRecord(ps.ev_rest[s & 1], st))) return e;

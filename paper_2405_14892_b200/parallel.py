@@ -72,10 +72,12 @@ class LibmvnCrdOps:
         from . import mvn_cov_matern
         mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, out=L)
 
-    @staticmethod
-    def potrf(L, n):
-        from . import mvn_potrf
-        return mvn_potrf(L, n)
+    potrf_method = 0         # 0: fp64 DMMA (default), 1: the trailing updates on the int8 tensor cores
+
+    @classmethod
+    def potrf(cls, L, n):
+        from . import mvn_potrf_ex
+        return mvn_potrf_ex(L, n, cls.potrf_method)
 
     @staticmethod
     def potrf_dist(L, n, group):
@@ -99,8 +101,11 @@ class LibmvnCrdOps:
         return mvn_prefix_finalize(M, S, NR)
 
 
-class LibmvnCrdOpsInt8(LibmvnCrdOps):
-    sov_method = 1
+def crd_ops(sov_method: int = 0, potrf_method: int = 0):
+    """LibmvnCrdOps with the chosen arithmetic for the SOV GEMM and the Cholesky updates (NEXT-4)."""
+    if sov_method == 0 and potrf_method == 0:
+        return LibmvnCrdOps
+    return type("LibmvnCrdOpsMixed", (LibmvnCrdOps,), {"sov_method": sov_method, "potrf_method": potrf_method})
 
 
 def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg, group=None, events=None,

@@ -26,8 +26,15 @@ def mvn():
     return m
 
 
+@pytest.fixture
+def always_int8(monkeypatch):
+    """Every trailing update on the int8 path (by default only kp = 8 super-panels with >= 4 tiles
+    per cluster take it, i.e. n >= 49,152)."""
+    monkeypatch.setenv("MVN_POTRF_OZ_ALWAYS", "1")
+
+
 @pytest.mark.parametrize("n,nu", [(300, 0.5), (2000, 1.5), (5000, 0.5), (9000, 0.5), (13 * 128 + 5, 1.5)])
-def test_potrf_int8_vs_oracle(torch, n, nu):
+def test_potrf_int8_vs_oracle(torch, always_int8, n, nu):
     import test_gpu_parity as P
     xy = np.random.default_rng(100 + n).uniform(size=(n, 2))
     beta = 0.1 if nu == 0.5 else 0.05
@@ -46,7 +53,7 @@ def test_potrf_int8_vs_oracle(torch, n, nu):
     assert d <= max(1e-13, 50 * cond * 2.2e-16), d                  # vs the fp64 DMMA factor
 
 
-def test_potrf_int8_not_spd_reports_row(torch):
+def test_potrf_int8_not_spd_reports_row(torch, always_int8):
     n = 1200
     A = np.eye(n)
     A[777, 777] = -1.0
@@ -54,7 +61,7 @@ def test_potrf_int8_not_spd_reports_row(torch):
     assert mvn().mvn_potrf_ex(T, n, INT8, raise_on_numeric=False) == 777
 
 
-def test_pipeline_int8_factor_vs_oracle(torch):
+def test_pipeline_int8_factor_vs_oracle(torch, always_int8):
     """Config B geometry end to end with the int8 factor (independent mode: the oracle factors Sigma
     itself) and both SOV arithmetics: |dlog P| <= 1e-8, identical regions."""
     cfg = W.small_config("Bp8", 70, 2000, 4, base="B")
@@ -74,3 +81,24 @@ def test_pipeline_int8_factor_vs_oracle(torch):
         assert np.max(np.abs(lp - ref.logp)) <= 1e-8
         k, _ = mvn().mvn_confidence_region(lp, cfg.conf)
         assert np.array_equal(k, ref.k_star)
+
+
+@pytest.mark.slow
+def test_potrf_int8_default_threshold_large(torch):
+    """n = 51,277 (kp = 8: the default int8 regime): against the fp64 DMMA factor elementwise and the
+    residual on 2,000 sampled entries (L L^T)_ij vs the oracle's Matern Sigma_ij."""
+    import test_gpu_parity as P
+    n = 400 * 128 + 77
+    xy = np.random.default_rng(9).uniform(size=(n, 2))
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, 0.03, 0.5, 1e-8)
+    R = T.clone()
+    assert mvn().mvn_potrf_ex(T, n, INT8) == -1
+    assert mvn().mvn_potrf(R, n) == -1
+    assert float((T - R).abs().max()) <= 1e-12
+    rng = np.random.default_rng(5)
+    ii = np.sort(rng.integers(0, n, 2000))
+    jj = np.array([rng.integers(0, i + 1) for i in ii])
+    got = np.einsum("ij,ij->i", P.tile_rows(T, n, ii, n), P.tile_rows(T, n, jj, n))
+    h = np.sqrt(((xy[ii] - xy[jj]) ** 2).sum(1))
+    want = oracle.matern(h, 1.0, 0.03, 0.5) + np.where(ii == jj, 1e-8, 0.0)
+    assert np.max(np.abs(got - want)) <= 1e-12
