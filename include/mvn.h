@@ -184,7 +184,10 @@ mvn_status mvn_potrf_info(mvn_ctx *ctx, int64_t *info, int32_t reset);
 typedef struct {
     int64_t n, nb;          /* order, tile size (128) */
     int32_t world, rank;    /* ranks, this rank (0 <= rank < world) */
-    int32_t kp;             /* tile columns per super-panel */
+    int32_t kp;             /* tile columns (and rows) per block */
+    int32_t prows;          /* 0 or 1: 1-D (column blocks over all ranks); P > 1: 2-D block-cyclic over a
+                               P x (world / P) grid, rank = pr * (world / P) + pc: block (I, J) of kp x kp
+                               tiles is owned by (I mod P, J mod (world / P)) */
 } mvn_dtiles;
 
 /* Bytes of the rank's local storage (0 for invalid d). */
@@ -194,13 +197,22 @@ int64_t mvn_dpanel_numel(mvn_dtiles d, int64_t s);
 /* a2 on the owned tiles only (arguments as mvn_cov_matern; d_xy holds all n sorted locations). */
 mvn_status mvn_dcov_matern(mvn_ctx *ctx, mvn_dtiles d, const double *d_xy, double sigma2, double beta, double nu,
                            double nugget, double *d_local);
-/* Factor the owned super-panel s in place (as mvn_potrf_panel; MVN_E_USAGE unless s % world == rank). */
+/* Factor super-panel s in place, on the rank holding its diagonal block (MVN_E_USAGE otherwise):
+ * 1-D: the whole super-panel (as mvn_potrf_panel); 2-D: the diagonal block only (kp x kp tiles). */
 mvn_status mvn_dpotrf_panel(mvn_ctx *ctx, mvn_dtiles d, double *d_local, int64_t s);
-/* Owned super-panel s -> broadcast buffer d_panel (mvn_dpanel_numel(d, s) doubles). */
+/* 2-D, every rank of super-panel s's process column: after the factored diagonal block arrived in
+ * d_panel (its leading kp(kp+1)/2 tiles), solve this rank's rows of the super-panel below it:
+ * per column c: update by the columns before c, then L_ic = A_ic L_cc^{-T} (no-op for 1-D). */
+mvn_status mvn_dpanel_trsm(mvn_ctx *ctx, mvn_dtiles d, double *d_local, int64_t s, const double *d_panel);
+/* This rank's tiles of super-panel s -> their places in the buffer d_panel (mvn_dpanel_numel(d, s)
+ * doubles; other places untouched): 1-D the owner packs everything; 2-D each rank of the process
+ * column packs its rows (the diagonal block's rank first, for mvn_dpanel_trsm), and the pieces are
+ * combined over the ranks (all-gather / broadcasts, above the ABI). */
 mvn_status mvn_dpanel_pack(mvn_ctx *ctx, mvn_dtiles d, const double *d_local, int64_t s, double *d_panel);
 /* A_ij -= sum_{c in super-panel s} L_ic L_jc^T, operands read from super-panel s's buffer, for every
  * owned tile column j of the super-panels >= sp_first (just_one != 0: super-panel sp_first only,
- * which must then be owned) and every i >= j. Requires sp_first > s. sm_reserve as mvn_potrf_update. */
+ * which must then be owned) and every owned i >= j (2-D: this rank's row blocks). Requires
+ * sp_first > s. sm_reserve as mvn_potrf_update. */
 mvn_status mvn_dpotrf_update(mvn_ctx *ctx, mvn_dtiles d, double *d_local, int64_t s, const double *d_panel,
                              int64_t sp_first, int32_t just_one, int32_t sm_reserve);
 /* Copy the owned tiles into their places in a full tile-packed buffer (other tiles untouched). */

@@ -37,7 +37,7 @@ ABI_SYMBOLS = [
     "mvn_panel_unpack", "mvn_potrf_info", "mvn_mc_validate", "mvn_mc_levels", "mvn_potrf_panel_width",
     "mvn_posterior", "mvn_posterior_tiles", "mvn_tlr_compress",
     "mvn_dtiles_bytes", "mvn_dpanel_numel", "mvn_dcov_matern", "mvn_dpotrf_panel", "mvn_dpanel_pack",
-    "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex", "mvn_potrf_ex",
+    "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex", "mvn_potrf_ex", "mvn_dpanel_trsm",
 ]
 
 
@@ -53,7 +53,7 @@ class mvn_tiles(ctypes.Structure):
 
 class mvn_dtiles(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("nb", ctypes.c_int64), ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("kp", ctypes.c_int32)]
+                ("kp", ctypes.c_int32), ("prows", ctypes.c_int32)]
 
 
 class mvn_qmc(ctypes.Structure):
@@ -139,6 +139,7 @@ def lib() -> ctypes.CDLL:
         "mvn_dpanel_pack": (S, [P, mvn_dtiles, P, I64, P]),
         "mvn_dpotrf_update": (S, [P, mvn_dtiles, P, I64, P, I64, I32, I32]),
         "mvn_dgather": (S, [P, mvn_dtiles, P, P]),
+        "mvn_dpanel_trsm": (S, [P, mvn_dtiles, P, I64, P]),
         "mvn_sov_prefix_ex": (S, [P, T, P, P, P, ctypes.POINTER(mvn_qmc), I32, P, P]),
         "mvn_potrf_ex": (S, [P, T, P, ctypes.POINTER(I64), I32]),
     }
@@ -350,21 +351,23 @@ def mvn_panel_unpack(panel, n: int, k: int, kp: int, t, stream=None):
 
 
 # ---- NEXT-1 distributed storage: a rank's owned tile columns only (include/mvn.h, mvn_dtiles)
-def dtiles(n: int, world: int, rank: int, kp: int) -> mvn_dtiles:
-    return mvn_dtiles(int(n), TILE, int(world), int(rank), int(kp))
+def dtiles(n: int, world: int, rank: int, kp: int, prows: int = 1) -> mvn_dtiles:
+    """prows = 1: 1-D (column blocks over the ranks); prows = P > 1: 2-D over a P x (world / P) grid."""
+    return mvn_dtiles(int(n), TILE, int(world), int(rank), int(kp), int(prows))
 
 
-def mvn_dtiles_bytes(n: int, world: int, rank: int, kp: int) -> int:
-    return int(lib().mvn_dtiles_bytes(dtiles(n, world, rank, kp)))
+def mvn_dtiles_bytes(n: int, world: int, rank: int, kp: int, prows: int = 1) -> int:
+    return int(lib().mvn_dtiles_bytes(dtiles(n, world, rank, kp, prows)))
 
 
 def mvn_dpanel_numel(n: int, world: int, rank: int, kp: int, s: int) -> int:
     return int(lib().mvn_dpanel_numel(dtiles(n, world, rank, kp), int(s)))
 
 
-def alloc_dtiles(n: int, world: int, rank: int, kp: int, device=None):
+def alloc_dtiles(n: int, world: int, rank: int, kp: int, device=None, prows: int = 1):
     import torch
-    return torch.empty(max(mvn_dtiles_bytes(n, world, rank, kp) // 8, 1), dtype=torch.float64, device=device or "cuda")
+    return torch.empty(max(mvn_dtiles_bytes(n, world, rank, kp, prows) // 8, 1), dtype=torch.float64,
+                       device=device or "cuda")
 
 
 def mvn_dcov_matern(xy_sorted, d: mvn_dtiles, sigma2, beta, nu, nugget, local, stream=None):
@@ -377,6 +380,11 @@ def mvn_dcov_matern(xy_sorted, d: mvn_dtiles, sigma2, beta, nu, nugget, local, s
 def mvn_dpotrf_panel(local, d: mvn_dtiles, s: int, stream=None):
     c = Context.get(local.device.index, stream)
     c.check(lib().mvn_dpotrf_panel(c.h, d, _dev_ptr(local), int(s)), "mvn_dpotrf_panel")
+
+
+def mvn_dpanel_trsm(local, d: mvn_dtiles, s: int, panel, stream=None):
+    c = Context.get(local.device.index, stream)
+    c.check(lib().mvn_dpanel_trsm(c.h, d, _dev_ptr(local), int(s), _dev_ptr(panel)), "mvn_dpanel_trsm")
 
 
 def mvn_dpanel_pack(local, d: mvn_dtiles, s: int, panel, stream=None):

@@ -28,10 +28,14 @@ __host__ __device__ inline int64_t tile_offset(int64_t i, int64_t j) {
 //   kPanel: the tiles (i, k .. min(i, k + kp - 1)), i >= k, of the super-panel (k, kp), row after
 //           row (the broadcast buffer of the distributed factorisation).
 // In every mode the tiles (i, c .. c + m) of one super-panel row are consecutive in memory.
+//   2-D  : kDist with P > 1 process rows — the tile rows are distributed too (row block I = i / kp
+//           owned by process row I mod P): a rank (pr, g) holds the tiles (i, j) of its row blocks
+//           and column blocks, row after row (2-D block-cyclic over a P x W grid, NEXT-1).
 struct TileMap {
     enum : int { kFull = 0, kDist = 1, kPanel = 2 };
     double *base = nullptr;
     int mode = kFull, W = 1, g = 0, kp = 1, k = 0;
+    int P = 1, pr = 0;                                     // process rows (kDist 2-D)
 
     // owned columns in [0, x) (kDist)
     __host__ __device__ int64_t owned_below(int64_t x) const {
@@ -46,17 +50,53 @@ struct TileMap {
         const int64_t Hp = u <= 0 ? 0 : u <= K ? u * (u - 1) / 2 : K * (K - 1) / 2 + K * (u - K);
         return P * K * Q * (Q - 1) / 2 + Q * H + R * Q * K + Hp;
     }
+    // owned tiles in the tile rows < i of this rank's row blocks (kDist, 2-D): per owned row block B
+    // the rows x give owned_below(x + 1) tiles each, i.e. owned_rows_below((B+1) kp) - owned_rows_below(B kp)
+    __host__ __device__ int64_t owned_rows_below_2d(int64_t i) const {
+        const int64_t I = i / kp;
+        int64_t t = 0;
+        for (int64_t B = pr; B < I; B += P) t += owned_rows_below((B + 1) * kp) - owned_rows_below(B * kp);
+        if (I % P == pr) t += owned_rows_below(i) - owned_rows_below(I * kp);
+        return t;
+    }
     __host__ __device__ int64_t index(int64_t i, int64_t j) const {
         if (mode == kFull) return (i * (i + 1)) / 2 + j;
-        if (mode == kDist) return owned_rows_below(i) + owned_below(j);
+        if (mode == kDist) return (P == 1 ? owned_rows_below(i) : owned_rows_below_2d(i)) + owned_below(j);
         const int64_t m = i - k;
         return (m <= kp ? m * (m + 1) / 2 : (int64_t)kp * (kp + 1) / 2 + (m - kp) * kp) + (j - k);
     }
     __host__ __device__ double *tile(int64_t i, int64_t j) const { return base + index(i, j) * (int64_t)kTile * kTile; }
     __host__ __device__ bool owns_col(int64_t j) const { return mode != kDist || (j / kp) % W == g; }
+    __host__ __device__ bool owns_row(int64_t i) const { return mode != kDist || P == 1 || (i / kp) % P == pr; }
     static TileMap full(double *b) { TileMap m; m.base = b; return m; }
     static TileMap dist(double *b, int W_, int g_, int kp_) { TileMap m; m.base = b; m.mode = kDist; m.W = W_; m.g = g_; m.kp = kp_; return m; }
     static TileMap panel(double *b, int k_, int kp_) { TileMap m; m.base = b; m.mode = kPanel; m.k = k_; m.kp = kp_; return m; }
+    static TileMap dist2(double *b, int P_, int pr_, int Q_, int pc_, int kp_) {
+        TileMap m = dist(b, Q_, pc_, kp_);
+        m.P = P_; m.pr = pr_;
+        return m;
+    }
+};
+
+// Row selection of the update enumerations: the tile rows i >= lo whose row block i / kp is owned by
+// process row pr of P (P = 1, lo = 0: every row).
+struct RowSel {
+    int P = 1, pr = 0, kp = 1, lo = 0;
+    // selected rows in [0, x)
+    __host__ __device__ int64_t count(int64_t x) const {
+        if (x <= lo) return 0;
+        return raw(x) - raw(lo);
+    }
+    __host__ __device__ int64_t raw(int64_t x) const {
+        if (P == 1) return x;
+        const int64_t Pk = (int64_t)kp * P, r = x % Pk - (int64_t)pr * kp;
+        return (x / Pk) * kp + (r < 0 ? 0 : r > kp ? kp : r);
+    }
+    // the row of raw index idx (the idx-th owned row counted from row 0)
+    __host__ __device__ int64_t nth_raw(int64_t idx) const {
+        if (P == 1) return idx;
+        return (idx / kp) * (int64_t)kp * P + (int64_t)pr * kp + idx % kp;
+    }
 };
 
 // Column-major enumeration of the trailing tiles (ti, tj), ti >= tj, over the tile columns
@@ -76,6 +116,27 @@ __device__ __forceinline__ void upd_item(int64_t item, int nt, int c0, int cs, i
 __host__ __device__ inline int64_t upd_items(int nt, int c0, int cs, int cb) {
     int64_t s = 0;
     for (int idx = 0; upd_col(idx, c0, cs, cb) < nt; ++idx) s += nt - upd_col(idx, c0, cs, cb);
+    return s;
+}
+
+// The same with a row selection: column tj holds the selected rows i >= tj.
+__host__ __device__ inline int64_t upd_col_count(const RowSel &rs, int nt, int tj) {
+    const int64_t lo = rs.lo > tj ? rs.lo : tj;
+    return lo >= nt ? 0 : rs.raw(nt) - rs.raw(lo);
+}
+__device__ __forceinline__ void upd_item_sel(int64_t item, int nt, int c0, int cs, int cb, const RowSel &rs, int &ti,
+                                             int &tj, int64_t &base, int &col) {
+    while (item >= base + upd_col_count(rs, nt, upd_col(col, c0, cs, cb))) {
+        base += upd_col_count(rs, nt, upd_col(col, c0, cs, cb));
+        ++col;
+    }
+    tj = upd_col(col, c0, cs, cb);
+    const int64_t lo = rs.lo > tj ? rs.lo : tj;
+    ti = (int)rs.nth_raw(rs.raw(lo) + (item - base));
+}
+__host__ __device__ inline int64_t upd_items_sel(int nt, int c0, int cs, int cb, const RowSel &rs) {
+    int64_t s = 0;
+    for (int idx = 0; upd_col(idx, c0, cs, cb) < nt; ++idx) s += upd_col_count(rs, nt, upd_col(idx, c0, cs, cb));
     return s;
 }
 

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) k_cov_matern(const MaternArgs p) {
     while ((int64_t)ti * (ti + 1) / 2 > id) --ti;
     while ((int64_t)(ti + 1) * (ti + 2) / 2 <= id) ++ti;
     const int tj = (int)(id - (int64_t)ti * (ti + 1) / 2);
-    if (!p.tm.owns_col(tj)) return;                      // distributed storage: another rank's column
+    if (!p.tm.owns_col(tj) || !p.tm.owns_row(ti)) return;   // distributed storage: another rank's tile
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = p.n;
     const int64_t r0 = (int64_t)ti * kTile, c0 = (int64_t)tj * kTile;

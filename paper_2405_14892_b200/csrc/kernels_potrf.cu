@@ -133,14 +133,17 @@ __global__ void __launch_bounds__(256) k_potrf_diag2(const TileMap tm, int k, in
 }
 
 // K3 (blocked): L_ik = A_ik L_kk^{-T} for one 64-row half of panel tile i (grid: 2 CTAs per tile).
-__global__ void __launch_bounds__(256) k_trsm2(const TileMap tm, int k) {
+// The tiles are the selected rows i > k (rs: all rows, or a process row's row blocks from rs.lo on);
+// L_kk is read through `dg` (the same storage, or the 2-D factorisation's panel buffer).
+__global__ void __launch_bounds__(256) k_trsm2(const TileMap tm, const TileMap dg, int k, const RowSel rs) {
     using namespace blk;
     extern __shared__ double sh[];
     double *X = sh;                        // [128 cols][SPX]: rows h*64 .. h*64+63 of A_ik
     double *Lk = sh + kTile * SPX;         // [128 cols][SP]
-    const int i = k + 1 + (blockIdx.x >> 1), h = blockIdx.x & 1;
+    const int64_t lo = rs.lo > k + 1 ? rs.lo : k + 1;
+    const int i = (int)rs.nth_raw(rs.raw(lo) + (blockIdx.x >> 1)), h = blockIdx.x & 1;
     double *Ti = tm.tile(i, k) + h * 64;
-    const double *Lkk = tm.tile(k, k);
+    const double *Lkk = dg.tile(k, k);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < kTile * 32; e += 256) {           // 128 cols x 32 pieces
         const int col = e >> 5, seg = e & 31;
@@ -181,8 +184,8 @@ constexpr int SMEM = STAGES * BK * (SA + SB) * 8;
 // dst: where C lives; src: where the panel's tiles L_ik, L_jk are read (the same storage, or the
 // broadcast panel buffer of the distributed factorisation).
 template <bool MAPPED>   // as k_update2
-__global__ void __launch_bounds__(128, 2) k_update(const TileMap dst, const TileMap src, int k, int kp, int nt, int c0,
-                                                   int cs, int cb) {
+__global__ void __launch_bounds__(128, 2) k_update(const TileMap dst, const TileMap src, const TileMap srcB, int k, int kp,
+                                                   int nt, int c0, int cs, int cb, const RowSel rs) {
     using namespace upd;
     extern __shared__ double sm[];
     double *As = sm;
@@ -193,9 +196,10 @@ __global__ void __launch_bounds__(128, 2) k_update(const TileMap dst, const Tile
     // the panel is the kp tile columns k .. k+kp-1 (K = 128 kp; tiles (ti, k..k+kp-1) are contiguous).
     int ti, tj, col = 0;
     int64_t base = 0;
-    upd_item(id, nt, c0, cs, cb, ti, tj, base, col);
+    if (MAPPED) upd_item_sel(id, nt, c0, cs, cb, rs, ti, tj, base, col);
+    else upd_item(id, nt, c0, cs, cb, ti, tj, base, col);
     const double *__restrict__ Lik = (MAPPED ? src.tile(ti, k) : src.base + tile_offset(ti, k)) + h * BM;   // column stride 128
-    const double *__restrict__ Ljk = MAPPED ? src.tile(tj, k) : src.base + tile_offset(tj, k);
+    const double *__restrict__ Ljk = MAPPED ? srcB.tile(tj, k) : src.base + tile_offset(tj, k);
     double *C = (MAPPED ? dst.tile(ti, tj) : dst.base + tile_offset(ti, tj)) + h * BM;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -290,8 +294,9 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // MAPPED = false: the full lower tile-packed buffer (dst.base == src.base, tile_offset addressing —
 // mvn_potrf's hot loop, register-lean); true: explicit TileMaps (NEXT-1 distributed storage).
 template <bool MAPPED>
-__global__ void __launch_bounds__(upd2::NT, 1) k_update2(const TileMap dst, const TileMap src, int k, int kp, int nt,
-                                                        int c0, int cs, int cb, int64_t nitems) {
+__global__ void __launch_bounds__(upd2::NT, 1) k_update2(const TileMap dst, const TileMap src, const TileMap srcB, int k,
+                                                        int kp, int nt, int c0, int cs, int cb, int64_t nitems,
+                                                        const RowSel rs) {
     using namespace upd2;
     extern __shared__ double sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
@@ -313,10 +318,11 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(const TileMap dst, cons
         const int lane = tid & 31;
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
             int ti, tj;
-            upd_item(item, nt, c0, cs, cb, ti, tj, base, col);
+            if (MAPPED) upd_item_sel(item, nt, c0, cs, cb, rs, ti, tj, base, col);
+            else upd_item(item, nt, c0, cs, cb, ti, tj, base, col);
             // kp consecutive tiles (a super-panel row is contiguous in every TileMap)
             const double *Lik = MAPPED ? src.tile(ti, k) : src.base + tile_offset(ti, k);
-            const double *Ljk = MAPPED ? src.tile(tj, k) : src.base + tile_offset(tj, k);
+            const double *Ljk = MAPPED ? srcB.tile(tj, k) : src.base + tile_offset(tj, k);
             for (int c = 0; c < kp * CHUNKS; ++c, ++q) {
                 const int st = q % STAGES;
                 mbar_wait(&empty[st], ((q / STAGES) & 1) ^ 1);
@@ -345,7 +351,8 @@ __global__ void __launch_bounds__(upd2::NT, 1) k_update2(const TileMap dst, cons
     double *stg = sm + OFF_STG + warp * 16 * kTile;   // column-major [16][128]
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         int ti, tj;
-        upd_item(item, nt, c0, cs, cb, ti, tj, base, col);
+        if (MAPPED) upd_item_sel(item, nt, c0, cs, cb, rs, ti, tj, base, col);
+        else upd_item(item, nt, c0, cs, cb, ti, tj, base, col);
         double acc[16][2][2];
 #pragma unroll
         for (int a = 0; a < 16; ++a)
@@ -446,23 +453,48 @@ cudaError_t potrf_streams(PotrfStreams &ps) {
 // ---- building blocks shared by mvn_potrf and the distributed factorisation (identical arithmetic)
 // Factor the kp tile columns k .. k+kp-1 (all updates from columns < k applied): POTRF + TRSM of
 // column k; for each further column k+j: update it with columns k .. k+j-1 (K = 128 j), POTRF, TRSM.
-cudaError_t launch_potrf_panel_map(int64_t n, const TileMap &tm, int k, int kp, int64_t *d_info, cudaStream_t st) {
+// row_end < nt: only the rows < row_end (the 2-D factorisation's diagonal block).
+cudaError_t launch_potrf_panel_map(int64_t n, const TileMap &tm, int k, int kp, int64_t *d_info, cudaStream_t st,
+                                   int row_end) {
     const int nt = (int)((n + kTile - 1) / kTile);
+    const int ne = (row_end <= 0 || row_end > nt) ? nt : row_end;
     kp = std::min(kp, nt - k);
     const size_t sm_diag = kTile * blk::SP * 8, sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
+    const RowSel all;
     for (int j = 0; j < kp; ++j) {
         const int c = k + j;
         if (j > 0) {
-            if (tm.mode == TileMap::kFull) k_update<false><<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tm, tm, k, j, nt, c, nt, 1);
-            else k_update<true><<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tm, tm, k, j, nt, c, nt, 1);
+            if (tm.mode == TileMap::kFull && ne == nt)
+                k_update<false><<<(unsigned)(2 * (nt - c)), 128, upd::SMEM, st>>>(tm, tm, tm, k, j, nt, c, nt, 1, all);
+            else k_update<true><<<(unsigned)(2 * (ne - c)), 128, upd::SMEM, st>>>(tm, tm, tm, k, j, ne, c, ne, 1, all);
         }
         k_potrf_diag2<<<1, 256, sm_diag, st>>>(tm, c, d_info);
-        if (nt - c - 1 > 0) k_trsm2<<<2 * (nt - c - 1), 256, sm_trsm, st>>>(tm, c);
+        if (ne - c - 1 > 0) k_trsm2<<<2 * (ne - c - 1), 256, sm_trsm, st>>>(tm, tm, c, all);
+    }
+    return cudaGetLastError();
+}
+
+// 2-D factorisation, the process column of super-panel (k, w): the selected (owned) rows >= k + w of
+// the local storage `tm` solved against the factored diagonal block read from the panel buffer `pb`:
+// per column c = k + j: update by the columns k .. c-1 (L_i from tm, L_c from pb), then TRSM with L_cc.
+cudaError_t launch_panel_trsm_map(int64_t n, const TileMap &tm, const TileMap &pb, int k, int w, const RowSel &rs,
+                                  cudaStream_t st) {
+    const int nt = (int)((n + kTile - 1) / kTile);
+    w = std::min(w, nt - k);
+    RowSel sel = rs;
+    sel.lo = k + w;
+    const int64_t rows = sel.count(nt);
+    if (rows <= 0) return cudaSuccess;
+    const size_t sm_trsm = kTile * (blk::SP + blk::SPX) * 8;
+    for (int j = 0; j < w; ++j) {
+        const int c = k + j;
+        if (j > 0) k_update<true><<<(unsigned)(2 * rows), 128, upd::SMEM, st>>>(tm, tm, pb, k, j, nt, c, nt, 1, sel);
+        k_trsm2<<<(unsigned)(2 * rows), 256, sm_trsm, st>>>(tm, pb, c, sel);
     }
     return cudaGetLastError();
 }
 cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int kp, int64_t *d_info, cudaStream_t st) {
-    return launch_potrf_panel_map(n, TileMap::full(tiles), k, kp, d_info, st);
+    return launch_potrf_panel_map(n, TileMap::full(tiles), k, kp, d_info, st, 0);
 }
 
 // A_ij -= sum_{c=k}^{k+kp-1} L_ic L_jc^T for the tile columns j = c0 + m cs + b (0 <= b < cb) and
@@ -470,22 +502,31 @@ cudaError_t launch_potrf_panel(int64_t n, double *tiles, int k, int kp, int64_t 
 // two CTAs per tile.
 cudaError_t launch_potrf_update_map(int64_t n, const TileMap &dst, const TileMap &src, int k, int kp, int c0, int cs,
                                     int cb, int sm_reserve, cudaStream_t st) {
+    return launch_potrf_update_map(n, dst, src, src, k, kp, c0, cs, cb, sm_reserve, RowSel(), st);
+}
+
+// dst: the updated storage; srcA / srcB: where L_ik / L_jk are read; rs: the rows of dst updated.
+cudaError_t launch_potrf_update_map(int64_t n, const TileMap &dst, const TileMap &src, const TileMap &srcB, int k, int kp,
+                                    int c0, int cs, int cb, int sm_reserve, const RowSel &rs, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
     if (c0 >= nt) return cudaSuccess;
     kp = std::min(kp, nt - k);
-    const int64_t items = upd_items(nt, c0, cs, cb);
+    const bool sel = rs.P != 1 || rs.lo > 0;
+    const int64_t items = sel ? upd_items_sel(nt, c0, cs, cb, rs) : upd_items(nt, c0, cs, cb);
+    if (items == 0) return cudaSuccess;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     static const bool use_persistent = [] { const char *e = getenv("MVN_POTRF_PERSISTENT"); return !(e && e[0] == '0'); }();
     const int avail = std::max(1, nsm - sm_reserve);
-    const bool mapped = dst.mode != TileMap::kFull || src.mode != TileMap::kFull || dst.base != src.base;
+    const bool mapped = dst.mode != TileMap::kFull || src.mode != TileMap::kFull || dst.base != src.base ||
+                        srcB.mode != TileMap::kFull || srcB.base != src.base || sel;
     if (use_persistent && items >= 2 * avail) {
-        if (mapped) k_update2<true><<<avail, upd2::NT, upd2::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb, items);
-        else k_update2<false><<<avail, upd2::NT, upd2::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb, items);
+        if (mapped) k_update2<true><<<avail, upd2::NT, upd2::SMEM, st>>>(dst, src, srcB, k, kp, nt, c0, cs, cb, items, rs);
+        else k_update2<false><<<avail, upd2::NT, upd2::SMEM, st>>>(dst, src, srcB, k, kp, nt, c0, cs, cb, items, rs);
     } else {
-        if (mapped) k_update<true><<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb);
-        else k_update<false><<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(dst, src, k, kp, nt, c0, cs, cb);
+        if (mapped) k_update<true><<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(dst, src, srcB, k, kp, nt, c0, cs, cb, rs);
+        else k_update<false><<<(unsigned)(2 * items), 128, upd::SMEM, st>>>(dst, src, srcB, k, kp, nt, c0, cs, cb, rs);
     }
     return cudaGetLastError();
 }
@@ -602,6 +643,7 @@ __global__ void __launch_bounds__(256) k_panel_copy(const TileMap from, const Ti
     int idx = blockIdx.y, c = k;
     while (idx >= nt - c) { idx -= nt - c; ++c; }
     const int i = c + idx;
+    if (!from.owns_row(i) || !to.owns_row(i)) return;     // 2-D storage: another process row's tile
     const double2 *f = reinterpret_cast<const double2 *>(from.tile(i, c));
     double2 *t = reinterpret_cast<double2 *>(to.tile(i, c));
     constexpr int PER = kTile * kTile / 2 / 8;             // double2 per CTA

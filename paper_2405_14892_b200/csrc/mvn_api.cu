@@ -388,14 +388,28 @@ mvn_status mvn_panel_unpack(mvn_ctx *c, mvn_tiles t, const double *d_panel, int6
     return MVN_OK;
 }
 
-// ---- NEXT-1 distributed storage: a rank holds only the tile columns it owns (TileMap::kDist)
+// ---- NEXT-1 distributed storage: a rank holds only the tiles it owns (TileMap::kDist), 1-D (tile
+// columns over all ranks) or 2-D (row blocks over prows process rows x column blocks over the rest)
 namespace {
+int dP(const mvn_dtiles &d) { return d.prows > 1 ? d.prows : 1; }
+int dQ(const mvn_dtiles &d) { return d.world / dP(d); }
+int dpr(const mvn_dtiles &d) { return d.rank / dQ(d); }
+int dpc(const mvn_dtiles &d) { return d.rank % dQ(d); }
 bool dtiles_ok(const mvn_dtiles &d) {
-    return d.n >= 1 && d.nb == mvn::kTile && d.world >= 1 && d.rank >= 0 && d.rank < d.world && d.kp >= 1 && d.kp <= 8;
+    return d.n >= 1 && d.nb == mvn::kTile && d.world >= 1 && d.rank >= 0 && d.rank < d.world && d.kp >= 1 && d.kp <= 8 &&
+           d.prows >= 0 && d.world % dP(d) == 0;
 }
 int64_t dtiles_nt(const mvn_dtiles &d) { return (d.n + d.nb - 1) / d.nb; }
 int64_t dtiles_S(const mvn_dtiles &d) { return (dtiles_nt(d) + d.kp - 1) / d.kp; }
-mvn::TileMap dmap(const mvn_dtiles &d, double *local) { return mvn::TileMap::dist(local, d.world, d.rank, d.kp); }
+mvn::TileMap dmap(const mvn_dtiles &d, double *local) {
+    if (dP(d) == 1) return mvn::TileMap::dist(local, d.world, d.rank, d.kp);
+    return mvn::TileMap::dist2(local, dP(d), dpr(d), dQ(d), dpc(d), d.kp);
+}
+mvn::RowSel drows(const mvn_dtiles &d) {
+    mvn::RowSel r;
+    r.P = dP(d); r.pr = dpr(d); r.kp = d.kp;
+    return r;
+}
 mvn::TileMap pmap(const mvn_dtiles &d, const double *panel, int64_t s) {
     const int64_t nt = dtiles_nt(d), k = s * d.kp;
     return mvn::TileMap::panel(const_cast<double *>(panel), (int)k, (int)std::min<int64_t>(d.kp, nt - k));
@@ -404,7 +418,7 @@ mvn::TileMap pmap(const mvn_dtiles &d, const double *panel, int64_t s) {
 
 size_t mvn_dtiles_bytes(mvn_dtiles d) {
     if (!dtiles_ok(d)) return 0;
-    return (size_t)dmap(d, nullptr).owned_rows_below(dtiles_nt(d)) * (size_t)(d.nb * d.nb) * sizeof(double);
+    return (size_t)dmap(d, nullptr).index(dtiles_nt(d), 0) * (size_t)(d.nb * d.nb) * sizeof(double);
 }
 
 int64_t mvn_dpanel_numel(mvn_dtiles d, int64_t s) {
@@ -428,17 +442,31 @@ mvn_status mvn_dcov_matern(mvn_ctx *c, mvn_dtiles d, const double *d_xy, double 
 mvn_status mvn_dpotrf_panel(mvn_ctx *c, mvn_dtiles d, double *d_local, int64_t s) {
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
-    if (!dtiles_ok(d) || !d_local || s < 0 || s >= dtiles_S(d) || s % d.world != d.rank)
-        return fail(c, MVN_E_USAGE, "mvn_dpotrf_panel: bad arguments (super-panel s must be this rank's)");
-    MVN_CUDA(c, mvn::launch_potrf_panel_map(d.n, dmap(d, d_local), (int)(s * d.kp), d.kp, c->d_info, c->stream));
+    if (!dtiles_ok(d) || !d_local || s < 0 || s >= dtiles_S(d) || s % dQ(d) != dpc(d) || s % dP(d) != dpr(d))
+        return fail(c, MVN_E_USAGE, "mvn_dpotrf_panel: bad arguments (super-panel s's diagonal block must be this rank's)");
+    const int64_t k = s * d.kp;
+    // 1-D: the whole super-panel; 2-D: its diagonal block only (the rows below: mvn_dpanel_trsm)
+    const int row_end = dP(d) == 1 ? 0 : (int)std::min<int64_t>(k + d.kp, dtiles_nt(d));
+    MVN_CUDA(c, mvn::launch_potrf_panel_map(d.n, dmap(d, d_local), (int)k, d.kp, c->d_info, c->stream, row_end));
+    return MVN_OK;
+}
+
+mvn_status mvn_dpanel_trsm(mvn_ctx *c, mvn_dtiles d, double *d_local, int64_t s, const double *d_panel) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!dtiles_ok(d) || !d_local || !d_panel || s < 0 || s >= dtiles_S(d) || s % dQ(d) != dpc(d))
+        return fail(c, MVN_E_USAGE, "mvn_dpanel_trsm: bad arguments (super-panel s must be in this rank's process column)");
+    if (dP(d) == 1) return MVN_OK;                                                  // 1-D: done by mvn_dpotrf_panel
+    MVN_CUDA(c, mvn::launch_panel_trsm_map(d.n, dmap(d, d_local), pmap(d, d_panel, s), (int)(s * d.kp), d.kp, drows(d),
+                                           c->stream));
     return MVN_OK;
 }
 
 mvn_status mvn_dpanel_pack(mvn_ctx *c, mvn_dtiles d, const double *d_local, int64_t s, double *d_panel) {
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
-    if (!dtiles_ok(d) || !d_local || !d_panel || s < 0 || s >= dtiles_S(d) || s % d.world != d.rank)
-        return fail(c, MVN_E_USAGE, "mvn_dpanel_pack: bad arguments (super-panel s must be this rank's)");
+    if (!dtiles_ok(d) || !d_local || !d_panel || s < 0 || s >= dtiles_S(d) || s % dQ(d) != dpc(d))
+        return fail(c, MVN_E_USAGE, "mvn_dpanel_pack: bad arguments (super-panel s must be in this rank's process column)");
     MVN_CUDA(c, mvn::launch_panel_copy_map(d.n, dmap(d, const_cast<double *>(d_local)), pmap(d, d_panel, s),
                                            (int)(s * d.kp), d.kp, c->stream));
     return MVN_OK;
@@ -451,13 +479,15 @@ mvn_status mvn_dpotrf_update(mvn_ctx *c, mvn_dtiles d, double *d_local, int64_t 
     const int64_t S = dtiles_S(d);
     if (!dtiles_ok(d) || !d_local || !d_panel || s < 0 || s >= S || sp_first <= s || sm_reserve < 0 || sm_reserve >= c->nsm)
         return fail(c, MVN_E_USAGE, "mvn_dpotrf_update: bad arguments (need 0 <= s < sp_first)");
-    // the first owned super-panel >= sp_first
-    const int64_t sp0 = sp_first + ((d.rank - sp_first % d.world) % d.world + d.world) % d.world;
+    // the first super-panel >= sp_first in this rank's process column
+    const int Q = dQ(d), pc = dpc(d);
+    const int64_t sp0 = sp_first + ((pc - sp_first % Q) % Q + Q) % Q;
     if (sp0 >= S || (just_one && sp0 != sp_first)) return MVN_OK;                 // nothing owned there
     const int64_t nt = dtiles_nt(d);
-    const int c0 = (int)(sp0 * d.kp), cs = just_one ? (int)nt : d.kp * d.world;
-    MVN_CUDA(c, mvn::launch_potrf_update_map(d.n, dmap(d, d_local), pmap(d, d_panel, s), (int)(s * d.kp),
-                                             d.kp, c0, cs, d.kp, sm_reserve, c->stream));
+    const int c0 = (int)(sp0 * d.kp), cs = just_one ? (int)nt : d.kp * Q;
+    const mvn::TileMap pm = pmap(d, d_panel, s);
+    MVN_CUDA(c, mvn::launch_potrf_update_map(d.n, dmap(d, d_local), pm, pm, (int)(s * d.kp), d.kp, c0, cs, d.kp,
+                                             sm_reserve, drows(d), c->stream));
     return MVN_OK;
 }
 
@@ -466,7 +496,7 @@ mvn_status mvn_dgather(mvn_ctx *c, mvn_dtiles d, const double *d_local, double *
     if (!c) return MVN_E_USAGE;
     if (!dtiles_ok(d) || !d_local || !d_tiles) return fail(c, MVN_E_USAGE, "mvn_dgather: bad arguments");
     const mvn::TileMap from = dmap(d, const_cast<double *>(d_local)), to = mvn::TileMap::full(d_tiles);
-    for (int64_t s = d.rank; s < dtiles_S(d); s += d.world)
+    for (int64_t s = dpc(d); s < dtiles_S(d); s += dQ(d))
         MVN_CUDA(c, mvn::launch_panel_copy_map(d.n, from, to, (int)(s * d.kp), d.kp, c->stream));
     return MVN_OK;
 }

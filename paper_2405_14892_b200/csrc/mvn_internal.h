@@ -41,9 +41,15 @@ cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, int kp, double *p
 // the same on explicit storages (TileMap, common.cuh): a rank's owned columns (NEXT-1 distributed
 // storage), the full buffer, or a super-panel broadcast buffer
 struct TileMap;
-cudaError_t launch_potrf_panel_map(int64_t n, const TileMap &tm, int k, int kp, int64_t *d_info, cudaStream_t st);
+struct RowSel;
+cudaError_t launch_potrf_panel_map(int64_t n, const TileMap &tm, int k, int kp, int64_t *d_info, cudaStream_t st,
+                                   int row_end);
 cudaError_t launch_potrf_update_map(int64_t n, const TileMap &dst, const TileMap &src, int k, int kp, int c0, int cs,
                                     int cb, int sm_reserve, cudaStream_t st);
+cudaError_t launch_potrf_update_map(int64_t n, const TileMap &dst, const TileMap &src, const TileMap &srcB, int k, int kp,
+                                    int c0, int cs, int cb, int sm_reserve, const RowSel &rs, cudaStream_t st);
+cudaError_t launch_panel_trsm_map(int64_t n, const TileMap &tm, const TileMap &pb, int k, int w, const RowSel &rs,
+                                  cudaStream_t st);
 cudaError_t launch_panel_copy_map(int64_t n, const TileMap &from, const TileMap &to, int k, int kp, cudaStream_t st);
 cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
                                   const TileMap &tm, cudaStream_t st);

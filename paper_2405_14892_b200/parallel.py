@@ -354,13 +354,15 @@ class CudaPotrfDistOps(CudaPotrfOps):
     def unpack(self, sp, on):
         pass                                     # updates read the broadcast buffer directly
 
-    def update(self, sp, c0, cs, cb, on, side_busy=True):
+    def update(self, sp, c0, cs, cb, on, side_busy=True, just_one=None):
         from . import mvn_dpotrf_update
         if c0 < self.nt:
             reserve = self.SIDE_SMS if (on == "main" and side_busy) else 0
-            # the schedule's two forms: the lookahead (one super-panel, cs = nt) or every owned
-            # super-panel from c0 on (cs = kp * W)
-            mvn_dpotrf_update(self.L, self.d, sp, self.panel_buf(sp), c0 // self.kp, just_one=cs >= self.nt,
+            # the 1-D schedule's two forms: the lookahead (one super-panel, cs = nt) or every owned
+            # super-panel from c0 on (cs = kp * W, c0 owned); the 2-D schedule says which explicitly
+            if just_one is None:
+                just_one = cs >= self.nt
+            mvn_dpotrf_update(self.L, self.d, sp, self.panel_buf(sp), c0 // self.kp, just_one=just_one,
                               sm_reserve=reserve, stream=self._st(on))
 
 
@@ -373,6 +375,108 @@ def potrf_distributed_local(local, n: int, group=None, kp: int | None = None) ->
     rank = dist.get_rank(group) if initialized else 0
     _cuda_info(local)
     return potrf_distributed(local, n, group, ops=CudaPotrfDistOps(local, n, world, rank, kp=kp))
+
+
+# ------------------------------------------------------------------------------------- NEXT-1, 2-D
+def potrf_2d_schedule(ops, pr: int, pc: int, P: int, Q: int):
+    """The per-rank step loop of the 2-D block-cyclic right-looking Cholesky on distributed storage
+    (block (I, J) of kp x kp tiles owned by rank (I mod P, J mod Q)), as a generator; the same
+    recurrence as mvn_potrf (bit-identical factor). Per super-step s (process column qs = s mod Q):
+      diag     : rank (s mod P, qs) factors the diagonal block and packs it (mvn_dpotrf_panel / pack);
+      yield ("diag", s, owner)   -> the diagonal block reaches the ranks of process column qs;
+      panel    : the ranks of column qs solve their rows below it and pack them (mvn_dpanel_trsm / pack);
+      yield ("panel", s, qs)     -> every rank receives the whole super-panel (its row blocks come
+                                    from ranks (I mod P, qs));
+      update   : every rank updates its own trailing tiles from the buffer (mvn_dpotrf_update).
+    The runner resumes the generator with a handle `ops.wait` understands."""
+    S = -(-ops.nt // ops.kp)
+    for s in range(S):
+        ps, qs = s % P, s % Q
+        if (pr, pc) == (ps, qs):
+            ops.panel(s, "main")
+            ops.pack(s, "main")
+        h = yield ("diag", s, (ps, qs))
+        ops.wait(h, "main")
+        if pc == qs:
+            ops.trsm(s, "main")
+            ops.pack(s, "main")
+        h = yield ("panel", s, qs)
+        ops.wait(h, "main")
+        if s + 1 < S:
+            ops.update(s, (s + 1) * ops.kp, ops.kp * Q, ops.kp, "main", side_busy=False, just_one=False)
+    ops.join()
+
+
+class CudaPotrf2DOps(CudaPotrfDistOps):
+    """potrf_2d_schedule's building blocks on a rank's 2-D distributed storage (mvn_dtiles with
+    prows = P): rank = pr * Q + pc holds the blocks (I, J) with I mod P = pr, J mod Q = pc."""
+
+    def __init__(self, local, n: int, P: int, Q: int, pr: int, pc: int, main=None, kp: int | None = None):
+        super().__init__(local, n, P * Q, pr * Q + pc, main=main, kp=kp)
+        from . import dtiles
+        self.P, self.Q, self.pr, self.pc = P, Q, pr, pc
+        self.d = dtiles(n, P * Q, pr * Q + pc, self.kp, P)
+
+    def trsm(self, sp, on):
+        from . import mvn_dpanel_trsm
+        mvn_dpanel_trsm(self.L, self.d, sp, self.panel_buf(sp), stream=self._st(on))
+
+    def row_block_range(self, sp: int, I: int):
+        """Element range [a, b) of row block I (tile rows I kp .. I kp + kp - 1, >= sp kp) in the
+        kPanel buffer of super-panel sp (tiles (i, k .. min(i, k+w-1)) row after row)."""
+        k = sp * self.kp
+        w = min(self.kp, self.nt - k)
+
+        def off(i):
+            m = i - k
+            return (m * (m + 1) // 2 if m <= w else w * (w + 1) // 2 + (m - w) * w) * TILE * TILE
+        lo, hi = max(I * self.kp, k), min((I + 1) * self.kp, self.nt)
+        return off(lo), off(hi)
+
+
+def potrf_distributed_2d(local, n: int, P: int, ops=None, kp: int | None = None) -> int:
+    """The 2-D block-cyclic factorisation over the default process group (W = P x Q ranks, rank =
+    pr * Q + pc) on distributed storage (`local`: this rank's mvn_dtiles buffer with prows = P,
+    Sigma generated by mvn_dcov_matern). The diagonal block goes to the process column by a
+    broadcast in the column's subgroup; each row block of the solved super-panel is broadcast from
+    its owner (I mod P, qs) to all ranks. Returns info (-1 = SPD, else the first failing row, agreed
+    by all ranks). `ops` defaults to CudaPotrf2DOps (tests pass host stand-ins)."""
+    W = dist.get_world_size()
+    rank = dist.get_rank()
+    if W % P:
+        raise ValueError(f"world size {W} is not a multiple of P = {P}")
+    Q = W // P
+    pr, pc = rank // Q, rank % Q
+    col_groups = [dist.new_group([p * Q + q for p in range(P)]) for q in range(Q)]   # same order on every rank
+    if ops is None:
+        _cuda_info(local)
+        ops = CudaPotrf2DOps(local, n, P, Q, pr, pc, kp=kp)
+    gen = potrf_2d_schedule(ops, pr, pc, P, Q)
+    req = next(gen, None)
+    while req is not None:
+        kind, sp = req[0], req[1]
+        buf = ops.panel_buf(sp)
+        if kind == "diag":
+            ps, qs = req[2]
+            if pc == qs:
+                a, b = ops.row_block_range(sp, sp)
+                dist.broadcast(buf[a:b], src=ps * Q + qs, group=col_groups[qs])
+        else:
+            qs = req[2]
+            for I in range(sp, -(-ops.nt // ops.kp)):
+                a, b = ops.row_block_range(sp, I)
+                if a < b:
+                    dist.broadcast(buf[a:b], src=(I % P) * Q + qs)
+        try:
+            req = gen.send(None)
+        except StopIteration:
+            req = None
+    info = ops.info() if hasattr(ops, "info") else _cuda_info(local)
+    big = 1 << 62
+    t = torch.tensor([info if info >= 0 else big], dtype=torch.int64, device=getattr(ops, "dev", "cpu"))
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    info = int(t.item())
+    return -1 if info == big else info
 
 
 def potrf_distributed(L, n: int, group=None, ops=None, force_collectives: bool = False) -> int:

@@ -256,3 +256,97 @@ def test_super_panel_widths(kp):
                         "tests/test_gpu_parity.py", "-k", "emulated or single_process or potrf_vs_oracle"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+# ------------------------------------------------------------------------------ 2-D block-cyclic
+def emulate_2d(torch, locs, n, P, Q):
+    """potrf_2d_schedule for the P x Q virtual ranks (rank = pr * Q + pc) on one device, in lockstep:
+    'diag' copies the diagonal block's prefix of the panel buffer from its owner to the process
+    column; 'panel' copies every row block of the super-panel from its owner (I mod P, qs) to every
+    other rank (event-ordered device copies standing in for the NCCL broadcasts)."""
+    from paper_2405_14892_b200.parallel import CudaPotrf2DOps, potrf_2d_schedule
+    W = P * Q
+    torch.cuda.synchronize()
+    mvn().mvn_potrf_info(0, reset=True)
+    ops = [CudaPotrf2DOps(locs[r], n, P, Q, r // Q, r % Q, main=torch.cuda.Stream()) for r in range(W)]
+    gens = [potrf_2d_schedule(ops[r], r // Q, r % Q, P, Q) for r in range(W)]
+    reqs = [next(g) for g in gens]
+    kp, nt = ops[0].kp, ops[0].nt
+    while True:
+        assert len({q[:2] for q in reqs}) == 1, reqs
+        kind, s = reqs[0][0], reqs[0][1]
+        evs = [o.record("main") for o in ops]                 # every rank's pack is done
+        handles = [None] * W
+        if kind == "diag":
+            ps, qs = reqs[0][2]
+            src = ps * Q + qs
+            k = s * kp
+            w = min(kp, nt - k)
+            a, b = 0, w * (w + 1) // 2 * NB * NB
+            for r in range(W):
+                if r % Q == qs and r != src:
+                    ops[r].main.wait_event(evs[src])
+                    with torch.cuda.stream(ops[r].main):
+                        ops[r].panel_buf(s)[a:b].copy_(ops[src].panel_buf(s)[a:b])
+        else:
+            qs = reqs[0][2]
+            for I in range(s, -(-nt // kp)):
+                src = (I % P) * Q + qs
+                a, b = ops[src].row_block_range(s, I)
+                if a >= b:
+                    continue
+                for r in range(W):
+                    if r != src:
+                        ops[r].main.wait_event(evs[src])
+                        with torch.cuda.stream(ops[r].main):
+                            ops[r].panel_buf(s)[a:b].copy_(ops[src].panel_buf(s)[a:b])
+        done = [o.record("main") for o in ops]
+        for r in range(W):                                     # nobody reuses a buffer before all copies
+            for q in range(W):
+                ops[r].main.wait_event(done[q])
+        nxt = []
+        for r, g in enumerate(gens):
+            try:
+                nxt.append(g.send(handles[r]))
+            except StopIteration:
+                nxt.append(None)
+        if all(q is None for q in nxt):
+            break
+        assert all(q is not None for q in nxt)
+        reqs = nxt
+    for o in ops:
+        torch.cuda.current_stream().wait_stream(o.main)
+    torch.cuda.synchronize()
+    return mvn().mvn_potrf_info(0, reset=True)
+
+
+@pytest.mark.parametrize("n,nu,P,Q", [(1000, 0.5, 1, 1), (1000, 0.5, 2, 1), (2000, 1.5, 2, 2), (130, 0.5, 2, 3),
+                                      (40 * NB + 77, 0.5, 2, 2), (3000, 0.5, 3, 2), (75 * NB, 0.5, 2, 4),
+                                      (48 * NB + 5, 1.5, 4, 2)])
+def test_emulated_2d_block_cyclic_matches_single_gpu(torch, n, nu, P, Q):
+    """NEXT-1, 2-D block-cyclic on distributed storage: P x Q virtual ranks each holding only their
+    blocks (memory ~1/(PQ)), the diagonal block factored by its owner, the panel rows solved by the
+    process column, every rank updating its own tiles from the panel buffer. The gathered factor is
+    bitwise equal to mvn_potrf, the storage partitions the matrix."""
+    xy = np.random.default_rng(int(2 * nu) + n + 7).uniform(size=(n, 2))
+    beta = 0.1 if nu == 0.5 else 0.05
+    d_xy = torch.from_numpy(xy).cuda()
+    ref = mvn().mvn_cov_matern(d_xy, 1.0, beta, nu, 1e-8)
+    assert mvn().mvn_potrf(ref, n) == -1
+    kp = mvn().mvn_potrf_panel_width(n)
+    W = P * Q
+    locs, total = [], 0
+    for r in range(W):
+        d = mvn().dtiles(n, W, r, kp, P)
+        loc = mvn().alloc_dtiles(n, W, r, kp, prows=P)
+        mvn().mvn_dcov_matern(d_xy, d, 1.0, beta, nu, 1e-8, loc)
+        locs.append(loc)
+        total += mvn().mvn_dtiles_bytes(n, W, r, kp, P)
+    assert total == mvn().mvn_tiles_bytes(n)
+    assert emulate_2d(torch, locs, n, P, Q) == -1
+    G = torch.full_like(ref, float("nan"))
+    for r in range(W):
+        mvn().mvn_dgather(locs[r], mvn().dtiles(n, W, r, kp, P), G)
+    torch.cuda.synchronize()
+    assert torch.equal(G, ref), f"max diff {float((G - ref).abs().max())}"
+
