@@ -8,6 +8,8 @@
 // DFMA/clk/SM) vs the fp64 arithmetic per element: distance (3), sqrt, x = h / beta as a product
 // with the host's 1/beta (1; a division costs ~10 plus a slow-path call), exp(-x) with sigma2
 // folded in (10, exp_neg_scaled), the nu = 3/2, 5/2 factor (1-2).
+#include <cstdlib>
+
 #include <math_constants.h>
 
 #include "common.cuh"
@@ -57,6 +59,14 @@ __device__ __forceinline__ double matern_poly(double x, double e) {
     return fma(fma(x, 1.0 / 3.0, 1.0) * x, e, e);
 }
 
+// The tiles with far pairs (x > 699): libm's sqrt and exp, out of line (keeps the fast path's
+// register budget).
+template <int NU2>
+static __device__ __noinline__ double matern_far(double d2, double ib, double sigma2) {
+    const double x = sqrt(d2) * ib;
+    return matern_poly<NU2>(x, sigma2 * exp(-x));
+}
+
 // sqrt(d) for d >= 0 without the special-operand branch of sqrt(): the MUFU reciprocal square-root
 // seed, one Newton step on it, then one on the root (error ~ ulp). The seed is taken at d + 1e-300
 // (= d for d > 1e-284; d = 0 then gives y = 1e150 and t = 0, so sqrt(0) = 0) — one add instead of
@@ -70,13 +80,16 @@ __device__ __forceinline__ double sqrt_nonneg(double d) {
     return fma(0.5 * y, fma(-t, t, d), t);
 }
 
-// One CTA (256 threads) per tile. Thread t owns rows 8 (t % 16) .. +7 of the tile (their locations
-// in registers) and the 8 columns t / 16 + 16 m, m < 8: per column four 16-byte stores of 8 rows
-// (16 lanes write a whole 1 KB column), and a column's location is one shared-memory read for 8
-// elements. The libm fallback for far pairs (x > 700, where sigma2 e^-x nears the bottom of the
+// One CTA (256 threads) per tile. Thread t owns RPT consecutive rows of the tile (their locations in
+// registers; RPT = 4: rows 4 (t % 32) .., the columns t / 32 + 8 m; RPT = 8: rows 8 (t % 16) .., the
+// columns t / 16 + 16 m): per column RPT / 2 16-byte stores, so each group of 128 / RPT lanes writes
+// one whole 1 KB column (coalesced), and a column's location is one shared-memory read for RPT
+// elements. The libm fallback for far pairs (x > 699, where sigma2 e^-x nears the bottom of the
 // normal range) is decided once per tile from the bounding boxes of its row and column locations.
-template <int NU2>
-__global__ void __launch_bounds__(256) k_cov_matern(const MaternArgs p) {
+template <int NU2, int RPT>
+__global__ void __launch_bounds__(256, 4) k_cov_matern(const MaternArgs p) {
+    constexpr int TPC = kTile / RPT;                     // threads per column
+    constexpr int CPI = 256 / TPC;                       // columns per step
     __shared__ double cx[kTile], cy[kTile], rxs[kTile], rys[kTile], tb[128], bb[8][4];
     __shared__ int fast_s;
     // blockIdx.x -> tile (ti, tj), ti >= tj, row-major enumeration of the lower triangle
@@ -128,38 +141,37 @@ __global__ void __launch_bounds__(256) k_cov_matern(const MaternArgs p) {
         const double ex = fmax(b[0][1] - b[1][0], b[1][1] - b[0][0]), ey = fmax(b[0][3] - b[1][2], b[1][3] - b[0][2]);
         fast_s = !p.libm && sqrt(ex * ex + ey * ey) * p.inv_beta <= 699.0;
     }
-    const int rq = (tid & 15) * 8, cg = tid >> 4;
+    const int rq = (tid % TPC) * RPT, cg = tid / TPC;
     __syncthreads();
-    double rx[8], ry[8];
+    double rx[RPT], ry[RPT];
 #pragma unroll
-    for (int h = 0; h < 8; ++h) { rx[h] = rxs[rq + h]; ry[h] = rys[rq + h]; }
+    for (int h = 0; h < RPT; ++h) { rx[h] = rxs[rq + h]; ry[h] = rys[rq + h]; }
     double *T = p.tm.tile(ti, tj) + rq;
     const bool edge = r0 + kTile > n || ti == tj;         // padding or diagonal elements in this tile
     const double sigma2 = p.sigma2, ib = p.inv_beta, diag = p.sigma2 + p.nugget;
     const bool fast = fast_s != 0;
 #pragma unroll 1
-    for (int m = 0; m < kTile / 16; ++m) {
-        const int col = cg + 16 * m;
+    for (int m = 0; m < kTile / CPI; ++m) {
+        const int col = cg + CPI * m;
         const double xc = cx[col], yc = cy[col];
-        double v[8];
+        double v[RPT];
         if (fast) {
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
+            for (int h = 0; h < RPT; ++h) {
                 const double dx = rx[h] - xc, dy = ry[h] - yc;
                 const double x = sqrt_nonneg(fma(dx, dx, dy * dy)) * ib;
                 v[h] = matern_poly<NU2>(x, exp_neg_scaled(x, tb));
             }
         } else {
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
+            for (int h = 0; h < RPT; ++h) {
                 const double dx = rx[h] - xc, dy = ry[h] - yc;
-                const double x = sqrt(fma(dx, dx, dy * dy)) * ib;
-                v[h] = matern_poly<NU2>(x, sigma2 * exp(-x));
+                v[h] = matern_far<NU2>(fma(dx, dx, dy * dy), ib, sigma2);
             }
         }
         if (edge) {
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
+            for (int h = 0; h < RPT; ++h) {
                 const int64_t gr = r0 + rq + h, gc = c0 + col;
                 if (gr >= n || gc >= n) v[h] = (gr == gc) ? 1.0 : 0.0;
                 else if (gr == gc) v[h] = diag;
@@ -167,8 +179,14 @@ __global__ void __launch_bounds__(256) k_cov_matern(const MaternArgs p) {
         }
         double2 *dst = reinterpret_cast<double2 *>(T + (int64_t)col * kTile);
 #pragma unroll
-        for (int h = 0; h < 4; ++h) dst[h] = make_double2(v[2 * h], v[2 * h + 1]);
+        for (int h = 0; h < RPT / 2; ++h) dst[h] = make_double2(v[2 * h], v[2 * h + 1]);
     }
+}
+
+// rows per thread: MVN_K1_RPT = 4 or 8 (experiment knob, read once; default 4)
+static int k1_rpt() {
+    static const int v = [] { const char *e = getenv("MVN_K1_RPT"); return (e && atoi(e) == 8) ? 8 : 4; }();
+    return v;
 }
 
 cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
@@ -180,9 +198,10 @@ cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, do
     a.libm = sigma2 < 0x1p-100 || sigma2 > 0x1p100;
     for (int j = 0; j < 128; ++j) a.tab[j] = (double)((long double)sigma2 * exp2l(-(long double)j / 128.0L));
     dim3 grid((unsigned)ntiles);
-    if (nu == 0.5) k_cov_matern<1><<<grid, 256, 0, st>>>(a);
-    else if (nu == 1.5) k_cov_matern<3><<<grid, 256, 0, st>>>(a);
-    else k_cov_matern<5><<<grid, 256, 0, st>>>(a);
+    const bool r8 = k1_rpt() == 8;
+    if (nu == 0.5) { if (r8) k_cov_matern<1, 8><<<grid, 256, 0, st>>>(a); else k_cov_matern<1, 4><<<grid, 256, 0, st>>>(a); }
+    else if (nu == 1.5) { if (r8) k_cov_matern<3, 8><<<grid, 256, 0, st>>>(a); else k_cov_matern<3, 4><<<grid, 256, 0, st>>>(a); }
+    else { if (r8) k_cov_matern<5, 8><<<grid, 256, 0, st>>>(a); else k_cov_matern<5, 4><<<grid, 256, 0, st>>>(a); }
     return cudaGetLastError();
 }
 
