@@ -712,7 +712,9 @@ def main():
         "potrf_method": "int8 tensor cores (NEXT-4, R25)" if args.potrf_method == 1 else "fp64 DMMA",
         "roofline": sov_roof,
         "potrf_roofline": {"achieved": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12, "peak": PEAK_FP64_TFLOPS,
-                           "frac": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12 / PEAK_FP64_TFLOPS},
+                           "frac": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12 / PEAK_FP64_TFLOPS,
+                           "unit": "TFLOP/s" if args.potrf_method == 0 else
+                           "fp64-equivalent TFLOP/s (trailing updates on the int8 tensor cores, R25) over the fp64 peak"},
         "clocks": clk,
         "gpu_launches": launches * args.steps,
         "e2e": e2e,

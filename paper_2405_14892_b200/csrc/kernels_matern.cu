@@ -86,8 +86,8 @@ __device__ __forceinline__ double sqrt_nonneg(double d) {
 // one whole 1 KB column (coalesced), and a column's location is one shared-memory read for RPT
 // elements. The libm fallback for far pairs (x > 699, where sigma2 e^-x nears the bottom of the
 // normal range) is decided once per tile from the bounding boxes of its row and column locations.
-template <int NU2, int RPT>
-__global__ void __launch_bounds__(256, 4) k_cov_matern(const MaternArgs p) {
+template <int NU2, int RPT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_cov_matern(const MaternArgs p) {
     constexpr int TPC = kTile / RPT;                     // threads per column
     constexpr int CPI = 256 / TPC;                       // columns per step
     __shared__ double cx[kTile], cy[kTile], rxs[kTile], rys[kTile], tb[128], bb[8][4];
@@ -183,10 +183,22 @@ __global__ void __launch_bounds__(256, 4) k_cov_matern(const MaternArgs p) {
     }
 }
 
-// rows per thread: MVN_K1_RPT = 4 or 8 (experiment knob, read once; default 4)
-static int k1_rpt() {
-    static const int v = [] { const char *e = getenv("MVN_K1_RPT"); return (e && atoi(e) == 8) ? 8 : 4; }();
+// variant (rows per thread, CTAs per SM): MVN_K1_VARIANT = 0 (4, 4: default), 1 (4, 5), 2 (2, 6),
+// 3 (2, 8), 4 (8, 4) — an experiment knob read once
+static int k1_variant() {
+    static const int v = [] { const char *e = getenv("MVN_K1_VARIANT"); const int x = e ? atoi(e) : 0; return x >= 0 && x <= 4 ? x : 0; }();
     return v;
+}
+
+template <int NU2>
+static void k1_launch(dim3 grid, const MaternArgs &a, cudaStream_t st) {
+    switch (k1_variant()) {
+        case 1: k_cov_matern<NU2, 4, 5><<<grid, 256, 0, st>>>(a); break;
+        case 2: k_cov_matern<NU2, 2, 6><<<grid, 256, 0, st>>>(a); break;
+        case 3: k_cov_matern<NU2, 2, 8><<<grid, 256, 0, st>>>(a); break;
+        case 4: k_cov_matern<NU2, 8, 4><<<grid, 256, 0, st>>>(a); break;
+        default: k_cov_matern<NU2, 4, 4><<<grid, 256, 0, st>>>(a); break;
+    }
 }
 
 cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
@@ -198,10 +210,9 @@ cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, do
     a.libm = sigma2 < 0x1p-100 || sigma2 > 0x1p100;
     for (int j = 0; j < 128; ++j) a.tab[j] = (double)((long double)sigma2 * exp2l(-(long double)j / 128.0L));
     dim3 grid((unsigned)ntiles);
-    const bool r8 = k1_rpt() == 8;
-    if (nu == 0.5) { if (r8) k_cov_matern<1, 8><<<grid, 256, 0, st>>>(a); else k_cov_matern<1, 4><<<grid, 256, 0, st>>>(a); }
-    else if (nu == 1.5) { if (r8) k_cov_matern<3, 8><<<grid, 256, 0, st>>>(a); else k_cov_matern<3, 4><<<grid, 256, 0, st>>>(a); }
-    else { if (r8) k_cov_matern<5, 8><<<grid, 256, 0, st>>>(a); else k_cov_matern<5, 4><<<grid, 256, 0, st>>>(a); }
+    if (nu == 0.5) k1_launch<1>(grid, a, st);
+    else if (nu == 1.5) k1_launch<3>(grid, a, st);
+    else k1_launch<5>(grid, a, st);
     return cudaGetLastError();
 }
 

@@ -1,6 +1,6 @@
 """K1 (k_cov_matern) alone at a BASELINE config: mean of 20 launches with CUDA events, as GB/s of
 algorithmic stores (8 n(n+1)/2 bytes... the full lower tiles, padding included) against the HBM peak.
-python tools/k1_time.py D   (MVN_K1_RPT = 4 or 8 selects the rows-per-thread variant)"""
+python tools/k1_time.py D   (MVN_K1_VARIANT = 0..4 selects the (rows per thread, CTAs per SM) variant)"""
 import json
 import os
 import sys
@@ -33,5 +33,5 @@ ms = float(np.median(ts))
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] \
     if os.path.exists("MEASURED_PEAKS.json") else 6442.9
 gbs = mvn.mvn_tiles_bytes(n) / (ms / 1e3) / 1e9
-print(f"cfg={cfg.name} n={n} rpt={os.environ.get('MVN_K1_RPT', '4')} k1_ms={ms:.3f} store_GBps={gbs:.0f} "
+print(f"cfg={cfg.name} n={n} variant={os.environ.get("MVN_K1_VARIANT", "0")} k1_ms={ms:.3f} store_GBps={gbs:.0f} "
       f"frac_hbm={gbs / peak:.3f}", flush=True)
