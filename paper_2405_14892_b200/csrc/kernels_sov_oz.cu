@@ -75,6 +75,11 @@ struct SovOzArgs {
     double *xch;              // [clusters][2 destination CTA][2 parity][128 rows][64]
     double *part;             // [2 * blocks][n_pad][2]: (max ell, sum e^{ell - max}) per CTA half-block
     int *flag;                // set when |y| >= 63.5 (outside the fixed y scale)
+    // soft cluster lockstep (L2 reuse of the shared L-slice stream; 0 = off): CTA 0's producer starts
+    // step t = b (nrb - 1) + rb - 1 only when every cluster that has step t - lag has issued it
+    int lag;
+    int *step_done;           // [max blocks * (nrb - 1)] issue counters (zeroed per launch)
+    const int *need;          // [max blocks]: clusters with more than b blocks
 };
 
 __device__ __forceinline__ uint64_t soz_shift(uint64_t seed, uint64_t r, uint64_t k) {
@@ -306,6 +311,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(soz::NT, 1) k_sov_oz
                 for (int rb = 1; rb < p.nrb; ++rb) {
                     const int nch = 4 * rb;
                     const int8_t *Arow = p.LA + 2ll * rb * (rb + 1) * HALF;
+                    const int64_t t = (int64_t)b * (p.nrb - 1) + rb - 1;
+                    if (crank == 0 && p.lag > 0 && t >= p.lag) {
+                        const int64_t tw = t - p.lag;
+                        const int need = p.need[tw / (p.nrb - 1)];
+                        int v;
+                        while (true) {
+                            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p.step_done + tw) : "memory");
+                            if (v >= need) break;
+                            __nanosleep(200);
+                        }
+                    }
                     for (int c = 0; c < nch; ++c, ++q) {
                         if (crank == 1 && c == 4 * (rb - 1)) { mbar_wait_cluster(yready, yw & 1); ++yw; }
                         const int st = q % STAGES;
@@ -318,6 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(soz::NT, 1) k_sov_oz
                                      " [%0], [%1], %2, [%3], %4;\n"
                                      ::"r"(smem_u32(d)), "l"(src), "r"(HALF), "r"(smem_u32(&full[st])), "h"((uint16_t)3) : "memory");
                     }
+                    if (crank == 0 && p.lag > 0) atomicAdd(p.step_done + t, 1);
                 }
             }
         }
@@ -513,8 +530,12 @@ cudaError_t launch_sov_oz(const SovOzLaunch &L, cudaStream_t st) {
     a.LA = L.LA; a.rowscale = L.rowscale; a.L = L.L; a.n = L.n; a.nrb = (int)((L.n + 127) / 128);
     a.n_pad = (int64_t)a.nrb * 128; a.a = L.a; a.G = L.G; a.N = L.N; a.seed = L.seed; a.cl = L.cl; a.YS = L.YS;
     a.xch = L.xch; a.part = L.part; a.flag = L.flag;
+    a.lag = L.lag; a.step_done = L.step_done; a.need = L.need;
     cudaError_t e = cudaMemsetAsync(L.flag, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
+    if (a.lag > 0 && a.nrb > 1 &&
+        (e = cudaMemsetAsync(L.step_done, 0, sizeof(int) * (size_t)L.max_blocks * (a.nrb - 1), st)) != cudaSuccess)
+        return e;
     k_sov_oz<<<2 * L.clusters, soz::NT, soz::SMEM, st>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return launch_reduce_blocks(L.part, 2 * L.nblk, L.n, a.n_pad, L.Mout, L.Sout, st);

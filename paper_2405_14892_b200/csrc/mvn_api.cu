@@ -620,6 +620,23 @@ mvn_status mvn_sov_prefix_ex(mvn_ctx *c, mvn_tiles t, const double *d_L, const d
     L.LA = (const int8_t *)c->mcLA; L.rowscale = (const double *)c->mcRS; L.L = d_L; L.n = t.n; L.a = d_a; L.G = c->G;
     L.N = q->N; L.seed = q->seed; L.cl = (const int64_t *)c->cta; L.YS = (int8_t *)c->Y; L.xch = (double *)c->sozX;
     L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S; L.flag = d_flag;
+    // soft cluster lockstep (MVN_SOV_OZ_LAG steps; 0 = off): clusters stay within `lag` row blocks of
+    // each other, so the L-slice chunks they all stream are served from L2 more often
+    static const int env_lag = [] { const char *e = getenv("MVN_SOV_OZ_LAG"); return e ? atoi(e) : 0; }();
+    if (env_lag > 0) {
+        int max_blocks = 0;
+        for (int g = 0; g < L.clusters; ++g) max_blocks = std::max<int>(max_blocks, (int)((cl[3 * g + 1] + 127) / 128));
+        std::vector<int> need((size_t)max_blocks, 0);
+        for (int g = 0; g < L.clusters; ++g)
+            for (int b = 0; b < (int)((cl[3 * g + 1] + 127) / 128); ++b) ++need[(size_t)b];
+        const int64_t nrb = (t.n + 127) / 128;
+        const size_t bytes = sizeof(int) * ((size_t)max_blocks * std::max<int64_t>(nrb - 1, 1) + max_blocks);
+        if ((s = ensure(c, &c->sync, &c->sync_cap, bytes)) != MVN_OK) return s;
+        int *d_sync = (int *)c->sync;
+        int *d_need = d_sync + (size_t)max_blocks * std::max<int64_t>(nrb - 1, 1);
+        MVN_CUDA(c, cudaMemcpyAsync(d_need, need.data(), sizeof(int) * max_blocks, cudaMemcpyHostToDevice, c->stream));
+        L.lag = env_lag; L.step_done = d_sync; L.need = d_need; L.max_blocks = max_blocks;
+    }
     MVN_CUDA(c, mvn::launch_sov_oz(L, c->stream));
     int h_big = 0;
     MVN_CUDA(c, cudaMemcpyAsync(&h_big, d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));

@@ -101,6 +101,10 @@ struct SovOzLaunch {
     double *part;            // [2 nblk][n_pad][2]
     double *Mout, *Sout;
     int *flag;               // device int: |y| >= 63.5 seen
+    int lag = 0;             // cluster lockstep distance in steps (0 = off)
+    int *step_done = nullptr;
+    const int *need = nullptr;
+    int max_blocks = 0;
 };
 cudaError_t sov_oz_init();
 int sov_oz_max_clusters(int nsm);

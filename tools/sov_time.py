@@ -1,6 +1,6 @@
 """Time the SOV sweep alone (CUDA events) on a BASELINE config: python tools/sov_time.py C [reps].
 Environment knobs of libmvn are read once per process (MVN_SOV_LAG, MVN_SOV_HINTS), so A/B runs
-use separate processes (tools/sov_ab.sh)."""
+use separate processes."""
 import os
 import sys
 
@@ -35,5 +35,5 @@ for it in range(reps + 1):
 lp = mvn.mvn_prefix_finalize(M, S, cfg.NR).cpu().numpy()
 ms = float(np.mean(ts)) if ts else float("nan")
 fr = n * (n - 1) * cfg.NR / (ms / 1e3) / 1e12 / 37.07
-print(f"cfg={cfg.name} lag={os.environ.get('MVN_SOV_LAG', 'def')} hints={os.environ.get('MVN_SOV_HINTS', 'def')} "
+print(f"cfg={cfg.name} lag={os.environ.get('MVN_SOV_LAG', 'def')} serial={os.environ.get('MVN_SOV_SERIAL', 'def')} "
       f"sov_ms={ms:.1f} frac={fr:.3f} logP[-1]={lp[-1]:.12f} logP[100]={lp[min(100, n - 1)]:.15f}", flush=True)
