@@ -270,6 +270,20 @@ mvn_status mvn_sov_prefix(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const do
 mvn_status mvn_sov_prefix_ex(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_a,
                              const double *d_b, const mvn_qmc *q, int32_t method, double *d_M, double *d_S);
 
+/* The same sweep as per-UNIT partials (SURVEY §8(b), §8(e)'s bitwise-deterministic combine): unit u
+ * = the global samples [128 u, min(128 u + 128, N*R)) (q->sample_begin / end are ignored). For the
+ * units [unit_begin, unit_end) it writes d_partial[u - unit_begin][k][2] = (max_g ell_k(g), sum_g
+ * exp(ell_k(g) - max)) over the unit's samples (device, caller-owned, n doubles x 2 per unit). A
+ * unit's partial does not depend on how the units are split over calls or ranks (its samples always
+ * sit on the same lanes of one 128-sample block), so concatenating the ranks' partials (all-gather)
+ * and reducing them in unit order with mvn_prefix_reduce gives the same bits on any number of GPUs.
+ * Errors as mvn_sov_prefix.                                                                      */
+mvn_status mvn_sov_prefix_units(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_a,
+                                const double *d_b, const mvn_qmc *q, int64_t unit_begin, int64_t unit_end,
+                                double *d_partial);
+/* (M, S) of `units` consecutive unit partials (layout above), combined in unit order (device). */
+mvn_status mvn_prefix_reduce(mvn_ctx *ctx, int64_t n, int64_t units, const double *d_partial, double *d_M, double *d_S);
+
 /* Multi-GPU combine helpers (reading R11): after all_reduce(MAX) of M into d_Mglob,
  *   S <- S * exp(M - Mglob), M <- Mglob  (elementwise, device; S = 0 where M = -inf).
  * Then all_reduce(SUM) of S and mvn_prefix_finalize.                                           */

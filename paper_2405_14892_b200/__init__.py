@@ -38,6 +38,7 @@ ABI_SYMBOLS = [
     "mvn_posterior", "mvn_posterior_tiles", "mvn_tlr_compress",
     "mvn_dtiles_bytes", "mvn_dpanel_numel", "mvn_dcov_matern", "mvn_dpotrf_panel", "mvn_dpanel_pack",
     "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex", "mvn_potrf_ex", "mvn_dpanel_trsm",
+    "mvn_sov_prefix_units", "mvn_prefix_reduce",
 ]
 
 
@@ -142,6 +143,8 @@ def lib() -> ctypes.CDLL:
         "mvn_dpanel_trsm": (S, [P, mvn_dtiles, P, I64, P]),
         "mvn_sov_prefix_ex": (S, [P, T, P, P, P, ctypes.POINTER(mvn_qmc), I32, P, P]),
         "mvn_potrf_ex": (S, [P, T, P, ctypes.POINTER(I64), I32]),
+        "mvn_sov_prefix_units": (S, [P, T, P, P, P, ctypes.POINTER(mvn_qmc), I64, I64, P]),
+        "mvn_prefix_reduce": (S, [P, I64, I64, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -458,6 +461,35 @@ def mvn_sov_prefix_ex(L, n: int, a, N: int, R: int, seed: int, begin: int = 0, e
     c.check(lib().mvn_sov_prefix_ex(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64),
                                     None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q), int(method),
                                     _dev_ptr(M), _dev_ptr(S)), "mvn_sov_prefix_ex")
+    return M, S
+
+
+def sov_units(N: int, R: int) -> int:
+    """Number of 128-sample units of N*R samples (mvn_sov_prefix_units)."""
+    return -(-int(N) * int(R) // 128)
+
+
+def mvn_sov_prefix_units(L, n: int, a, N: int, R: int, seed: int, unit_begin: int, unit_end: int, b=None,
+                         partial=None):
+    """Per-unit partials [unit_end - unit_begin][n][2] (CUDA float64) of the fp64 sweep."""
+    import torch
+    c = Context.get(L.device.index)
+    partial = torch.empty((unit_end - unit_begin, n, 2), dtype=torch.float64, device=L.device) if partial is None else partial
+    q = mvn_qmc(int(N), int(R), int(seed), 0, int(N) * int(R))
+    c.check(lib().mvn_sov_prefix_units(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64),
+                                       None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q),
+                                       int(unit_begin), int(unit_end), _dev_ptr(partial)), "mvn_sov_prefix_units")
+    return partial
+
+
+def mvn_prefix_reduce(partial, M=None, S=None):
+    """(M, S) of the unit partials [units][n][2], combined in unit order."""
+    import torch
+    units, n = partial.shape[0], partial.shape[1]
+    c = Context.get(partial.device.index)
+    M = torch.empty(n, dtype=torch.float64, device=partial.device) if M is None else M
+    S = torch.empty(n, dtype=torch.float64, device=partial.device) if S is None else S
+    c.check(lib().mvn_prefix_reduce(c.h, n, units, _dev_ptr(partial), _dev_ptr(M), _dev_ptr(S)), "mvn_prefix_reduce")
     return M, S
 
 

@@ -22,6 +22,8 @@
 //   * k_reduce_blocks combines the block partials of every prefix in fixed order (deterministic).
 // The lattice point w (reading R8) is generated in registers; the n x NR matrices R, A, B of
 // Alg. 2 are never materialised.
+#include <algorithm>
+
 #include "common.cuh"
 #include "gemm_dmma.cuh"
 #include "mvn_internal.h"
@@ -117,6 +119,8 @@ struct SovArgs {
     const int *need;          // [max blocks]
     int hints;                // L2 cache-policy hints on the producer's copies
     int serial_rb;            // row blocks rb <= serial_rb * 128 / w: GEMM of rb waits for the chain of rb-1
+    int unit_mode;            // 1: blocks are the global 128-sample units (deterministic per-unit partials)
+    int64_t part_stride;      // rows per block in `part` (n_pad, or n for the caller's unit partials)
 };
 
 // Sample blocks of a CTA: its `count` samples are split into nblk = ceil(count / 128) blocks whose
@@ -126,8 +130,19 @@ struct SovArgs {
 // CTA -> one 72-wide block; with 32-wide granularity it was 96, 29 % of the DMMA work padding).
 // Block b starts at sample offset off and holds cnt <= w samples (only the last block can have
 // cnt < w).
+// Unit mode (a CTA's range is whole 128-sample units of the global sample index): block b is unit b
+// of the range, so a unit's samples sit on the same lanes whatever the partition (W-independent
+// per-unit partials).
 struct BlockGeom { int64_t off; int cnt, w; };
-__device__ __forceinline__ BlockGeom block_geom(int64_t count, int b) {
+__device__ __forceinline__ BlockGeom block_geom(int64_t count, int b, int unit_mode = 0) {
+    if (unit_mode) {
+        BlockGeom g;
+        g.off = (int64_t)b * sovk::NB;
+        const int64_t left = count - g.off;
+        g.cnt = (int)(left < sovk::NB ? left : sovk::NB);
+        g.w = (g.cnt + 7) & ~7;
+        return g;
+    }
     const int64_t units = (count + 7) / 8, nblk = (count + sovk::NB - 1) / sovk::NB;
     const int64_t q = units / nblk, r = units % nblk;
     BlockGeom g;
@@ -151,7 +166,7 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
     uint32_t q = 0;
     const uint64_t pol_L = policy_evict_last(), pol_Y = policy_evict_first();
     for (int b = 0; b < nblk; ++b) {
-        const int w = block_geom(count, b).w, sbw = w + 4;    // this block's Y-history row stride
+        const int w = block_geom(count, b, p.unit_mode).w, sbw = w + 4;    // this block's Y-history row stride
         if (p.lag > 0 && lane == 0) atomicAdd(p.step_done + (int64_t)b * p.nrb, 1);   // row block 0: no GEMM
         for (int rb = 1; rb < p.nrb; ++rb) {
             const int64_t row0 = (int64_t)rb * M;
@@ -448,7 +463,7 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
         uint32_t q = 0;
         const int warp = tid >> 5;
         for (int b = 0; b < nblk; ++b) {
-            const int u = block_geom(count, b).w >> 3;          // 8-column fragments of the block
+            const int u = block_geom(count, b, p.unit_mode).w >> 3;   // 8-column fragments of the block
             const int sbw = 8 * u + 4;                          // the block's Y-history row stride
             // layout 2 x 4 (u % 4 == 0): column group warp / 2; layout 4 x 2: half warp / 4
             const int half = warp >> 2, u0 = (u + 1) >> 1;
@@ -473,7 +488,7 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
         // ============================================================ chain warps
         const int j = tid - NGEMM;
         for (int b = 0; b < nblk; ++b) {
-            const BlockGeom bg = block_geom(count, b);
+            const BlockGeom bg = block_geom(count, b, p.unit_mode);
             const int64_t g0 = g_first + bg.off;
             const int cnt = bg.cnt;
             const int w = bg.w;
@@ -506,7 +521,7 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
                         if (mm != -CUDART_INF)
                             for (int qq = 0; qq < nw; ++qq)
                                 if (ps[2 * qq] != -CUDART_INF) ss += ps[2 * qq + 1] * exp(ps[2 * qq] - mm);
-                        *reinterpret_cast<double2 *>(p.part + (blk * p.n_pad + k) * 2) = make_double2(mm, ss);
+                        *reinterpret_cast<double2 *>(p.part + (blk * p.part_stride + k) * 2) = make_double2(mm, ss);
                     }
                 }
             }
@@ -544,6 +559,22 @@ cudaError_t sov_init() {
 int sov_block_samples() { return sovk::NB; }
 int sov_y_stride() { return sovk::SB; }
 
+// Unit mode: the global units [u0, u1) of 128 samples (the last one clipped at g_end) over `grid`
+// CTAs, floor/ceil(units / grid) whole units each; block index = unit - u0.
+int64_t sov_partition_units(int64_t u0, int64_t u1, int64_t g_end, int grid, int64_t *cta) {
+    const int64_t nu = u1 - u0, base = nu / grid, rem = nu % grid;
+    int64_t u = u0;
+    for (int c = 0; c < grid; ++c) {
+        const int64_t k = base + (c < rem ? 1 : 0);
+        const int64_t g = u * sovk::NB, ge = std::min<int64_t>((u + k) * sovk::NB, g_end);
+        cta[3 * c] = g;
+        cta[3 * c + 1] = k > 0 ? ge - g : 0;
+        cta[3 * c + 2] = u - u0;
+        u += k;
+    }
+    return nu;
+}
+
 // Balanced partition of [g_begin, g_end) over `grid` CTAs: CTA c gets a contiguous share of
 // floor/ceil(nsamp/grid) samples, processed as blocks of 128 (last one narrowed to 32k).
 int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta) {
@@ -565,6 +596,7 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
     a.L = L.L; a.n = L.n; a.nrb = (int)((L.n + 63) / 64); a.a = L.a; a.b = L.b; a.G = L.G; a.N = L.N;
     a.seed = L.seed; a.cta = L.cta; a.n_pad = (int64_t)a.nrb * 64; a.Y = L.Y; a.part = L.part;
     a.lag = L.lag; a.step_done = L.step_done; a.need = L.need; a.hints = L.hints; a.serial_rb = L.serial_rb;
+    a.unit_mode = L.unit_mode; a.part_stride = L.unit_mode ? L.n : a.n_pad;
     if (a.lag > 0) {
         cudaError_t e = cudaMemsetAsync(L.step_done, 0, sizeof(int) * (size_t)L.max_blocks * a.nrb, st);
         if (e != cudaSuccess) return e;
@@ -573,6 +605,7 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
     else k_sov<false><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (L.unit_mode) return cudaSuccess;                       // the caller reduces the unit partials
     return launch_reduce_blocks(L.part, L.nblk, L.n, a.n_pad, L.Mout, L.Sout, st);
 }
 

@@ -528,13 +528,12 @@ mvn_status mvn_lattice_shifts(uint64_t seed, int32_t R, int64_t n, uint64_t *D) 
     return MVN_OK;
 }
 
-mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
-                          const mvn_qmc *q, double *d_M, double *d_S) {
-    DevGuard dev_guard(c);
-    if (!c) return MVN_E_USAGE;
-    if (!tiles_ok(t) || !d_L || !d_a || !q || !d_M || !d_S || q->N < 1 || q->R < 1 || q->sample_begin < 0 ||
-        q->sample_end <= q->sample_begin || q->sample_end > q->N * (int64_t)q->R)
-        return fail(c, MVN_E_USAGE, "mvn_sov_prefix: bad arguments (need nb=128, 0 <= begin < end <= N*R)");
+namespace {
+// The fp64 sweep. Sample mode (u0 < 0): the range [q->sample_begin, q->sample_end), balanced over the
+// CTAs, reduced to (M, S). Unit mode: the global 128-sample units [u0, u1), whole units per CTA, the
+// per-unit partials left in d_partial ([u1 - u0][n][2]).
+mvn_status sov_prefix_impl(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
+                           const mvn_qmc *q, int64_t u0, int64_t u1, double *d_partial, double *d_M, double *d_S) {
     mvn_status s;
     if ((s = ensure_generators(c, t.n)) != MVN_OK) return s;
     {   // NaN limits or a_k > b_k: MVN_E_USAGE (synchronises on a 4-byte flag before the sweep)
@@ -545,17 +544,21 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
         MVN_CUDA(c, cudaStreamSynchronize(c->stream));
         if (h_flag) return fail(c, MVN_E_USAGE, "mvn_sov_prefix: a limit is NaN or a_k > b_k");
     }
-    const int64_t nsamp = q->sample_end - q->sample_begin;
+    const bool units = u0 >= 0;
+    const int64_t NR = q->N * (int64_t)q->R;
+    const int64_t nsamp = units ? std::min<int64_t>(u1 * 128, NR) - u0 * 128 : q->sample_end - q->sample_begin;
     mvn::SovLaunch L;
     L.L = d_L; L.n = t.n; L.a = d_a; L.b = d_b; L.G = c->G; L.N = q->N; L.seed = q->seed;
-    L.g_begin = q->sample_begin; L.g_end = q->sample_end;
-    L.grid = (int)std::min<int64_t>(nsamp, c->nsm);
+    L.g_begin = units ? u0 * 128 : q->sample_begin; L.g_end = units ? std::min<int64_t>(u1 * 128, NR) : q->sample_end;
+    L.grid = (int)std::min<int64_t>(units ? u1 - u0 : nsamp, c->nsm);
     std::vector<int64_t> cta((size_t)L.grid * 3);
-    L.nblk = mvn::sov_partition(q->sample_begin, q->sample_end, L.grid, cta.data());
+    L.nblk = units ? mvn::sov_partition_units(u0, u1, L.g_end, L.grid, cta.data())
+                   : mvn::sov_partition(q->sample_begin, q->sample_end, L.grid, cta.data());
+    L.unit_mode = units ? 1 : 0;
     const int64_t n_pad = (t.n + 63) / 64 * 64;
     const int ys = mvn::sov_y_stride();
     if ((s = ensure(c, &c->Y, &c->Y_cap, (size_t)L.grid * n_pad * ys * sizeof(double))) != MVN_OK) return s;
-    if ((s = ensure(c, &c->part, &c->part_cap, (size_t)L.nblk * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
+    if (!units && (s = ensure(c, &c->part, &c->part_cap, (size_t)L.nblk * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
     if ((s = ensure(c, &c->cta, &c->cta_cap, cta.size() * sizeof(int64_t))) != MVN_OK) return s;
     // soft lockstep: need[b] = CTAs with more than b sample blocks; counters [max_blocks][nrb]
     static const int env_lag = [] { const char *e = getenv("MVN_SOV_LAG"); return e ? atoi(e) : 0; }();   // off: measured no gain (r01)
@@ -563,6 +566,7 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
     const int bs = mvn::sov_block_samples();
     int max_blocks = 0;
     for (int g = 0; g < L.grid; ++g) max_blocks = std::max<int>(max_blocks, (int)((cta[3 * g + 1] + bs - 1) / bs));
+    max_blocks = std::max(max_blocks, 1);
     std::vector<int> sync_host((size_t)max_blocks, 0);
     for (int g = 0; g < L.grid; ++g)
         for (int b = 0; b < (int)((cta[3 * g + 1] + bs - 1) / bs); ++b) ++sync_host[(size_t)b];
@@ -574,12 +578,41 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
                                 cudaMemcpyHostToDevice, c->stream));
     L.lag = env_lag; L.step_done = d_sync; L.need = d_sync + (size_t)max_blocks * nrb; L.max_blocks = max_blocks;
     L.hints = env_hints;
-    static const int env_serial = [] { const char *e = getenv("MVN_SOV_SERIAL"); return e ? atoi(e) : 0; }();   // off: measured no gain (r01)
+    static const int env_serial = [] { const char *e = getenv("MVN_SOV_SERIAL"); return e ? atoi(e) : 0; }();   // off: measured no gain (r01, r02)
     L.serial_rb = env_serial;
     MVN_CUDA(c, cudaMemcpyAsync(c->cta, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     L.cta = (const int64_t *)c->cta;
-    L.Y = (double *)c->Y; L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S;
+    L.Y = (double *)c->Y; L.part = units ? d_partial : (double *)c->part; L.Mout = d_M; L.Sout = d_S;
     MVN_CUDA(c, mvn::launch_sov(L, c->stream));
+    return MVN_OK;
+}
+}  // namespace
+
+mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
+                          const mvn_qmc *q, double *d_M, double *d_S) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !d_L || !d_a || !q || !d_M || !d_S || q->N < 1 || q->R < 1 || q->sample_begin < 0 ||
+        q->sample_end <= q->sample_begin || q->sample_end > q->N * (int64_t)q->R)
+        return fail(c, MVN_E_USAGE, "mvn_sov_prefix: bad arguments (need nb=128, 0 <= begin < end <= N*R)");
+    return sov_prefix_impl(c, t, d_L, d_a, d_b, q, -1, -1, nullptr, d_M, d_S);
+}
+
+mvn_status mvn_sov_prefix_units(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
+                                const mvn_qmc *q, int64_t unit_begin, int64_t unit_end, double *d_partial) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    const int64_t U = q ? (q->N * (int64_t)q->R + 127) / 128 : 0;
+    if (!tiles_ok(t) || !d_L || !d_a || !q || !d_partial || q->N < 1 || q->R < 1 || unit_begin < 0 ||
+        unit_end <= unit_begin || unit_end > U)
+        return fail(c, MVN_E_USAGE, "mvn_sov_prefix_units: bad arguments (need nb=128, 0 <= unit_begin < unit_end <= ceil(N*R/128))");
+    return sov_prefix_impl(c, t, d_L, d_a, d_b, q, unit_begin, unit_end, d_partial, nullptr, nullptr);
+}
+
+mvn_status mvn_prefix_reduce(mvn_ctx *c, int64_t n, int64_t units, const double *d_partial, double *d_M, double *d_S) {
+    DevGuard dev_guard(c);
+    if (!c || n < 1 || units < 1 || !d_partial || !d_M || !d_S) return fail(c, MVN_E_USAGE, "mvn_prefix_reduce: bad arguments");
+    MVN_CUDA(c, mvn::launch_reduce_blocks(d_partial, units, n, n, d_M, d_S, c->stream));
     return MVN_OK;
 }
 

@@ -74,11 +74,13 @@ struct SovLaunch {
     int max_blocks = 0;
     int hints = 1;           // L2 cache-policy hints
     int serial_rb = 0;       // row blocks whose GEMM waits for the previous chain (no fp64 contention)
+    int unit_mode = 0;       // 1: blocks = global 128-sample units, partials [units][n][2] left in `part`
 };
 cudaError_t sov_init();
 int sov_block_samples();
 int sov_y_stride();
 int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta);
+int64_t sov_partition_units(int64_t u0, int64_t u1, int64_t g_end, int grid, int64_t *cta);
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
 cudaError_t launch_reduce_blocks(const double *part, int64_t nblk, int64_t n, int64_t n_pad, double *M, double *S,
                                  cudaStream_t st);

@@ -52,6 +52,33 @@ def combine_prefix(M: torch.Tensor, S: torch.Tensor, group=None, rescale=None,
     return M, S
 
 
+def combine_units_deterministic(partial: torch.Tensor, group=None, reduce=None,
+                                force_collectives: bool = False) -> tuple[torch.Tensor, torch.Tensor]:
+    """SURVEY §8(e)'s bitwise-deterministic combine: every rank holds the per-unit partials
+    [units][n][2] of its contiguous unit range (mvn_sov_prefix_units over shard_range(U, rank, W));
+    the ranks' ranges are all-gathered (padded to the longest with (-inf, 0) units, which the
+    reduction skips) and reduced in global unit order (mvn_prefix_reduce). The result is the same
+    bits on every rank and for every W. `reduce` defaults to mvn_prefix_reduce (tests pass a host
+    stand-in)."""
+    if reduce is None:
+        from . import mvn_prefix_reduce as reduce
+    if not (dist.is_available() and dist.is_initialized()) or \
+            (dist.get_world_size(group) == 1 and not (force_collectives or FORCE_COLLECTIVES)):
+        return reduce(partial)
+    W = dist.get_world_size(group)
+    cnt = torch.tensor([partial.shape[0]], dtype=torch.int64, device=partial.device)
+    cnts = [torch.empty_like(cnt) for _ in range(W)]
+    dist.all_gather(cnts, cnt, group=group)
+    mx = int(max(int(c.item()) for c in cnts))
+    pad = torch.empty((mx, partial.shape[1], 2), dtype=partial.dtype, device=partial.device)
+    pad[..., 0] = float("-inf")
+    pad[..., 1] = 0.0
+    pad[:partial.shape[0]] = partial
+    parts = [torch.empty_like(pad) for _ in range(W)]
+    dist.all_gather(parts, pad, group=group)
+    return reduce(torch.cat(parts, 0).contiguous())
+
+
 def broadcast_L(L: torch.Tensor, group=None, src: int = 0, force_collectives: bool = False) -> torch.Tensor:
     """C1: rank `src` (group rank) sends the tile-packed factor to every rank (NCCL over NVLink), in
     place. A no-op without a process group, and on one rank unless collectives are forced."""

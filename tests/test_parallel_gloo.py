@@ -93,3 +93,56 @@ def test_distributed_combine_matches_single_process(world):
         lp = M + np.log(S) - math.log(N * R)
         assert np.max(np.abs(lp - lp1)) <= 1e-13
     assert np.array_equal(out[0][0], out[world - 1][0])        # every rank holds the same result
+
+
+# ------------------------------------------------------------------ deterministic per-unit combine
+def units_partial(L, a, N, R, seed, u0, u1):
+    """Oracle per-unit partials [u1-u0][n][2] for 128-sample units of the global sample index."""
+    import oracle
+    from oracle import lattice
+    n = L.shape[0]
+    G, D = lattice.generators(n), lattice.shifts(seed, R, n)
+    out = []
+    for u in range(u0, u1):
+        g, ge = 128 * u, min(128 * u + 128, N * R)
+        parts = []
+        while g < ge:                              # a unit can straddle a shift boundary
+            r, j0 = g // N, g % N + 1
+            J = min(ge - g, N - j0 + 1)
+            parts.append(oracle.sov_unit(L, a, np.full(n, np.inf), G, D[r], j0, J)[0])
+            g += J
+        M, S = oracle.combine_units(np.array(parts))
+        out.append(np.stack([M, S], -1))
+    return np.array(out)
+
+
+def host_reduce(P):
+    import oracle
+    M, S = oracle.combine_units(P.numpy())
+    return torch.from_numpy(M), torch.from_numpy(S)
+
+
+def _worker_units(rank, world, port, out):
+    from paper_2405_14892_b200.parallel import combine_units_deterministic
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    L, a, N, R, seed = problem()
+    U = -(-N * R // 128)
+    u0, u1 = shard_range(U, rank, world)
+    P = torch.from_numpy(units_partial(L, a, N, R, seed, u0, u1))
+    M, S = combine_units_deterministic(P, reduce=host_reduce)
+    out[rank] = (M.numpy().copy(), S.numpy().copy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_deterministic_unit_combine_is_bitwise_W_independent(world):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_units, args=(world, free_port(), out), nprocs=world, join=True)
+    L, a, N, R, seed = problem()
+    U = -(-N * R // 128)
+    M1, S1 = host_reduce(torch.from_numpy(units_partial(L, a, N, R, seed, 0, U)))
+    for r in range(world):
+        M, S = out[r]
+        assert np.array_equal(M, M1.numpy()) and np.array_equal(S, S1.numpy())
