@@ -307,18 +307,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(soz::NT, 1) k_sov_oz
         // ------------------------------------------------------------ producer: my operand, to both CTAs
         if (lane == 0) {
             uint32_t q = 0, yw = 0;
+            bool lockstep = p.lag > 0;              // a performance hint only: given up if it ever stalls
             for (int b = 0; b < nblk; ++b) {
                 for (int rb = 1; rb < p.nrb; ++rb) {
                     const int nch = 4 * rb;
                     const int8_t *Arow = p.LA + 2ll * rb * (rb + 1) * HALF;
                     const int64_t t = (int64_t)b * (p.nrb - 1) + rb - 1;
-                    if (crank == 0 && p.lag > 0 && t >= p.lag) {
+                    if (crank == 0 && lockstep && t >= p.lag) {
+                        // wait (bounded: ~0.5 s, e.g. clusters not co-resident under MPS) until every
+                        // cluster with step t - lag has issued it
                         const int64_t tw = t - p.lag;
                         const int need = p.need[tw / (p.nrb - 1)];
                         int v;
-                        while (true) {
+                        for (int spin = 0;; ++spin) {
                             asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p.step_done + tw) : "memory");
                             if (v >= need) break;
+                            if (spin > (1 << 21)) { lockstep = false; break; }
                             __nanosleep(200);
                         }
                     }
@@ -334,7 +338,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(soz::NT, 1) k_sov_oz
                                      " [%0], [%1], %2, [%3], %4;\n"
                                      ::"r"(smem_u32(d)), "l"(src), "r"(HALF), "r"(smem_u32(&full[st])), "h"((uint16_t)3) : "memory");
                     }
-                    if (crank == 0 && p.lag > 0) atomicAdd(p.step_done + t, 1);
+                    if (crank == 0 && p.lag > 0) atomicAdd(p.step_done + t, 1);   // also after giving up: others may wait
                 }
             }
         }

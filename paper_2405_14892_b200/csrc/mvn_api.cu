@@ -653,9 +653,10 @@ mvn_status mvn_sov_prefix_ex(mvn_ctx *c, mvn_tiles t, const double *d_L, const d
     L.LA = (const int8_t *)c->mcLA; L.rowscale = (const double *)c->mcRS; L.L = d_L; L.n = t.n; L.a = d_a; L.G = c->G;
     L.N = q->N; L.seed = q->seed; L.cl = (const int64_t *)c->cta; L.YS = (int8_t *)c->Y; L.xch = (double *)c->sozX;
     L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S; L.flag = d_flag;
-    // soft cluster lockstep (MVN_SOV_OZ_LAG steps; 0 = off): clusters stay within `lag` row blocks of
-    // each other, so the L-slice chunks they all stream are served from L2 more often
-    static const int env_lag = [] { const char *e = getenv("MVN_SOV_OZ_LAG"); return e ? atoi(e) : 0; }();
+    // soft cluster lockstep (MVN_SOV_OZ_LAG steps, default 1; 0 = off): clusters stay within `lag` row
+    // blocks of each other, so the L-slice chunks they all stream are served from L2 more often.
+    // Measured at D: lag 0 / 1 / 3 / 8 -> 5.79-5.84 / 5.45 / 5.56 / 5.67 s (profiles/r02_sov_int8.md).
+    static const int env_lag = [] { const char *e = getenv("MVN_SOV_OZ_LAG"); return e ? atoi(e) : 1; }();
     if (env_lag > 0) {
         int max_blocks = 0;
         for (int g = 0; g < L.clusters; ++g) max_blocks = std::max<int>(max_blocks, (int)((cl[3 * g + 1] + 127) / 128));
