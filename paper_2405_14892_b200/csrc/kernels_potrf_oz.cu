@@ -202,20 +202,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(poz::NT, 1) k_upd_oz
             for (int j = 0; j < 64; ++j) acc[j] = 0.0;
             mbar_wait(tfull, it & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
-#pragma unroll 1
-            for (int l = 0; l < 4; ++l) {
-                const double sc = ldexp(1.0, -7 * (poz_level(crank, l) + 2));
+            // per 16-column group: the 4 levels' loads in flight together, one wait
 #pragma unroll
-                for (int cg = 0; cg < 64; cg += 16) {
-                    uint32_t v[16];
+            for (int cg = 0; cg < 64; cg += 16) {
+                uint32_t v[4][16];
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
                     const uint32_t addr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(l * kTile + h * 64 + cg);
                     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-                                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                                 : "=r"(v[l][0]), "=r"(v[l][1]), "=r"(v[l][2]), "=r"(v[l][3]), "=r"(v[l][4]), "=r"(v[l][5]),
+                                   "=r"(v[l][6]), "=r"(v[l][7]), "=r"(v[l][8]), "=r"(v[l][9]), "=r"(v[l][10]), "=r"(v[l][11]),
+                                   "=r"(v[l][12]), "=r"(v[l][13]), "=r"(v[l][14]), "=r"(v[l][15])
                                  : "r"(addr));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[cg + j] = fma((double)(int32_t)v[j], sc, acc[cg + j]);
+                for (int l = 0; l < 4; ++l) {
+                    const double sc = ldexp(1.0, -7 * (poz_level(crank, l) + 2));
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[cg + j] = fma((double)(int32_t)v[l][j], sc, acc[cg + j]);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -237,10 +242,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(poz::NT, 1) k_upd_oz
             const double sr = p.rs[(int64_t)(ti - p.k - p.w) * kTile + row];
             const double *rsj = p.rs + (int64_t)(tj - p.k - p.w) * kTile + h * 64;
             double *C = p.tiles + tile_offset(ti, tj) + (int64_t)(h * 64) * kTile + row;
+            // in batches of 16 columns: all loads of a batch in flight before the first use (the
+            // epilogue must finish before this warp can drain the next tile's accumulators)
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                const double v = (acc[j] + __ldcg(X + j)) * sr * __ldg(rsj + j);
-                C[(int64_t)j * kTile] -= v;
+            for (int jb = 0; jb < 64; jb += 16) {
+                double cv[16], xv[16], rv[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    cv[j] = C[(int64_t)(jb + j) * kTile];
+                    xv[j] = __ldcg(X + jb + j);
+                    rv[j] = __ldg(rsj + jb + j);
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) C[(int64_t)(jb + j) * kTile] = cv[j] - (acc[jb + j] + xv[j]) * sr * rv[j];
             }
         }
     }

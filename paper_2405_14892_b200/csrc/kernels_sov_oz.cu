@@ -112,14 +112,15 @@ __device__ __forceinline__ void soz_drain(uint32_t tmem, int quarter, int crank,
         double P[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) P[i] = 0.0;
+        uint32_t v[4][16];                                 // the 4 levels' loads in flight together
+#pragma unroll
+        for (int l = 0; l < 4; ++l) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(l * soz::RB + cg), v[l]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-            uint32_t v[16];
-            tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(l * soz::RB + cg), v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
             const double sc = ldexp(1.0, -7 * (soz_level(crank, l) + 2));
 #pragma unroll
-            for (int i = 0; i < 16; ++i) P[i] = fma((double)(int32_t)v[i], sc, P[i]);
+            for (int i = 0; i < 16; ++i) P[i] = fma((double)(int32_t)v[l][i], sc, P[i]);
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -449,8 +450,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(soz::NT, 1) k_sov_oz
                     ++xp;
                     const double *X = p.xch + (((int64_t)clu * 2 + crank) * 2 + (rb & 1)) * RB * CS;
                     named_sync(BAR_CH, 64);                      // scl complete
-                    for (int li = 0; li < RB; ++li)
-                        Ssm[li * CS + jj] = (Ssm[li * CS + jj] + __ldcg(X + li * CS + jj)) * scl[li];
+                    for (int l0 = 0; l0 < RB; l0 += 16) {          // 16 loads in flight, then use
+                        double xv[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) xv[i] = __ldcg(X + (l0 + i) * CS + jj);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            Ssm[(l0 + i) * CS + jj] = (Ssm[(l0 + i) * CS + jj] + xv[i]) * scl[l0 + i];
+                    }
                 }
                 named_sync(BAR_CH, 64);
                 soz_chain_rowblock(p, smo, rb, jj, m, valid, r, jl, ell, YS, tid_ch);
