@@ -191,29 +191,6 @@ __device__ __forceinline__ void soz_chain_rowblock(const SovOzArgs &p, uint8_t *
             ell += lq;
             S[li * CS + jj] = y;
             ELL8[i * CS + jj] = ell;
-            // y -> 8 digits of y / 128 (reading R24): exact rint of the scaled residual
-            {
-                big |= !(fabs(y) < 63.5);
-                double v = y * 0x1p-7;
-                const int pos = li & 15, sh = (pos & 7) * 8;
-#pragma unroll
-                for (int qd = 0; qd < NSL; ++qd) {
-                    v *= 128.0;
-                    const double t = rint(v);
-                    v -= t;
-                    const uint64_t byte = (uint64_t)((uint32_t)(int)t & 0xffu) << sh;
-                    if (pos < 8) dlo[qd] = (pos == 0 ? 0ull : dlo[qd]) | byte;
-                    else dhi[qd] = (pos == 8 ? 0ull : dhi[qd]) | byte;
-                }
-                if ((li & 15) == 15 || k + 1 == p.n) {
-                    const int kk = (int)(k & 31) & ~15;         // 16-row group inside the 32-row chunk
-                    int8_t *dst = YS + (k >> 5) * (int64_t)HALF + ((m >> 3) << 8) + ((kk >> 4) << 7) + ((m & 7) << 4);
-#pragma unroll
-                    for (int qd = 0; qd < NSL; ++qd)
-                        *reinterpret_cast<uint4 *>(dst + qd * SLICE) =
-                            make_uint4((uint32_t)dlo[qd], (uint32_t)(dlo[qd] >> 32), (uint32_t)dhi[qd], (uint32_t)(dhi[qd] >> 32));
-                }
-            }
             if (i + 1 < 8) s = s_next + Ld[i * RB + li + 1] * y;
 #pragma unroll
             for (int d = 2; d < 8; ++d)
@@ -254,6 +231,43 @@ __device__ __forceinline__ void soz_chain_rowblock(const SovOzArgs &p, uint8_t *
         double yv[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) yv[i] = S[(rb0 + i) * CS + jj];
+        // the sub-block's y -> 8 digits each of y / 128 (reading R24: exact rint of the scaled
+        // residual), off the row recursion's critical path: 8 independent y at a time; a 16-row group
+        // of the Y-digit history (two sub-blocks) is stored as one 16-byte word per slice
+        {
+            uint64_t half[NSL];
+#pragma unroll
+            for (int qd = 0; qd < NSL; ++qd) half[qd] = 0ull;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double y = i < nrows ? yv[i] : 0.0;
+                big |= !(fabs(y) < 63.5);
+                double v = y * 0x1p-7;
+#pragma unroll
+                for (int qd = 0; qd < NSL; ++qd) {
+                    v *= 128.0;
+                    const double t = rint(v);
+                    v -= t;
+                    half[qd] |= (uint64_t)((uint32_t)(int)t & 0xffu) << (8 * i);
+                }
+            }
+            if ((sb & 1) == 0) {
+#pragma unroll
+                for (int qd = 0; qd < NSL; ++qd) { dlo[qd] = half[qd]; dhi[qd] = 0ull; }
+            } else {
+#pragma unroll
+                for (int qd = 0; qd < NSL; ++qd) dhi[qd] = half[qd];
+            }
+            if ((sb & 1) == 1 || left <= 8) {
+                const int64_t k0 = row0 + (rb0 & ~15);          // first row of the 16-row group
+                const int kk = (int)(k0 & 31);
+                int8_t *dst = YS + (k0 >> 5) * (int64_t)HALF + ((m >> 3) << 8) + ((kk >> 4) << 7) + ((m & 7) << 4);
+#pragma unroll
+                for (int qd = 0; qd < NSL; ++qd)
+                    *reinterpret_cast<uint4 *>(dst + qd * SLICE) =
+                        make_uint4((uint32_t)dlo[qd], (uint32_t)(dlo[qd] >> 32), (uint32_t)dhi[qd], (uint32_t)(dhi[qd] >> 32));
+            }
+        }
 #pragma unroll 2
         for (int li = rb0 + 8; li < RB; ++li) {
             double t = S[li * CS + jj];
