@@ -614,12 +614,12 @@ def main():
     # host, H2D of sorted locations and limits, a2..a8, D2H of log P, a10). N > 1: the same steps
     # through parallel.crd_step on every rank from pinned host buffers, max over ranks.
     e2e = None
-    if not args.no_e2e and not multi and args.sov_method == 0 and args.potrf_method == 0:
+    if not args.no_e2e and not multi:
         ts = []
         for it in range(4):                      # one warm-up call (allocations), three timed
             t0 = time.perf_counter()
             out = mvn.mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
-                              cfg.seed_lattice, cfg.conf)
+                              cfg.seed_lattice, cfg.conf, method=args.sov_method | (args.potrf_method << 1))
             t1 = time.perf_counter()
             if it > 0:
                 ts.append(t1 - t0)

@@ -47,7 +47,7 @@ int main(int argc, char **argv) {
     mvn_ctx *ctx = NULL;
     mvn_status st = mvn_create(0, NULL, &ctx);
     if (st != MVN_OK) { fprintf(stderr, "mvn_create: status %d (needs a B200)\n", (int)st); return (int)st; }
-    mvn_crd_problem p = {n, xy, mu, 1.0, 0.1, 0.5, 1e-8, 0.0, N, R, 3001, conf, 4};
+    mvn_crd_problem p = {n, xy, mu, 1.0, 0.1, 0.5, 1e-8, 0.0, N, R, 3001, conf, 4, 0};
     mvn_crd_result r = {order, logP, kstar, tie, -1, {0}};
     st = mvn_crd(ctx, &p, &r);
     if (st != MVN_OK) { fprintf(stderr, "mvn_crd: %s\n", mvn_last_error(ctx)); mvn_destroy(ctx); return (int)st; }

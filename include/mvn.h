@@ -399,7 +399,12 @@ typedef struct {
     uint64_t seed;
     const double *conf;    /* host, nconf levels in (0,1) */
     int64_t nconf;
+    int32_t method;        /* 0: fp64 throughout; bit 0 (MVN_CRD_SOV_INT8): the SOV GEMM on the int8 tensor
+                              cores (mvn_sov_prefix_ex); bit 1 (MVN_CRD_POTRF_INT8): the Cholesky
+                              updates too (mvn_potrf_ex) — NEXT-4 mixed precision */
 } mvn_crd_problem;
+#define MVN_CRD_SOV_INT8 1
+#define MVN_CRD_POTRF_INT8 2
 
 typedef struct {
     int64_t *order;        /* host out, n: original index of sorted position k */

@@ -902,12 +902,15 @@ mvn_status mvn_crd(mvn_ctx *c, const mvn_crd_problem *p, mvn_crd_result *out) {
     if ((s = mvn_cov_matern(c, t, dxy, p->sigma2, p->beta, p->nu, p->nugget, dL)) != MVN_OK) return s;
     MVN_CUDA(c, cudaEventRecord(ev[2], c->stream));
     int64_t info = -1;
-    s = mvn_potrf(c, t, dL, &info);
+    if (p->method & ~(MVN_CRD_SOV_INT8 | MVN_CRD_POTRF_INT8)) return fail(c, MVN_E_USAGE, "mvn_crd: unknown method bits");
+    s = mvn_potrf_ex(c, t, dL, &info, (p->method & MVN_CRD_POTRF_INT8) ? MVN_POTRF_INT8 : MVN_POTRF_FP64);
     out->info = info;
     if (s != MVN_OK) return s;
     MVN_CUDA(c, cudaEventRecord(ev[3], c->stream));
     mvn_qmc q{p->N, p->R, p->seed, 0, p->N * (int64_t)p->R};
-    if ((s = mvn_sov_prefix(c, t, dL, da, nullptr, &q, dM, dS)) != MVN_OK) return s;
+    if ((s = mvn_sov_prefix_ex(c, t, dL, da, nullptr, &q, (p->method & MVN_CRD_SOV_INT8) ? MVN_SOV_INT8 : MVN_SOV_FP64,
+                               dM, dS)) != MVN_OK)
+        return s;
     MVN_CUDA(c, cudaEventRecord(ev[4], c->stream));
     if ((s = mvn_prefix_finalize(c, n, q.N * (int64_t)q.R, dM, dS, dlp)) != MVN_OK) return s;
     MVN_CUDA(c, cudaEventRecord(ev[5], c->stream));

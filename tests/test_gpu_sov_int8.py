@@ -111,3 +111,21 @@ def test_sov_int8_y_out_of_range(torch):
     # s = 0 exactly (Sigma = I): what remains is the device log Phibar(30) against scipy's, a fixed
     # relative bias (measured 4.2e-15) that adds up over the 200 identical rows
     assert np.all(np.abs(lp - want) <= 1e-12 + 1e-14 * np.abs(want))
+
+
+@pytest.mark.parametrize("method", [1, 3])
+def test_mvn_crd_mixed_precision_vs_oracle(torch, monkeypatch, method):
+    """The public end-to-end C call with the mixed-precision bits (1: int8 SOV GEMM, 3: and the int8
+    Cholesky updates, forced on at this size) on config B's geometry: the north_star bars against
+    the oracle's own pipeline (independent mode): |dlog P| <= 1e-8, identical order and regions."""
+    monkeypatch.setenv("MVN_POTRF_OZ_ALWAYS", "1")
+    cfg = W.small_config("crd8", 50, 2000, 4, base="B")
+    inp = W.make_inputs(cfg)
+    out = mvn().mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                        cfg.seed_lattice, cfg.conf, method=method)
+    ref = oracle.crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                     cfg.seed_lattice, cfg.conf, chunk=1000, nthreads=0)
+    assert out.info == -1
+    assert np.array_equal(out.order, ref.order)
+    assert np.max(np.abs(out.logP - ref.logp)) <= 1e-8
+    assert np.array_equal(out.k_star, ref.k_star)
