@@ -215,6 +215,7 @@ def run_mc(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")    # stdout: the one JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     inp = W.make_inputs(cfg)
     n = cfg.n
@@ -538,6 +539,8 @@ def main():
     torch.cuda.set_device(local)
     multi = world > 1 or args.force_dist                 # the multi-GPU code path
     if multi:
+        # NCCL's banner / debug lines go to stdout by default: keep stdout for the one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
