@@ -739,5 +739,18 @@ def main():
     return 0
 
 
+def _stdout_json_only():
+    """Keep the process's stdout for the one JSON line: native libraries (NCCL's version banner and
+    debug lines, CUDA) write to file descriptor 1 directly, so fd 1 is pointed at stderr and Python's
+    sys.stdout (where the JSON line is printed) keeps the original stdout."""
+    try:
+        keep = os.dup(1)
+        os.dup2(2, 1)
+        sys.stdout = os.fdopen(keep, "w", buffering=1)
+    except OSError:
+        pass
+
+
 if __name__ == "__main__":
+    _stdout_json_only()
     sys.exit(main())
