@@ -284,6 +284,41 @@ mvn_status mvn_sov_prefix_units(mvn_ctx *ctx, mvn_tiles t, const double *d_L, co
 /* (M, S) of `units` consecutive unit partials (layout above), combined in unit order (device). */
 mvn_status mvn_prefix_reduce(mvn_ctx *ctx, int64_t n, int64_t units, const double *d_partial, double *d_M, double *d_S);
 
+/* ---------------------------------------------------------------------------------------------
+ * NEXT-1: the sweep over ROW PHASES, for an L that is not resident in one buffer (P:81, P:609-645:
+ * the paper's dense runs keep the tiles distributed). The sweep of mvn_sov_prefix (same samples,
+ * same arithmetic, same bits of (M, S)) is cut into consecutive ranges of tile rows; each call
+ * brings only the tiles of its rows — the rank's own tiles plus the others' broadcast over NVLink
+ * (parallel.sov_distributed), or slices of a full buffer. Between calls the sweep keeps, per sample,
+ * its log weight and its Y history (one slot of n_pad x (w + 4) doubles per 128-sample block).
+ *
+ * mvn_sweep_begin: checks the limits (as mvn_sov_prefix; b may be NULL = +inf), copies a, b and the
+ *   lattice generators, allocates the state (stream-ordered, on the context's stream). *out owns it
+ *   until mvn_sweep_end / mvn_sweep_free.
+ * mvn_sweep_rows: tile rows [tile_row_begin, tile_row_end) of L; tile_row_begin must be where the
+ *   previous call stopped (0 first), tile_row_end <= ceil(n / 128). d_rows (device, caller-owned,
+ *   read by kernels on the stream: keep it unchanged until they are done) holds the tiles (i, j),
+ *   begin <= i < end, j <= i, row after row: tile (i, j) at (i(i+1)/2 + j - begin(begin+1)/2) * nb^2
+ *   doubles — the same order as the full tile-packed buffer, so a slice of it can be passed.
+ * mvn_sweep_end: after the last row, the block partials -> (M, S) as mvn_sov_prefix; frees the state.
+ * mvn_sweep_free: frees the state without results (any time). Errors: MVN_E_USAGE for calls out of
+ *   order or bad arguments (the state stays valid), MVN_E_CUDA.                                  */
+typedef struct mvn_sweep mvn_sweep;
+mvn_status mvn_sweep_begin(mvn_ctx *ctx, int64_t n, const double *d_a, const double *d_b, const mvn_qmc *q,
+                           mvn_sweep **out);
+mvn_status mvn_sweep_rows(mvn_sweep *sw, const double *d_rows, int64_t tile_row_begin, int64_t tile_row_end);
+mvn_status mvn_sweep_end(mvn_sweep *sw, double *d_M, double *d_S);
+void mvn_sweep_free(mvn_sweep *sw);
+
+/* Distributed storage -> row slice: the element offset, in a rank's local buffer (mvn_dtiles
+ * layout), of its first tile in tile row i (i = ceil(n/128): the total), so the rank's tiles of rows
+ * [b, e) are local[off(b) .. off(e)) — one contiguous piece to broadcast. mvn_drows_unpack places
+ * rank d.rank's piece of rows [b, e) (d_piece = that range, device) into the row slice d_rows
+ * (layout of mvn_sweep_rows); other tiles untouched. -1 / MVN_E_USAGE for invalid arguments.     */
+int64_t mvn_drows_offset(mvn_dtiles d, int64_t tile_row);
+mvn_status mvn_drows_unpack(mvn_ctx *ctx, mvn_dtiles d, const double *d_piece, int64_t tile_row_begin,
+                            int64_t tile_row_end, double *d_rows);
+
 /* Multi-GPU combine helpers (reading R11): after all_reduce(MAX) of M into d_Mglob,
  *   S <- S * exp(M - Mglob), M <- Mglob  (elementwise, device; S = 0 where M = -inf).
  * Then all_reduce(SUM) of S and mvn_prefix_finalize.                                           */

@@ -38,7 +38,8 @@ ABI_SYMBOLS = [
     "mvn_posterior", "mvn_posterior_tiles", "mvn_tlr_compress",
     "mvn_dtiles_bytes", "mvn_dpanel_numel", "mvn_dcov_matern", "mvn_dpotrf_panel", "mvn_dpanel_pack",
     "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex", "mvn_potrf_ex", "mvn_dpanel_trsm",
-    "mvn_sov_prefix_units", "mvn_prefix_reduce",
+    "mvn_sov_prefix_units", "mvn_prefix_reduce", "mvn_sweep_begin", "mvn_sweep_rows", "mvn_sweep_end",
+    "mvn_sweep_free", "mvn_drows_offset", "mvn_drows_unpack",
 ]
 
 
@@ -145,6 +146,12 @@ def lib() -> ctypes.CDLL:
         "mvn_potrf_ex": (S, [P, T, P, ctypes.POINTER(I64), I32]),
         "mvn_sov_prefix_units": (S, [P, T, P, P, P, ctypes.POINTER(mvn_qmc), I64, I64, P]),
         "mvn_prefix_reduce": (S, [P, I64, I64, P, P, P]),
+        "mvn_sweep_begin": (S, [P, I64, P, P, ctypes.POINTER(mvn_qmc), ctypes.POINTER(P)]),
+        "mvn_sweep_rows": (S, [P, P, I64, I64]),
+        "mvn_sweep_end": (S, [P, P, P]),
+        "mvn_sweep_free": (None, [P]),
+        "mvn_drows_offset": (I64, [mvn_dtiles, I64]),
+        "mvn_drows_unpack": (S, [P, mvn_dtiles, P, I64, I64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -443,6 +450,86 @@ def mvn_sov_prefix(L, n: int, a, N: int, R: int, seed: int, begin: int = 0, end:
                                  None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q),
                                  _dev_ptr(M), _dev_ptr(S)), "mvn_sov_prefix")
     return M, S
+
+
+class mvn_sweep:
+    """Handle of mvn_sweep_begin (the SOV sweep over row phases, NEXT-1): the samples' log weights and
+    Y histories between mvn_sweep_rows calls. Freed by mvn_sweep_end / mvn_sweep_free (or on garbage
+    collection)."""
+
+    def __init__(self, h, n: int, device):
+        self.h, self.n, self.device = h, n, device
+        self.nt = -(-n // TILE)
+        self.next = 0
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.mvn_sweep_free(self.h)
+            self.h = None
+
+
+def mvn_sweep_begin(n: int, a, N: int, R: int, seed: int, begin: int = 0, end: int | None = None, b=None,
+                    stream=None) -> mvn_sweep:
+    import torch
+    c = Context.get(a.device.index, stream)
+    end = N * R if end is None else end
+    q = mvn_qmc(int(N), int(R), int(seed), int(begin), int(end))
+    h = ctypes.c_void_p()
+    c.check(lib().mvn_sweep_begin(c.h, int(n), _dev_ptr(a, torch.float64),
+                                  None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q),
+                                  ctypes.byref(h)), "mvn_sweep_begin")
+    return mvn_sweep(h, int(n), a.device)
+
+
+def mvn_sweep_rows(sw: mvn_sweep, rows, tile_row_begin: int, tile_row_end: int, stream=None):
+    """rows: the tiles of tile rows [begin, end) in packed order (tile_rows_slice of a full buffer, or
+    a slice assembled from the ranks' storage with mvn_drows_unpack)."""
+    import torch
+    c = Context.get(sw.device.index, stream)
+    if not sw.h:
+        raise MvnError(-1, "mvn_sweep_rows: sweep already ended")
+    c.check(lib().mvn_sweep_rows(sw.h, _dev_ptr(rows, torch.float64), int(tile_row_begin), int(tile_row_end)),
+            "mvn_sweep_rows")
+    sw.next = int(tile_row_end)
+
+
+def mvn_sweep_end(sw: mvn_sweep, M=None, S=None, stream=None):
+    """(M, S) of the sweep (as mvn_sov_prefix); frees the handle."""
+    import torch
+    c = Context.get(sw.device.index, stream)
+    M = torch.empty(sw.n, dtype=torch.float64, device=sw.device) if M is None else M
+    S = torch.empty(sw.n, dtype=torch.float64, device=sw.device) if S is None else S
+    c.check(lib().mvn_sweep_end(sw.h, _dev_ptr(M), _dev_ptr(S)), "mvn_sweep_end")
+    sw.h = None
+    return M, S
+
+
+def mvn_sweep_free(sw: mvn_sweep):
+    if sw.h:
+        Context.get(sw.device.index)
+        lib().mvn_sweep_free(sw.h)
+        sw.h = None
+
+
+def tile_rows_range(tile_row_begin: int, tile_row_end: int) -> tuple[int, int]:
+    """Element range of tile rows [begin, end) in the full tile-packed buffer."""
+    b, e = int(tile_row_begin), int(tile_row_end)
+    return b * (b + 1) // 2 * TILE * TILE, e * (e + 1) // 2 * TILE * TILE
+
+
+def tile_rows_slice(L, tile_row_begin: int, tile_row_end: int):
+    lo, hi = tile_rows_range(tile_row_begin, tile_row_end)
+    return L[lo:hi]
+
+
+def mvn_drows_offset(d: mvn_dtiles, tile_row: int) -> int:
+    return int(lib().mvn_drows_offset(d, int(tile_row)))
+
+
+def mvn_drows_unpack(d: mvn_dtiles, piece, tile_row_begin: int, tile_row_end: int, rows, stream=None):
+    c = Context.get(rows.device.index, stream)
+    c.check(lib().mvn_drows_unpack(c.h, d, _dev_ptr(piece), int(tile_row_begin), int(tile_row_end), _dev_ptr(rows)),
+            "mvn_drows_unpack")
 
 
 SOV_FP64, SOV_INT8 = 0, 1

@@ -662,6 +662,31 @@ cudaError_t launch_panel_copy_map(int64_t n, const TileMap &from, const TileMap 
     return cudaGetLastError();
 }
 
+// Tile-row copy: the tiles (i, j), tb <= i < te, j <= i, that `from` owns, to their places in `to`
+// (the row slice of mvn_sweep_rows: a full map whose base is offset to tile row tb). grid (8, tiles
+// of the rows, 8): one CTA per (tile, 1/8), row-major tile enumeration from (tb, 0).
+__global__ void __launch_bounds__(256) k_rows_copy(const TileMap from, const TileMap to, int tb) {
+    const int64_t id = (int64_t)blockIdx.x + (int64_t)tb * (tb + 1) / 2;
+    int ti = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
+    while ((int64_t)ti * (ti + 1) / 2 > id) --ti;
+    while ((int64_t)(ti + 1) * (ti + 2) / 2 <= id) ++ti;
+    const int tj = (int)(id - (int64_t)ti * (ti + 1) / 2);
+    if (!from.owns_col(tj) || !from.owns_row(ti)) return;
+    const double2 *f = reinterpret_cast<const double2 *>(from.tile(ti, tj));
+    double2 *t = reinterpret_cast<double2 *>(to.tile(ti, tj));
+    constexpr int PER = kTile * kTile / 2 / 8;
+    const int e0 = blockIdx.y * PER;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < PER; e += 256) t[e0 + e] = f[e0 + e];
+}
+
+cudaError_t launch_rows_copy_map(const TileMap &from, const TileMap &to, int tb, int te, cudaStream_t st) {
+    const int64_t ntiles = (int64_t)te * (te + 1) / 2 - (int64_t)tb * (tb + 1) / 2;
+    if (ntiles <= 0) return cudaSuccess;
+    k_rows_copy<<<dim3((unsigned)ntiles, 8), 256, 0, st>>>(from, to, tb);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_panel_copy(int64_t n, double *tiles, int k, int kp, double *panel, bool to_panel, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
     const TileMap full = TileMap::full(tiles), pan = TileMap::panel(panel, k, std::min(kp, nt - k));

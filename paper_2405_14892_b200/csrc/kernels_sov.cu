@@ -121,6 +121,15 @@ struct SovArgs {
     int serial_rb;            // row blocks rb <= serial_rb * 128 / w: GEMM of rb waits for the chain of rb-1
     int unit_mode;            // 1: blocks are the global 128-sample units (deterministic per-unit partials)
     int64_t part_stride;      // rows per block in `part` (n_pad, or n for the caller's unit partials)
+    // row phases (mvn_sweep_rows): this launch runs row blocks [rb0, rb1) of every sample block; the
+    // chain state that crosses row blocks is the log weight ell (ell[g - g_base] between launches)
+    // and the Y history, which then needs one slot per sample block (yoff[cta]: the CTA's first slot,
+    // in doubles from Y; the CTA's blocks follow at n_pad * (w + 4) each). Whole sweep: rb0 = 0,
+    // rb1 = nrb, ell = yoff = null (one Y slot per CTA, reused by its blocks).
+    int rb0, rb1;
+    double *ell;
+    int64_t g_base;
+    const int64_t *yoff;
 };
 
 // Sample blocks of a CTA: its `count` samples are split into nblk = ceil(count / 128) blocks whose
@@ -134,7 +143,7 @@ struct SovArgs {
 // of the range, so a unit's samples sit on the same lanes whatever the partition (W-independent
 // per-unit partials).
 struct BlockGeom { int64_t off; int cnt, w; };
-__device__ __forceinline__ BlockGeom block_geom(int64_t count, int b, int unit_mode = 0) {
+__host__ __device__ __forceinline__ BlockGeom block_geom(int64_t count, int b, int unit_mode = 0) {
     if (unit_mode) {
         BlockGeom g;
         g.off = (int64_t)b * sovk::NB;
@@ -153,13 +162,20 @@ __device__ __forceinline__ BlockGeom block_geom(int64_t count, int b, int unit_m
     return g;
 }
 
+// Y-history slot of sample block b of this CTA (see SovArgs::yoff)
+__device__ __forceinline__ double *y_slot(const SovArgs &p, int64_t count, int b) {
+    if (!p.yoff) return p.Y + (int64_t)blockIdx.x * p.n_pad * sovk::SB;
+    int64_t off = p.yoff[blockIdx.x];
+    for (int i = 0; i < b; ++i) off += p.n_pad * (block_geom(count, i, p.unit_mode).w + 4);
+    return p.Y + off;
+}
+
 // ------------------------------------------------------------------------------------ producer
 // One warp streams K-chunks (BK columns of the L row panel + BK rows of the Y history) into the
 // STAGES-deep ring: the L columns by cp.async (one 16-byte piece per lane per column), the Y rows by
 // one TMA bulk copy. The chunk of row block r whose Y rows come from row
 // block r-1 is only issued after the chain warps have published Y_{r-1} (barrier Y_READY).
-__device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const double *Yslot, int64_t count, int nblk,
-                                             int lane) {
+__device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, int64_t count, int nblk, int lane) {
     using namespace sovk;
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
     uint64_t *empty = full + STAGES;
@@ -167,8 +183,9 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
     const uint64_t pol_L = policy_evict_last(), pol_Y = policy_evict_first();
     for (int b = 0; b < nblk; ++b) {
         const int w = block_geom(count, b, p.unit_mode).w, sbw = w + 4;    // this block's Y-history row stride
+        const double *Yslot = y_slot(p, count, b);
         if (p.lag > 0 && lane == 0) atomicAdd(p.step_done + (int64_t)b * p.nrb, 1);   // row block 0: no GEMM
-        for (int rb = 1; rb < p.nrb; ++rb) {
+        for (int rb = p.rb0 > 1 ? p.rb0 : 1; rb < p.rb1; ++rb) {
             const int64_t row0 = (int64_t)rb * M;
             const int R = (int)(row0 / kTile), hh = (int)(row0 % kTile);
             if (p.lag > 0) {
@@ -192,7 +209,8 @@ __device__ __forceinline__ void sov_producer(const SovArgs &p, double *sm, const
             // chain gets the fp64 pipe to itself (7x faster per row than next to DMMA) —
             // cheaper than overlapping where the GEMM of a row block is shorter than the contended chain.
             // (the GEMM of a row block scales with the block width w; the chain does not)
-            const int c_sync = rb * w <= p.serial_rb * NB ? 0 : CPB * (rb - 1);
+            // (first row block of a later phase: Y_{rb-1} was written by the previous launch)
+            const int c_sync = rb == p.rb0 ? -1 : rb * w <= p.serial_rb * NB ? 0 : CPB * (rb - 1);
             for (int c = 0; c < CPB * rb; ++c, ++q) {
                 if (c == c_sync) named_sync(BAR_YREADY, N_YREADY);
                 const int st = q % STAGES;
@@ -447,7 +465,6 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
     const int tid = threadIdx.x;
     const int64_t g_first = p.cta[blockIdx.x * 3], count = p.cta[blockIdx.x * 3 + 1], blk_first = p.cta[blockIdx.x * 3 + 2];
     const int nblk = (int)((count + NB - 1) / NB);
-    double *Yslot = p.Y + (int64_t)blockIdx.x * p.n_pad * SB;
     if (tid == 0) {
         uint64_t *full = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
         for (int s = 0; s < STAGES; ++s) {
@@ -468,7 +485,7 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
             // layout 2 x 4 (u % 4 == 0): column group warp / 2; layout 4 x 2: half warp / 4
             const int half = warp >> 2, u0 = (u + 1) >> 1;
             const int wn0 = (u & 3) == 0 ? (warp >> 1) * 2 * u : half * 8 * u0;
-            for (int rb = 1; rb < p.nrb; ++rb) {
+            for (int rb = p.rb0 > 1 ? p.rb0 : 1; rb < p.rb1; ++rb) {
 #define MVN_G2(U) case U: if (half == 0) sov_gemm_rowblock<16, (U + 1) / 2>(sm, rb, tid, wn0, sbw, q); \
                           else sov_gemm_rowblock<16, U / 2>(sm, rb, tid, wn0, sbw, q); break;
                 switch (u) {
@@ -496,8 +513,9 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
             const uint64_t r = g / (uint64_t)p.N;
             const uint64_t jl = g - r * (uint64_t)p.N + 1ull;    // 1-based lattice index
             const int64_t blk = blk_first + b;
-            double ell = 0.0;
-            for (int rb = 0; rb < p.nrb; ++rb) {
+            double *Yslot = y_slot(p, count, b);
+            double ell = (p.ell && p.rb0 > 0 && j < cnt) ? p.ell[g - p.g_base] : 0.0;
+            for (int rb = p.rb0; rb < p.rb1; ++rb) {
                 chain_load<HAS_B>(p, sm, rb, j);                  // Ld / a / G of this row block
                 cp_async_commit();
                 if (rb > 0) named_sync(BAR_SFULL, N_SFULL);       // S_rb written by the GEMM warps
@@ -525,10 +543,11 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
                     }
                 }
             }
+            if (p.ell && j < cnt) p.ell[(int64_t)g - p.g_base] = ell;   // for the next row phase
         }
     } else {
         // ============================================================ producer warp
-        sov_producer(p, sm, Yslot, count, nblk, tid & 31);
+        sov_producer(p, sm, count, nblk, tid & 31);
     }
 }
 
@@ -591,12 +610,26 @@ int64_t sov_partition(int64_t g_begin, int64_t g_end, int grid, int64_t *cta) {
     return blk;
 }
 
+// Row phases: Y slot offsets (doubles) of each CTA's first sample block, one slot of n_pad x (w + 4)
+// per block (block_geom widths); returns the total doubles.
+int64_t sov_phase_yoff(const int64_t *cta, int grid, int64_t n_pad, int unit_mode, int64_t *yoff) {
+    int64_t off = 0;
+    for (int c = 0; c < grid; ++c) {
+        yoff[c] = off;
+        const int64_t count = cta[3 * c + 1];
+        const int nb = (int)((count + sovk::NB - 1) / sovk::NB);
+        for (int b = 0; b < nb; ++b) off += n_pad * (block_geom(count, b, unit_mode).w + 4);
+    }
+    return off;
+}
+
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
     SovArgs a;
     a.L = L.L; a.n = L.n; a.nrb = (int)((L.n + 63) / 64); a.a = L.a; a.b = L.b; a.G = L.G; a.N = L.N;
     a.seed = L.seed; a.cta = L.cta; a.n_pad = (int64_t)a.nrb * 64; a.Y = L.Y; a.part = L.part;
     a.lag = L.lag; a.step_done = L.step_done; a.need = L.need; a.hints = L.hints; a.serial_rb = L.serial_rb;
     a.unit_mode = L.unit_mode; a.part_stride = L.unit_mode ? L.n : a.n_pad;
+    a.rb0 = L.rb1 > 0 ? L.rb0 : 0; a.rb1 = L.rb1 > 0 ? L.rb1 : a.nrb; a.ell = L.ell; a.g_base = L.g_begin; a.yoff = L.yoff;
     if (a.lag > 0) {
         cudaError_t e = cudaMemsetAsync(L.step_done, 0, sizeof(int) * (size_t)L.max_blocks * a.nrb, st);
         if (e != cudaSuccess) return e;
@@ -605,7 +638,7 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
     else k_sov<false><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (L.unit_mode) return cudaSuccess;                       // the caller reduces the unit partials
+    if (L.unit_mode || L.rb1 > 0) return cudaSuccess;          // the caller reduces the partials
     return launch_reduce_blocks(L.part, L.nblk, L.n, a.n_pad, L.Mout, L.Sout, st);
 }
 

@@ -609,6 +609,143 @@ mvn_status mvn_sov_prefix_units(mvn_ctx *c, mvn_tiles t, const double *d_L, cons
     return sov_prefix_impl(c, t, d_L, d_a, d_b, q, unit_begin, unit_end, d_partial, nullptr, nullptr);
 }
 
+}  // extern "C"
+
+struct mvn_sweep {
+    mvn_ctx *c = nullptr;
+    int64_t n = 0, nt = 0, n_pad = 0, next = 0, nblk = 0, g_begin = 0, g_end = 0, N = 0;
+    uint64_t seed = 0;
+    int grid = 0;
+    double *a = nullptr, *b = nullptr, *Y = nullptr, *part = nullptr, *ell = nullptr;
+    uint64_t *G = nullptr;
+    int64_t *cta = nullptr, *yoff = nullptr;
+};
+
+namespace {
+void sweep_release(mvn_sweep *sw) {
+    if (!sw) return;
+    cudaStream_t st = sw->c ? sw->c->stream : nullptr;
+    for (void *p : {(void *)sw->a, (void *)sw->b, (void *)sw->Y, (void *)sw->part, (void *)sw->ell, (void *)sw->G,
+                    (void *)sw->cta, (void *)sw->yoff})
+        if (p) cudaFreeAsync(p, st);
+    delete sw;
+}
+template <class T>
+cudaError_t sweep_alloc(T **p, size_t count, cudaStream_t st) {
+    return cudaMallocAsync(reinterpret_cast<void **>(p), std::max<size_t>(count, 1) * sizeof(T), st);
+}
+}  // namespace
+
+extern "C" {
+
+mvn_status mvn_sweep_begin(mvn_ctx *c, int64_t n, const double *d_a, const double *d_b, const mvn_qmc *q,
+                           mvn_sweep **out) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!out || n < 1 || !d_a || !q || q->N < 1 || q->R < 1 || q->sample_begin < 0 ||
+        q->sample_end <= q->sample_begin || q->sample_end > q->N * (int64_t)q->R)
+        return fail(c, MVN_E_USAGE, "mvn_sweep_begin: bad arguments (0 <= begin < end <= N*R)");
+    *out = nullptr;
+    mvn_status s;
+    if ((s = ensure_generators(c, n)) != MVN_OK) return s;
+    {
+        int *d_flag = reinterpret_cast<int *>(c->d_info) + 2;
+        int h_flag = 0;
+        MVN_CUDA(c, mvn::launch_check_limits(n, d_a, d_b, d_flag, c->stream));
+        MVN_CUDA(c, cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (h_flag) return fail(c, MVN_E_USAGE, "mvn_sweep_begin: a limit is NaN or a_k > b_k");
+    }
+    mvn_sweep *sw = new mvn_sweep;
+    sw->c = c; sw->n = n; sw->nt = (n + mvn::kTile - 1) / mvn::kTile; sw->n_pad = (n + 63) / 64 * 64;
+    sw->g_begin = q->sample_begin; sw->g_end = q->sample_end; sw->N = q->N; sw->seed = q->seed;
+    const int64_t nsamp = sw->g_end - sw->g_begin;
+    sw->grid = (int)std::min<int64_t>(nsamp, c->nsm);
+    std::vector<int64_t> cta((size_t)sw->grid * 3), yoff((size_t)sw->grid);
+    sw->nblk = mvn::sov_partition(sw->g_begin, sw->g_end, sw->grid, cta.data());
+    const int64_t ydoubles = mvn::sov_phase_yoff(cta.data(), sw->grid, sw->n_pad, 0, yoff.data());
+    cudaStream_t st = c->stream;
+    cudaError_t e = cudaSuccess;
+    if (!e) e = sweep_alloc(&sw->a, (size_t)n, st);
+    if (!e && d_b) e = sweep_alloc(&sw->b, (size_t)n, st);
+    if (!e) e = sweep_alloc(&sw->G, (size_t)n, st);
+    if (!e) e = sweep_alloc(&sw->cta, cta.size(), st);
+    if (!e) e = sweep_alloc(&sw->yoff, yoff.size(), st);
+    if (!e) e = sweep_alloc(&sw->Y, (size_t)ydoubles, st);
+    if (!e) e = sweep_alloc(&sw->part, (size_t)sw->nblk * sw->n_pad * 2, st);
+    if (!e) e = sweep_alloc(&sw->ell, (size_t)nsamp, st);
+    if (!e) e = cudaMemcpyAsync(sw->a, d_a, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+    if (!e && d_b) e = cudaMemcpyAsync(sw->b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+    if (!e) e = cudaMemcpyAsync(sw->G, c->G, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, st);
+    if (!e) e = cudaMemcpyAsync(sw->cta, cta.data(), sizeof(int64_t) * cta.size(), cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaMemcpyAsync(sw->yoff, yoff.data(), sizeof(int64_t) * yoff.size(), cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaStreamSynchronize(st);               // the host vectors above go out of scope
+    if (e) {
+        sweep_release(sw);
+        return cuda_fail(c, e, "mvn_sweep_begin");
+    }
+    *out = sw;
+    return MVN_OK;
+}
+
+mvn_status mvn_sweep_rows(mvn_sweep *sw, const double *d_rows, int64_t tb, int64_t te) {
+    if (!sw) return MVN_E_USAGE;
+    mvn_ctx *c = sw->c;
+    DevGuard dev_guard(c);
+    if (!d_rows || tb != sw->next || te <= tb || te > sw->nt)
+        return fail(c, MVN_E_USAGE, "mvn_sweep_rows: rows must continue where the previous call stopped (tile_row_begin = " +
+                                        std::to_string(sw->next) + ", begin < end <= " + std::to_string(sw->nt) + ")");
+    mvn::SovLaunch L;
+    // the kernels address tile (i, j) as L + (i(i+1)/2 + j) nb^2; only rows [tb, te) are read
+    const int64_t shift = tb * (tb + 1) / 2 * (int64_t)mvn::kTile * mvn::kTile;
+    L.L = reinterpret_cast<const double *>(reinterpret_cast<uintptr_t>(d_rows) - (uintptr_t)shift * sizeof(double));
+    L.n = sw->n; L.a = sw->a; L.b = sw->b; L.G = sw->G; L.N = sw->N; L.seed = sw->seed;
+    L.g_begin = sw->g_begin; L.g_end = sw->g_end; L.cta = sw->cta; L.nblk = sw->nblk; L.grid = sw->grid;
+    L.Y = sw->Y; L.part = sw->part; L.lag = 0; L.hints = 1;
+    const int64_t nrb = sw->n_pad / 64;
+    L.rb0 = (int)(2 * tb); L.rb1 = (int)std::min<int64_t>(2 * te, nrb);
+    L.ell = sw->ell; L.yoff = sw->yoff;
+    MVN_CUDA(c, mvn::launch_sov(L, c->stream));
+    sw->next = te;
+    return MVN_OK;
+}
+
+mvn_status mvn_sweep_end(mvn_sweep *sw, double *d_M, double *d_S) {
+    if (!sw) return MVN_E_USAGE;
+    mvn_ctx *c = sw->c;
+    DevGuard dev_guard(c);
+    if (!d_M || !d_S || sw->next != sw->nt)
+        return fail(c, MVN_E_USAGE, "mvn_sweep_end: bad arguments or rows missing (next tile row " + std::to_string(sw->next) +
+                                        " of " + std::to_string(sw->nt) + ")");
+    MVN_CUDA(c, mvn::launch_reduce_blocks(sw->part, sw->nblk, sw->n, sw->n_pad, d_M, d_S, c->stream));
+    sweep_release(sw);
+    return MVN_OK;
+}
+
+void mvn_sweep_free(mvn_sweep *sw) {
+    if (!sw) return;
+    DevGuard dev_guard(sw->c);
+    sweep_release(sw);
+}
+
+int64_t mvn_drows_offset(mvn_dtiles d, int64_t i) {
+    if (!dtiles_ok(d) || i < 0 || i > dtiles_nt(d)) return -1;
+    return dmap(d, nullptr).index(i, 0) * (int64_t)(d.nb * d.nb);
+}
+
+mvn_status mvn_drows_unpack(mvn_ctx *c, mvn_dtiles d, const double *d_piece, int64_t tb, int64_t te, double *d_rows) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!dtiles_ok(d) || !d_piece || !d_rows || tb < 0 || te <= tb || te > dtiles_nt(d))
+        return fail(c, MVN_E_USAGE, "mvn_drows_unpack: bad arguments");
+    const uintptr_t from_shift = (uintptr_t)mvn_drows_offset(d, tb) * sizeof(double);
+    const uintptr_t to_shift = (uintptr_t)(tb * (tb + 1) / 2) * mvn::kTile * mvn::kTile * sizeof(double);
+    const mvn::TileMap from = dmap(d, reinterpret_cast<double *>(reinterpret_cast<uintptr_t>(d_piece) - from_shift));
+    const mvn::TileMap to = mvn::TileMap::full(reinterpret_cast<double *>(reinterpret_cast<uintptr_t>(d_rows) - to_shift));
+    MVN_CUDA(c, mvn::launch_rows_copy_map(from, to, (int)tb, (int)te, c->stream));
+    return MVN_OK;
+}
+
 mvn_status mvn_prefix_reduce(mvn_ctx *c, int64_t n, int64_t units, const double *d_partial, double *d_M, double *d_S) {
     DevGuard dev_guard(c);
     if (!c || n < 1 || units < 1 || !d_partial || !d_M || !d_S) return fail(c, MVN_E_USAGE, "mvn_prefix_reduce: bad arguments");

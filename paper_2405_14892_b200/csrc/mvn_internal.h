@@ -51,6 +51,7 @@ cudaError_t launch_potrf_update_map(int64_t n, const TileMap &dst, const TileMap
 cudaError_t launch_panel_trsm_map(int64_t n, const TileMap &tm, const TileMap &pb, int k, int w, const RowSel &rs,
                                   cudaStream_t st);
 cudaError_t launch_panel_copy_map(int64_t n, const TileMap &from, const TileMap &to, int k, int kp, cudaStream_t st);
+cudaError_t launch_rows_copy_map(const TileMap &from, const TileMap &to, int tb, int te, cudaStream_t st);
 cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
                                   const TileMap &tm, cudaStream_t st);
 
@@ -75,7 +76,14 @@ struct SovLaunch {
     int hints = 1;           // L2 cache-policy hints
     int serial_rb = 0;       // row blocks whose GEMM waits for the previous chain (no fp64 contention)
     int unit_mode = 0;       // 1: blocks = global 128-sample units, partials [units][n][2] left in `part`
+    // row phases (mvn_sweep_rows): rb1 > 0 runs row blocks [rb0, rb1) only, carrying the log weights
+    // in ell[g - g_begin] and the Y histories in per-block slots (yoff: sov_phase_yoff); the
+    // partials stay in `part` (no reduce)
+    int rb0 = 0, rb1 = 0;
+    double *ell = nullptr;
+    const int64_t *yoff = nullptr;
 };
+int64_t sov_phase_yoff(const int64_t *cta, int grid, int64_t n_pad, int unit_mode, int64_t *yoff);
 cudaError_t sov_init();
 int sov_block_samples();
 int sov_y_stride();

@@ -551,3 +551,109 @@ def potrf_distributed(L, n: int, group=None, ops=None, force_collectives: bool =
 def _cuda_info(L) -> int:
     from . import mvn_potrf_info
     return mvn_potrf_info(L.device.index, reset=True)
+
+
+# ---------------------------------------------------------------------------- NEXT-1, the SOV sweep
+def sov_phases(nt: int, phase_rows: int) -> list[tuple[int, int]]:
+    """Consecutive tile-row ranges [b, e) of phase_rows rows covering [0, nt)."""
+    phase_rows = max(int(phase_rows), 1)
+    return [(b, min(b + phase_rows, nt)) for b in range(0, nt, phase_rows)]
+
+
+def sov_rows_schedule(ops, nphases: int):
+    """The per-rank loop of the sweep over distributed L: the pieces of phase p + 1 are broadcast
+    while phase p sweeps. comm(p) issues the broadcasts of phase p (asynchronous: the NCCL stream
+    waits only for the work already queued, so issuing comm(p + 1) BEFORE queueing sweep(p) lets
+    the transfer overlap it); wait(h) orders the compute stream after them; assemble(p) places the
+    ranks' pieces in the row slice (a copy kernel on the compute stream, so it runs after sweep(p - 1)
+    has read the slice); sweep(p) runs the kernels of the phase's rows. A receive buffer is rewritten
+    by comm(p + 1) only after assemble(p), queued before it, has read it."""
+    h = ops.comm(0) if nphases else None
+    for p in range(nphases):
+        ops.wait(h)
+        ops.assemble(p)
+        h = ops.comm(p + 1) if p + 1 < nphases else None
+        ops.sweep(p)
+
+
+class CudaSovRowsOps:
+    """sov_rows_schedule's building blocks on a rank's distributed storage (mvn_dtiles, 1-D or 2-D):
+    rank r's tiles of rows [b, e) are one contiguous piece of its buffer (mvn_drows_offset), broadcast
+    from r to every rank (this rank's own piece straight from its storage) and placed in the row
+    slice by mvn_drows_unpack; mvn_sweep_rows then runs the phase."""
+
+    def __init__(self, local, n: int, world: int, rank: int, kp: int, prows: int, phases, sweep, group=None,
+                 use_comm: bool = True):
+        from . import dtiles, mvn_drows_offset, tile_rows_range
+        self.local, self.n, self.world, self.rank = local, n, world, rank
+        self.phases, self.sw, self.group, self.use_comm = phases, sweep, group, use_comm
+        nt = -(-n // 128)
+        self.d = [dtiles(n, world, r, kp, prows) for r in range(world)]
+        self.off = [[mvn_drows_offset(self.d[r], i) for i in range(nt + 1)] for r in range(world)]
+        piece = max((self.off[r][e] - self.off[r][b] for r in range(world) for b, e in phases), default=0)
+        slc = max((tile_rows_range(b, e)[1] - tile_rows_range(b, e)[0] for b, e in phases), default=0)
+        dev = local.device
+        self.recv = {r: torch.empty(max(piece, 1), dtype=torch.float64, device=dev) for r in range(world) if r != rank}
+        self.rows = torch.empty(max(slc, 1), dtype=torch.float64, device=dev)
+
+    def piece(self, r: int, p: int):
+        b, e = self.phases[p]
+        lo, hi = self.off[r][b], self.off[r][e]
+        return self.local[lo:hi] if r == self.rank else self.recv[r][:hi - lo]
+
+    def comm(self, p: int):
+        if not self.use_comm:
+            return None
+        hs = []
+        for r in range(self.world):
+            buf = self.piece(r, p)
+            if buf.numel() == 0:
+                continue
+            src = dist.get_global_rank(self.group, r) if self.group is not None else r
+            hs.append(dist.broadcast(buf, src=src, group=self.group, async_op=True))
+        return hs
+
+    def wait(self, hs):
+        for h in hs or ():
+            h.wait()
+
+    def slice(self, p: int):
+        from . import tile_rows_range
+        b, e = self.phases[p]
+        lo, hi = tile_rows_range(b, e)
+        return self.rows[:hi - lo]
+
+    def assemble(self, p: int):
+        from . import mvn_drows_unpack
+        b, e = self.phases[p]
+        out = self.slice(p)
+        for r in range(self.world):
+            pc = self.piece(r, p)
+            if pc.numel():
+                mvn_drows_unpack(self.d[r], pc, b, e, out)
+
+    def sweep(self, p: int):
+        from . import mvn_sweep_rows
+        b, e = self.phases[p]
+        mvn_sweep_rows(self.sw, self.slice(p), b, e)
+
+
+def sov_distributed(local, n: int, d_a, N: int, R: int, seed: int, begin: int, end: int, kp: int, prows: int = 1,
+                    group=None, phase_rows: int = 8, force_collectives: bool = False):
+    """The SOV sweep of samples [begin, end) on this rank with L on DISTRIBUTED storage (`local`:
+    this rank's mvn_dtiles buffer, e.g. after potrf_distributed_local / potrf_distributed_2d), phase
+    after phase of `phase_rows` tile rows, each phase's rows gathered from all ranks over NCCL while
+    the previous phase sweeps. Returns this rank's (M, S) — bitwise those of mvn_sov_prefix on the
+    full L for the same range — to be combined over the ranks as usual (combine_prefix)."""
+    from . import mvn_sweep_begin, mvn_sweep_end
+    initialized = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if initialized else 1
+    rank = dist.get_rank(group) if initialized else 0
+    use_comm = initialized and (world > 1 or force_collectives or FORCE_COLLECTIVES)
+    nt = -(-n // 128)
+    phases = sov_phases(nt, phase_rows)
+    sw = mvn_sweep_begin(n, d_a, N, R, seed, begin, end)
+    ops = CudaSovRowsOps(local, n, world, rank, kp, prows, phases, sw, group=group, use_comm=use_comm)
+    sov_rows_schedule(ops, len(phases))
+    return mvn_sweep_end(sw)
+

@@ -107,3 +107,26 @@ def test_broadcast_L_forced_is_identity(nccl):
     broadcast_L(T, force_collectives=True)
     torch.cuda.synchronize()
     assert torch.equal(T, T0)
+
+
+def test_sov_distributed_with_nccl_broadcasts(nccl):
+    """The sweep over distributed L (NEXT-1) on the one-rank NCCL communicator with the phase
+    broadcasts forced (issued asynchronously before the previous phase's sweep, waited on before
+    the assembly): (M, S) bitwise equal to mvn_sov_prefix on the same factor."""
+    import torch
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200.parallel import sov_distributed
+    n = 40 * 128 + 77
+    xy = np.random.default_rng(4).uniform(size=(n, 2))
+    d_xy = torch.from_numpy(xy).cuda()
+    kp = mvn.mvn_potrf_panel_width(n)
+    loc = mvn.alloc_dtiles(n, 1, 0, kp)
+    L = mvn.mvn_cov_matern(d_xy, 1.0, 0.05, 1.5, 1e-8)
+    assert mvn.mvn_potrf(L, n) == -1
+    assert loc.numel() == L.numel()             # W = 1: the local layout is the full tile-packed one
+    loc.copy_(L)
+    a = torch.from_numpy(np.random.default_rng(5).normal(0.3, 1.0, n)).cuda()
+    M, S = sov_distributed(loc, n, a, 2000, 3, 7, 100, 5900, kp, phase_rows=6, force_collectives=True)
+    M0, S0 = mvn.mvn_sov_prefix(L, n, a, 2000, 3, 7, 100, 5900)
+    torch.cuda.synchronize()
+    assert torch.equal(M, M0) and torch.equal(S, S0)
