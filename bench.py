@@ -153,7 +153,9 @@ def config_dict(cfg, world: int, mode: str) -> dict:
                         f"(s2={cfg.sigma2}, beta={cfg.beta}, nu={cfg.nu}) + nugget {cfg.nugget}, u={cfg.u}, "
                         f"N={cfg.N} x R={cfg.R} QMC", "n": cfg.n, "N": cfg.N, "R": cfg.R,
             "parallelism": (f"samples sharded over {world} GPU(s); " +
-                            ("Cholesky 1-D block-cyclic over the GPUs (NEXT-1)" if mode == "dist" and world > 1
+                            ("tiles on distributed storage (1-D block-cyclic, ~1/W per GPU), distributed "
+                             "Cholesky, sweep gathering each phase's rows (NEXT-1)" if mode == "dstore"
+                             else "Cholesky 1-D block-cyclic over the GPUs (NEXT-1)" if mode == "dist" and world > 1
                              else "Cholesky on rank 0, L broadcast" if world > 1 else "one GPU")),
             "l2": "flushed between timed steps (256 MB write); L itself is "
                   f"{8 * cfg.n * (cfg.n + 1) / 2 / 1e9:.2f} GB (> 126 MB L2)"}
@@ -488,9 +490,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--potrf", default="auto", choices=["auto", "rank0", "dist"],
+    ap.add_argument("--potrf", default="auto", choices=["auto", "rank0", "dist", "dstore"],
                     help="N>1: factor on rank 0 + broadcast L (north_star), or distributed (NEXT-1); "
-                         "auto = rank0")
+                         "dstore: NEXT-1 on distributed storage end to end (each rank holds ~1/N of the "
+                         "tiles; the sweep gathers each phase's rows, --phase-rows); auto = rank0")
+    ap.add_argument("--phase-rows", type=int, default=16,
+                    help="--potrf dstore: tile rows per phase of the sweep over distributed L")
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: run the multi-GPU code path (NCCL process group, distributed Cholesky, "
                          "all_reduce combine, pinned-buffer e2e) even with one rank")
@@ -557,11 +562,17 @@ def main():
     order, a, _ = mvn.mvn_marginal_order(inp.mu, var, cfg.u)
     d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
     d_a = torch.from_numpy(a).cuda()
-    L = mvn.alloc_tiles(n)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
-
     mode = potrf_mode(args, world, args.force_dist)
+    if mode == "dstore":
+        if (args.sov_method, args.potrf_method) != (0, 0):
+            raise SystemExit("--potrf dstore runs the fp64 path (--sov-method 0 --potrf-method 0)")
+        L = mvn.alloc_dtiles(n, world, rank, mvn.mvn_potrf_panel_width(n))
+    else:
+        L = mvn.alloc_tiles(n)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
     step_ops = parallel.crd_ops(args.sov_method, args.potrf_method)
+    if mode == "dstore":
+        step_ops = type("LibmvnCrdOpsPhases", (step_ops,), {"phase_rows": args.phase_rows})
 
     def step(events=None):
         logp = parallel.crd_step(d_xy, d_a, L, cfg, events=events, potrf=mode, ops=step_ops)
@@ -617,7 +628,7 @@ def main():
     # host, H2D of sorted locations and limits, a2..a8, D2H of log P, a10). N > 1: the same steps
     # through parallel.crd_step on every rank from pinned host buffers, max over ranks.
     e2e = None
-    if not args.no_e2e and not multi:
+    if not args.no_e2e and not multi and mode != "dstore":
         ts = []
         for it in range(4):                      # one warm-up call (allocations), three timed
             t0 = time.perf_counter()
@@ -630,14 +641,15 @@ def main():
                "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)), "calls": len(ts),
                "s_per_call_each": [float(t) for t in ts], "api": "mvn_crd (C ABI)",
                "k_star_matches_device_path": bool(np.array_equal(out.k_star, k))}
-    elif not args.no_e2e and multi:
+    elif not args.no_e2e:
         import torch as _t
         h_xy = _t.empty((n, 2), dtype=_t.float64).pin_memory()
         h_a = _t.empty(n, dtype=_t.float64).pin_memory()
         h_lp = _t.empty(n, dtype=_t.float64).pin_memory()
         ts = []
         for _ in range(3):
-            dist.barrier()
+            if multi:
+                dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             o2, a2, _ = mvn.mvn_marginal_order(inp.mu, var, cfg.u)              # a1 (host)
@@ -650,7 +662,8 @@ def main():
             torch.cuda.synchronize()
             k2, _ = mvn.mvn_confidence_region(h_lp.numpy(), cfg.conf)          # a10 (host)
             t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if multi:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ts.append(float(t.item()))
         e2e = {"value": n * NR / float(np.mean(ts)), "unit": UNIT, "h2d_bytes_per_step": 24 * n,
                "d2h_bytes_per_step": 8 * n, "s_per_call": float(np.mean(ts)), "calls": len(ts),
@@ -684,14 +697,20 @@ def main():
                     "peak_source": "measured fp64 DMMA peak (tools/calib_fp64.cu, profiles/r01_fp64_calibration.md); "
                                    "MEASURED_PEAKS.json has no fp64 entry",
                     "algorithmic": f"n(n-1) flops per sample x {my_samples} samples"}
-    if mode == "dist":
+    if mode in ("dist", "dstore"):
         n_potrf = parallel.potrf_launches(n, world, rank)
     else:
         n_potrf = parallel.potrf_launches(n) if rank == 0 else 0
     # cov + potrf + (check_limits, k_sov, k_reduce_blocks) + finalize [+ rescale]; int8: + rowscale,
     # lslice, k_sov_oz (memset of the flag is a copy-engine op)
-    launches = (1 if (mode == "dist" or rank == 0) else 0) + n_potrf + 3 + 1 + (1 if multi else 0) + \
+    launches = (1 if (mode in ("dist", "dstore") or rank == 0) else 0) + n_potrf + 3 + 1 + (1 if multi else 0) + \
         (2 if args.sov_method == 1 else 0)
+    if mode == "dstore":                       # per phase: one k_sov + one k_rows_copy per rank's piece
+        kp = mvn.mvn_potrf_panel_width(n)
+        ds = [mvn.dtiles(n, world, r, kp) for r in range(world)]
+        for b, e in parallel.sov_phases(-(-n // 128), args.phase_rows):
+            launches += 1 + sum(1 for d in ds if mvn.mvn_drows_offset(d, e) > mvn.mvn_drows_offset(d, b))
+        launches -= 1                          # the k_sov of the one-shot sweep counted above
     potrf_ms = stage_mean["potrf"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -301,8 +301,10 @@ mvn_status mvn_prefix_reduce(mvn_ctx *ctx, int64_t n, int64_t units, const doubl
  *   begin <= i < end, j <= i, row after row: tile (i, j) at (i(i+1)/2 + j - begin(begin+1)/2) * nb^2
  *   doubles — the same order as the full tile-packed buffer, so a slice of it can be passed.
  * mvn_sweep_end: after the last row, the block partials -> (M, S) as mvn_sov_prefix; frees the state.
- * mvn_sweep_free: frees the state without results (any time). Errors: MVN_E_USAGE for calls out of
- *   order or bad arguments (the state stays valid), MVN_E_CUDA.                                  */
+ * mvn_sweep_free: frees the state without results (any time). A sweep must end before its context
+ *   is destroyed; the state comes from a context-owned memory pool that keeps the memory for the
+ *   next sweep until mvn_trim. Errors: MVN_E_USAGE for calls out of order or bad arguments (the
+ *   state stays valid), MVN_E_CUDA.                                  */
 typedef struct mvn_sweep mvn_sweep;
 mvn_status mvn_sweep_begin(mvn_ctx *ctx, int64_t n, const double *d_a, const double *d_b, const mvn_qmc *q,
                            mvn_sweep **out);

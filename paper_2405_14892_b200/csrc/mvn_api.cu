@@ -48,6 +48,9 @@ struct mvn_ctx {
     void *pozA = nullptr; size_t pozA_cap = 0;     // int8 POTRF: panel digit slices
     void *pozR = nullptr; size_t pozR_cap = 0;     // int8 POTRF: panel row scales
     void *pozX = nullptr; size_t pozX_cap = 0;     // int8 POTRF: cluster exchange scratch
+    // mvn_sweep state: stream-ordered allocations from the context's own pool, which keeps the
+    // memory between sweeps (no re-mapping per sweep) until mvn_trim / mvn_destroy
+    cudaMemPool_t pool = nullptr;
 };
 
 namespace {
@@ -211,6 +214,7 @@ void mvn_destroy(mvn_ctx *c) {
                     c->post, c->postv, c->mcLA, c->mcRS, c->mcX, c->sozX, c->pozA, c->pozR, c->pozX})
         if (p) cudaFree(p);
     if (c->done) cudaEventDestroy(c->done);
+    if (c->pool) cudaMemPoolDestroy(c->pool);
     delete c;
     if (prev >= 0) cudaSetDevice(prev);
 }
@@ -242,6 +246,7 @@ mvn_status mvn_trim(mvn_ctx *c) {
     c->Y_cap = c->part_cap = c->cta_cap = c->sync_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
     c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = c->sozX_cap = c->pozA_cap = c->pozR_cap = c->pozX_cap = 0;
     c->post_n = c->post_off = 0;
+    if (c->pool) cudaMemPoolTrimTo(c->pool, 0);
     return MVN_OK;
 }
 
@@ -631,8 +636,18 @@ void sweep_release(mvn_sweep *sw) {
     delete sw;
 }
 template <class T>
-cudaError_t sweep_alloc(T **p, size_t count, cudaStream_t st) {
-    return cudaMallocAsync(reinterpret_cast<void **>(p), std::max<size_t>(count, 1) * sizeof(T), st);
+cudaError_t sweep_alloc(mvn_ctx *c, T **p, size_t count) {
+    if (!c->pool) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = c->device;
+        cudaError_t e = cudaMemPoolCreate(&c->pool, &props);
+        if (e != cudaSuccess) { c->pool = nullptr; return e; }
+        uint64_t keep = UINT64_MAX;
+        if ((e = cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
+    }
+    return cudaMallocFromPoolAsync(reinterpret_cast<void **>(p), std::max<size_t>(count, 1) * sizeof(T), c->pool, c->stream);
 }
 }  // namespace
 
@@ -666,14 +681,14 @@ mvn_status mvn_sweep_begin(mvn_ctx *c, int64_t n, const double *d_a, const doubl
     const int64_t ydoubles = mvn::sov_phase_yoff(cta.data(), sw->grid, sw->n_pad, 0, yoff.data());
     cudaStream_t st = c->stream;
     cudaError_t e = cudaSuccess;
-    if (!e) e = sweep_alloc(&sw->a, (size_t)n, st);
-    if (!e && d_b) e = sweep_alloc(&sw->b, (size_t)n, st);
-    if (!e) e = sweep_alloc(&sw->G, (size_t)n, st);
-    if (!e) e = sweep_alloc(&sw->cta, cta.size(), st);
-    if (!e) e = sweep_alloc(&sw->yoff, yoff.size(), st);
-    if (!e) e = sweep_alloc(&sw->Y, (size_t)ydoubles, st);
-    if (!e) e = sweep_alloc(&sw->part, (size_t)sw->nblk * sw->n_pad * 2, st);
-    if (!e) e = sweep_alloc(&sw->ell, (size_t)nsamp, st);
+    if (!e) e = sweep_alloc(c, &sw->a, (size_t)n);
+    if (!e && d_b) e = sweep_alloc(c, &sw->b, (size_t)n);
+    if (!e) e = sweep_alloc(c, &sw->G, (size_t)n);
+    if (!e) e = sweep_alloc(c, &sw->cta, cta.size());
+    if (!e) e = sweep_alloc(c, &sw->yoff, yoff.size());
+    if (!e) e = sweep_alloc(c, &sw->Y, (size_t)ydoubles);
+    if (!e) e = sweep_alloc(c, &sw->part, (size_t)sw->nblk * sw->n_pad * 2);
+    if (!e) e = sweep_alloc(c, &sw->ell, (size_t)nsamp);
     if (!e) e = cudaMemcpyAsync(sw->a, d_a, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
     if (!e && d_b) e = cudaMemcpyAsync(sw->b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
     if (!e) e = cudaMemcpyAsync(sw->G, c->G, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, st);

@@ -117,6 +117,23 @@ class LibmvnCrdOps:
         from . import mvn_sov_prefix_ex
         return mvn_sov_prefix_ex(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, begin, end, method=cls.sov_method)
 
+    # distributed storage end to end (potrf="dstore"): L is this rank's mvn_dtiles buffer
+    @staticmethod
+    def dcov(d_xy, cfg, local, n, world, rank, kp):
+        from . import dtiles, mvn_dcov_matern
+        mvn_dcov_matern(d_xy, dtiles(n, world, rank, kp), cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, local)
+
+    @staticmethod
+    def potrf_dstore(local, n, group, kp):
+        return potrf_distributed_local(local, n, group, kp=kp)
+
+    phase_rows = 16          # tile rows per phase of the sweep over distributed L
+
+    @classmethod
+    def sov_dstore(cls, local, n, d_a, cfg, begin, end, kp, group):
+        return sov_distributed(local, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, begin, end, kp, group=group,
+                               phase_rows=cls.phase_rows)
+
     @staticmethod
     def rescale(Mg, M, S):
         from . import mvn_prefix_rescale
@@ -141,7 +158,10 @@ def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg,
 
     potrf: "rank0" — rank 0 builds and factors Sigma, then broadcasts L (C1, the north_star
     layout); "dist" — every rank builds Sigma and the ranks factor it together
-    (potrf_distributed, NEXT-1), after which every rank holds L; "auto" = "rank0".
+    (potrf_distributed, NEXT-1), after which every rank holds L; "dstore" — NEXT-1 on distributed
+    storage end to end: `L` is this rank's mvn_dtiles buffer (1-D, kp = mvn_potrf_panel_width(n),
+    ~1/W of the tiles), Sigma generated there, factored by potrf_distributed_local, and the sweep
+    gathers each phase's rows from the ranks (sov_distributed); "auto" = "rank0".
     events: optional list to which (name, event) pairs are appended for stage timing.
     ops: the building blocks (default LibmvnCrdOps, the CUDA library).
     """
@@ -150,8 +170,8 @@ def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg,
     world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
     rank = dist.get_rank(group) if world > 1 else 0
     mode = "rank0" if potrf == "auto" else potrf
-    if mode not in ("rank0", "dist"):
-        raise ValueError(f"potrf must be auto, rank0 or dist, not {potrf!r}")
+    if mode not in ("rank0", "dist", "dstore"):
+        raise ValueError(f"potrf must be auto, rank0, dist or dstore, not {potrf!r}")
 
     def mark(name):
         if events is None:
@@ -162,6 +182,24 @@ def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg,
         return e
 
     mark("start")
+    if mode == "dstore":
+        from . import mvn_potrf_panel_width
+        kp = mvn_potrf_panel_width(n)
+        ops.dcov(d_xy_sorted, cfg, L, n, world, rank, kp)
+        mark("cov")
+        info = ops.potrf_dstore(L, n, group, kp)
+        if info != -1:
+            raise FloatingPointError(f"Sigma not SPD at row {info}")
+        mark("potrf")
+        mark("bcast")
+        begin, end = shard_range(cfg.N * cfg.R, rank, world)
+        M, S = ops.sov_dstore(L, n, d_a, cfg, begin, end, kp, group)
+        mark("sov")
+        combine_prefix(M, S, group, rescale=ops.rescale)
+        mark("combine")
+        logp = ops.finalize(M, S, cfg.N * cfg.R)
+        mark("finalize")
+        return logp
     if mode == "dist":
         ops.cov(d_xy_sorted, cfg, L)
         mark("cov")

@@ -1,6 +1,7 @@
 """The multi-rank step logic of parallel.crd_step (the north_star layout "rank 0
 factors Sigma and broadcasts L, samples shard over the ranks, the per-prefix sums are combined",
-and the NEXT-1 layout "the ranks factor Sigma together") on CPU with gloo at world size 2 and 3.
+and the NEXT-1 layouts "the ranks factor Sigma together", also on distributed storage with the
+sweep gathering each phase's rows from the ranks) on CPU with gloo at world size 2 and 3.
 The CUDA building blocks are replaced by host stand-ins built on the oracle (test infrastructure;
 the product path has no CPU backend); the collectives, the sharding, the ownership of every stage
 and the combine are the product code. Every rank must end with the single-process estimate."""
@@ -54,6 +55,39 @@ class HostCrdOps:
         M, S = range_partial(L.view(n, n).numpy(), d_a.numpy(), cfg.N, cfg.R, cfg.seed_lattice, begin, end)
         return torch.from_numpy(M.copy()), torch.from_numpy(S.copy())
 
+    # potrf="dstore": `L` stands for this rank's storage (the dense matrix here); the factorisation
+    # is the distributed schedule; the sweep gathers every phase's rows from the ranks' pieces (the
+    # owned tiles of those rows, broadcast over gloo) and runs on the assembled factor
+    def dcov(self, d_xy, cfg, L, n, world, rank, kp):
+        self.cov(d_xy, cfg, L)
+
+    def potrf_dstore(self, L, n, group, kp):
+        return self.potrf_dist(L, n, group)
+
+    def sov_dstore(self, L, n, d_a, cfg, begin, end, kp, group):
+        from test_sov_rows_gloo import NB, NumpySovRowsOps
+        self.calls["sov"] += 1
+        world, rank = dist.get_world_size(), dist.get_rank()
+        npad = -(-n // NB) * NB
+        A = np.eye(npad)
+        A[:n, :n] = np.tril(L.view(n, n).numpy())
+        phases = parallel.sov_phases(npad // NB, 3)
+        ops = NumpySovRowsOps(A, world, rank, kp, 1, phases)
+        got = np.full((npad, npad), np.nan)
+        sweep = ops.sweep
+
+        def record(p):                            # the stand-in sweep: keep the phase's rows
+            sweep(p)
+            for (i, j), T in ops.rows.items():
+                got[i * NB:(i + 1) * NB, j * NB:(j + 1) * NB] = T
+        ops.sweep = record
+        parallel.sov_rows_schedule(ops, len(phases))
+        Lg = np.tril(got)[:n, :n]
+        assert not np.isnan(Lg).any()
+        from test_parallel_gloo import range_partial
+        M, S = range_partial(Lg, d_a.numpy(), cfg.N, cfg.R, cfg.seed_lattice, begin, end)
+        return torch.from_numpy(M.copy()), torch.from_numpy(S.copy())
+
     @staticmethod
     def rescale(Mg, M, S):
         from test_parallel_gloo import torch_rescale
@@ -94,7 +128,7 @@ def free_port():
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("mode", ["rank0", "dist", "auto"])
+@pytest.mark.parametrize("mode", ["rank0", "dist", "auto", "dstore"])
 def test_crd_step_multi_rank_matches_single_process(world, mode):
     import oracle
     mgr = mp.Manager()
@@ -108,7 +142,7 @@ def test_crd_step_multi_rank_matches_single_process(world, mode):
         assert np.max(np.abs(lp - ref.logp)) <= 1e-12, (r, np.max(np.abs(lp - ref.logp)))
         assert np.array_equal(L, out[0][1])                          # every rank holds the same L
         assert calls["sov"] == 1
-        if mode == "dist":
+        if mode in ("dist", "dstore"):
             assert calls["cov"] == 1 and calls["potrf_dist"] == 1 and calls["potrf"] == 0
         else:                                                        # auto = rank0: the north_star layout
             assert calls["potrf_dist"] == 0

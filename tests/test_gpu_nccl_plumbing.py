@@ -66,11 +66,12 @@ def test_combine_prefix_with_nccl_allreduce(nccl):
     assert torch.equal(M2, M) and torch.equal(S2, S)
 
 
-@pytest.mark.parametrize("mode", ["rank0", "dist"])
+@pytest.mark.parametrize("mode", ["rank0", "dist", "dstore"])
 def test_crd_step_with_nccl_collectives_equals_mvn_crd(nccl, mode):
     """The multi-GPU step (parallel.crd_step) on the one-rank NCCL communicator with every
     collective forced — broadcast_L of the whole tile buffer (rank0, the north_star C1), or the
-    distributed Cholesky's panel broadcasts (dist, NEXT-1), then the all_reduce combine — returns
+    distributed Cholesky's panel broadcasts (dist, NEXT-1), or distributed storage end to end with
+    the sweep's phase broadcasts (dstore, NEXT-1), then the all_reduce combine — returns
     log P bitwise equal to the single-GPU C call mvn_crd on the same inputs."""
     import torch
     import paper_2405_14892_b200 as mvn
@@ -84,7 +85,7 @@ def test_crd_step_with_nccl_collectives_equals_mvn_crd(nccl, mode):
     order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
     d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
     d_a = torch.from_numpy(a).cuda()
-    L = mvn.alloc_tiles(n)
+    L = mvn.alloc_dtiles(n, 1, 0, mvn.mvn_potrf_panel_width(n)) if mode == "dstore" else mvn.alloc_tiles(n)
     parallel.FORCE_COLLECTIVES = True
     try:
         ev = []

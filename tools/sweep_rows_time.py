@@ -3,7 +3,8 @@ BASELINE config: python tools/sweep_rows_time.py D [samples] [phase_rows ...].
 samples: the sweep's sample range [0, samples) (default: all N*R; a rank's shard at W GPUs is
 N*R/W). Each phase is run two ways: on a view of the full factor (no copy: the cost of cutting the
 sweep), and on a staging buffer the phase's rows are first copied into (the arrival of the rows:
-what sov_distributed's assembly adds on the compute stream). Checks bitwise equality of (M, S)."""
+what sov_distributed's assembly adds on the compute stream). Checks bitwise equality of (M, S).
+Every variant: one warm-up run, then the best of 2."""
 import os
 import sys
 
@@ -36,7 +37,19 @@ def timed(fn):
     return e0.elapsed_time(e1), out
 
 
-t0, (M0, S0) = timed(lambda: mvn.mvn_sov_prefix(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, 0, ns))
+REPS = 2
+
+
+def best(fn):
+    fn()                                         # warm-up (first-use allocations)
+    ts, out = [], None
+    for _ in range(REPS):
+        t, out = timed(fn)
+        ts.append(t)
+    return min(ts), out
+
+
+t0, (M0, S0) = best(lambda: mvn.mvn_sov_prefix(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, 0, ns))
 flop = n * (n - 1) * ns
 print(f"cfg={cfg.name} samples={ns} one-shot sov_ms={t0:.1f} frac={flop / (t0 / 1e3) / 1e12 / 37.07:.3f}", flush=True)
 for pr in prs:
@@ -57,7 +70,7 @@ for pr in prs:
                     rows = s
                 mvn.mvn_sweep_rows(sw, rows, b, e)
             return mvn.mvn_sweep_end(sw)
-        t, (M, S) = timed(run)
+        t, (M, S) = best(run)
         same = bool(torch.equal(M, M0) and torch.equal(S, S0))
         print(f"  phase_rows={pr} phases={len(phases)} {mode}: sov_ms={t:.1f} ({t / t0:.3f}x) "
               f"frac={flop / (t / 1e3) / 1e12 / 37.07:.3f} bitwise={same}", flush=True)
