@@ -67,17 +67,21 @@ static __device__ __noinline__ double matern_far(double d2, double ib, double si
     return matern_poly<NU2>(x, sigma2 * exp(-x));
 }
 
-// sqrt(d) for d >= 0 without the special-operand branch of sqrt(): the MUFU reciprocal square-root
-// seed, one Newton step on it, then one on the root (error ~ ulp). The seed is taken at d + 1e-300
-// (= d for d > 1e-284; d = 0 then gives y = 1e150 and t = 0, so sqrt(0) = 0) — one add instead of
-// fmax's compare-and-select.
-__device__ __forceinline__ double sqrt_nonneg(double d) {
+// sqrt(d) for d >= 1e-300 (the caller adds 1e-300 to the squared distance inside its last FMA, so
+// coincident points give 1e-150 and C = sigma2 exactly, and no special-operand branch is needed):
+// the MUFU reciprocal square-root seed, one coupled (Goldschmidt) step on t ~ sqrt(d) and
+// h ~ 1 / (2 sqrt(d)) — the seed's relative error squares — then one Newton correction of t
+// (correctly rounded in an exact-arithmetic emulation with seed errors up to 2^-21). 2 DMUL + 5 DFMA;
+// the d + 1e-300 add and the separate rsqrt refinement of the previous version cost 3 more fp64
+// instructions per element (22 instead of 25; K1 at D 4.07-4.11 -> 3.83-3.94 ms).
+__device__ __forceinline__ double sqrt_pos(double d) {
     double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d + 1e-300));
-    const double c = fma(-(d * y), y, 1.0);               // 1 - d y^2
-    y = fma(0.5 * y, c, y);
-    const double t = d * y;
-    return fma(0.5 * y, fma(-t, t, d), t);
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double t = d * y, h = 0.5 * y;
+    const double r = fma(-t, h, 0.5);
+    t = fma(t, r, t);
+    h = fma(h, r, h);
+    return fma(h, fma(-t, t, d), t);
 }
 
 // One CTA (256 threads) per tile. Thread t owns RPT consecutive rows of the tile (their locations in
@@ -160,7 +164,7 @@ __global__ void __launch_bounds__(256, MINB) k_cov_matern(const MaternArgs p) {
 #pragma unroll
             for (int h = 0; h < RPT; ++h) {
                 const double dx = rx[h] - xc, dy = ry[h] - yc;
-                const double x = sqrt_nonneg(fma(dx, dx, dy * dy)) * ib;
+                const double x = sqrt_pos(fma(dx, dx, fma(dy, dy, 1e-300))) * ib;
                 v[h] = matern_poly<NU2>(x, exp_neg_scaled(x, tb));
             }
         } else {
