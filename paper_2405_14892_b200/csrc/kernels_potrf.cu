@@ -60,19 +60,72 @@ __device__ __forceinline__ void blk_gemm_sub(double *X, int ldx, int r0, int r1,
 }
 
 // Rows r of X (columns c0..c0+32) solve x L_cc^T = x: x_j = (x_j - sum_{t<j} x_t L(j,t)) / L(j,j),
-// L(j,t) = Lm[(lc + t) * ldl + lc + j] (warp-uniform broadcast). One thread per row.
-__device__ __forceinline__ void blk_solve32(double *X, int ldx, int c0, int r, const double *Lm, int ldl, int lc) {
+// L(j,t) = Lm[(lc + t) * ldl + lc + j] (warp-uniform broadcast). One thread per row, the row in 32
+// registers, right-looking: once x_j is final it is subtracted from every later x_q at once, so
+// the 31 updates of a step are independent; the division by L(j,j) is a product with rd[j] =
+// 1 / L(j,j) (shared memory, from the factorisation), so the critical path is 32 multiplies, not
+// 32 divisions or the 528 dependent FMAs of the dot-product order. Fully unrolled (static register
+// indices); a rolled step loop with registers rotating down one place per step has a 20x smaller
+// code but executes 2x the instructions and measured 2-5x slower (k_potrf_diag2 100 us, k_trsm2
+// 78 us against 60 / 17 us).
+__device__ __forceinline__ void blk_solve32(double *X, int ldx, int c0, int r, const double *Lm, int ldl, int lc,
+                                            const double *rd) {
+    double x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = X[(c0 + j) * ldx + r];
+#pragma unroll
     for (int j = 0; j < 32; ++j) {
-        double s0 = X[(c0 + j) * ldx + r], s1 = 0.0;
-        int t = 0;
-        for (; t + 2 <= j; t += 2) {
-            s0 -= X[(c0 + t) * ldx + r] * Lm[(lc + t) * ldl + lc + j];
-            s1 -= X[(c0 + t + 1) * ldx + r] * Lm[(lc + t + 1) * ldl + lc + j];
-        }
-        if (t < j) s0 -= X[(c0 + t) * ldx + r] * Lm[(lc + t) * ldl + lc + j];
-        X[(c0 + j) * ldx + r] = (s0 + s1) / Lm[(lc + j) * ldl + lc + j];
+        const double *Lj = Lm + (lc + j) * ldl + lc;      // column j of the block: L(q, j) = Lj[q]
+        x[j] *= rd[j];
+#pragma unroll
+        for (int q = 1; q < 32; ++q)                      // constant trip count: fully unrolled
+            if (q > j) x[q] -= x[j] * Lj[q];
     }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) X[(c0 + j) * ldx + r] = x[j];
 }
+
+// One warp factors the 32 x 32 diagonal block at (c0, c0) of A (column-major, ld): lane i holds row
+// i in registers; step j broadcasts the pivot and column j by shuffles (right-looking, the same
+// operations in the same order as a column-by-column shared-memory factorisation, except that the
+// column is scaled by rsqrt(d_jj), computed beside sqrt(d_jj) instead of a division after it: the
+// step's critical path is shuffle, rsqrt, multiply, shuffle, FMA). rd[j] = rsqrt(d_jj) for the
+// substitution below the block. Returns the first non-positive pivot's column in the block (-1:
+// all positive); the block is written back only when it succeeded.
+__device__ __forceinline__ int blk_potrf32(double *A, int ld, int c0, int lane, double *rd) {
+    double d[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) d[q] = q <= lane ? A[(c0 + q) * ld + c0 + lane] : 0.0;
+    int bad = -1;                                        // (no early exit: keeps the loop unrolled)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const double djj = __shfl_sync(0xffffffffu, d[j], j);
+        if (bad < 0 && !(djj > 0.0)) bad = j;              // warp-uniform
+        const double ljj = sqrt(djj), rinv = rsqrt(djj);
+        const double lij = lane > j ? d[j] * rinv : lane == j ? ljj : d[j];
+        d[j] = lij;
+        if (lane == 0) rd[j] = rinv;
+#pragma unroll
+        for (int q = 1; q < 32; ++q)                      // constant trip count: fully unrolled
+            if (q > j) {
+                const double lqj = __shfl_sync(0xffffffffu, lij, q);
+                if (lane >= q) d[q] -= lij * lqj;
+            }
+    }
+    if (bad >= 0) return bad;
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+        if (q <= lane) A[(c0 + q) * ld + c0 + lane] = d[q];
+    return -1;
+}
+
+// The 32-column block loops of K2 / K3: rolled (MVN_PANEL_CB_ROLLED=1, one copy of the block code)
+// or unrolled by the compiler (default: 4 copies)
+#if defined(MVN_PANEL_CB_ROLLED) && MVN_PANEL_CB_ROLLED
+#define MVN_CB_UNROLL _Pragma("unroll 1")
+#else
+#define MVN_CB_UNROLL
+#endif
 
 // K2 (blocked): POTRF of the 128 x 128 diagonal tile k in shared memory. Per 32-column block cb:
 // DMMA update of rows >= 32cb by the finished columns, one-warp factorisation of the 32 x 32
@@ -80,6 +133,7 @@ __device__ __forceinline__ void blk_solve32(double *X, int ldx, int c0, int r, c
 __global__ void __launch_bounds__(256) k_potrf_diag2(const TileMap tm, int k, int64_t *__restrict__ info) {
     using namespace blk;
     extern __shared__ double A[];          // [128 cols][SP]
+    __shared__ double rdg[kTile];          // 1 / L(j, j)
     __shared__ int failed;
     double *T = tm.tile(k, k);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -92,6 +146,7 @@ __global__ void __launch_bounds__(256) k_potrf_diag2(const TileMap tm, int k, in
     cp_async_wait<0>();
     __syncthreads();
     if (failed) return;
+    MVN_CB_UNROLL
     for (int cb = 0; cb < 4; ++cb) {
         const int c0 = cb * 32;
         if (cb > 0) {
@@ -99,31 +154,13 @@ __global__ void __launch_bounds__(256) k_potrf_diag2(const TileMap tm, int k, in
             __syncthreads();
         }
         if (warp == 0) {                   // 32 x 32 diagonal block, lane = row
-            for (int j = 0; j < 32; ++j) {
-                const double d = A[(c0 + j) * SP + c0 + j];
-                const bool bad = !(d > 0.0);
-                if (bad) {
-                    if (lane == 0) { failed = 1; *info = (int64_t)k * kTile + c0 + j; }
-                    break;
-                }
-                const double ljj = sqrt(d);
-                __syncwarp();
-                if (lane == j) A[(c0 + j) * SP + c0 + j] = ljj;
-                double lij = 0.0;
-                if (lane > j) {
-                    lij = A[(c0 + j) * SP + c0 + lane] / ljj;
-                    A[(c0 + j) * SP + c0 + lane] = lij;
-                }
-                __syncwarp();
-                if (lane > j)
-                    for (int q = j + 1; q <= lane; ++q) A[(c0 + q) * SP + c0 + lane] -= lij * A[(c0 + j) * SP + c0 + q];
-                __syncwarp();
-            }
+            const int bad = blk_potrf32(A, SP, c0, lane, rdg + c0);
+            if (bad >= 0 && lane == 0) { failed = 1; *info = (int64_t)k * kTile + c0 + bad; }
         }
         __syncthreads();
         if (failed) return;
         const int r = c0 + 32 + tid;
-        if (r < kTile) blk_solve32(A, SP, c0, r, A, SP, c0);
+        if (r < kTile) blk_solve32(A, SP, c0, r, A, SP, c0, rdg + c0);
         __syncthreads();
     }
     for (int e = tid; e < kTile * kTile; e += 256) {
@@ -140,6 +177,7 @@ __global__ void __launch_bounds__(256) k_trsm2(const TileMap tm, const TileMap d
     extern __shared__ double sh[];
     double *X = sh;                        // [128 cols][SPX]: rows h*64 .. h*64+63 of A_ik
     double *Lk = sh + kTile * SPX;         // [128 cols][SP]
+    __shared__ double rdk[kTile];          // 1 / L_kk(j, j)
     const int64_t lo = rs.lo > k + 1 ? rs.lo : k + 1;
     const int i = (int)rs.nth_raw(rs.raw(lo) + (blockIdx.x >> 1)), h = blockIdx.x & 1;
     double *Ti = tm.tile(i, k) + h * 64;
@@ -156,13 +194,16 @@ __global__ void __launch_bounds__(256) k_trsm2(const TileMap tm, const TileMap d
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    if (tid < kTile) rdk[tid] = 1.0 / Lk[tid * SP + tid];
+    __syncthreads();
+    MVN_CB_UNROLL
     for (int cb = 0; cb < 4; ++cb) {
         const int c0 = cb * 32;
         if (cb > 0) {
             blk_gemm_sub(X, SPX, 0, 64, c0, c0, Lk, SP, c0, warp, 8, lane);
             __syncthreads();
         }
-        if (tid < 64) blk_solve32(X, SPX, c0, tid, Lk, SP, c0);
+        if (tid < 64) blk_solve32(X, SPX, c0, tid, Lk, SP, c0, rdk + c0);
         __syncthreads();
     }
     for (int e = tid; e < kTile * 32; e += 256) {
