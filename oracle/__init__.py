@@ -78,4 +78,4 @@ from .pipeline import (  # noqa: E402
 )
 from .mcval import mc_z, mc_first, mc_counts, mc_levels  # noqa: E402
 from .posterior import posterior, posterior_field  # noqa: E402
-from .tlr import tlr_compress, compress_tile  # noqa: E402
+from .tlr import tlr_compress, compress_tile, tlr_cholesky  # noqa: E402

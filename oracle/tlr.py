@@ -66,3 +66,57 @@ def tlr_compress(S: np.ndarray, eps: float, nb: int = NB, mode: str = "abs"):
             out[I * nb:(I + 1) * nb, J * nb:(J + 1) * nb] = At
             out[J * nb:(J + 1) * nb, I * nb:(I + 1) * nb] = At.T
     return out[:n, :n], ranks, sig
+
+
+def tlr_cholesky(S: np.ndarray, eps: float, nb: int = NB, mode: str = "abs"):
+    """NEXT-3: the TLR Cholesky of Alg. 1 l.7-8 ("compression of the covariance matrix into the
+    TLR format", box (a) "can be performed using both dense and TLR computations"), reading
+    R26: Sigma is compressed at eps (tlr_compress, R23), then the tile columns are
+    factored left to right; for column j
+
+        T_i  = Stilde_ij - sum_{k<j} Ltilde_ik Ltilde_jk^T      (i >= j; every Ltilde_ik low rank)
+        L_jj = chol(T_j)                                       (dense diagonal tile)
+        L_ij = T_i L_jj^{-T}                                   (i > j)
+        Ltilde_ij = rank-k truncation of L_ij at eps            (R23's rule, one SVD per tile)
+
+    i.e. every off-diagonal tile of L is truncated once, when its column is complete (the updates
+    are applied to the exact low-rank products, not re-truncated after each one; reading R26).
+    Library primitives per step: the oracle's Crout Cholesky (C) for L_jj, a triangular solve for
+    L_ij, numpy's SVD for the truncation.
+
+    Returns (Ltilde, ranks_L, sig_L, ranks_S, info): Ltilde n x n lower (low-rank tiles
+    reconstructed), ranks_L / ranks_S the ranks of L's / Sigma's off-diagonal tiles at
+    I(I-1)/2 + J, sig_L the singular values of each L_ij before truncation (near-tie detection),
+    info = -1 or the first failing global row (then Ltilde is partial)."""
+    import scipy.linalg as sla
+    from .pipeline import cholesky as crout
+
+    S = np.asarray(S, dtype=np.float64)
+    n = S.shape[0]
+    nt = -(-n // nb)
+    St, ranks_S, _ = tlr_compress(S, eps, nb, mode)
+    L = np.zeros((n, n))
+    ranks_L = np.zeros(max(nt * (nt - 1) // 2, 0), dtype=np.int64)
+    sig_L = np.zeros((len(ranks_L), nb))
+
+    def blk(I):
+        return slice(I * nb, min((I + 1) * nb, n))
+
+    for j in range(nt):
+        cj = blk(j)
+        T = St[j * nb:, cj] - L[j * nb:, :j * nb] @ L[cj, :j * nb].T      # sum over k < j, tile by tile equal
+        Ljj, info = crout(T[:cj.stop - cj.start])
+        if info >= 0:
+            return L, ranks_L, sig_L, ranks_S, j * nb + info
+        L[cj, cj] = Ljj
+        for I in range(j + 1, nt):
+            rI = blk(I)
+            Tij = T[rI.start - j * nb:rI.stop - j * nb]
+            Lij = sla.solve_triangular(Ljj, Tij.T, lower=True).T            # T_i L_jj^{-T}
+            P = np.zeros((nb, nb))
+            P[:Lij.shape[0], :Lij.shape[1]] = Lij
+            Lt, k, s = compress_tile(P, eps, mode)
+            t = I * (I - 1) // 2 + j
+            ranks_L[t], sig_L[t] = k, s
+            L[rI, cj] = Lt[:Lij.shape[0], :Lij.shape[1]]
+    return L, ranks_L, sig_L, ranks_S, -1

@@ -91,3 +91,82 @@ def test_relative_frobenius_mode(eps):
         assert np.linalg.norm(A - Ak1) > eps * np.linalg.norm(A)
     _, r_abs, _ = oracle.tlr_compress(S, eps * np.linalg.norm(A), mode="abs")
     assert 0 <= k <= 128 and r_abs[0] >= 0
+
+
+# ---- NEXT-3: the TLR Cholesky (oracle/tlr.py tlr_cholesky, reading R26) ----
+
+def _matern(g, base="B", nu=None):
+    cfg = W.small_config("tlr", g, 10, 1, base=base)
+    inp = W.make_inputs(cfg)
+    return oracle.covariance(inp.xy, cfg.sigma2, cfg.beta, cfg.nu if nu is None else nu, cfg.nugget)
+
+
+def test_tlr_cholesky_eps_zero_is_dense_cholesky():
+    """eps = 0 keeps every singular triplet: the factor is the dense Crout factor (rounding only)."""
+    S = _matern(19)                                       # n = 361: 3 tile rows, ragged last tile
+    L, rL, _, rS, info = oracle.tlr_cholesky(S, 0.0)
+    Ld, infod = oracle.cholesky(S)
+    assert info == -1 and infod == -1
+    assert np.all(rS == 128) and rL.max() == 128 and len(rL) == 3
+    assert np.max(np.abs(L - Ld)) < 1e-12
+
+
+def test_tlr_cholesky_diag_plus_low_rank_is_exact():
+    """Sigma = D + F F^T (F of rank r): every off-diagonal tile of Sigma AND of its Cholesky factor
+    has rank exactly r (the factor of a diagonal-plus-rank-r matrix is semiseparable of rank r), so
+    with eps far below the kept and far above the dropped singular values the TLR factor is the exact
+    Cholesky factor."""
+    rng = np.random.default_rng(7)
+    n, r = 450, 6
+    F = rng.standard_normal((n, r))
+    S = F @ F.T + np.diag(rng.uniform(1.0, 3.0, n))
+    L, rL, sL, rS, info = oracle.tlr_cholesky(S, 1e-8)
+    assert info == -1
+    assert list(rS) == [r] * 6 and list(rL) == [r] * 6
+    assert np.max(np.abs(L - np.linalg.cholesky(S))) < 1e-12
+    assert np.all(sL[:, r] < 1e-12) and np.all(sL[:, r - 1] > 1e-6)
+
+
+@pytest.mark.parametrize("eps,mode", [(1e-2, "abs"), (1e-4, "abs"), (1e-6, "abs"), (1e-3, "fro")])
+def test_tlr_cholesky_residual_is_the_truncation(eps, mode):
+    """What the algorithm fixes: (Ltilde Ltilde^T - Stilde)_IJ = (L_IJ - Ltilde_IJ) L_JJ^T for I > J
+    and 0 on the diagonal tiles (T_J = L_JJ L_JJ^T), so the off-diagonal residual is bounded by the
+    dropped singular value times ||L_JJ||_2 — a dropped update term, a transposed operand or a wrong
+    tile index breaks it."""
+    S = _matern(20, base="C", nu=1.5) if mode == "abs" and eps < 1e-5 else _matern(20)
+    nb = 128
+    L, rL, sL, rS, info = oracle.tlr_cholesky(S, eps, mode=mode)
+    assert info == -1
+    St, rS2, _ = oracle.tlr_compress(S, eps, mode=mode)
+    assert np.array_equal(rS, rS2)
+    R = L @ L.T - St
+    n, nt = S.shape[0], -(-S.shape[0] // nb)
+    scale = np.max(np.abs(S))
+    for J in range(nt):
+        cJ = slice(J * nb, min((J + 1) * nb, n))
+        assert np.max(np.abs(R[cJ, cJ])) < 1e-13 * scale * nt
+        nLJJ = np.linalg.norm(L[cJ, cJ], 2)
+        for I in range(J + 1, nt):
+            rI = slice(I * nb, min((I + 1) * nb, n))
+            t = I * (I - 1) // 2 + J
+            k = rL[t]
+            tail = sL[t][k] if k < nb else 0.0
+            res = np.linalg.norm(R[rI, cJ], 2)
+            assert res <= tail * nLJJ * (1 + 1e-8) + 1e-13 * scale * nt
+            if mode == "abs":
+                assert res < eps * nLJJ
+                assert k == 0 or sL[t][k - 1] >= eps
+    assert rL.max() <= 128 and rL.min() >= 0
+
+
+def test_tlr_cholesky_reports_the_failing_row():
+    """A non-positive pivot at a known row (off-diagonal tiles zero: rank 0) is reported there."""
+    n = 300
+    S = np.eye(n)
+    S[200, 200] = -1.0
+    L, rL, _, rS, info = oracle.tlr_cholesky(S, 1e-3)
+    assert info == 200
+    assert np.all(rS == 0)
+    S[200, 200] = 1.0
+    L, rL, _, _, info = oracle.tlr_cholesky(S, 1e-3)
+    assert info == -1 and np.array_equal(L, np.eye(n)) and np.all(rL == 0)
