@@ -480,6 +480,109 @@ def run_tlr(args):
     return 0
 
 
+def tlr_update_flops(ranks: np.ndarray, nt: int) -> float:
+    """Algorithmic flops of the factored updates of the TLR Cholesky (R26): per (i, j, k), k < j <= i,
+    4 nb r_ik r_jk (M = V_ik^T V_jk, Z = U_ik M) + 2 nb^2 r_jk (T_i -= Z U_jk^T), nb = 128."""
+    r = np.zeros((nt, nt))
+    for I in range(1, nt):
+        r[I, :I] = ranks[I * (I - 1) // 2:I * (I - 1) // 2 + I]
+    tot = 0.0
+    for j in range(1, nt):
+        rj = r[j, :j]                                  # r_jk, k < j
+        ri = r[j:, :j].copy()                          # r_ik, i >= j (row j itself: r_jk)
+        tot += 4.0 * 128 * float((ri * rj).sum()) + 2.0 * 128 ** 2 * float(rj.sum()) * (nt - j)
+    return tot
+
+
+def run_tlr_potrf(args):
+    """NEXT-3: the TLR Cholesky (mvn_tlr_potrf, R26) against the dense DMMA Cholesky (mvn_potrf) on the
+    same matrix: the paper's accuracy setting — n = 40,000 sites (200 x 200 jittered grid),
+    exponential kernel, sigma^2 = 1, beta = 0.1 — at eps = --tlr-eps, in the order Alg. 1 factors
+    (sorted by marginal probability, R1) or in the grid's own order (--tlr-order spatial: the setting
+    of the paper's rank figure, where tiles are low rank). Both timed on the device with
+    CUDA events (Sigma copied into the working buffer outside the events; the TLR time includes the
+    compression of Sigma). value = TLR time; roofline = the factored-update flops (tlr_update_flops)
+    over the TLR time against the fp64 DMMA peak."""
+    import torch
+    import paper_2405_14892_b200 as mvn
+    torch.cuda.set_device(0)
+    cfg = W.small_config("tlr-40K", args.tlr_g, 10_000, 8, base="B")
+    inp = W.make_inputs(cfg)
+    n = cfg.n
+    if args.tlr_order == "sorted":
+        order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
+    else:
+        order = np.arange(n)
+    d_xs = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+    base = mvn.mvn_cov_matern(d_xs, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    T = torch.empty_like(base)
+    nt = -(-n // 128)
+    noff = nt * (nt - 1) // 2
+    U = torch.empty((noff, args.tlr_kmax, 128), dtype=torch.float64, device="cuda")
+    V = torch.empty_like(U)
+    st = torch.cuda.current_stream()
+
+    def timed(fn):
+        ts = []
+        for it in range(args.warmup + args.steps):
+            T.copy_(base)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            out = fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                ts.append(e0.elapsed_time(e1))
+        return float(np.mean(ts)), out
+
+    clocks = ClockSampler(0)
+    clocks.start()
+    ms_tlr, f = timed(lambda: mvn.mvn_tlr_potrf(T, n, args.tlr_eps, mode=args.tlr_mode, kmax=args.tlr_kmax, U=U, V=V))
+    ms_dense, info_d = timed(lambda: mvn.mvn_potrf(T, n, raise_on_numeric=False))
+    clk = clocks.stop()
+    rL, rS = f.ranks.cpu().numpy(), f.ranks_sigma.cpu().numpy()
+    flops = tlr_update_flops(rL, nt)
+    achieved = flops / (ms_tlr / 1e3) / 1e12
+    dense_flops = float(n) ** 3 / 3
+    line = {"metric": "TLR Cholesky time (NEXT-3)", "value": ms_tlr, "unit": "ms", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_tlr, "higher_is_better": False,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{n} sites ({args.tlr_g}x{args.tlr_g} jittered grid, exponential kernel s2=1, "
+                                   f"beta=0.1), {args.tlr_order} order, 128-wide tiles, eps={args.tlr_eps:g} "
+                                   f"(P:368, P:439)", "n": n, "order": args.tlr_order, "eps": args.tlr_eps,
+                       "mode": args.tlr_mode, "kmax": args.tlr_kmax},
+            "dense_potrf_ms": ms_dense, "dense_tflops": dense_flops / (ms_dense / 1e3) / 1e12,
+            "tlr_over_dense": ms_tlr / ms_dense, "info": f.info, "dense_info": int(info_d),
+            "ranks_L": {"mean": float(rL.mean()), "p90": float(np.percentile(rL, 90)), "max": int(rL.max())},
+            "ranks_sigma": {"mean": float(rS.mean()), "max": int(rS.max())},
+            "update_flops": flops, "update_flops_over_dense_potrf": flops / dense_flops,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
+                         "algorithmic": "factored updates 4 nb r_ik r_jk + 2 nb^2 r_jk per (i, j, k) over the TLR "
+                                        "time (compressions and panels count as overhead)"},
+            "clocks": clk, "gpu_launches": tlr_potrf_launches(nt) * args.steps}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def tlr_potrf_launches(nt: int) -> int:
+    """Kernels mvn_tlr_potrf launches (mvn_api.cu / kernels_tlr.cu launch_tlr_potrf): the compression
+    of Sigma, per column j the expansion, 3 per chunk of k (M, Z, accumulate), K2, K3 and the
+    compression of the column, and the final expansion."""
+    need = max(1, (nt // 2) * ((nt + 1) // 2))
+    chunk = max(min(need, 2048), nt)
+    cnt = 2 if nt > 1 else 0
+    for j in range(nt):
+        rows = nt - j
+        kc = max(1, min(j, chunk // rows))
+        for k0 in range(0, j, kc):
+            kcc = min(kc, j - k0)
+            nsplit = min(kcc, max(1, (2 * 148 + 4 * rows - 1) // (4 * rows)))
+            cnt += 3 + (1 if nsplit > 1 else 0)
+        cnt += 1 + (3 if rows > 1 else 0)
+    return cnt
+
+
 # --------------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -505,13 +608,17 @@ def main():
     ap.add_argument("--potrf-method", type=int, default=0, choices=[0, 1],
                     help="crd: 0 = Cholesky updates on fp64 DMMA (default); 1 = on the int8 tensor cores (NEXT-4, R25)")
     ap.add_argument("--shard", default="1,2,4,8", help="--workload shard: the world sizes W whose rank-0 share is timed")
-    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr", "shard"],
+    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr", "tlr-potrf", "shard"],
                     help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
                          "posterior: NEXT-4 conditioning (paper size: 200x200 sites, 6,250 observations); "
                          "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU; "
                          "tlr: NEXT-3 TLR compression at the paper's 40K-site accuracy setting; "
                          "shard: the SOV over rank 0's 1/W sample share for each W in --shard (one GPU)")
     ap.add_argument("--tlr-eps", type=float, default=1e-3, help="--workload tlr: accuracy eps (R23)")
+    ap.add_argument("--tlr-order", default="sorted", choices=["sorted", "spatial"],
+                    help="--workload tlr-potrf: factor Sigma in the sorted order (Alg. 1) or the grid order")
+    ap.add_argument("--tlr-kmax", type=int, default=128, help="--workload tlr-potrf: factor slot width")
+    ap.add_argument("--tlr-g", type=int, default=200, help="--workload tlr-potrf: grid side (n = g^2)")
     ap.add_argument("--tlr-mode", type=int, default=0, choices=[0, 1],
                     help="--workload tlr: 0 = keep sigma_i >= eps, 1 = relative Frobenius error <= eps per tile")
     ap.add_argument("--mc-samples", type=int, default=50_000, help="--workload mc: draws (paper: N = 50,000, P:595)")
@@ -526,6 +633,8 @@ def main():
         return run_mc(args, cfg)
     if args.workload == "tlr":
         return run_tlr(args)
+    if args.workload == "tlr-potrf":
+        return run_tlr_potrf(args)
     if args.workload == "posterior":
         return run_posterior(args)
     if args.workload == "potrf-dist":

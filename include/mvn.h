@@ -424,6 +424,31 @@ enum { MVN_TLR_ABS = 0, MVN_TLR_REL_FRO = 1 };
 mvn_status mvn_tlr_compress(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, double eps, int32_t mode, int32_t *d_ranks);
 
 /* ---------------------------------------------------------------------------------------------
+ * NEXT-3: the TLR Cholesky (Alg. 1 l.7-8: "compression of the covariance matrix into the TLR
+ * format"; step (a) "can be performed using both dense and TLR computations. However, (b),
+ * (c), and (d) are only performed in dense"). Reading R26 (oracle/tlr.py
+ * tlr_cholesky):
+ *   1. every off-diagonal tile of Sigma is compressed at eps (mvn_tlr_compress's rule, R23) into
+ *      factors U_t V_t^T;
+ *   2. tile column j = 0 .. nt-1: T_i = Stilde_ij - sum_{k<j} U_ik (V_ik^T V_jk) U_jk^T (i >= j, the
+ *      updates applied in factored form: 4 128 r_ik r_jk + 2 128^2 r_jk flops instead of 2 128^3),
+ *      L_jj = chol(T_j), L_ij = T_i L_jj^{-T}, and each L_ij is truncated at eps once (U_t V_t^T);
+ *   3. the off-diagonal tiles of d_tiles receive Ltilde = U_t V_t^T reconstructed, so that
+ *      mvn_sov_prefix (dense) reads the TLR factor unchanged.
+ * d_tiles: in Sigma (tile-packed, sorted order), out the factor: L_jj dense on the diagonal,
+ * Ltilde_ij off it. d_U, d_V (device, caller-owned, mvn_tlr_slots_bytes(t, kmax) bytes each): slot
+ * t = I(I-1)/2 + J holds U_t, V_t as column-major 128 x kmax blocks at t 128 kmax doubles (first
+ * r_t columns used); on return the factors of Ltilde. d_ranks (device int32, nt(nt-1)/2): the ranks
+ * r_t of Ltilde; d_ranks_sigma (nullable): Sigma's ranks after step 1. kmax in [1, 128] is the slot
+ * width (memory per slot pair = 2 128 kmax doubles; kmax = 64 fits both factors in the bytes of a
+ * dense tile). *info (host): -1, or the first failing global row (MVN_E_NUMERIC). MVN_E_NOMEM if a
+ * tile needed a rank above kmax (stored truncated to kmax; the factor is then not at accuracy eps;
+ * reported before a failing pivot, which the truncation may have caused). MVN_E_USAGE as mvn_tlr_compress, or kmax outside [1, 128]. Synchronises (info).            */
+size_t mvn_tlr_slots_bytes(mvn_tiles t, int32_t kmax);
+mvn_status mvn_tlr_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, double eps, int32_t mode, int32_t kmax,
+                         double *d_U, double *d_V, int32_t *d_ranks, int32_t *d_ranks_sigma, int64_t *info);
+
+/* ---------------------------------------------------------------------------------------------
  * End-to-end CRD (Alg. 1) on one GPU with HOST buffers: upload, a1..a10, download.
  * This is the call a user makes; bench.py's "e2e" number times it.                             */
 typedef struct {

@@ -39,7 +39,7 @@ ABI_SYMBOLS = [
     "mvn_dtiles_bytes", "mvn_dpanel_numel", "mvn_dcov_matern", "mvn_dpotrf_panel", "mvn_dpanel_pack",
     "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex", "mvn_potrf_ex", "mvn_dpanel_trsm",
     "mvn_sov_prefix_units", "mvn_prefix_reduce", "mvn_sweep_begin", "mvn_sweep_rows", "mvn_sweep_end",
-    "mvn_sweep_free", "mvn_drows_offset", "mvn_drows_unpack",
+    "mvn_sweep_free", "mvn_drows_offset", "mvn_drows_unpack", "mvn_tlr_slots_bytes", "mvn_tlr_potrf",
 ]
 
 
@@ -134,6 +134,8 @@ def lib() -> ctypes.CDLL:
         "mvn_posterior": (S, [P, ctypes.POINTER(mvn_posterior_problem), P, P, ctypes.POINTER(I64)]),
         "mvn_posterior_tiles": (S, [P, T, P, P]),
         "mvn_tlr_compress": (S, [P, T, P, D, I32, P]),
+        "mvn_tlr_slots_bytes": (ctypes.c_size_t, [T, I32]),
+        "mvn_tlr_potrf": (S, [P, T, P, D, I32, I32, P, P, P, P, ctypes.POINTER(I64)]),
         "mvn_dtiles_bytes": (ctypes.c_size_t, [mvn_dtiles]),
         "mvn_dpanel_numel": (I64, [mvn_dtiles, I64]),
         "mvn_dcov_matern": (S, [P, mvn_dtiles, P, D, D, D, D, P]),
@@ -694,6 +696,44 @@ def mvn_tlr_compress(t, n: int, eps: float, ranks=None, mode: int = TLR_ABS):
                                    _dev_ptr(ranks, torch.int32)),
             "mvn_tlr_compress")
     return ranks
+
+
+@dataclass
+class TlrFactor:
+    """mvn_tlr_potrf's outputs besides the factor itself (in the tile buffer): the factor slots of
+    the off-diagonal tiles (U_t, V_t: [tiles][kmax columns][128] views of 128 x kmax column-major
+    blocks), the ranks of L~ and of Sigma~, and info."""
+    U: object
+    V: object
+    ranks: object
+    ranks_sigma: object
+    kmax: int
+    info: int
+
+
+def mvn_tlr_potrf(t, n: int, eps: float, mode: int = TLR_ABS, kmax: int = TILE, raise_on_numeric: bool = True,
+                  U=None, V=None) -> TlrFactor:
+    """TLR Cholesky in place (reading R26): Sigma's off-diagonal tiles compressed at eps, the tile
+    columns factored with the updates in factored form, every L tile truncated at eps once; on
+    return `t` holds L~ (dense diagonal tiles, off-diagonal tiles U V^T reconstructed for the dense
+    SOV)."""
+    import torch
+    c = Context.get(t.device.index)
+    nt = -(-n // TILE)
+    noff = nt * (nt - 1) // 2
+    if U is None:
+        U = torch.empty((max(noff, 1), kmax, TILE), dtype=torch.float64, device=t.device)
+    if V is None:
+        V = torch.empty((max(noff, 1), kmax, TILE), dtype=torch.float64, device=t.device)
+    ranks = torch.zeros(max(noff, 1), dtype=torch.int32, device=t.device)
+    ranks_s = torch.zeros(max(noff, 1), dtype=torch.int32, device=t.device)
+    info = ctypes.c_int64(-1)
+    st = lib().mvn_tlr_potrf(c.h, tiles(n), _dev_ptr(t, torch.float64), float(eps), int(mode), int(kmax),
+                             _dev_ptr(U, torch.float64), _dev_ptr(V, torch.float64), _dev_ptr(ranks, torch.int32),
+                             _dev_ptr(ranks_s, torch.int32), ctypes.byref(info))
+    if not (st == MVN_E_NUMERIC and not raise_on_numeric):
+        c.check(st, "mvn_tlr_potrf")
+    return TlrFactor(U, V, ranks, ranks_s, kmax, int(info.value))
 
 
 @dataclass

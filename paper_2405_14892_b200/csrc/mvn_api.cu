@@ -48,6 +48,7 @@ struct mvn_ctx {
     void *pozA = nullptr; size_t pozA_cap = 0;     // int8 POTRF: panel digit slices
     void *pozR = nullptr; size_t pozR_cap = 0;     // int8 POTRF: panel row scales
     void *pozX = nullptr; size_t pozX_cap = 0;     // int8 POTRF: cluster exchange scratch
+    void *tlrW = nullptr; size_t tlrW_cap = 0;     // TLR Cholesky: panel + M / Z chunks + overflow flag
     // mvn_sweep state: stream-ordered allocations from the context's own pool, which keeps the
     // memory between sweeps (no re-mapping per sweep) until mvn_trim / mvn_destroy
     cudaMemPool_t pool = nullptr;
@@ -211,7 +212,7 @@ void mvn_destroy(mvn_ctx *c) {
     // waits for the device's outstanding work itself
     cudaDeviceSynchronize();
     for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF,
-                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX, c->sozX, c->pozA, c->pozR, c->pozX})
+                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX, c->sozX, c->pozA, c->pozR, c->pozX, c->tlrW})
         if (p) cudaFree(p);
     if (c->done) cudaEventDestroy(c->done);
     if (c->pool) cudaMemPoolDestroy(c->pool);
@@ -241,10 +242,10 @@ mvn_status mvn_trim(mvn_ctx *c) {
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX, &c->sozX, &c->pozA, &c->pozR, &c->pozX})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX, &c->sozX, &c->pozA, &c->pozR, &c->pozX, &c->tlrW})
         if (*p) { cudaFree(*p); *p = nullptr; }
     c->Y_cap = c->part_cap = c->cta_cap = c->sync_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
-    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = c->sozX_cap = c->pozA_cap = c->pozR_cap = c->pozX_cap = 0;
+    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = c->sozX_cap = c->pozA_cap = c->pozR_cap = c->pozX_cap = c->tlrW_cap = 0;
     c->post_n = c->post_off = 0;
     if (c->pool) cudaMemPoolTrimTo(c->pool, 0);
     return MVN_OK;
@@ -1020,6 +1021,46 @@ mvn_status mvn_tlr_compress(mvn_ctx *c, mvn_tiles t, double *d_tiles, double eps
         (mode == MVN_TLR_REL_FRO && !(eps <= 1.0)))
         return fail(c, MVN_E_USAGE, "mvn_tlr_compress: bad arguments (need nb=128, eps >= 0, mode 0 or 1, eps <= 1 for mode 1)");
     MVN_CUDA(c, mvn::launch_tlr_compress(t.n, d_tiles, eps, mode, d_ranks, c->stream));
+    return MVN_OK;
+}
+
+size_t mvn_tlr_slots_bytes(mvn_tiles t, int32_t kmax) {
+    if (!tiles_ok(t) || kmax < 1 || kmax > (int32_t)mvn::kTile) return 0;
+    return sizeof(double) * mvn::tlr_slot_doubles(t.n, kmax);
+}
+
+mvn_status mvn_tlr_potrf(mvn_ctx *c, mvn_tiles t, double *d_tiles, double eps, int32_t mode, int32_t kmax, double *d_U,
+                         double *d_V, int32_t *d_ranks, int32_t *d_ranks_sigma, int64_t *info) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !d_tiles || !info || !(eps >= 0.0) || (mode != MVN_TLR_ABS && mode != MVN_TLR_REL_FRO) ||
+        (mode == MVN_TLR_REL_FRO && !(eps <= 1.0)) || kmax < 1 || kmax > (int32_t)mvn::kTile)
+        return fail(c, MVN_E_USAGE, "mvn_tlr_potrf: bad arguments (need nb=128, eps >= 0, mode 0 or 1, eps <= 1 for mode 1, 1 <= kmax <= 128)");
+    const int64_t nt = (t.n + t.nb - 1) / t.nb;
+    if (nt > 1 && (!d_U || !d_V || !d_ranks)) return fail(c, MVN_E_USAGE, "mvn_tlr_potrf: factor slots and ranks required");
+    // M / Z chunks: at most 2,048 tiles each (256 MB), at least one tile column's worth
+    const int64_t need = std::max<int64_t>(1, (nt / 2) * ((nt + 1) / 2));
+    const int64_t chunk = std::max<int64_t>(std::min<int64_t>(need, 2048), nt);
+    const size_t wbytes = sizeof(double) * mvn::tlr_work_doubles(t.n, chunk);
+    mvn_status s;
+    if ((s = ensure(c, &c->tlrW, &c->tlrW_cap, wbytes + 256)) != MVN_OK) return s;
+    int *overflow = (int *)((char *)c->tlrW + wbytes);
+    const int64_t minus1 = -1;
+    MVN_CUDA(c, cudaMemsetAsync(overflow, 0, sizeof(int), c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    MVN_CUDA(c, mvn::launch_tlr_potrf(t.n, d_tiles, eps, mode, kmax, d_U, d_V, d_ranks, d_ranks_sigma, (double *)c->tlrW,
+                                      chunk, overflow, c->d_info, c->stream));
+    int ovf = 0;
+    MVN_CUDA(c, cudaMemcpyAsync(info, c->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaMemcpyAsync(&ovf, overflow, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    MVN_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (*info >= t.n) *info = -1;
+    // a rank above kmax first: the truncation to kmax is not at accuracy eps and may itself be what
+    // made a later pivot non-positive
+    if (ovf > 0)
+        return fail(c, MVN_E_NOMEM, "mvn_tlr_potrf: a tile needs rank " + std::to_string(ovf) + " > kmax = " + std::to_string(kmax));
+    if (*info >= 0)
+        return fail(c, MVN_E_NUMERIC, "mvn_tlr_potrf: matrix not positive definite at row " + std::to_string(*info));
     return MVN_OK;
 }
 

@@ -134,6 +134,12 @@ cudaError_t launch_permute_sym(const double *src, int64_t off, const int64_t *or
 // NEXT-3 (part): fixed-accuracy TLR compression of the off-diagonal tiles (kernels_tlr.cu)
 cudaError_t tlr_init();
 cudaError_t launch_tlr_compress(int64_t n, double *tiles, double eps, int mode, int *ranks, cudaStream_t st);
+// NEXT-3: the TLR Cholesky (R26): factor slots, workspace, the column loop
+size_t tlr_slot_doubles(int64_t n, int kmax);
+size_t tlr_work_doubles(int64_t n, int64_t chunk_slots);
+cudaError_t launch_tlr_potrf(int64_t n, double *tiles, double eps, int mode, int kmax, double *U, double *V,
+                             int *ranks, int *ranks_sigma, double *work, int64_t chunk_slots, int *overflow,
+                             int64_t *d_info, cudaStream_t st);
 
 // NEXT-2: Monte-Carlo validation
 cudaError_t mc_init();

@@ -51,7 +51,9 @@ def check_vs_oracle(T, S, ranks_gpu, eps, n, mode="abs"):
             if k != ko:      # only a near tie at the threshold may differ
                 lo, hi = min(k, ko), max(k, ko)
                 if mode == "abs":
-                    assert np.all(np.abs(sig[t][lo:hi] - eps) <= 1e-12), (I, J, k, ko, sig[t][lo:hi])
+                    # the GPU drops the QR's trailing block once ||R_22||_F <= 1e-6 eps (kernels_tlr.cu),
+                    # which moves a singular value by at most that
+                    assert np.all(np.abs(sig[t][lo:hi] - eps) <= 1e-12 + 2e-6 * eps), (I, J, k, ko, sig[t][lo:hi])
                 else:            # the smaller rank is feasible up to rounding of the tail sum
                     tot = np.sum(sig[t] ** 2)
                     assert np.sum(sig[t][lo:] ** 2) <= eps * eps * tot * (1 + 1e-9) + 1e-28, (I, J, k, ko)
@@ -59,7 +61,7 @@ def check_vs_oracle(T, S, ranks_gpu, eps, n, mode="abs"):
             E = S[rs, cs] - G[rs, cs]
             if mode == "abs":
                 e2 = np.linalg.norm(E, 2)
-                assert (e2 < eps + 1e-12) if eps > 0 else np.max(np.abs(E)) < 1e-13, (I, J, k, ko, e2, sig[t][max(k - 2, 0):k + 2])
+                assert (e2 < eps * (1 + 2e-6) + 1e-12) if eps > 0 else np.max(np.abs(E)) < 1e-13, (I, J, k, ko, e2, sig[t][max(k - 2, 0):k + 2])
             else:
                 ef, af = np.linalg.norm(E), np.linalg.norm(S[rs, cs])
                 assert ef <= eps * af * (1 + 1e-9) + 1e-13, (I, J, k, ko, ef, af)
@@ -67,7 +69,8 @@ def check_vs_oracle(T, S, ranks_gpu, eps, n, mode="abs"):
                 # the kept subspace of a tile moves by (rounding perturbation) / (sigma_k - sigma_k+1)
                 sg = sig[t]
                 gap = sg[k - 1] - sg[k] if 0 < k < NB else np.inf
-                tol = 1e-12 + 1e-13 * sg[0] * (1.0 + sg[0] / gap)
+                tau = 1e-6 * eps * (1.0 if mode == "abs" else np.linalg.norm(S[rs, cs]))   # the dropped R_22
+                tol = 1e-12 + (1e-13 * sg[0] + tau) * (1.0 + sg[0] / gap)
                 assert np.max(np.abs(G[rs, cs] - St[rs, cs])) <= tol, (I, J, k, gap)
             t += 1
     for I in range(nt):                       # diagonal tiles untouched
