@@ -539,6 +539,27 @@ def run_tlr_potrf(args):
     clocks.start()
     ms_tlr, f = timed(lambda: mvn.mvn_tlr_potrf(T, n, args.tlr_eps, mode=args.tlr_mode, kmax=args.tlr_kmax, U=U, V=V))
     ms_dense, info_d = timed(lambda: mvn.mvn_potrf(T, n, raise_on_numeric=False))
+    # the SOV sweep on L~: dense (k_sov on the reconstructed tiles) vs the factored update
+    # (k_sov_tlr), the same samples; T holds the last dense factor, so refactor with TLR first
+    T.copy_(base)
+    f = mvn.mvn_tlr_potrf(T, n, args.tlr_eps, mode=args.tlr_mode, kmax=args.tlr_kmax, U=U, V=V)
+    a_ord = np.ascontiguousarray(cfg.u - inp.mu[order])
+    d_a = torch.from_numpy(a_ord).cuda()
+    ns = args.tlr_sov_samples
+    sov = {}
+    for name, fn in [("dense", lambda: mvn.mvn_sov_prefix(T, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, 0, ns)),
+                     ("factored", lambda: mvn.mvn_sov_prefix_tlr(T, f, n, d_a, cfg.N, cfg.R, cfg.seed_lattice, 0, ns))]:
+        ts = []
+        for it in range(args.warmup + args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            M_, S_ = fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                ts.append(e0.elapsed_time(e1))
+        lp = (M_ + torch.log(S_) - math.log(ns)).cpu().numpy()
+        sov[name] = {"ms": float(np.mean(ts)), "logp": lp}
     clk = clocks.stop()
     rL, rS = f.ranks.cpu().numpy(), f.ranks_sigma.cpu().numpy()
     flops = tlr_update_flops(rL, nt)
@@ -556,6 +577,8 @@ def run_tlr_potrf(args):
             "ranks_L": {"mean": float(rL.mean()), "p90": float(np.percentile(rL, 90)), "max": int(rL.max())},
             "ranks_sigma": {"mean": float(rS.mean()), "max": int(rS.max())},
             "update_flops": flops, "update_flops_over_dense_potrf": flops / dense_flops,
+            "sov_on_Ltilde": {"samples": ns, "dense_ms": sov["dense"]["ms"], "factored_ms": sov["factored"]["ms"],
+                              "max_abs_dlogP": float(np.max(np.abs(sov["dense"]["logp"] - sov["factored"]["logp"])))},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
                          "algorithmic": "factored updates 4 nb r_ik r_jk + 2 nb^2 r_jk per (i, j, k) over the TLR "
@@ -619,6 +642,8 @@ def main():
                     help="--workload tlr-potrf: factor Sigma in the sorted order (Alg. 1) or the grid order")
     ap.add_argument("--tlr-kmax", type=int, default=128, help="--workload tlr-potrf: factor slot width")
     ap.add_argument("--tlr-g", type=int, default=200, help="--workload tlr-potrf: grid side (n = g^2)")
+    ap.add_argument("--tlr-sov-samples", type=int, default=10_000,
+                    help="--workload tlr-potrf: samples of the dense vs factored SOV sweep on L~")
     ap.add_argument("--tlr-mode", type=int, default=0, choices=[0, 1],
                     help="--workload tlr: 0 = keep sigma_i >= eps, 1 = relative Frobenius error <= eps per tile")
     ap.add_argument("--mc-samples", type=int, default=50_000, help="--workload mc: draws (paper: N = 50,000, P:595)")

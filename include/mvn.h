@@ -445,6 +445,18 @@ mvn_status mvn_tlr_compress(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, double e
  * tile needed a rank above kmax (stored truncated to kmax; the factor is then not at accuracy eps;
  * reported before a failing pivot, which the truncation may have caused). MVN_E_USAGE as mvn_tlr_compress, or kmax outside [1, 128]. Synchronises (info).            */
 size_t mvn_tlr_slots_bytes(mvn_tiles t, int32_t kmax);
+
+/* The SOV sweep of mvn_sov_prefix with the update in factored form (SURVEY §8(f) rank 3 "factored
+ * SOV update A -= U(V^T Y)"): for the rows of tile row T, s = sum_{J<T} U_TJ (V_TJ^T Y_J) from
+ * mvn_tlr_potrf's factor slots (d_U, d_V, d_ranks, kmax as returned there) plus the dense diagonal
+ * tile L_TT read from d_L (tile-packed; only the diagonal tiles are read). Same samples, lattice,
+ * Phi chain and outputs (d_M, d_S) as mvn_sov_prefix on the reconstructed factor, equal to it up to
+ * summation order. The paper itself keeps this step dense; the factored form costs
+ * 4 128 r_TJ + 256 r_TJ flops per sample and tile instead of 2 128^2, so it pays only for ranks
+ * below ~43. USAGE as mvn_sov_prefix, or kmax outside [1, 128], or missing slots for n > 128. */
+mvn_status mvn_sov_prefix_tlr(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_U, const double *d_V,
+                              const int32_t *d_ranks, int32_t kmax, const double *d_a, const double *d_b,
+                              const mvn_qmc *q, double *d_M, double *d_S);
 mvn_status mvn_tlr_potrf(mvn_ctx *ctx, mvn_tiles t, double *d_tiles, double eps, int32_t mode, int32_t kmax,
                          double *d_U, double *d_V, int32_t *d_ranks, int32_t *d_ranks_sigma, int64_t *info);
 

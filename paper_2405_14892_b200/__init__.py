@@ -40,6 +40,7 @@ ABI_SYMBOLS = [
     "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex", "mvn_potrf_ex", "mvn_dpanel_trsm",
     "mvn_sov_prefix_units", "mvn_prefix_reduce", "mvn_sweep_begin", "mvn_sweep_rows", "mvn_sweep_end",
     "mvn_sweep_free", "mvn_drows_offset", "mvn_drows_unpack", "mvn_tlr_slots_bytes", "mvn_tlr_potrf",
+    "mvn_sov_prefix_tlr",
 ]
 
 
@@ -136,6 +137,7 @@ def lib() -> ctypes.CDLL:
         "mvn_tlr_compress": (S, [P, T, P, D, I32, P]),
         "mvn_tlr_slots_bytes": (ctypes.c_size_t, [T, I32]),
         "mvn_tlr_potrf": (S, [P, T, P, D, I32, I32, P, P, P, P, ctypes.POINTER(I64)]),
+        "mvn_sov_prefix_tlr": (S, [P, T, P, P, P, P, I32, P, P, ctypes.POINTER(mvn_qmc), P, P]),
         "mvn_dtiles_bytes": (ctypes.c_size_t, [mvn_dtiles]),
         "mvn_dpanel_numel": (I64, [mvn_dtiles, I64]),
         "mvn_dcov_matern": (S, [P, mvn_dtiles, P, D, D, D, D, P]),
@@ -709,6 +711,23 @@ class TlrFactor:
     ranks_sigma: object
     kmax: int
     info: int
+
+
+def mvn_sov_prefix_tlr(L, f: "TlrFactor", n: int, a, N: int, R: int, seed: int, begin: int = 0,
+                       end: int | None = None, b=None, M=None, S=None):
+    """mvn_sov_prefix with the factored update s = sum_J U_TJ (V_TJ^T Y_J) from mvn_tlr_potrf's factor
+    slots (f); L supplies the dense diagonal tiles. Returns CUDA (M, S)."""
+    import torch
+    c = Context.get(L.device.index)
+    end = N * R if end is None else end
+    M = torch.empty(n, dtype=torch.float64, device=L.device) if M is None else M
+    S = torch.empty(n, dtype=torch.float64, device=L.device) if S is None else S
+    q = mvn_qmc(int(N), int(R), int(seed), int(begin), int(end))
+    c.check(lib().mvn_sov_prefix_tlr(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(f.U, torch.float64),
+                                     _dev_ptr(f.V, torch.float64), _dev_ptr(f.ranks, torch.int32), int(f.kmax),
+                                     _dev_ptr(a, torch.float64), None if b is None else _dev_ptr(b, torch.float64),
+                                     ctypes.byref(q), _dev_ptr(M), _dev_ptr(S)), "mvn_sov_prefix_tlr")
+    return M, S
 
 
 def mvn_tlr_potrf(t, n: int, eps: float, mode: int = TLR_ABS, kmax: int = TILE, raise_on_numeric: bool = True,

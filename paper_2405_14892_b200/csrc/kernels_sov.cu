@@ -130,6 +130,11 @@ struct SovArgs {
     double *ell;
     int64_t g_base;
     const int64_t *yoff;
+    // NEXT-3 factored update (k_sov_tlr): off-diagonal tiles of L as U_t V_t^T in slots of 128 x tkmax
+    // (mvn_tlr_potrf), t = I(I-1)/2 + J, rank tranks[t]; the diagonal tiles are read from L
+    const double *tU = nullptr, *tV = nullptr;
+    const int *tranks = nullptr;
+    int tkmax = 0;
 };
 
 // Sample blocks of a CTA: its `count` samples are split into nblk = ceil(count / 128) blocks whose
@@ -551,6 +556,208 @@ __global__ void __launch_bounds__(sovk::NT, 1) k_sov(SovArgs p) {
     }
 }
 
+// ------------------------------------------------------------------------------------ NEXT-3
+// k_sov_tlr: the sweep with the SOV update in factored form, s_k = sum_J U_TJ (V_TJ^T Y_J) over the
+// tiles J < T of the row's tile row T ("factored SOV update A -= U(V^T Y)";
+// the paper itself keeps (b)-(d) dense, which k_sov on the reconstructed L~ does). Same
+// samples, lattice, chain (chain_load / chain_rowblock) and partials as k_sov; the GEMM warps run
+// per 64-row block rb (tile row T = rb / 2, half h = rb % 2):
+//   for each J < T with rank r: W = V_TJ(:, c0:c0+64)^T Y_J (<= 64 x w, K = 128, Y_J staged in
+//   shared memory), acc += U_TJ(64h:64h+64, c0:c0+64) W; for h = 1 also the dense part of the
+//   diagonal tile, acc += L_TT(64:128, 0:64) Y_T(0:64).
+// The GEMM of rb starts after the chain of rb - 1 (no overlap: the S tile is the accumulator, which
+// keeps one fragment array per thread live). No producer warp: the operands come from L2 (U, V: direct fragment loads; Y: staged, ld.global.cg since the CTA's Y slot is rewritten
+// by every sample block). Flops per (sample, tile): 2 x (2 128 r) + 2 64 r x 2 halves, vs 2 128^2
+// dense: the factored form pays when r < ~43.
+namespace sovt {
+constexpr int NG = sovk::NGEMM, NTH = NG + sovk::NCHAIN;  // 8 GEMM warps + 4 chain warps, no producer
+constexpr int BAR_G = 4;                                   // the GEMM warps' staging barrier
+constexpr int SW = sovk::NB + 4;                           // W / staged-Y row stride (== 4 mod 16)
+constexpr int OFF_W = 0, OFF_BS = OFF_W + 64 * SW;         // inside k_sov's ring region (unused here)
+static_assert(OFF_BS + 16 * SW <= sovk::OFF_S, "TLR staging must fit the ring region");
+}  // namespace sovt
+
+// acc(8 rows of warp wp x w) += A(8 x K) * B(K x w): A fragments straight from global (a(m, k) =
+// A[m * am + k * ak], m = the warp's row 8 wp + lane / 4), B rows staged 16 at a time from the Y
+// history (rows y0 + k, stride sbw, `cg` loads) or read from the W tile in shared memory.
+template <int NF>
+__device__ __forceinline__ void tlr_rows_gemm(double (&acc)[16][2], const double *__restrict__ A, int64_t am, int64_t ak,
+                                              int K, const double *Y, int64_t y0, int sbw, const double *Wsm,
+                                              double *BS, int w, int tid) {
+    using namespace sovt;
+    const int lane = tid & 31, wp = tid >> 5;
+    const int mrow = 8 * wp + (lane >> 2);
+    for (int k0 = 0; k0 < K; k0 += 16) {
+        const double *Bs;
+        int bstride;
+        if (Y) {
+            named_sync(BAR_G, NG);                        // the previous chunk's reads of BS are done
+            for (int e = tid; e < 16 * w; e += NG) {
+                const int kk = e / w, nn = e - kk * w;
+                BS[kk * SW + nn] = (k0 + kk < K) ? __ldcg(Y + (y0 + k0 + kk) * sbw + nn) : 0.0;
+            }
+            named_sync(BAR_G, NG);
+            Bs = BS;
+            bstride = SW;
+        } else {
+            Bs = Wsm + (int64_t)k0 * SW;
+            bstride = SW;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 16; kk += 4) {
+            const int kr = kk + (lane & 3);
+            const double a = (k0 + kr < K) ? __ldg(A + (int64_t)mrow * am + (int64_t)(k0 + kr) * ak) : 0.0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const double b = Bs[kr * bstride + 8 * f + (lane >> 2)];
+                dmma(acc[f][0], acc[f][1], a, b);
+            }
+        }
+    }
+}
+
+// S(8 rows of warp wp, :) += acc (the warp's own fragments of the S tile)
+template <int NF>
+__device__ __forceinline__ void tlr_add_to_s(double *sm, const double (&acc)[16][2], int tid) {
+    double *S = sm + sovk::OFF_S;
+    const int lane = tid & 31, m = 8 * (tid >> 5) + (lane >> 2);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        double2 *d = reinterpret_cast<double2 *>(S + m * sovk::SS + 8 * f + 2 * (lane & 3));
+        const double2 v = *d;
+        *d = make_double2(v.x + acc[f][0], v.y + acc[f][1]);
+    }
+}
+
+template <int NF>
+__device__ __forceinline__ void tlr_tile_term(const SovArgs &p, double *sm, const double *Yslot, int sbw, int T, int J,
+                                              int h, int w, int tid) {
+    using namespace sovt;
+    const int64_t t = (int64_t)T * (T - 1) / 2 + J;
+    const int r = p.tranks[t];
+    const double *U = p.tU + t * 128 * (int64_t)p.tkmax, *V = p.tV + t * 128 * (int64_t)p.tkmax;
+    double *Wsm = sm + OFF_W, *BS = sm + OFF_BS;
+    const int lane = tid & 31, wp = tid >> 5;
+    for (int c0 = 0; c0 < r; c0 += 64) {
+        const int rc = r - c0 < 64 ? r - c0 : 64;
+        double acc[16][2];
+        // W (rc x w) = V(:, c0 + m)^T Y_J: a(m, k) = V[(c0 + m) 128 + k]; rows m >= rc are not read
+        // (a warp's rows past rc compute garbage-free zeros: its A pointer is clamped, the rows dropped)
+#pragma unroll
+        for (int f = 0; f < 16; ++f) acc[f][0] = acc[f][1] = 0.0;
+        const int mrow = 8 * wp + (lane >> 2);
+        const double *Vw = V + (int64_t)c0 * 128 + (mrow < rc ? 0 : -(int64_t)mrow * 128);   // row m -> column c0 + m (clamped to c0)
+        tlr_rows_gemm<NF>(acc, Vw, 128, 1, 128, Yslot, (int64_t)J * 128, sbw, nullptr, BS, w, tid);
+        named_sync(BAR_G, NG);                            // the previous W's readers are done
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const int col = 8 * f + 2 * (lane & 3);
+            const bool ok = mrow < rc;
+            Wsm[mrow * SW + col] = ok ? acc[f][0] : 0.0;
+            Wsm[mrow * SW + col + 1] = ok ? acc[f][1] : 0.0;
+        }
+        named_sync(BAR_G, NG);
+        // S(64h + m, :) += U(64h + m, c0 + k) W(k, :), k < rc
+#pragma unroll
+        for (int f = 0; f < 16; ++f) acc[f][0] = acc[f][1] = 0.0;
+        tlr_rows_gemm<NF>(acc, U + (int64_t)c0 * 128 + 64 * h, 1, 128, rc, nullptr, 0, 0, Wsm, BS, w, tid);
+        tlr_add_to_s<NF>(sm, acc, tid);
+    }
+}
+
+template <int NF>
+__device__ __forceinline__ void tlr_gemm_rowblock(const SovArgs &p, double *sm, const double *Yslot, int sbw, int rb,
+                                                  int w, int tid) {
+    using namespace sovt;
+    const int T = rb >> 1, h = rb & 1;
+    named_sync(sovk::BAR_YREADY, NTH);                    // chain(rb - 1) done: Y rows of rb - 1, S free
+    {
+        double *S = sm + sovk::OFF_S;
+        const int lane = tid & 31, m = 8 * (tid >> 5) + (lane >> 2);
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            *reinterpret_cast<double2 *>(S + m * sovk::SS + 8 * f + 2 * (lane & 3)) = make_double2(0.0, 0.0);
+    }
+    for (int J = 0; J < T; ++J) tlr_tile_term<NF>(p, sm, Yslot, sbw, T, J, h, w, tid);
+    if (h == 1) {                                         // dense part of the diagonal tile: L_TT(64:, 0:64) Y_T(0:64)
+        double acc[16][2];
+#pragma unroll
+        for (int f = 0; f < 16; ++f) acc[f][0] = acc[f][1] = 0.0;
+        const double *Ltt = p.L + tile_offset(T, T) + 64;
+        tlr_rows_gemm<NF>(acc, Ltt, 1, 128, 64, Yslot, (int64_t)T * 128, sbw, nullptr, sm + OFF_BS, w, tid);
+        tlr_add_to_s<NF>(sm, acc, tid);
+    }
+    named_arrive(sovk::BAR_SFULL, NTH);
+}
+
+template <bool HAS_B>
+__global__ void __launch_bounds__(sovt::NTH, 1) k_sov_tlr(SovArgs p) {
+    using namespace sovk;
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x;
+    const int64_t g_first = p.cta[blockIdx.x * 3], count = p.cta[blockIdx.x * 3 + 1], blk_first = p.cta[blockIdx.x * 3 + 2];
+    const int nblk = (int)((count + NB - 1) / NB);
+    if (tid < NGEMM) {
+        // ============================================================ GEMM warps (factored update)
+        for (int b = 0; b < nblk; ++b) {
+            const int w = block_geom(count, b, p.unit_mode).w, sbw = w + 4;
+            const double *Yslot = y_slot(p, count, b);
+            for (int rb = 1; rb < p.nrb; ++rb) {
+#define MVN_TG(F) case F: tlr_gemm_rowblock<F>(p, sm, Yslot, sbw, rb, w, tid); break;
+                switch (w >> 3) {
+                    MVN_TG(1) MVN_TG(2) MVN_TG(3) MVN_TG(4) MVN_TG(5) MVN_TG(6) MVN_TG(7) MVN_TG(8)
+                    MVN_TG(9) MVN_TG(10) MVN_TG(11) MVN_TG(12) MVN_TG(13) MVN_TG(14) MVN_TG(15) MVN_TG(16)
+                    default: break;
+                }
+#undef MVN_TG
+            }
+            named_sync(BAR_YREADY, sovt::NTH);            // the block's last chain is done (balances its arrival)
+        }
+    } else {
+        // ============================================================ chain warps (as k_sov)
+        const int j = tid - NGEMM;
+        for (int b = 0; b < nblk; ++b) {
+            const BlockGeom bg = block_geom(count, b, p.unit_mode);
+            const int64_t g0 = g_first + bg.off;
+            const int cnt = bg.cnt;
+            const int w = bg.w;
+            const uint64_t g = (uint64_t)(g0 + (j < cnt ? j : 0));
+            const uint64_t r = g / (uint64_t)p.N;
+            const uint64_t jl = g - r * (uint64_t)p.N + 1ull;
+            const int64_t blk = blk_first + b;
+            double *Yslot = y_slot(p, count, b);
+            double ell = 0.0;
+            for (int rb = 0; rb < p.nrb; ++rb) {
+                chain_load<HAS_B>(p, sm, rb, j);
+                cp_async_commit();
+                if (rb > 0) named_sync(BAR_SFULL, sovt::NTH);
+                cp_async_wait<0>();
+                named_sync(BAR_CHAIN, NCHAIN);
+                if (j < M) sm[OFF_DINV + j] = 1.0 / sm[OFF_LD + j * M + j];
+                named_sync(BAR_CHAIN, NCHAIN);
+                if (j < ((w + 31) & ~31)) chain_rowblock<HAS_B>(p, sm, Yslot, rb, j, cnt, w, r, jl, ell);
+                __threadfence();
+                named_arrive(BAR_YREADY, sovt::NTH);
+                named_sync(BAR_CHAIN, NCHAIN);
+                if (j < M) {
+                    const int64_t k = (int64_t)rb * M + j;
+                    if (k < p.n) {
+                        const double *ps = sm + OFF_PS + j * 8;
+                        const int nw = (w + 31) >> 5;
+                        double mm = -CUDART_INF;
+                        for (int qq = 0; qq < nw; ++qq) mm = fmax(mm, ps[2 * qq]);
+                        double ss = 0.0;
+                        if (mm != -CUDART_INF)
+                            for (int qq = 0; qq < nw; ++qq)
+                                if (ps[2 * qq] != -CUDART_INF) ss += ps[2 * qq + 1] * exp(ps[2 * qq] - mm);
+                        *reinterpret_cast<double2 *>(p.part + (blk * p.part_stride + k) * 2) = make_double2(mm, ss);
+                    }
+                }
+            }
+        }
+    }
+}
+
 // K6: combine block partials per prefix in ascending block order.
 __global__ void k_reduce_blocks(const double *__restrict__ part, int64_t nblk, int64_t n, int64_t n_pad,
                                 double *__restrict__ Mo, double *__restrict__ So) {
@@ -572,6 +779,8 @@ cudaError_t sov_init() {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_sov<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sovk::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(k_sov<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sovk::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_sov_tlr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sovk::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_sov_tlr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sovk::SMEM))) return e;
     return cudaSuccess;
 }
 
@@ -634,7 +843,12 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
         cudaError_t e = cudaMemsetAsync(L.step_done, 0, sizeof(int) * (size_t)L.max_blocks * a.nrb, st);
         if (e != cudaSuccess) return e;
     }
-    if (L.b) k_sov<true><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
+    a.tU = L.tU; a.tV = L.tV; a.tranks = L.tranks; a.tkmax = L.tkmax;
+    if (L.tU) {                                          // NEXT-3 factored update (whole sweeps only)
+        if (L.rb1 > 0 || L.lag > 0) return cudaErrorInvalidValue;
+        if (L.b) k_sov_tlr<true><<<L.grid, sovt::NTH, sovk::SMEM, st>>>(a);
+        else k_sov_tlr<false><<<L.grid, sovt::NTH, sovk::SMEM, st>>>(a);
+    } else if (L.b) k_sov<true><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
     else k_sov<false><<<L.grid, sovk::NT, sovk::SMEM, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -538,8 +538,15 @@ namespace {
 // The fp64 sweep. Sample mode (u0 < 0): the range [q->sample_begin, q->sample_end), balanced over the
 // CTAs, reduced to (M, S). Unit mode: the global 128-sample units [u0, u1), whole units per CTA, the
 // per-unit partials left in d_partial ([u1 - u0][n][2]).
+struct TlrSlots {
+    const double *U = nullptr, *V = nullptr;
+    const int *ranks = nullptr;
+    int kmax = 0;
+};
+
 mvn_status sov_prefix_impl(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
-                           const mvn_qmc *q, int64_t u0, int64_t u1, double *d_partial, double *d_M, double *d_S) {
+                           const mvn_qmc *q, int64_t u0, int64_t u1, double *d_partial, double *d_M, double *d_S,
+                           const TlrSlots *tlr = nullptr) {
     mvn_status s;
     if ((s = ensure_generators(c, t.n)) != MVN_OK) return s;
     {   // NaN limits or a_k > b_k: MVN_E_USAGE (synchronises on a 4-byte flag before the sweep)
@@ -589,6 +596,10 @@ mvn_status sov_prefix_impl(mvn_ctx *c, mvn_tiles t, const double *d_L, const dou
     MVN_CUDA(c, cudaMemcpyAsync(c->cta, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     L.cta = (const int64_t *)c->cta;
     L.Y = (double *)c->Y; L.part = units ? d_partial : (double *)c->part; L.Mout = d_M; L.Sout = d_S;
+    if (tlr) {
+        L.tU = tlr->U; L.tV = tlr->V; L.tranks = tlr->ranks; L.tkmax = tlr->kmax;
+        L.lag = 0;
+    }
     MVN_CUDA(c, mvn::launch_sov(L, c->stream));
     return MVN_OK;
 }
@@ -602,6 +613,22 @@ mvn_status mvn_sov_prefix(mvn_ctx *c, mvn_tiles t, const double *d_L, const doub
         q->sample_end <= q->sample_begin || q->sample_end > q->N * (int64_t)q->R)
         return fail(c, MVN_E_USAGE, "mvn_sov_prefix: bad arguments (need nb=128, 0 <= begin < end <= N*R)");
     return sov_prefix_impl(c, t, d_L, d_a, d_b, q, -1, -1, nullptr, d_M, d_S);
+}
+
+mvn_status mvn_sov_prefix_tlr(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_U, const double *d_V,
+                              const int32_t *d_ranks, int32_t kmax, const double *d_a, const double *d_b, const mvn_qmc *q,
+                              double *d_M, double *d_S) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    const int64_t nt = (t.n + 127) / 128;
+    if (!tiles_ok(t) || !d_L || !d_a || !q || !d_M || !d_S || q->N < 1 || q->R < 1 || q->sample_begin < 0 ||
+        q->sample_end <= q->sample_begin || q->sample_end > q->N * (int64_t)q->R || kmax < 1 || kmax > 128 ||
+        (nt > 1 && (!d_U || !d_V || !d_ranks)))
+        return fail(c, MVN_E_USAGE, "mvn_sov_prefix_tlr: bad arguments (need nb=128, 0 <= begin < end <= N*R, 1 <= kmax <= 128, factor slots)");
+    TlrSlots ts;
+    ts.U = d_U; ts.V = d_V; ts.ranks = d_ranks; ts.kmax = kmax;
+    if (nt == 1) { ts.U = ts.V = d_L; }               // no off-diagonal tile: the slots are never read
+    return sov_prefix_impl(c, t, d_L, d_a, d_b, q, -1, -1, nullptr, d_M, d_S, &ts);
 }
 
 mvn_status mvn_sov_prefix_units(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,

@@ -82,6 +82,10 @@ struct SovLaunch {
     int rb0 = 0, rb1 = 0;
     double *ell = nullptr;
     const int64_t *yoff = nullptr;
+    // NEXT-3: the factored SOV update (k_sov_tlr) from mvn_tlr_potrf's factor slots
+    const double *tU = nullptr, *tV = nullptr;
+    const int *tranks = nullptr;
+    int tkmax = 0;
 };
 int64_t sov_phase_yoff(const int64_t *cta, int grid, int64_t n_pad, int unit_mode, int64_t *yoff);
 cudaError_t sov_init();

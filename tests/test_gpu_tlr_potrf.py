@@ -244,3 +244,58 @@ def test_tlr_potrf_sampled_large(torch, nu, beta, eps):
         else:
             assert np.linalg.norm(R, 2) < eps * nLJJ * (1 + 2e-6) + 1e-12 * nt, (I, J)
     assert 0 < f.ranks.max().item() <= 128
+
+
+# ---- the factored SOV update (mvn_sov_prefix_tlr) ----
+
+@pytest.mark.parametrize("base,g,eps,N,R,nb", [("B", 23, 1e-5, 300, 2, False), ("A", 30, 1e-3, 500, 1, True),
+                                              ("B", 17, 1e-8, 250, 3, False)])
+def test_sov_factored_update_vs_dense_and_oracle(torch, base, g, eps, N, R, nb):
+    """The factored update reaches the dense sweep on the reconstructed L~ (summation order only) and
+    the oracle's SOV on the same L~; ragged n, several sample blocks and shifts, a finite b."""
+    import test_gpu_parity as P
+    cfg = W.small_config("tlrsov", g, N, R, base=base)
+    T, S, a = sorted_cov(torch, cfg)
+    n = cfg.n
+    f = mvn().mvn_tlr_potrf(T, n, eps)
+    assert f.info == -1
+    b = torch.from_numpy(a + 2.5).cuda() if nb else None
+    bn = (a + 2.5) if nb else np.full(n, np.inf)
+    Mt, St = mvn().mvn_sov_prefix_tlr(T, f, n, torch.from_numpy(a).cuda(), N, R, 5, b=b)
+    Md, Sd = mvn().mvn_sov_prefix(T, n, torch.from_numpy(a).cuda(), N, R, 5, b=b)
+    NR = N * R
+    lt, ld = P.logp_from(Mt.cpu().numpy(), St.cpu().numpy(), NR), P.logp_from(Md.cpu().numpy(), Sd.cpu().numpy(), NR)
+    assert np.max(np.abs(lt - ld)) <= 1e-11
+    Mo, So = P.oracle_range(dense_lower(T, n), a, bn, N, R, 5, 0, NR)
+    assert np.max(np.abs(lt - P.logp_from(Mo, So, NR))) <= 1e-10
+
+
+def test_sov_factored_update_exact_low_rank_and_widths(torch):
+    """Sigma = D + F F^T (exact rank 5 tiles): the factored sweep equals the oracle on numpy's
+    Cholesky factor; sample ranges giving block widths 8 ... 128 (both GEMM fragment counts)."""
+    import test_gpu_parity as P
+    rng = np.random.default_rng(11)
+    n, r = 400, 5
+    F = rng.standard_normal((n, r)) * 0.3
+    Sg = F @ F.T + np.diag(rng.uniform(0.5, 1.5, n))
+    T = mvn().mvn_pack_lower(torch.from_numpy(Sg).cuda(), n)
+    f = mvn().mvn_tlr_potrf(T, n, 1e-9)
+    assert list(f.ranks.cpu().numpy()) == [r] * 6
+    a = np.sort(rng.normal(-0.5, 0.5, n))
+    da = torch.from_numpy(a).cuda()
+    Lnp = np.linalg.cholesky(Sg)
+    for begin, end in [(0, 148 * 8), (3, 3 + 148 * 40 + 17), (0, 148 * 128 + 300)]:
+        Mt, St = mvn().mvn_sov_prefix_tlr(T, f, n, da, 10_000, 3, 9, begin, end)
+        Mo, So = P.oracle_range(Lnp, a, np.full(n, np.inf), 10_000, 3, 9, begin, end)
+        lt = P.logp_from(Mt.cpu().numpy(), St.cpu().numpy(), end - begin)
+        assert np.max(np.abs(lt - P.logp_from(Mo, So, end - begin))) <= 1e-10
+
+
+def test_sov_factored_update_errors(torch):
+    n = 300
+    T = mvn().alloc_tiles(n, "cuda")
+    a = torch.zeros(n, dtype=torch.float64, device="cuda")
+    f = mvn().TlrFactor(torch.zeros(1, dtype=torch.float64, device="cuda"), torch.zeros(1, dtype=torch.float64, device="cuda"),
+                        torch.zeros(3, dtype=torch.int32, device="cuda"), torch.zeros(3, dtype=torch.int32, device="cuda"), 0, -1)
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_sov_prefix_tlr(T, f, n, a, 100, 1, 1)          # kmax = 0
