@@ -595,13 +595,20 @@ def tlr_potrf_launches(nt: int) -> int:
     need = max(1, (nt // 2) * ((nt + 1) // 2))
     chunk = max(min(need, 2048), nt)
     cnt = 2 if nt > 1 else 0
+    def chunks(ka, kb, rows):
+        c = 0
+        kc = max(1, min(kb - ka, chunk // rows))
+        for k0 in range(ka, kb, kc):
+            kcc = min(kc, kb - k0)
+            nsplit = min(kcc, max(1, (2 * 148 + 4 * rows - 1) // (4 * rows)))
+            c += 3 + (1 if nsplit > 1 else 0)
+        return c
     for j in range(nt):
         rows = nt - j
-        kc = max(1, min(j, chunk // rows))
-        for k0 in range(0, j, kc):
-            kcc = min(kc, j - k0)
-            nsplit = min(kcc, max(1, (2 * 148 + 4 * rows - 1) // (4 * rows)))
-            cnt += 3 + (1 if nsplit > 1 else 0)
+        if j >= 2:
+            cnt += chunks(0, j - 1, rows)                 # the columns k < j - 1 (overlapping the compression of j - 1)
+        if j >= 1:
+            cnt += chunks(j - 1, j, rows)                 # k = j - 1, after it
         cnt += 1 + (3 if rows > 1 else 0)
     return cnt
 

@@ -554,20 +554,71 @@ size_t tlr_slot_doubles(int64_t n, int kmax) {
     return (size_t)(nt * (nt - 1) / 2) * 128 * (size_t)kmax;
 }
 
-// Workspace (doubles): the panel (nt tiles) + M and Z chunks of `chunk_slots` tiles each.
+// Workspace (doubles): two panels (nt tiles each, alternating columns) + M and Z chunks of
+// `chunk_slots` tiles each.
 size_t tlr_work_doubles(int64_t n, int64_t chunk_slots) {
     const int64_t nt = (n + kTile - 1) / kTile;
-    return (size_t)(nt + 2 * chunk_slots) * kTile * kTile;
+    return (size_t)(2 * nt + 2 * chunk_slots) * kTile * kTile;
 }
 
+namespace {
+// T_i -= sum_{k in [ka, kb)} U_ik (V_ik^T V_jk) U_jk^T for the panel tiles i = j .. nt-1, in chunks
+// of at most chunk_slots / rows columns k (M, Z, accumulate; split-K when the column has few tiles)
+cudaError_t tlr_update_range(TlrGemm g, int ka, int kb, int64_t chunk_slots, double *Mw, cudaStream_t st) {
+    using namespace tlrg;
+    const int rows = g.nt - g.j;
+    const int kc_max = (int)std::max<int64_t>(1, std::min<int64_t>(kb - ka, chunk_slots / rows));
+    cudaError_t e;
+    for (int k0 = ka; k0 < kb; k0 += kc_max) {
+        g.k0 = k0;
+        g.kc = std::min(kc_max, kb - k0);
+        g.nsplit = 1;
+        g.mode = kM;
+        if ((e = tlr_gemm(g, (int64_t)rows * g.kc, st)) != cudaSuccess) return e;
+        g.mode = kZ;
+        if ((e = tlr_gemm(g, (int64_t)rows * g.kc, st)) != cudaSuccess) return e;
+        // few panel tiles: split the k range so that >= ~2 CTAs per SM accumulate
+        g.nsplit = (int)std::min<int64_t>(g.kc, std::max<int64_t>(1, (2 * 148 + 4 * rows - 1) / (4 * rows)));
+        g.mode = kAcc;
+        if ((e = tlr_gemm(g, (int64_t)rows * g.nsplit, st)) != cudaSuccess) return e;
+        if (g.nsplit > 1) {
+            k_tlr_reduce<<<dim3(128 * 128 / 256, (unsigned)rows), 256, 0, st>>>(g.pnl, Mw, g.nsplit);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+struct SideStream {      // the compression stream of launch_tlr_potrf and its two events
+    cudaStream_t s = nullptr;
+    cudaEvent_t panel_done = nullptr, comp_done = nullptr;
+    ~SideStream() {
+        if (panel_done) cudaEventDestroy(panel_done);
+        if (comp_done) cudaEventDestroy(comp_done);
+        if (s) cudaStreamDestroy(s);     // released once its queued work completes
+    }
+};
+}  // namespace
+
+// Column j's tile compressions (side stream) overlap the next column's updates by the columns
+// k < j (main stream); only the k = j term waits for them. The panel alternates between two
+// buffers, so column j + 1 is assembled while column j's tiles are still being read.
 cudaError_t launch_tlr_potrf(int64_t n, double *tiles, double eps, int mode, int kmax, double *U, double *V,
                              int *ranks, int *ranks_sigma, double *work, int64_t chunk_slots, int *overflow,
                              int64_t *d_info, cudaStream_t st) {
     using namespace tlrg;
     const int nt = (int)((n + kTile - 1) / kTile);
     const int64_t noff = (int64_t)nt * (nt - 1) / 2, T2 = (int64_t)kTile * kTile;
-    double *pnl = work, *Mw = work + nt * T2, *Zw = Mw + chunk_slots * T2;
+    double *pnls[2] = {work, work + nt * T2};
+    double *Mw = work + 2 * nt * T2, *Zw = Mw + chunk_slots * T2;
     cudaError_t e;
+    SideStream side;
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    // the compressions are on the critical path (column j's factors feed column j + 1): high priority
+    if ((e = cudaStreamCreateWithPriority(&side.s, cudaStreamNonBlocking, prio_hi)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&side.panel_done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&side.comp_done, cudaEventDisableTiming)) != cudaSuccess) return e;
     // (1) Sigma's off-diagonal tiles compressed at eps into the slots (Alg. 1 l.7, R23)
     if (noff > 0) {
         TlrJob job;
@@ -585,7 +636,6 @@ cudaError_t launch_tlr_potrf(int64_t n, double *tiles, double eps, int mode, int
     g.nt = nt;
     g.kmax = kmax;
     g.tiles = tiles;
-    g.pnl = pnl;
     g.U = U;
     g.V = V;
     g.Mw = Mw;
@@ -593,37 +643,29 @@ cudaError_t launch_tlr_potrf(int64_t n, double *tiles, double eps, int mode, int
     g.ranks = ranks;
     for (int j = 0; j < nt; ++j) {
         const int rows = nt - j;                             // panel tiles i = j .. nt-1
+        double *pnl = pnls[j & 1];
         g.j = j;
+        g.pnl = pnl;
         // T_j = Sigma_jj (dense), T_i = U_ij V_ij^T of Sigma (i > j)
         if ((e = cudaMemcpyAsync(pnl, tiles + tile_offset(j, j), sizeof(double) * T2, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
             return e;
         g.mode = kExpandPanel;
         if ((e = tlr_gemm(g, rows - 1, st)) != cudaSuccess) return e;
-        // T_i -= sum_{k<j} U_ik (V_ik^T V_jk) U_jk^T, in chunks of kc columns k
-        const int kc_max = (int)std::max<int64_t>(1, std::min<int64_t>(j, chunk_slots / rows));
-        for (int k0 = 0; k0 < j; k0 += kc_max) {
-            g.k0 = k0;
-            g.kc = std::min(kc_max, j - k0);
-            g.mode = kM;
-            if ((e = tlr_gemm(g, (int64_t)rows * g.kc, st)) != cudaSuccess) return e;
-            g.mode = kZ;
-            if ((e = tlr_gemm(g, (int64_t)rows * g.kc, st)) != cudaSuccess) return e;
-            // few panel tiles: split the k range so that >= ~2 CTAs per SM accumulate
-            g.nsplit = (int)std::min<int64_t>(g.kc, std::max<int64_t>(1, (2 * 148 + 4 * rows - 1) / (4 * rows)));
-            g.mode = kAcc;
-            if ((e = tlr_gemm(g, (int64_t)rows * g.nsplit, st)) != cudaSuccess) return e;
-            if (g.nsplit > 1) {
-                k_tlr_reduce<<<dim3(128 * 128 / 256, (unsigned)rows), 256, 0, st>>>(pnl, Mw, g.nsplit);
-                if ((e = cudaGetLastError()) != cudaSuccess) return e;
-            }
-            g.nsplit = 1;
+        // T_i -= sum_{k<j} U_ik (V_ik^T V_jk) U_jk^T: the columns k < j - 1 while column j - 1 is
+        // being compressed, then k = j - 1 after it
+        if (j >= 2 && (e = tlr_update_range(g, 0, j - 1, chunk_slots, Mw, st)) != cudaSuccess) return e;
+        if (j >= 1) {
+            if ((e = cudaStreamWaitEvent(st, side.comp_done, 0)) != cudaSuccess) return e;
+            if ((e = tlr_update_range(g, j - 1, j, chunk_slots, Mw, st)) != cudaSuccess) return e;
         }
         // L_jj = chol(T_j), L_ij = T_i L_jj^{-T}: the dense K2 / K3 kernels on the panel
         if ((e = launch_potrf_panel_map(n, TileMap::panel(pnl, j, 1), j, 1, d_info, st, 0)) != cudaSuccess) return e;
         if ((e = cudaMemcpyAsync(tiles + tile_offset(j, j), pnl, sizeof(double) * T2, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
             return e;
-        // Ltilde_ij = truncation of L_ij at eps, into slot (i, j)
+        // Ltilde_ij = truncation of L_ij at eps, into slot (i, j), on the side stream
         if (rows > 1) {
+            if ((e = cudaEventRecord(side.panel_done, st)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(side.s, side.panel_done, 0)) != cudaSuccess) return e;
             TlrJob job;
             job.src = pnl;
             job.src_mode = 1;
@@ -632,11 +674,13 @@ cudaError_t launch_tlr_potrf(int64_t n, double *tiles, double eps, int mode, int
             job.V = V;
             job.kmax = kmax;
             job.overflow = overflow;
-            k_tlr_compress<<<(unsigned)(rows - 1), tlr::NT, tlr::SMEM, st>>>(job, eps, mode, ranks);
+            k_tlr_compress<<<(unsigned)(rows - 1), tlr::NT, tlr::SMEM, side.s>>>(job, eps, mode, ranks);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            if ((e = cudaEventRecord(side.comp_done, side.s)) != cudaSuccess) return e;
         }
     }
-    // the dense SOV reads Ltilde reconstructed (steps (b)-(d) stay dense)
+    // join, then the dense SOV reads Ltilde reconstructed (steps (b)-(d) stay dense)
+    if ((e = cudaStreamWaitEvent(st, side.comp_done, 0)) != cudaSuccess) return e;
     g.mode = kExpandAll;
     return tlr_gemm(g, noff, st);
 }
