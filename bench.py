@@ -590,11 +590,11 @@ def run_tlr_potrf(args):
 
 def tlr_potrf_launches(nt: int) -> int:
     """Kernels mvn_tlr_potrf launches (mvn_api.cu / kernels_tlr.cu launch_tlr_potrf): the compression
-    of Sigma, per column j the expansion, 3 per chunk of k (M, Z, accumulate), K2, K3 and the
+    of Sigma (one launch per column), per column j the expansion, 3 per chunk of k (M, Z, accumulate), K2, K3 and the
     compression of the column, and the final expansion."""
     need = max(1, (nt // 2) * ((nt + 1) // 2))
     chunk = max(min(need, 2048), nt)
-    cnt = 2 if nt > 1 else 0
+    cnt = (nt - 1) + 1 if nt > 1 else 0                   # Sigma's columns, the final expansion
     def chunks(ka, kb, rows):
         c = 0
         kc = max(1, min(kb - ka, chunk // rows))

@@ -19,6 +19,8 @@
 //     tile in reconstructed form, which the dense POTRF / SOV consume unchanged); k is recorded.
 // Work is O(sweeps * 128^3) per tile on the fp64 ALU; used for the accuracy study, not on the
 // timed path.
+#include <vector>
+
 #include "common.cuh"
 #include "gemm_dmma.cuh"
 #include "mvn_internal.h"
@@ -47,6 +49,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 //  src_mode 0: every off-diagonal tile (I, J) of the full tile-packed buffer, t = blockIdx.x;
 //  src_mode 1: the tiles (i, j), i = j + 1 + blockIdx.x, of one tile column held in the panel
 //              workspace (tile i at src + (i - j) 128^2; the TLR Cholesky, R26), t = i(i-1)/2 + j;
+//  src_mode 2: the same tiles of column j read from the full tile-packed buffer;
 //  U == nullptr: the compressed tile is written back in place (reconstructed, R23);
 //  U != nullptr: the factors are written instead, U_t = A V_k (128 x k) and V_t = V_k (128 x k),
 //              column-major in the slot t of stride 128 kmax; a rank above kmax sets *overflow and
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(const TlrJob job, d
     } else {
         const int64_t i = (int64_t)job.j + 1 + blockIdx.x;
         t = i * (i - 1) / 2 + job.j;
-        T = job.src + (i - job.j) * (int64_t)NB * NB;
+        T = job.src_mode == 1 ? job.src + (i - job.j) * (int64_t)NB * NB : job.src + tile_offset(i, job.j);
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < NB * NB; e += NT) X[(e >> 7) * LD + (e & 127)] = T[e];
@@ -444,6 +447,7 @@ struct TlrGemm {
     int mode = 0, nt = 0, j = 0, k0 = 0, kc = 0, kmax = 0, nsplit = 1;
     double *tiles = nullptr, *pnl = nullptr, *U = nullptr, *V = nullptr, *Mw = nullptr, *Zw = nullptr;
     const int *ranks = nullptr;
+    const int *ranks_s = nullptr;      // Sigma's ranks (kExpandPanel)
 };
 
 // grid: (entries, 4 blocks of 64 x 64); 128 threads (2 x 2 warps of 32 x 32); MODE = g.mode
@@ -474,7 +478,8 @@ __global__ void __launch_bounds__(tlrg::NT) k_tlr_gemm(const TlrGemm g) {
             while ((int64_t)(I + 1) * I / 2 <= t) ++I;
             C = g.tiles + tile_offset(I, t - (int64_t)I * (I - 1) / 2);
         }
-        tlr_seg_gemm<false, false>(c, g.U + t * S, g.V + t * S, g.ranks[t], 128, 128, m0, n0, As, Bs);
+        tlr_seg_gemm<false, false>(c, g.U + t * S, g.V + t * S, MODE == kExpandPanel ? g.ranks_s[t] : g.ranks[t], 128, 128,
+                                   m0, n0, As, Bs);
     } else if (MODE == kM || MODE == kZ) {
         const int64_t i = g.j + e / g.kc, k = g.k0 + e % g.kc;
         const int64_t tik = i * (i - 1) / 2 + k, tjk = (int64_t)g.j * (g.j - 1) / 2 + k;
@@ -589,13 +594,16 @@ cudaError_t tlr_update_range(TlrGemm g, int ka, int kb, int64_t chunk_slots, dou
     return cudaSuccess;
 }
 
-struct SideStream {      // the compression stream of launch_tlr_potrf and its two events
-    cudaStream_t s = nullptr;
+struct SideStream {      // the compression streams of launch_tlr_potrf and their events
+    cudaStream_t s = nullptr, sg = nullptr;
     cudaEvent_t panel_done = nullptr, comp_done = nullptr;
+    std::vector<cudaEvent_t> sig_done;   // Sigma's column j compressed
     ~SideStream() {
         if (panel_done) cudaEventDestroy(panel_done);
         if (comp_done) cudaEventDestroy(comp_done);
-        if (s) cudaStreamDestroy(s);     // released once its queued work completes
+        for (cudaEvent_t e : sig_done) if (e) cudaEventDestroy(e);
+        if (s) cudaStreamDestroy(s);     // released once their queued work completes
+        if (sg) cudaStreamDestroy(sg);
     }
 };
 }  // namespace
@@ -615,22 +623,32 @@ cudaError_t launch_tlr_potrf(int64_t n, double *tiles, double eps, int mode, int
     SideStream side;
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (nt > 1 && !ranks_sigma) return cudaErrorInvalidValue;   // the caller provides Sigma's rank array
     // the compressions are on the critical path (column j's factors feed column j + 1): high priority
     if ((e = cudaStreamCreateWithPriority(&side.s, cudaStreamNonBlocking, prio_hi)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&side.panel_done, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&side.comp_done, cudaEventDisableTiming)) != cudaSuccess) return e;
-    // (1) Sigma's off-diagonal tiles compressed at eps into the slots (Alg. 1 l.7, R23)
-    if (noff > 0) {
+    // (1) Sigma's off-diagonal tiles compressed at eps into the slots (Alg. 1 l.7, R23), column by
+    // column on a low-priority stream that runs ahead of the factorisation and fills the SMs its
+    // critical path leaves idle; column j's expansion waits for its event. Sigma's ranks go to
+    // ranks_sigma (the slots and `ranks` then receive L~'s)
+    if ((e = cudaStreamCreateWithPriority(&side.sg, cudaStreamNonBlocking, prio_lo)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(side.comp_done, st)) != cudaSuccess) return e;   // Sigma's tiles are ready (re-recorded per column below)
+    if ((e = cudaStreamWaitEvent(side.sg, side.comp_done, 0)) != cudaSuccess) return e;
+    side.sig_done.assign((size_t)std::max(nt - 1, 0), nullptr);
+    for (int j = 0; j + 1 < nt; ++j) {
+        if ((e = cudaEventCreateWithFlags(&side.sig_done[j], cudaEventDisableTiming)) != cudaSuccess) return e;
         TlrJob job;
         job.src = tiles;
+        job.src_mode = 2;
+        job.j = j;
         job.U = U;
         job.V = V;
         job.kmax = kmax;
         job.overflow = overflow;
-        k_tlr_compress<<<(unsigned)noff, tlr::NT, tlr::SMEM, st>>>(job, eps, mode, ranks);
+        k_tlr_compress<<<(unsigned)(nt - 1 - j), tlr::NT, tlr::SMEM, side.sg>>>(job, eps, mode, ranks_sigma);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        if (ranks_sigma && (e = cudaMemcpyAsync(ranks_sigma, ranks, sizeof(int) * noff, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-            return e;
+        if ((e = cudaEventRecord(side.sig_done[j], side.sg)) != cudaSuccess) return e;
     }
     TlrGemm g;
     g.nt = nt;
@@ -641,6 +659,7 @@ cudaError_t launch_tlr_potrf(int64_t n, double *tiles, double eps, int mode, int
     g.Mw = Mw;
     g.Zw = Zw;
     g.ranks = ranks;
+    g.ranks_s = ranks_sigma;
     for (int j = 0; j < nt; ++j) {
         const int rows = nt - j;                             // panel tiles i = j .. nt-1
         double *pnl = pnls[j & 1];
@@ -649,6 +668,7 @@ cudaError_t launch_tlr_potrf(int64_t n, double *tiles, double eps, int mode, int
         // T_j = Sigma_jj (dense), T_i = U_ij V_ij^T of Sigma (i > j)
         if ((e = cudaMemcpyAsync(pnl, tiles + tile_offset(j, j), sizeof(double) * T2, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
             return e;
+        if (rows > 1 && (e = cudaStreamWaitEvent(st, side.sig_done[j], 0)) != cudaSuccess) return e;
         g.mode = kExpandPanel;
         if ((e = tlr_gemm(g, rows - 1, st)) != cudaSuccess) return e;
         // T_i -= sum_{k<j} U_ik (V_ik^T V_jk) U_jk^T: the columns k < j - 1 while column j - 1 is

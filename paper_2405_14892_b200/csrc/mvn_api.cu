@@ -1070,8 +1070,10 @@ mvn_status mvn_tlr_potrf(mvn_ctx *c, mvn_tiles t, double *d_tiles, double eps, i
     const int64_t chunk = std::max<int64_t>(std::min<int64_t>(need, 2048), nt);
     const size_t wbytes = sizeof(double) * mvn::tlr_work_doubles(t.n, chunk);
     mvn_status s;
-    if ((s = ensure(c, &c->tlrW, &c->tlrW_cap, wbytes + 256)) != MVN_OK) return s;
+    const int64_t noff = nt * (nt - 1) / 2;
+    if ((s = ensure(c, &c->tlrW, &c->tlrW_cap, wbytes + 256 + sizeof(int32_t) * (size_t)noff)) != MVN_OK) return s;
     int *overflow = (int *)((char *)c->tlrW + wbytes);
+    if (!d_ranks_sigma) d_ranks_sigma = (int32_t *)((char *)c->tlrW + wbytes + 256);   // Sigma's ranks, not returned
     const int64_t minus1 = -1;
     MVN_CUDA(c, cudaMemsetAsync(overflow, 0, sizeof(int), c->stream));
     MVN_CUDA(c, cudaMemcpyAsync(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
