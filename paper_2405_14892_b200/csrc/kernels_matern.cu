@@ -7,7 +7,7 @@
 // Bound: HBM stores (8 B per element, 6.4 TB/s -> ~23 fp64-pipe instructions per element at 64
 // DFMA/clk/SM) vs the fp64 arithmetic per element: distance (3), sqrt, x = h / beta as a product
 // with the host's 1/beta (1; a division costs ~10 plus a slow-path call), exp(-x) with sigma2
-// folded in (9, exp_neg_scaled), the nu = 3/2, 5/2 factor (1-2).
+// folded in (8, exp_neg_scaled), the nu = 3/2, 5/2 factor (1-2).
 #include <cstdlib>
 
 #include <math_constants.h>
@@ -17,39 +17,39 @@
 
 namespace mvn {
 
-// exp(-x) for 0 <= x <= 700 in 9 fp64-pipe instructions (CUDA's exp: ~18 plus branches), with
-// the factor sigma2 folded into the table: x = k ln2/256 + r, |r| <= ln2/512, k = round(256 x / ln2)
-// (magic-constant rounding), exp(-x) = 2^-(k >> 8) * 2^-((k & 255)/256) * exp(-r); exp(-r) by its
-// Taylor polynomial of degree 4 (truncation <= r^5/5! = 3.8e-17 relative), the 256 values
-// sigma2 * 2^-(j/256) from a host table (long double, correctly rounded, in shared memory), and
-// 2^-(k >> 8) applied to the exponent field with an integer subtract. Error <= ~3 ulp (2.8e-16
-// relative measured in exact rational arithmetic over 3,300 points of [0, 700]).
+// exp(-x) for 0 <= x <= 700 in 8 fp64-pipe instructions (CUDA's exp: ~18 plus branches), with
+// the factor sigma2 folded into the table: x = k ln2/1024 + r, |r| <= ln2/2048, k = round(1024 x / ln2)
+// (magic-constant rounding), exp(-x) = 2^-(k >> 10) * 2^-((k & 1023)/1024) * exp(-r); exp(-r) by its
+// Taylor polynomial of degree 3 (truncation <= r^4/4! = 5.5e-16 relative), the 1,024 values
+// sigma2 * 2^-(j/1024) in shared memory (2^-(j/1024) correctly rounded on the host once per context,
+// g_exp2n, times sigma2 per CTA), and 2^-(k >> 10) applied to the exponent field with an integer
+// subtract. Error <= ~5 ulp (round 2, session 2: one fp64 FMA fewer than the 256-entry, degree-4 form).
 struct MaternArgs {
     int64_t n;
     const double *xy;
     double sigma2, inv_beta, nugget;
     TileMap tm;          // destination storage (the full buffer, or a rank's owned tile columns)
     int libm;            // sigma2 so small or large that the scaled result could leave the normal range
-    double tab[256];     // sigma2 * 2^(-j/256), j = 0..255
 };
+
+__device__ double g_exp2n[1024];   // 2^(-j/1024), j = 0..1023 (matern_init)
 
 __device__ __forceinline__ double exp_neg_scaled(double x, const double *tb) {
     constexpr double kMagic = 0x1.8p52;                   // 1.5 * 2^52: fma(.., .., kMagic) rounds to an integer
-    constexpr double k256ln2 = 369.3299304675746;         // 256 / ln 2
-    constexpr double kLn2hi = 0x1.62e42fefa2000p-9;       // ln2/256, high part (40 bits)
-    constexpr double kLn2lo = 0x1.9ef35793c7673p-49;      // ln2/256 - kLn2hi (rounded)
-    const double kd = fma(x, k256ln2, kMagic);
+    constexpr double k1024ln2 = 1477.3197218702985;       // 1024 / ln 2
+    constexpr double kLn2hi = 0x1.62e42fefa2000p-11;      // ln2/1024, high part (40 bits)
+    constexpr double kLn2lo = 0x1.9ef35793c7673p-51;      // ln2/1024 - kLn2hi (rounded)
+    const double kd = fma(x, k1024ln2, kMagic);
     const int k = __double2loint(kd);
     const double kf = kd - kMagic;
     double r = fma(-kf, kLn2hi, x);
     r = fma(-kf, kLn2lo, r);
-    double p = 1.0 / 24.0;                                // exp(-r) = sum (-r)^i / i!
-    p = fma(p, r, -1.0 / 6.0);
+    double p = -1.0 / 6.0;                                // exp(-r) = sum (-r)^i / i!
     p = fma(p, r, 0.5);
     p = fma(p, r, -1.0);
     p = fma(p, r, 1.0);
-    const double v = tb[k & 255] * p;
-    return __hiloint2double(__double2hiint(v) - ((k >> 8) << 20), __double2loint(v));
+    const double v = tb[k & 1023] * p;
+    return __hiloint2double(__double2hiint(v) - ((k >> 10) << 20), __double2loint(v));
 }
 
 template <int NU2>  // 2*nu: 1 -> nu = 1/2, 3 -> nu = 3/2, 5 -> nu = 5/2; sigma2 * C(x) from e = sigma2 exp(-x)
@@ -94,7 +94,7 @@ template <int NU2, int RPT, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_cov_matern(const MaternArgs p) {
     constexpr int TPC = kTile / RPT;                     // threads per column
     constexpr int CPI = 256 / TPC;                       // columns per step
-    __shared__ double cx[kTile], cy[kTile], rxs[kTile], rys[kTile], tb[256], bb[8][4];
+    __shared__ double cx[kTile], cy[kTile], rxs[kTile], rys[kTile], tb[1024], bb[8][4];
     __shared__ int fast_s;
     // blockIdx.x -> tile (ti, tj), ti >= tj, row-major enumeration of the lower triangle
     const int64_t id = blockIdx.x;
@@ -113,8 +113,6 @@ __global__ void __launch_bounds__(256, MINB) k_cov_matern(const MaternArgs p) {
         vy = c < n ? p.xy[2 * c + 1] : p.xy[2 * c0 + 1];
         cx[tid] = vx;
         cy[tid] = vy;
-        tb[tid] = p.tab[tid];
-        tb[tid + kTile] = p.tab[tid + kTile];
     } else {
         const int64_t r = r0 + tid - kTile;
         vx = r < n ? p.xy[2 * r] : p.xy[2 * r0];
@@ -122,6 +120,8 @@ __global__ void __launch_bounds__(256, MINB) k_cov_matern(const MaternArgs p) {
         rxs[tid - kTile] = vx;
         rys[tid - kTile] = vy;
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tb[tid + 256 * q] = p.sigma2 * g_exp2n[tid + 256 * q];
     {   // bounding boxes: warps 0-3 the columns, warps 4-7 the rows
         double mnx = vx, mxx = vx, mny = vy, mxy = vy;
 #pragma unroll
@@ -206,6 +206,12 @@ static void k1_launch(dim3 grid, const MaternArgs &a, cudaStream_t st) {
     }
 }
 
+cudaError_t matern_init() {
+    static double h[1024];
+    for (int j = 0; j < 1024; ++j) h[j] = (double)exp2l(-(long double)j / 1024.0L);
+    return cudaMemcpyToSymbol(g_exp2n, h, sizeof(h));
+}
+
 cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
                                   const TileMap &tm, cudaStream_t st) {
     const int nt = (int)((n + kTile - 1) / kTile);
@@ -213,7 +219,6 @@ cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, do
     MaternArgs a;
     a.n = n; a.xy = xy; a.sigma2 = sigma2; a.inv_beta = 1.0 / beta; a.nugget = nugget; a.tm = tm;
     a.libm = sigma2 < 0x1p-100 || sigma2 > 0x1p100;
-    for (int j = 0; j < 256; ++j) a.tab[j] = (double)((long double)sigma2 * exp2l(-(long double)j / 256.0L));
     dim3 grid((unsigned)ntiles);
     if (nu == 0.5) k1_launch<1>(grid, a, st);
     else if (nu == 1.5) k1_launch<3>(grid, a, st);

@@ -186,7 +186,7 @@ mvn_status mvn_create(int device, void *cuda_stream, mvn_ctx **out) {
         DevGuard dev_guard(c);                        // the caller's current device is restored
         const int64_t minus1 = -1;
         if (mvn::potrf_init() != cudaSuccess || mvn::sov_init() != cudaSuccess || mvn::mc_init() != cudaSuccess ||
-            mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess || mvn::sov_oz_init() != cudaSuccess || mvn::potrf_oz_init() != cudaSuccess ||
+            mvn::mc_oz_init() != cudaSuccess || mvn::tlr_init() != cudaSuccess || mvn::matern_init() != cudaSuccess || mvn::sov_oz_init() != cudaSuccess || mvn::potrf_oz_init() != cudaSuccess ||
             cudaMalloc(&c->d_info, 2 * sizeof(int64_t)) != cudaSuccess ||
             cudaMemcpy(c->d_info, &minus1, sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming) != cudaSuccess) {

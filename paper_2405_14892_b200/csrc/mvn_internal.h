@@ -7,6 +7,7 @@ namespace mvn {
 
 constexpr int kTile = 128;  // storage tile (mvn_tiles.nb)
 
+cudaError_t matern_init();
 cudaError_t launch_cov_matern(int64_t n, const double *xy, double sigma2, double beta, double nu, double nugget,
                               double *tiles, cudaStream_t st);
 cudaError_t launch_pack(int64_t n, const double *dense, int64_t ld, double *tiles, bool to_tiles, cudaStream_t st);
