@@ -74,7 +74,7 @@ from .lattice import primes, generators, shifts, splitmix64_mix, lattice_w  # no
 from .matern import matern, covariance  # noqa: E402
 from .pipeline import (  # noqa: E402
     Phi, Phibar, Phiinv, sov_step, cholesky, marginal_order, sov_units, sov_unit,
-    combine_units, prefix_logp, per_shift_logp, region, crd, crd_cov,
+    combine_units, prefix_logp, per_shift_logp, shift_stats, region, crd, crd_cov,
 )
 from .mcval import mc_z, mc_first, mc_counts, mc_levels  # noqa: E402
 from .posterior import posterior, posterior_field  # noqa: E402

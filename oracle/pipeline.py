@@ -129,6 +129,24 @@ def per_shift_logp(partials: np.ndarray, N: int, R: int, chunk: int) -> np.ndarr
     return np.array(out)
 
 
+def shift_stats(logp_shift: np.ndarray):
+    """O6: from the per-shift estimates log P^(r)_k (R x n, equal N per shift) the
+    combined log P_k = log(mean_r P^(r)_k) (= the mean over all N R samples, R11) and the relative
+    standard error across the R randomised shifts, sd_r(P^(r)_k) / (sqrt(R) mean_r P^(r)_k) (ddof 1)
+    — the QMC error estimate of randomly shifted lattice rules; about the standard error of log P_k.
+    Evaluated relative to max_r log P^(r)_k, so P far below the double range is no problem."""
+    L = np.asarray(logp_shift, dtype=np.float64)
+    R = L.shape[0]
+    m = np.max(L, axis=0)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        x = np.where(np.isfinite(m), np.exp(L - m), 0.0)          # P^(r) / max_r P^(r)
+        xm = np.mean(x, axis=0)
+        logp = np.where(xm > 0, m + np.log(xm), -np.inf)
+        sd = np.std(x, axis=0, ddof=1) if R > 1 else np.zeros_like(xm)
+        rel = np.where(xm > 0, sd / (math.sqrt(R) * xm), np.nan)
+    return logp, rel
+
+
 def region(logp: np.ndarray, conf, tie_tol: float = 1e-8):
     """O7: running min (R12), k*(c) = max{k : log P_k >= log c} (Eq. 4), near-tie flags."""
     lp = np.minimum.accumulate(np.asarray(logp, dtype=np.float64))

@@ -284,3 +284,40 @@ def test_marginal_order_ties_and_limits():
     assert list(order) == [1, 4, 0, 2, 3]          # descending z, ties by ascending index
     assert np.array_equal(a, 0.2 - mu[order])
     assert pM[1] == pytest.approx(ndtr(0.8), rel=1e-15)
+
+
+# ----------------------------------------------------------------------------- O6 shift statistics
+def test_shift_stats_pins():
+    """oracle.shift_stats: (1) the combined estimate is the mean over all N R samples
+    (equal N per shift), i.e. prefix_logp of the full partials; (2) zero-variance integrands (n = 1,
+    diagonal Sigma: every sample gives the same product) have rel_se = 0 exactly; (3) it matches the
+    textbook sd / sqrt(R) on P^(r) where P is representable, and stays finite far below the double
+    range (log P ~ -1000), where exp(log P^(r)) underflows."""
+    rng = np.random.default_rng(3)
+    n, N, R = 40, 300, 6
+    A = rng.standard_normal((n, n)) * 0.2
+    S = A @ A.T + np.eye(n)
+    L, _ = oracle.cholesky(S)
+    a = rng.normal(-0.3, 0.4, n)
+    b = np.full(n, INF)
+    G = lattice.generators(n)
+    D = lattice.shifts(11, R, n)
+    parts = oracle.sov_units(L, a, b, G, D, N, R, N)
+    M, Sm = oracle.combine_units(parts)
+    full = oracle.prefix_logp(M, Sm, N * R)
+    lps = oracle.per_shift_logp(parts, N, R, N)
+    logp, rel = oracle.shift_stats(lps)
+    assert np.max(np.abs(logp - full)) <= 1e-13
+    P = np.exp(lps)
+    want = np.std(P, axis=0, ddof=1) / math.sqrt(R) / np.mean(P, axis=0)
+    assert np.max(np.abs(rel - want)) <= 1e-12
+    assert rel[0] <= 1e-15 and np.all(rel[1:] > 0)       # P_1 = Phibar(a_1 / L_11) for every sample (n = 1)
+    # diagonal Sigma: zero variance across shifts
+    Ld = np.diag(rng.uniform(0.5, 2.0, n))
+    pd = oracle.sov_units(Ld, a, b, G, D, N, R, N)
+    _, reld = oracle.shift_stats(oracle.per_shift_logp(pd, N, R, N))
+    assert np.max(reld) <= 1e-12
+    # far below the double range: the same statistics after a shift of log P by -1000
+    logp2, rel2 = oracle.shift_stats(lps - 1000.0)
+    assert np.all(np.isfinite(rel2)) and np.max(np.abs(rel2 - rel)) <= 1e-12
+    assert np.max(np.abs(logp2 - (logp - 1000.0))) <= 1e-12
