@@ -623,6 +623,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-shift-se", action="store_true",
+                    help="skip the untimed per-shift sweeps that give the QMC standard error (qmc_error)")
     ap.add_argument("--potrf", default="auto", choices=["auto", "rank0", "dist", "dstore"],
                     help="N>1: factor on rank 0 + broadcast L (north_star), or distributed (NEXT-1); "
                          "dstore: NEXT-1 on distributed storage end to end (each rank holds ~1/N of the "
@@ -811,6 +813,22 @@ def main():
                "api": "parallel.crd_step from pinned host buffers, max over ranks",
                "k_star_matches_device_path": bool(np.array_equal(k2, k))}
 
+    # ---- QMC error of the estimates (untimed): the per-shift estimates log P^(r) (one sweep per
+    # shift, mvn_sov_prefix_shifts) and the relative standard error across the R shifts (O6, R11)
+    qmc_err = None
+    if rank == 0 and world == 1 and mode != "dstore" and not args.no_shift_se:
+        t0 = time.perf_counter()
+        Ls = mvn.mvn_sov_prefix_shifts(L, n, d_a, cfg.N, cfg.R, cfg.seed_lattice).cpu().numpy()
+        lps, rse = mvn.mvn_prefix_shift_stats(Ls)
+        ks = [int(x) for x in k]
+        fin = np.isfinite(lp)
+        qmc_err = {"R": cfg.R, "what": "relative standard error of P_k across the R randomised lattice shifts "
+                                      "(sd_r P^(r)_k / (sqrt(R) mean_r P^(r)_k), ~ the standard error of log P_k)",
+                   "rel_se_at_k_star": [float(rse[x - 1]) if x > 0 else None for x in ks],
+                   "max_rel_se_up_to_max_k_star": float(np.nanmax(rse[:max(ks)])) if max(ks) > 0 else None,
+                   "combined_vs_step_max_abs_dlogP": float(np.max(np.abs(lps[fin] - lp[fin]))),
+                   "seconds": time.perf_counter() - t0}
+
     # ---- roofline of the dominant kernel (k_sov, SOV GEMM + chain), from the live stage times
     sov_ms = stage_mean["sov"]
     my_begin, my_end = parallel.shard_range(NR, rank, world)
@@ -882,6 +900,7 @@ def main():
         "gpu_launches": launches * args.steps,
         "e2e": e2e,
         "k_star": [int(x) for x in k],
+        "qmc_error": qmc_err,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         thr = cpu_threads()

@@ -330,6 +330,19 @@ mvn_status mvn_prefix_rescale(mvn_ctx *ctx, int64_t n, const double *d_Mglob, do
 mvn_status mvn_prefix_finalize(mvn_ctx *ctx, int64_t n, int64_t NR, const double *d_M,
                                const double *d_S, double *d_logP);
 
+/* Per-shift estimates (reading R11: "mean(p)", over R randomly shifted
+ * lattices): row r of d_logP_shift (device, [R][n]) receives log P^(r)_k, the estimate of shift r
+ * alone (the sample range [r N, (r + 1) N) of mvn_sov_prefix, one sweep per shift). With
+ * mvn_prefix_shift_stats (host) they give the combined log P_k = log mean_r P^(r)_k (= the
+ * all-sample estimate, N equal per shift) and the relative standard error across the shifts,
+ * rel_se_k = sd_r(P^(r)_k) / (sqrt(R) mean_r P^(r)_k) (sample sd, R - 1; ~ the standard error of
+ * log P_k; 0 for R = 1; NaN where every P^(r)_k = 0), evaluated relative to max_r log P^(r)_k so
+ * nothing underflows. The QMC error estimate of the regions; not part of the timed path.
+ * Errors: USAGE as mvn_sov_prefix.                                                              */
+mvn_status mvn_sov_prefix_shifts(mvn_ctx *ctx, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
+                                 const mvn_qmc *q, double *d_logP_shift);
+mvn_status mvn_prefix_shift_stats(int64_t n, int32_t R, const double *logP_shift, double *logP, double *rel_se);
+
 /* ---------------------------------------------------------------------------------------------
  * a10. Confidence regions (Eq. 4-5; readings R12, R16). HOST.
  * logP: n host doubles in sorted order. Running minimum first (ulp guard), then for each level

@@ -40,7 +40,7 @@ ABI_SYMBOLS = [
     "mvn_dpotrf_update", "mvn_dgather", "mvn_sov_prefix_ex", "mvn_potrf_ex", "mvn_dpanel_trsm",
     "mvn_sov_prefix_units", "mvn_prefix_reduce", "mvn_sweep_begin", "mvn_sweep_rows", "mvn_sweep_end",
     "mvn_sweep_free", "mvn_drows_offset", "mvn_drows_unpack", "mvn_tlr_slots_bytes", "mvn_tlr_potrf",
-    "mvn_sov_prefix_tlr",
+    "mvn_sov_prefix_tlr", "mvn_sov_prefix_shifts", "mvn_prefix_shift_stats",
 ]
 
 
@@ -138,6 +138,8 @@ def lib() -> ctypes.CDLL:
         "mvn_tlr_slots_bytes": (ctypes.c_size_t, [T, I32]),
         "mvn_tlr_potrf": (S, [P, T, P, D, I32, I32, P, P, P, P, ctypes.POINTER(I64)]),
         "mvn_sov_prefix_tlr": (S, [P, T, P, P, P, P, I32, P, P, ctypes.POINTER(mvn_qmc), P, P]),
+        "mvn_sov_prefix_shifts": (S, [P, T, P, P, P, ctypes.POINTER(mvn_qmc), P]),
+        "mvn_prefix_shift_stats": (S, [I64, I32, P, P, P]),
         "mvn_dtiles_bytes": (ctypes.c_size_t, [mvn_dtiles]),
         "mvn_dpanel_numel": (I64, [mvn_dtiles, I64]),
         "mvn_dcov_matern": (S, [P, mvn_dtiles, P, D, D, D, D, P]),
@@ -454,6 +456,30 @@ def mvn_sov_prefix(L, n: int, a, N: int, R: int, seed: int, begin: int = 0, end:
                                  None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q),
                                  _dev_ptr(M), _dev_ptr(S)), "mvn_sov_prefix")
     return M, S
+
+
+def mvn_sov_prefix_shifts(L, n: int, a, N: int, R: int, seed: int, b=None, out=None):
+    """log P^(r)_k of every shift r (one sweep per shift): CUDA float64 [R][n]."""
+    import torch
+    c = Context.get(L.device.index)
+    out = torch.empty((R, n), dtype=torch.float64, device=L.device) if out is None else out
+    q = mvn_qmc(int(N), int(R), int(seed), 0, int(N) * int(R))
+    c.check(lib().mvn_sov_prefix_shifts(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64),
+                                        None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q),
+                                        _dev_ptr(out, torch.float64)), "mvn_sov_prefix_shifts")
+    return out
+
+
+def mvn_prefix_shift_stats(logp_shift: np.ndarray):
+    """(log P, rel_se) from the per-shift estimates (host, R x n): the combined estimate and the
+    relative standard error across the shifts (mvn_prefix_shift_stats)."""
+    Ls = np.ascontiguousarray(logp_shift, dtype=np.float64)
+    R, n = Ls.shape
+    lp, se = np.empty(n), np.empty(n)
+    st = lib().mvn_prefix_shift_stats(n, R, _np_ptr(Ls), _np_ptr(lp), _np_ptr(se))
+    if st != MVN_OK:
+        raise MvnError(st, "mvn_prefix_shift_stats: bad arguments")
+    return lp, se
 
 
 class mvn_sweep:

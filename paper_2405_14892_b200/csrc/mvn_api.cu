@@ -873,6 +873,51 @@ mvn_status mvn_prefix_finalize(mvn_ctx *c, int64_t n, int64_t NR, const double *
     return MVN_OK;
 }
 
+mvn_status mvn_sov_prefix_shifts(mvn_ctx *c, mvn_tiles t, const double *d_L, const double *d_a, const double *d_b,
+                                 const mvn_qmc *q, double *d_logP_shift) {
+    DevGuard dev_guard(c);
+    if (!c) return MVN_E_USAGE;
+    if (!tiles_ok(t) || !d_L || !d_a || !q || !d_logP_shift || q->N < 1 || q->R < 1)
+        return fail(c, MVN_E_USAGE, "mvn_sov_prefix_shifts: bad arguments (need nb=128, N >= 1, R >= 1)");
+    mvn_status s;
+    // (M, S) of one shift in the context's small-vector scratch (n x 2); every shift's sweep is the
+    // sample range [r N, (r + 1) N) of mvn_sov_prefix, finalised into row r of d_logP_shift
+    if ((s = ensure(c, &c->crd_vec, &c->crd_vec_cap, sizeof(double) * 2 * (size_t)t.n)) != MVN_OK) return s;
+    double *dM = (double *)c->crd_vec, *dS = dM + t.n;
+    for (int32_t r = 0; r < q->R; ++r) {
+        mvn_qmc qr = *q;
+        qr.sample_begin = (int64_t)r * q->N;
+        qr.sample_end = qr.sample_begin + q->N;
+        if ((s = sov_prefix_impl(c, t, d_L, d_a, d_b, &qr, -1, -1, nullptr, dM, dS)) != MVN_OK) return s;
+        MVN_CUDA(c, mvn::launch_finalize(t.n, q->N, dM, dS, d_logP_shift + (int64_t)r * t.n, c->stream));
+    }
+    return MVN_OK;
+}
+
+mvn_status mvn_prefix_shift_stats(int64_t n, int32_t R, const double *logP_shift, double *logP, double *rel_se) {
+    if (n < 1 || R < 1 || !logP_shift || !logP || !rel_se) return MVN_E_USAGE;
+    for (int64_t k = 0; k < n; ++k) {
+        double m = -INFINITY;
+        for (int32_t r = 0; r < R; ++r) m = std::max(m, logP_shift[(int64_t)r * n + k]);
+        if (!(m > -INFINITY)) {
+            logP[k] = -INFINITY;
+            rel_se[k] = NAN;
+            continue;
+        }
+        double sx = 0.0;
+        for (int32_t r = 0; r < R; ++r) sx += std::exp(logP_shift[(int64_t)r * n + k] - m);
+        const double xm = sx / R;
+        double ss = 0.0;
+        for (int32_t r = 0; r < R; ++r) {
+            const double d = std::exp(logP_shift[(int64_t)r * n + k] - m) - xm;
+            ss += d * d;
+        }
+        logP[k] = m + std::log(xm);
+        rel_se[k] = R > 1 ? std::sqrt(ss / (R - 1)) / (std::sqrt((double)R) * xm) : 0.0;
+    }
+    return MVN_OK;
+}
+
 mvn_status mvn_confidence_region(int64_t n, const double *logP, const double *conf, int64_t nconf, int64_t *k_out,
                                  int32_t *near_tie) {
     if (n < 0 || (n > 0 && !logP) || nconf < 0 || (nconf > 0 && (!conf || !k_out))) return MVN_E_USAGE;

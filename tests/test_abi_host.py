@@ -96,3 +96,23 @@ def test_confidence_region_vs_oracle():
         mvn.mvn_confidence_region(np.array([-0.1]), [1.0])
     with pytest.raises(mvn.MvnError):
         mvn.mvn_confidence_region(np.array([np.nan]), [0.5])
+
+
+def test_prefix_shift_stats_vs_oracle():
+    """mvn_prefix_shift_stats (host C) against oracle.shift_stats: random per-shift estimates, a row
+    far below the double range, an exactly equal row (rel_se 0), an all -inf row (NaN), R = 1."""
+    rng = np.random.default_rng(4)
+    R, n = 8, 50
+    L = np.cumsum(-rng.uniform(0.0, 0.2, (1, n)), axis=1) + rng.normal(0, 0.05, (R, n))
+    L[:, 10] -= 1000.0
+    L[:, 11] = -3.25
+    L[:, 12] = -np.inf
+    lp, se = mvn.mvn_prefix_shift_stats(L)
+    lpo, seo = oracle.shift_stats(L)
+    fin = np.isfinite(lpo)
+    assert np.array_equal(fin, np.isfinite(lp))
+    assert np.max(np.abs(lp[fin] - lpo[fin])) <= 1e-13
+    assert np.max(np.abs(se[fin] - seo[fin])) <= 1e-13
+    assert se[11] == 0.0 and np.isnan(se[12]) and lp[12] == -np.inf
+    lp1, se1 = mvn.mvn_prefix_shift_stats(L[:1])
+    assert np.array_equal(lp1[fin], L[0][fin]) and np.all(se1[fin] == 0.0)
