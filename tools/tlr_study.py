@@ -3,7 +3,9 @@ TLR-compressed covariance through the same CUDA path (POTRF -> SOV -> regions), 
 synthetic settings: n = 40,000 sites, exponential kernel (nu = 1/2), sigma^2 = 1, range beta = 0.033
 (weak), 0.1 (medium), 0.234 (strong) (Fig. 5 captions). Inputs: jittered 200 x 200 grid, GP
 mean draw (workloads.gp_mean_draw), u = 0, N*R = 10,000 x 8. Every step runs in libmvn; no oracle.
-Prints one JSON object per (beta, eps) and writes gpurun_out/tlr_study.json."""
+TLR_CHOL=1 (round 2): the TLR Cholesky itself (mvn_tlr_potrf, R26: Sigma compressed, updates in
+factored form, every L tile truncated at eps) instead of the dense POTRF of the compressed Sigma.
+Prints one JSON object per (beta, eps) and writes gpurun_out/tlr_study[_chol]_mode<m>.json."""
 import json
 import math
 import os
@@ -44,6 +46,7 @@ def main():
     betas = [float(b) for b in os.environ.get("TLR_BETAS", "0.033,0.1,0.234").split(",")]
     epss = [float(e) for e in os.environ.get("TLR_EPS", "1e-1,1e-2,1e-3,1e-4").split(",")]
     mode = int(os.environ.get("TLR_MODE", "0"))          # 0: sigma_i >= eps, 1: relative Frobenius per tile
+    chol = os.environ.get("TLR_CHOL", "0") == "1"
     out = []
     for beta in betas:
         cfg = W.small_config(f"tlr_b{beta}", g, N, R, base="B", beta=beta)
@@ -70,15 +73,31 @@ def main():
             del Tg
             T.copy_(base)
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            ranks = mvn.mvn_tlr_compress(T, n, eps, mode=mode)
-            ev1.record()
-            torch.cuda.synchronize()
-            ms = ev0.elapsed_time(ev1)
-            ranks = ranks.cpu().numpy()
-            info, lp = run(T, n, a, N, R, cfg.seed_lattice)
-            rec = {"beta": beta, "n": n, "eps": eps, "mode": mode, "compress_ms": ms, "info": info,
-                   "ranks_sorted_order": rank_stats(ranks), "ranks_spatial_order": rank_stats(rg)}
+            if chol:
+                ev0.record()
+                f = mvn.mvn_tlr_potrf(T, n, eps, mode=mode, raise_on_numeric=False)
+                ev1.record()
+                torch.cuda.synchronize()
+                ms = ev0.elapsed_time(ev1)
+                ranks, info = f.ranks_sigma.cpu().numpy(), f.info
+                lp = None
+                if info == -1:
+                    M, S = mvn.mvn_sov_prefix(T, n, torch.from_numpy(a).cuda(), N, R, cfg.seed_lattice)
+                    lp = mvn.mvn_prefix_finalize(M, S, N * R).cpu().numpy()
+                rec = {"beta": beta, "n": n, "eps": eps, "mode": mode, "tlr_potrf_ms": ms, "info": info,
+                       "ranks_sorted_order": rank_stats(ranks), "ranks_L": rank_stats(f.ranks.cpu().numpy()),
+                       "ranks_spatial_order": rank_stats(rg)}
+                del f
+            else:
+                ev0.record()
+                ranks = mvn.mvn_tlr_compress(T, n, eps, mode=mode)
+                ev1.record()
+                torch.cuda.synchronize()
+                ms = ev0.elapsed_time(ev1)
+                ranks = ranks.cpu().numpy()
+                info, lp = run(T, n, a, N, R, cfg.seed_lattice)
+                rec = {"beta": beta, "n": n, "eps": eps, "mode": mode, "compress_ms": ms, "info": info,
+                       "ranks_sorted_order": rank_stats(ranks), "ranks_spatial_order": rank_stats(rg)}
             if lp is not None:
                 k = mvn.mvn_confidence_region(lp, CONF)[0]
                 P_d, P_t = np.exp(lp_d), np.exp(lp)
@@ -91,8 +110,8 @@ def main():
         del T, base
         torch.cuda.empty_cache()
     os.makedirs("gpurun_out", exist_ok=True)
-    with open(f"gpurun_out/tlr_study_mode{mode}.json", "w") as f:
-        json.dump(out, f, indent=1)
+    with open(f"gpurun_out/tlr_study{'_chol' if chol else ''}_mode{mode}.json", "w") as fo:
+        json.dump(out, fo, indent=1)
 
 
 if __name__ == "__main__":
