@@ -234,6 +234,10 @@ typedef struct {
     uint64_t seed;         /* shift seed */
     int64_t sample_begin;  /* global sample range [begin, end) processed by this call */
     int64_t sample_end;    /*   0 <= begin < end <= N*R  (a rank's shard, or everything) */
+    const uint64_t *d_gen; /* nullable (device, n): the lattice generators G_k to use instead of R8's
+                              sqrt-prime ones (e.g. a component-by-component rule);
+                              w = (floor((j G_k + D_k^r mod 2^64) / 2^12) + 1/2) 2^-52 as in R8.
+                              NULL (aggregate initialisers that omit it): the library's table. */
 } mvn_qmc;
 
 /* ---------------------------------------------------------------------------------------------

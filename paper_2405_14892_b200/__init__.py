@@ -61,7 +61,7 @@ class mvn_dtiles(ctypes.Structure):
 
 class mvn_qmc(ctypes.Structure):
     _fields_ = [("N", ctypes.c_int64), ("R", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("sample_begin", ctypes.c_int64), ("sample_end", ctypes.c_int64)]
+                ("sample_begin", ctypes.c_int64), ("sample_end", ctypes.c_int64), ("d_gen", ctypes.c_void_p)]
 
 
 class mvn_mc(ctypes.Structure):
@@ -444,14 +444,15 @@ def mvn_lattice_shifts(seed: int, R: int, n: int) -> np.ndarray:
 
 
 def mvn_sov_prefix(L, n: int, a, N: int, R: int, seed: int, begin: int = 0, end: int | None = None,
-                   b=None, M=None, S=None):
-    """One SOV/QMC sweep over global samples [begin, end). Returns CUDA (M, S), n each."""
+                   b=None, M=None, S=None, gen=None):
+    """One SOV/QMC sweep over global samples [begin, end). Returns CUDA (M, S), n each. gen: optional
+    CUDA uint64 (as int64) tensor of n lattice generators replacing R8's table (mvn_qmc.d_gen)."""
     import torch
     c = Context.get(L.device.index)
     end = N * R if end is None else end
     M = torch.empty(n, dtype=torch.float64, device=L.device) if M is None else M
     S = torch.empty(n, dtype=torch.float64, device=L.device) if S is None else S
-    q = mvn_qmc(int(N), int(R), int(seed), int(begin), int(end))
+    q = mvn_qmc(int(N), int(R), int(seed), int(begin), int(end), None if gen is None else _dev_ptr(gen))
     c.check(lib().mvn_sov_prefix(c.h, tiles(n), _dev_ptr(L, torch.float64), _dev_ptr(a, torch.float64),
                                  None if b is None else _dev_ptr(b, torch.float64), ctypes.byref(q),
                                  _dev_ptr(M), _dev_ptr(S)), "mvn_sov_prefix")

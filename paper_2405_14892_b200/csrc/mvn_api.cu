@@ -561,7 +561,7 @@ mvn_status sov_prefix_impl(mvn_ctx *c, mvn_tiles t, const double *d_L, const dou
     const int64_t NR = q->N * (int64_t)q->R;
     const int64_t nsamp = units ? std::min<int64_t>(u1 * 128, NR) - u0 * 128 : q->sample_end - q->sample_begin;
     mvn::SovLaunch L;
-    L.L = d_L; L.n = t.n; L.a = d_a; L.b = d_b; L.G = c->G; L.N = q->N; L.seed = q->seed;
+    L.L = d_L; L.n = t.n; L.a = d_a; L.b = d_b; L.G = q->d_gen ? q->d_gen : c->G; L.N = q->N; L.seed = q->seed;
     L.g_begin = units ? u0 * 128 : q->sample_begin; L.g_end = units ? std::min<int64_t>(u1 * 128, NR) : q->sample_end;
     L.grid = (int)std::min<int64_t>(units ? u1 - u0 : nsamp, c->nsm);
     std::vector<int64_t> cta((size_t)L.grid * 3);
@@ -719,7 +719,7 @@ mvn_status mvn_sweep_begin(mvn_ctx *c, int64_t n, const double *d_a, const doubl
     if (!e) e = sweep_alloc(c, &sw->ell, (size_t)nsamp);
     if (!e) e = cudaMemcpyAsync(sw->a, d_a, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
     if (!e && d_b) e = cudaMemcpyAsync(sw->b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
-    if (!e) e = cudaMemcpyAsync(sw->G, c->G, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, st);
+    if (!e) e = cudaMemcpyAsync(sw->G, q->d_gen ? q->d_gen : c->G, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, st);
     if (!e) e = cudaMemcpyAsync(sw->cta, cta.data(), sizeof(int64_t) * cta.size(), cudaMemcpyHostToDevice, st);
     if (!e) e = cudaMemcpyAsync(sw->yoff, yoff.data(), sizeof(int64_t) * yoff.size(), cudaMemcpyHostToDevice, st);
     if (!e) e = cudaStreamSynchronize(st);               // the host vectors above go out of scope
@@ -830,7 +830,7 @@ mvn_status mvn_sov_prefix_ex(mvn_ctx *c, mvn_tiles t, const double *d_L, const d
     if ((s = ensure(c, &c->part, &c->part_cap, (size_t)(2 * L.nblk) * n_pad * 2 * sizeof(double))) != MVN_OK) return s;
     if ((s = ensure(c, &c->cta, &c->cta_cap, cl.size() * sizeof(int64_t))) != MVN_OK) return s;
     MVN_CUDA(c, cudaMemcpyAsync(c->cta, cl.data(), cl.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
-    L.LA = (const int8_t *)c->mcLA; L.rowscale = (const double *)c->mcRS; L.L = d_L; L.n = t.n; L.a = d_a; L.G = c->G;
+    L.LA = (const int8_t *)c->mcLA; L.rowscale = (const double *)c->mcRS; L.L = d_L; L.n = t.n; L.a = d_a; L.G = q->d_gen ? q->d_gen : c->G;
     L.N = q->N; L.seed = q->seed; L.cl = (const int64_t *)c->cta; L.YS = (int8_t *)c->Y; L.xch = (double *)c->sozX;
     L.part = (double *)c->part; L.Mout = d_M; L.Sout = d_S; L.flag = d_flag;
     // soft cluster lockstep (MVN_SOV_OZ_LAG steps, default 1; 0 = off): clusters stay within `lag` row

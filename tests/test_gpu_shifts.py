@@ -54,3 +54,31 @@ def test_shift_estimates_errors(torch):
     a = torch.zeros(n, dtype=torch.float64, device="cuda")
     with pytest.raises(mvn().MvnError):
         mvn().mvn_sov_prefix_shifts(T, n, a, 0, 2, 1)
+
+
+def test_custom_lattice_generators(torch):
+    """mvn_qmc.d_gen: caller-supplied generators G_k replace R8's table; against the
+    oracle's sweep with the same G (same shifts), and R8's own table through d_gen = the default."""
+    import test_gpu_parity as P
+    from oracle import lattice
+    cfg = W.small_config("gen", 17, 600, 2, base="B")
+    inp, order, a = P.sorted_inputs(cfg)
+    T = P.gpu_cov(torch, inp.xy[order], cfg)
+    n = cfg.n
+    assert mvn().mvn_potrf(T, n) == -1
+    da = torch.from_numpy(a).cuda()
+    rng = np.random.default_rng(8)
+    G = (rng.integers(0, 2 ** 63, n, dtype=np.uint64) * np.uint64(2) + np.uint64(1))      # odd 64-bit generators
+    dG = torch.from_numpy(G.view(np.int64)).cuda()
+    M, S = mvn().mvn_sov_prefix(T, n, da, cfg.N, cfg.R, 5, gen=dG)
+    Lg = P.to_dense_lower(T, n)
+    D = lattice.shifts(5, cfg.R, n)
+    parts = [oracle.sov_unit(Lg, a, np.full(n, np.inf), G, D[r], 1, cfg.N)[0] for r in range(cfg.R)]
+    Mo, So = oracle.combine_units(np.array(parts))
+    lg = P.logp_from(M.cpu().numpy(), S.cpu().numpy(), cfg.NR)
+    assert np.max(np.abs(lg - P.logp_from(Mo, So, cfg.NR))) <= 1e-10
+    G8 = np.array(lattice.generators(n), dtype=np.uint64)
+    M8, S8 = mvn().mvn_sov_prefix(T, n, da, cfg.N, cfg.R, 5, gen=torch.from_numpy(G8.view(np.int64)).cuda())
+    M0, S0 = mvn().mvn_sov_prefix(T, n, da, cfg.N, cfg.R, 5)
+    assert torch.equal(M8, M0) and torch.equal(S8, S0)
+    assert np.max(np.abs(lg - P.logp_from(M0.cpu().numpy(), S0.cpu().numpy(), cfg.NR))) > 1e-6   # a different point set
