@@ -62,6 +62,30 @@ struct TlrJob {
     int *overflow = nullptr;
 };
 
+// 1/x, sqrt(x), 1/sqrt(x) for normal positive (rcp: nonzero) x: the MUFU fp64 seed (~2^-23) and
+// Newton steps (quadratic: two reach ~2^-46, the third ~1 ulp)
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) y = y * fma(-0.5 * x, y * y, 1.5);
+    return y;
+}
+__device__ __forceinline__ double sqrt_nr(double x) {
+    const double y = rsqrt_nr(x), t = x * y;
+    return fma(fma(-t, t, x), 0.5 * y, t);          // one Newton correction of t = x / sqrt(x)
+}
+
 __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(const TlrJob job, double eps, int mode,
                                                             int *__restrict__ ranks) {
     using namespace tlr;
@@ -230,6 +254,11 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(const TlrJob job, d
     // the columns of X past kq are zero: rotate only the first kq (rounded up to even; a zero column
     // never rotates)
     const int mq = kq_s + (kq_s & 1);
+    // this group's pair: positions p and mq - 1 - p; the columns there at step s are
+    // rr_col(pos, s), advanced by one per step (mq - 1 -> 1; position 0 fixed) instead of a runtime
+    // modulo per step (two integer divisions, ~60 instructions)
+    const int pg = warp + NW * grp;
+    int ca = pg, cb = mq - 1 - pg;
     for (int sweep = 0; sweep < MAX_SWEEPS && mq > 1; ++sweep) {
         // flag slot of this sweep; the other slot is the one a lagging warp may still be reading for
         // the previous sweep's exit test
@@ -237,10 +266,9 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(const TlrJob job, d
         if (tid == 0) chg = 0;
         __syncthreads();
         for (int s = 0; s < mq - 1; ++s) {
-            const int p = warp + NW * grp;
-            const bool active = 2 * p < mq;       // a pair for this 8-lane group (none past mq / 2)
+            const bool active = 2 * pg < mq;      // a pair for this 8-lane group (none past mq / 2)
             if (active) {
-                double *ai = X + rr_col(p, s, mq) * LD, *aj = X + rr_col(mq - 1 - p, s, mq) * LD;
+                double *ai = X + ca * LD, *aj = X + cb * LD;
                 double2 x[NB / 16], y[NB / 16];   // elements 2 l8 + 16 m (+1)
                 double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
@@ -258,9 +286,13 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(const TlrJob job, d
                     ga += __shfl_xor_sync(gmask, ga, o);
                 }
                 if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0 && al + be >= floor2) {
-                    const double zeta = (be - al) / (2.0 * ga);
-                    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+                    // rotation (c, s) from MUFU-seeded reciprocals / square roots refined by Newton
+                    // steps (~1 ulp; the IEEE div / sqrt sequences were the step's longest latency chain)
+                    const double zeta = be == al ? 0.0 : (be - al) * rcp_nr(2.0 * ga);   // (no 0 * inf for a subnormal ga)
+                    const double az = fabs(zeta);
+                    const double tt = az > 1e100 ? 0.5 / zeta                 // 1 / (2 zeta): sqrt(1 + zeta^2) ~ |zeta|
+                                                 : copysign(rcp_nr(az + sqrt_nr(fma(zeta, zeta, 1.0))), zeta);
+                    const double c = rsqrt_nr(fma(tt, tt, 1.0)), sn = c * tt;
 #pragma unroll
                     for (int m = 0; m < NB / 16; ++m) {
                         *reinterpret_cast<double2 *>(ai + 2 * l8 + 16 * m) = make_double2(c * x[m].x - sn * y[m].x, c * x[m].y - sn * y[m].y);
@@ -269,6 +301,8 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(const TlrJob job, d
                     if (l8 == 0) chg = 1;
                 }
             }
+            if (ca != 0) ca = ca == mq - 1 ? 1 : ca + 1;
+            cb = cb == mq - 1 ? 1 : cb + 1;
             __syncthreads();
         }
         if (!chg) break;
