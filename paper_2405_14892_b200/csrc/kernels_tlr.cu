@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(tlr::NT, 1) k_tlr_compress(const TlrJob job, d
                     be += __shfl_xor_sync(gmask, be, o);
                     ga += __shfl_xor_sync(gmask, ga, o);
                 }
-                if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0 && al + be >= floor2) {
+                if (ga * ga > 1e-30 * al * be && ga != 0.0 && al + be >= floor2) {   // |ga| > 1e-15 sqrt(al be), no sqrt
                     // rotation (c, s) from MUFU-seeded reciprocals / square roots refined by Newton
                     // steps (~1 ulp; the IEEE div / sqrt sequences were the step's longest latency chain)
                     const double zeta = be == al ? 0.0 : (be - al) * rcp_nr(2.0 * ga);   // (no 0 * inf for a subnormal ga)
