@@ -97,10 +97,13 @@ mvn_status mvn_marginal_order(int64_t n, const double *mu, const double *var_dia
 /* ---------------------------------------------------------------------------------------------
  * a2. Matérn covariance tiles (Eq. 6, as printed: no sqrt(2 nu) scaling, R14):
  *   Sigma_kl = sigma2 * M_nu(h/beta) + nugget * delta_kl,  h = ||x_k - x_l||_2  (Euclidean)
- *   nu = 0.5: e^{-x};  nu = 1.5: (1+x) e^{-x};  nu = 2.5: (1 + x + x^2/3) e^{-x}.
+ *   nu = 0.5: e^{-x};  nu = 1.5: (1+x) e^{-x};  nu = 2.5: (1 + x + x^2/3) e^{-x} (closed forms, the
+ *   fast kernels); any other 0 < nu <= 50: M_nu(x) = 2^{1-nu}/Gamma(nu) x^nu K_nu(x) with K_nu by
+ *   Temme's series (x <= 2) / Steed's continued fraction (x > 2) and the forward recurrence (e.g.
+ *   the wind fit's nu = 1.43391); M_nu(0) = 1.
  * d_xy: n x 2 row-major device doubles, ALREADY in sorted order (x_{o(k)}). d_tiles: device,
  * mvn_tiles_bytes(t) bytes, fully written (including padding). Exactly symmetric.
- * MVN_E_USAGE for sigma2 <= 0, beta <= 0, nugget < 0, or nu not in {0.5, 1.5, 2.5}.            */
+ * MVN_E_USAGE for sigma2 <= 0, beta <= 0, nugget < 0, or nu outside (0, 50].                    */
 mvn_status mvn_cov_matern(mvn_ctx *ctx, mvn_tiles t, const double *d_xy, double sigma2, double beta,
                           double nu, double nugget, double *d_tiles);
 

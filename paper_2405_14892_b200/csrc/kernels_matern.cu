@@ -8,6 +8,7 @@
 // DFMA/clk/SM) vs the fp64 arithmetic per element: distance (3), sqrt, x = h / beta as a product
 // with the host's 1/beta (1; a division costs ~10 plus a slow-path call), exp(-x) with sigma2
 // folded in (8, exp_neg_scaled), the nu = 3/2, 5/2 factor (1-2).
+#include <cmath>
 #include <cstdlib>
 
 #include <math_constants.h>
@@ -24,13 +25,89 @@ namespace mvn {
 // sigma2 * 2^-(j/1024) in shared memory (2^-(j/1024) correctly rounded on the host once per context,
 // g_exp2n, times sigma2 per CTA), and 2^-(k >> 10) applied to the exponent field with an integer
 // subtract. Error <= ~5 ulp (round 2, session 2: one fp64 FMA fewer than the 256-entry, degree-4 form).
+// General nu (Eq. 6 with any nu > 0; P:446's wind fit has nu = 1.43391): K_nu(x) by Temme's method —
+// nu = nl + mu, |mu| <= 1/2: for x <= 2 Temme's series for K_mu and K_mu+1, for x > 2 Steed's
+// continued fraction CF2 (Thompson-Barnett form) — then the forward recurrence
+// K_{mu+i+1} = 2 (mu+i)/x K_{mu+i} + K_{mu+i-1} (stable for K). Everything that depends on nu only is
+// computed on the host in long double (the Gamma-function terms, mu pi / sin(mu pi), and the
+// reciprocals of the iterations' denominators), so a Temme step has no division and a CF2 step one.
+namespace matg {
+constexpr int TMAX = 32, CMAX = 112;  // Temme / CF2 caps (x <= 2: c_k <= 1/k!^2 -> 1e-30 by k = 18; CF2 just above x = 2 needs ~100: 64 left 2e-14)
+}
+struct MaternGen {
+    double mu, fact, gam1, gam2, gp, gm, pref;         // gp, gm = Gamma(1 + mu), Gamma(1 - mu); pref = 2^(1-nu) / Gamma(nu)
+    int nl;
+    double rq[matg::TMAX], rim[matg::TMAX], rip[matg::TMAX];   // 1/(k^2 - mu^2), 1/(k - mu), 1/(k + mu), k >= 1
+    double ria[matg::CMAX], rinv[matg::CMAX];                  // CF2: 1/a_i (a_i = -(1/4 - mu^2) - i(i-1)), 1/i
+};
+
 struct MaternArgs {
     int64_t n;
     const double *xy;
     double sigma2, inv_beta, nugget;
     TileMap tm;          // destination storage (the full buffer, or a rank's owned tile columns)
     int libm;            // sigma2 so small or large that the scaled result could leave the normal range
+    MaternGen gen;       // general nu only
 };
+
+// sigma2 * 2^(1-nu)/Gamma(nu) * x^nu * K_nu(x), x > 0 (Eq. 6)
+__device__ __forceinline__ double matern_general(double x, double sigma2, const MaternGen &g) {
+    if (x < 1e-100) return sigma2;                        // coincident points: the limit sigma2
+    const double mu = g.mu, mu2 = mu * mu;
+    double kmu, k1;
+    if (x <= 2.0) {
+        const double x2 = 0.5 * x, d = -log(x2);          // d = ln(2/x)
+        const double e = mu * d;
+        const double E = exp(e), Ei = 1.0 / E;
+        const double ch = 0.5 * (E + Ei), sh_e = e == 0.0 ? 1.0 : sinh(e) / e;   // (E - 1/E) / 2e would cancel for small e
+        double ff = g.fact * (g.gam1 * ch + g.gam2 * sh_e * d);
+        double p = 0.5 * E * g.gp;                        // 0.5 (x/2)^-mu Gamma(1 + mu)
+        double q = 0.5 * Ei * g.gm;                       // 0.5 (x/2)^mu Gamma(1 - mu)
+        double c = 1.0, sum = ff, sum1 = p;
+        const double dd = x2 * x2;
+        for (int k = 1; k < matg::TMAX; ++k) {
+            ff = (k * ff + p + q) * g.rq[k];
+            c *= dd * g.rinv[k];
+            p *= g.rim[k];
+            q *= g.rip[k];
+            const double del = c * ff;
+            sum += del;
+            sum1 += c * (p - k * ff);
+            if (fabs(del) < fabs(sum) * 1e-17) break;
+        }
+        kmu = sum;
+        k1 = sum1 * (2.0 / x);
+    } else {
+        double b = 2.0 * (1.0 + x), d = 1.0 / b, h = d, delh = d, q1 = 0.0, q2 = 1.0;
+        const double a1 = 0.25 - mu2;
+        double q = a1, c = a1, a = -a1, s = 1.0 + q * delh;
+        for (int i = 2; i < matg::CMAX; ++i) {
+            a -= 2 * (i - 1);
+            c = -a * c * g.rinv[i];
+            const double qnew = (q1 - b * q2) * g.ria[i];
+            q1 = q2;
+            q2 = qnew;
+            q += c * qnew;
+            b += 2.0;
+            d = 1.0 / (b + a * d);
+            delh = (b * d - 1.0) * delh;
+            h += delh;
+            const double dels = q * delh;
+            s += dels;
+            if (fabs(dels) < fabs(s) * 1e-17) break;
+        }
+        h = a1 * h;
+        kmu = sqrt(CUDART_PI / (2.0 * x)) * exp(-x) / s;
+        k1 = kmu * (mu + x + 0.5 - h) / x;
+    }
+    const double x2i = 2.0 / x;
+    for (int i = 1; i <= g.nl; ++i) {                    // K_{mu+i+1} = 2 (mu+i)/x K_{mu+i} + K_{mu+i-1}
+        const double kt = (mu + i) * x2i * k1 + kmu;
+        kmu = k1;
+        k1 = kt;
+    }
+    return sigma2 * g.pref * exp((mu + g.nl) * log(x)) * kmu;
+}
 
 __device__ double g_exp2n[1024];   // 2^(-j/1024), j = 0..1023 (matern_init)
 
@@ -52,7 +129,7 @@ __device__ __forceinline__ double exp_neg_scaled(double x, const double *tb) {
     return __hiloint2double(__double2hiint(v) - ((k >> 10) << 20), __double2loint(v));
 }
 
-template <int NU2>  // 2*nu: 1 -> nu = 1/2, 3 -> nu = 3/2, 5 -> nu = 5/2; sigma2 * C(x) from e = sigma2 exp(-x)
+template <int NU2>  // 2*nu: 1 -> nu = 1/2, 3 -> nu = 3/2, 5 -> nu = 5/2; sigma2 * C(x) from e = sigma2 exp(-x) (0: general nu)
 __device__ __forceinline__ double matern_poly(double x, double e) {
     if (NU2 == 1) return e;
     if (NU2 == 3) return fma(x, e, e);
@@ -160,7 +237,13 @@ __global__ void __launch_bounds__(256, MINB) k_cov_matern(const MaternArgs p) {
         const int col = cg + CPI * m;
         const double xc = cx[col], yc = cy[col];
         double v[RPT];
-        if (fast) {
+        if (NU2 == 0) {                                   // general nu: Temme / CF2 per element
+#pragma unroll
+            for (int h = 0; h < RPT; ++h) {
+                const double dx = rx[h] - xc, dy = ry[h] - yc;
+                v[h] = matern_general(sqrt(fma(dx, dx, dy * dy)) * ib, sigma2, p.gen);
+            }
+        } else if (fast) {
 #pragma unroll
             for (int h = 0; h < RPT; ++h) {
                 const double dx = rx[h] - xc, dy = ry[h] - yc;
@@ -206,6 +289,38 @@ static void k1_launch(dim3 grid, const MaternArgs &a, cudaStream_t st) {
     }
 }
 
+// Host side of the general-nu K1: nu = nl + mu, |mu| <= 1/2 (nl = round(nu)), the Gamma terms of
+// Temme's series in long double — gam1 = (1/Gamma(1-mu) - 1/Gamma(1+mu)) / (2 mu) by its Taylor form
+// -gamma + (gamma zeta(2)/2 - zeta(3)/3 - gamma^3/6) mu^2 where the difference would cancel (|mu| <
+// 1e-4), gam2 = (1/Gamma(1-mu) + 1/Gamma(1+mu)) / 2 — and the iteration reciprocals.
+void matern_general_setup(double nu, MaternGen &g) {
+    const int nl = (int)floor(nu + 0.5);
+    const long double mu = (long double)nu - nl;
+    const long double pi = 3.141592653589793238462643383279502884L;
+    const long double eg = 0.577215664901532860606512090082402431L, z2 = pi * pi / 6, z3 = 1.202056903159594285399738161511449991L;
+    const long double gampl = 1.0L / tgammal(1.0L + mu), gammi = 1.0L / tgammal(1.0L - mu);
+    g.mu = (double)mu;
+    g.nl = nl;
+    g.gp = (double)tgammal(1.0L + mu);
+    g.gm = (double)tgammal(1.0L - mu);
+    g.gam2 = (double)(0.5L * (gammi + gampl));
+    g.gam1 = fabsl(mu) < 1e-4L ? (double)(-eg + (eg * z2 / 2 - z3 / 3 - eg * eg * eg / 6) * mu * mu)
+                               : (double)((gammi - gampl) / (2.0L * mu));
+    g.fact = fabsl(mu) < 1e-12L ? 1.0 : (double)(pi * mu / sinl(pi * mu));
+    g.pref = (double)(powl(2.0L, 1.0L - (long double)nu) / tgammal((long double)nu));
+    for (int k = 0; k < matg::TMAX; ++k) {
+        g.rq[k] = k ? (double)(1.0L / ((long double)k * k - mu * mu)) : 0.0;
+        g.rim[k] = k ? (double)(1.0L / ((long double)k - mu)) : 0.0;
+        g.rip[k] = k ? (double)(1.0L / ((long double)k + mu)) : 0.0;
+    }
+    const long double a1 = 0.25L - mu * mu;
+    for (int i = 0; i < matg::CMAX; ++i) {
+        const long double ai = -a1 - (long double)i * (i - 1);
+        g.ria[i] = i >= 2 ? (double)(1.0L / ai) : 0.0;
+        g.rinv[i] = i >= 1 ? (double)(1.0L / i) : 0.0;
+    }
+}
+
 cudaError_t matern_init() {
     static double h[1024];
     for (int j = 0; j < 1024; ++j) h[j] = (double)exp2l(-(long double)j / 1024.0L);
@@ -222,7 +337,11 @@ cudaError_t launch_cov_matern_map(int64_t n, const double *xy, double sigma2, do
     dim3 grid((unsigned)ntiles);
     if (nu == 0.5) k1_launch<1>(grid, a, st);
     else if (nu == 1.5) k1_launch<3>(grid, a, st);
-    else k1_launch<5>(grid, a, st);
+    else if (nu == 2.5) k1_launch<5>(grid, a, st);
+    else {
+        matern_general_setup(nu, a.gen);
+        k_cov_matern<0, 4, 2><<<grid, 256, 0, st>>>(a);
+    }
     return cudaGetLastError();
 }
 

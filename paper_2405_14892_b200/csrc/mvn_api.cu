@@ -301,8 +301,8 @@ mvn_status mvn_cov_matern(mvn_ctx *c, mvn_tiles t, const double *d_xy, double si
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!tiles_ok(t) || !d_xy || !d_tiles || !(sigma2 > 0) || !(beta > 0) || !(nugget >= 0) ||
-        !(nu == 0.5 || nu == 1.5 || nu == 2.5))
-        return fail(c, MVN_E_USAGE, "mvn_cov_matern: need nb=128, sigma2>0, beta>0, nugget>=0, nu in {0.5,1.5,2.5}");
+        !(nu > 0 && nu <= 50))
+        return fail(c, MVN_E_USAGE, "mvn_cov_matern: need nb=128, sigma2>0, beta>0, nugget>=0, 0 < nu <= 50");
     MVN_CUDA(c, mvn::launch_cov_matern(t.n, d_xy, sigma2, beta, nu, nugget, d_tiles, c->stream));
     return MVN_OK;
 }
@@ -439,7 +439,7 @@ mvn_status mvn_dcov_matern(mvn_ctx *c, mvn_dtiles d, const double *d_xy, double 
                            double nugget, double *d_local) {
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
-    if (!dtiles_ok(d) || !d_xy || !d_local || !(sigma2 > 0) || !(beta > 0) || !(nugget >= 0) || !(nu == 0.5 || nu == 1.5 || nu == 2.5))
+    if (!dtiles_ok(d) || !d_xy || !d_local || !(sigma2 > 0) || !(beta > 0) || !(nugget >= 0) || !(nu > 0 && nu <= 50))
         return fail(c, MVN_E_USAGE, "mvn_dcov_matern: bad arguments");
     MVN_CUDA(c, mvn::launch_cov_matern_map(d.n, d_xy, sigma2, beta, nu, nugget, dmap(d, d_local), c->stream));
     return MVN_OK;
@@ -1011,7 +1011,7 @@ mvn_status mvn_posterior(mvn_ctx *c, const mvn_posterior_problem *p, double *mu_
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     if (!p || !mu_post || !var_post || !info || p->n < 1 || p->m < 1 || !p->xy || !p->mu || !p->obs || !p->y ||
-        !(p->tau > 0) || !(p->sigma2 > 0) || !(p->beta > 0) || !(p->nugget >= 0) || !(p->nu == 0.5 || p->nu == 1.5 || p->nu == 2.5))
+        !(p->tau > 0) || !(p->sigma2 > 0) || !(p->beta > 0) || !(p->nugget >= 0) || !(p->nu > 0 && p->nu <= 50))
         return fail(c, MVN_E_USAGE, "mvn_posterior: bad arguments");
     const int64_t n = p->n, m = p->m;
     std::vector<char> seen((size_t)n, 0);

@@ -71,4 +71,5 @@ def test_mc_and_posterior_and_matern_reject_bad_arguments(torch):
     mvn().mvn_posterior(xy, np.zeros(60), np.array([1, 5]), np.zeros(2), 1.0, 0.1, 0.5, 1e-8, 0.5)
     usage(mvn().mvn_posterior_tiles, np.arange(59))       # n differs from the last posterior
     usage(mvn().mvn_posterior_tiles, np.zeros(60, dtype=np.int64))   # not a permutation
-    usage(mvn().mvn_cov_matern, torch.from_numpy(xy).cuda(), 1.0, 0.1, 1.0, 1e-8)   # nu = 1 unsupported
+    usage(mvn().mvn_cov_matern, torch.from_numpy(xy).cuda(), 1.0, 0.1, 0.0, 1e-8)   # nu must be in (0, 50]
+    usage(mvn().mvn_cov_matern, torch.from_numpy(xy).cuda(), 1.0, 0.1, 51.0, 1e-8)

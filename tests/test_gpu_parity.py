@@ -427,3 +427,35 @@ def test_full_config_all_samples_regions(torch_cuda, name, method):
     assert d_indep <= (1e-7 if name == "E" else LOGP_TOL), d_indep
     k_i, tie_i = oracle.region(lp_i, cfg.conf)
     assert all(kg == ki or t for kg, ki, t in zip(k_g, k_i, tie_i)), (list(k_g), list(k_i))
+
+
+# General nu (Eq. 6 with K_nu: Temme's series / Steed's CF2 / forward recurrence on the GPU) against the
+# oracle's scipy.special.kv: fractional nu (the wind fit's 1.43391), mu = 0 exactly (integer nu),
+# tiny |mu| (the Taylor form of gam1), half-integer nu outside the closed forms (mu = -1/2), large nu,
+# and ranges putting x on both sides of the series / continued-fraction switch at 2.
+@pytest.mark.parametrize("n,nu,beta", [(400, 1.43391, 0.1), (300, 0.3, 0.05), (300, 1.0, 0.2), (300, 1.00003, 0.1),
+                                       (200, 3.5, 0.15), (200, 7.2, 0.3), (129, 0.75, 0.02), (260, 2.0, 0.5)])
+def test_matern_general_nu_vs_oracle(torch_cuda, n, nu, beta):
+    torch = torch_cuda
+    xy = np.random.default_rng(int(nu * 1000) + n).uniform(size=(n, 2))
+    xy[7] = xy[3]                                        # coincident points: the limit sigma2
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.3, beta, nu, 1e-8)
+    G = to_dense_lower(T, n)
+    S = oracle.covariance(xy, 1.3, beta, nu, 1e-8)
+    low = np.tril(S)
+    rel = np.abs(G - low) / np.maximum(np.abs(low), 1e-300)
+    worst = np.max(np.where(low > 1e-280, rel, 0.0))
+    # the bar against the oracle is its own error: scipy's kv is off by up to ~6e-14 relative near
+    # x = 2 for fractional nu (measured against 30-digit mpmath, tools/nu_diag.py) — the GPU is then
+    # checked against mpmath itself on the worst entries at 1e-14
+    assert worst <= 1e-13, worst
+    assert np.all(np.abs(G[low <= 1e-280]) <= 1e-279)   # underflow region (x ~ 650+): both ~0
+    assert G[7, 3] == 1.3
+    assert np.array_equal(np.diag(G), np.diag(S))
+    import mpmath as mp
+    mp.mp.dps = 30
+    for t in np.argsort(np.where(low > 1e-280, rel, 0.0).ravel())[::-1][:6]:
+        i, j = divmod(int(t), n)
+        x = mp.sqrt(mp.mpf(xy[i, 0] - xy[j, 0]) ** 2 + mp.mpf(xy[i, 1] - xy[j, 1]) ** 2) / beta
+        ref = 1.3 / (2 ** (mp.mpf(nu) - 1) * mp.gamma(nu)) * x ** nu * mp.besselk(nu, x)
+        assert abs(G[i, j] - ref) <= 1e-14 * ref, (nu, float(x), float(abs(G[i, j] - ref) / ref))
