@@ -248,6 +248,21 @@ def test_crd_config_A_independent_vs_oracle(torch_cuda):
     assert not np.any(ref.near_tie)
 
 
+def test_crd_general_nu_independent_vs_oracle(torch_cuda):
+    """Alg. 1 end to end through the public mvn_crd with the wind fit's smoothness nu = 1.43391 (P:446;
+    general-nu K1) on config A's geometry, against the oracle's own pipeline (independent mode)."""
+    cfg = W.small_config("A-nu", 20, 4000, 5, base="A", nu=1.43391, beta=0.08)
+    inp = W.make_inputs(cfg)
+    out = mvn().mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                        cfg.seed_lattice, cfg.conf)
+    ref = oracle.crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                     cfg.seed_lattice, cfg.conf, chunk=500, nthreads=16)
+    assert out.info == -1
+    assert np.array_equal(out.order, ref.order)
+    assert np.max(np.abs(out.logP - ref.logp)) <= LOGP_TOL
+    assert np.array_equal(out.k_star, ref.k_star) or np.any(ref.near_tie)
+
+
 @pytest.mark.slow
 def test_crd_config_B_independent_vs_oracle(torch_cuda):
     """Config B (n = 4,900) end to end; the oracle runs all 1e5 samples on the host cores."""
