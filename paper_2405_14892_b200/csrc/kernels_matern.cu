@@ -106,7 +106,9 @@ __device__ __forceinline__ double matern_general(double x, double sigma2, const 
         kmu = k1;
         k1 = kt;
     }
-    return sigma2 * g.pref * exp((mu + g.nl) * log(x)) * kmu;
+    const double r = sigma2 * g.pref * exp((mu + g.nl) * log(x)) * kmu;
+    // K_nu(x) ~ Gamma(nu)/2 (2/x)^nu overflows for a large nu at a tiny x, where C = sigma2 (1 - O(x^2))
+    return isfinite(r) ? r : sigma2;
 }
 
 __device__ double g_exp2n[1024];   // 2^(-j/1024), j = 0..1023 (matern_init)

@@ -248,6 +248,37 @@ def test_crd_config_A_independent_vs_oracle(torch_cuda):
     assert not np.any(ref.near_tie)
 
 
+def test_matern_general_nu_extremes(torch_cuda):
+    """General nu at the edges: nu = 40 with near-coincident points (K_nu overflows: the limit sigma2),
+    far pairs (underflow to 0), nu = 0.05 (C(x) - sigma2 ~ x^(2 nu): still 8 % below sigma2 at
+    x = 3e-11); finite everywhere and within the oracle's bar where the oracle is finite."""
+    torch = torch_cuda
+    rng = np.random.default_rng(9)
+    xy = rng.uniform(size=(200, 2))
+    xy[5] = xy[4] + 1e-12
+    for nu, beta in [(40.0, 0.05), (0.05, 0.1), (12.5, 0.003)]:
+        G = to_dense_lower(mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 2.0, beta, nu, 0.0), 200)
+        S = oracle.covariance(xy, 2.0, beta, nu, 0.0)
+        low = np.tril(S)
+        assert np.all(np.isfinite(G))
+        ok = np.isfinite(low) & (low > 1e-280)
+        relm = np.where(ok, np.abs(G - np.where(ok, low, 0.0)) / np.where(ok, low, 1.0), 0.0)
+        assert np.max(relm) <= 1e-12, (nu, np.max(relm))            # the oracle's kv at large nu / x
+        import mpmath as mp
+        mp.mp.dps = 30
+        for t in np.argsort(relm.ravel())[::-1][:4]:                  # the worst entries against 30 digits
+            i, j = divmod(int(t), 200)
+            x = mp.sqrt(mp.mpf(xy[i, 0] - xy[j, 0]) ** 2 + mp.mpf(xy[i, 1] - xy[j, 1]) ** 2) / beta
+            ref = 2.0 / (2 ** (mp.mpf(nu) - 1) * mp.gamma(nu)) * x ** nu * mp.besselk(nu, x)
+            # + the condition of e^-x to the rounding of x = h / beta itself (|d ln C / dx| ~ 1 at large x)
+            tol = 2e-14 + 4e-16 * float(x)
+            assert abs(G[i, j] - ref) <= tol * ref, (nu, float(x), float(abs(G[i, j] - ref) / ref))
+        if nu > 1:                                       # x ~ 1e-10: C = sigma2 (1 - O(x^2)) (oracle: inf * 0)
+            assert G[5, 4] == pytest.approx(2.0, rel=1e-12)
+        else:                                            # nu < 1: C(x) - sigma2 ~ x^(2 nu), far from 0 here
+            assert np.isfinite(low[5, 4]) and abs(G[5, 4] - low[5, 4]) <= 1e-13 * low[5, 4]
+
+
 def test_crd_general_nu_independent_vs_oracle(torch_cuda):
     """Alg. 1 end to end through the public mvn_crd with the wind fit's smoothness nu = 1.43391 (P:446;
     general-nu K1) on config A's geometry, against the oracle's own pipeline (independent mode)."""
