@@ -495,10 +495,15 @@ typedef struct {
     int64_t nconf;
     int32_t method;        /* 0: fp64 throughout; bit 0 (MVN_CRD_SOV_INT8): the SOV GEMM on the int8 tensor
                               cores (mvn_sov_prefix_ex); bit 1 (MVN_CRD_POTRF_INT8): the Cholesky
-                              updates too (mvn_potrf_ex) — NEXT-4 mixed precision */
+                              updates too (mvn_potrf_ex) — NEXT-4 mixed precision; bit 2 (MVN_CRD_TLR):
+                              step (a) as the TLR Cholesky at accuracy tlr_eps (mvn_tlr_potrf, mode
+                              MVN_TLR_ABS, slots of 128 columns in the context; steps (b)-(d) dense on
+                              L~) — NEXT-3; not with bit 1 */
+    double tlr_eps;        /* MVN_CRD_TLR: the accuracy eps (>= 0); ignored otherwise */
 } mvn_crd_problem;
 #define MVN_CRD_SOV_INT8 1
 #define MVN_CRD_POTRF_INT8 2
+#define MVN_CRD_TLR 4
 
 typedef struct {
     int64_t *order;        /* host out, n: original index of sorted position k */

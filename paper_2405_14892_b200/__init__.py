@@ -81,7 +81,7 @@ class mvn_crd_problem(ctypes.Structure):
                 ("sigma2", ctypes.c_double), ("beta", ctypes.c_double), ("nu", ctypes.c_double),
                 ("nugget", ctypes.c_double), ("u", ctypes.c_double), ("N", ctypes.c_int64),
                 ("R", ctypes.c_int32), ("seed", ctypes.c_uint64), ("conf", ctypes.c_void_p),
-                ("nconf", ctypes.c_int64), ("method", ctypes.c_int32)]
+                ("nconf", ctypes.c_int64), ("method", ctypes.c_int32), ("tlr_eps", ctypes.c_double)]
 
 
 class mvn_crd_result(ctypes.Structure):
@@ -792,10 +792,14 @@ class CrdOutput:
     ms_stage: tuple
 
 
+CRD_SOV_INT8, CRD_POTRF_INT8, CRD_TLR = 1, 2, 4
+
+
 def mvn_crd(xy: np.ndarray, mu: np.ndarray, sigma2, beta, nu, nugget, u, N, R, seed, conf, device: int = 0,
-            pinned_out=None, method: int = 0) -> CrdOutput:
+            pinned_out=None, method: int = 0, tlr_eps: float = 0.0) -> CrdOutput:
     """End-to-end Alg. 1 through the C ABI with HOST buffers (upload, a1..a10, download).
-    method: 0 fp64; bit 0 the SOV GEMM on the int8 tensor cores, bit 1 the Cholesky updates too."""
+    method: 0 fp64; bit 0 the SOV GEMM on the int8 tensor cores, bit 1 the Cholesky updates too;
+    bit 2 (CRD_TLR) the TLR Cholesky at accuracy tlr_eps (NEXT-3)."""
     xy = np.ascontiguousarray(xy, dtype=np.float64)
     mu = np.ascontiguousarray(mu, dtype=np.float64)
     cf = np.ascontiguousarray(conf, dtype=np.float64)
@@ -806,7 +810,7 @@ def mvn_crd(xy: np.ndarray, mu: np.ndarray, sigma2, beta, nu, nugget, u, N, R, s
     k = np.empty(max(len(cf), 1), dtype=np.int64)
     tie = np.empty(max(len(cf), 1), dtype=np.int32)
     prob = mvn_crd_problem(n, _np_ptr(xy), _np_ptr(mu), sigma2, beta, nu, nugget, u, int(N), int(R), int(seed),
-                           _np_ptr(cf) if cf.size else None, len(cf), int(method))
+                           _np_ptr(cf) if cf.size else None, len(cf), int(method), float(tlr_eps))
     res = mvn_crd_result(_np_ptr(order), _np_ptr(logP), _np_ptr(k), _np_ptr(tie), -1)
     c.check(lib().mvn_crd(c.h, ctypes.byref(prob), ctypes.byref(res)), "mvn_crd")
     return CrdOutput(order, logP, k[:len(cf)], tie[:len(cf)].astype(bool), int(res.info), tuple(res.ms_stage))

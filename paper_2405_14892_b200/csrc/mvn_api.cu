@@ -49,6 +49,7 @@ struct mvn_ctx {
     void *pozR = nullptr; size_t pozR_cap = 0;     // int8 POTRF: panel row scales
     void *pozX = nullptr; size_t pozX_cap = 0;     // int8 POTRF: cluster exchange scratch
     void *tlrW = nullptr; size_t tlrW_cap = 0;     // TLR Cholesky: panel + M / Z chunks + overflow flag
+    void *tlrS = nullptr; size_t tlrS_cap = 0;     // mvn_crd with MVN_CRD_TLR: the factor slots U, V and ranks
     // mvn_sweep state: stream-ordered allocations from the context's own pool, which keeps the
     // memory between sweeps (no re-mapping per sweep) until mvn_trim / mvn_destroy
     cudaMemPool_t pool = nullptr;
@@ -212,7 +213,7 @@ void mvn_destroy(mvn_ctx *c) {
     // waits for the device's outstanding work itself
     cudaDeviceSynchronize();
     for (void *p : {c->Y, c->part, c->cta, c->sync, (void *)c->G, (void *)c->d_info, c->crd_L, c->crd_vec, c->mcZ, c->mcF,
-                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX, c->sozX, c->pozA, c->pozR, c->pozX, c->tlrW})
+                    c->post, c->postv, c->mcLA, c->mcRS, c->mcX, c->sozX, c->pozA, c->pozR, c->pozX, c->tlrW, c->tlrS})
         if (p) cudaFree(p);
     if (c->done) cudaEventDestroy(c->done);
     if (c->pool) cudaMemPoolDestroy(c->pool);
@@ -242,10 +243,10 @@ mvn_status mvn_trim(mvn_ctx *c) {
     DevGuard dev_guard(c);
     if (!c) return MVN_E_USAGE;
     cudaStreamSynchronize(c->stream);
-    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX, &c->sozX, &c->pozA, &c->pozR, &c->pozX, &c->tlrW})
+    for (void **p : {&c->Y, &c->part, &c->cta, &c->sync, &c->crd_L, &c->crd_vec, &c->mcZ, &c->mcF, &c->post, &c->postv, &c->mcLA, &c->mcRS, &c->mcX, &c->sozX, &c->pozA, &c->pozR, &c->pozX, &c->tlrW, &c->tlrS})
         if (*p) { cudaFree(*p); *p = nullptr; }
     c->Y_cap = c->part_cap = c->cta_cap = c->sync_cap = c->crd_L_cap = c->crd_vec_cap = c->mcZ_cap = c->mcF_cap = 0;
-    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = c->sozX_cap = c->pozA_cap = c->pozR_cap = c->pozX_cap = c->tlrW_cap = 0;
+    c->post_cap = c->postv_cap = c->mcLA_cap = c->mcRS_cap = c->mcX_cap = c->sozX_cap = c->pozA_cap = c->pozR_cap = c->pozX_cap = c->tlrW_cap = c->tlrS_cap = 0;
     c->post_n = c->post_off = 0;
     if (c->pool) cudaMemPoolTrimTo(c->pool, 0);
     return MVN_OK;
@@ -1169,8 +1170,20 @@ mvn_status mvn_crd(mvn_ctx *c, const mvn_crd_problem *p, mvn_crd_result *out) {
     if ((s = mvn_cov_matern(c, t, dxy, p->sigma2, p->beta, p->nu, p->nugget, dL)) != MVN_OK) return s;
     MVN_CUDA(c, cudaEventRecord(ev[2], c->stream));
     int64_t info = -1;
-    if (p->method & ~(MVN_CRD_SOV_INT8 | MVN_CRD_POTRF_INT8)) return fail(c, MVN_E_USAGE, "mvn_crd: unknown method bits");
-    s = mvn_potrf_ex(c, t, dL, &info, (p->method & MVN_CRD_POTRF_INT8) ? MVN_POTRF_INT8 : MVN_POTRF_FP64);
+    if (p->method & ~(MVN_CRD_SOV_INT8 | MVN_CRD_POTRF_INT8 | MVN_CRD_TLR)) return fail(c, MVN_E_USAGE, "mvn_crd: unknown method bits");
+    if (p->method & MVN_CRD_TLR) {
+        if ((p->method & MVN_CRD_POTRF_INT8) || !(p->tlr_eps >= 0.0))
+            return fail(c, MVN_E_USAGE, "mvn_crd: MVN_CRD_TLR needs tlr_eps >= 0 and excludes MVN_CRD_POTRF_INT8");
+        const size_t slot = mvn_tlr_slots_bytes(t, (int32_t)mvn::kTile);
+        const int64_t nt = (n + mvn::kTile - 1) / mvn::kTile, noff = nt * (nt - 1) / 2;
+        if ((s = ensure(c, &c->tlrS, &c->tlrS_cap, 2 * slot + sizeof(int32_t) * (size_t)std::max<int64_t>(noff, 1) + 256)) != MVN_OK)
+            return s;
+        double *U = (double *)c->tlrS, *V = (double *)((char *)c->tlrS + slot);
+        int32_t *rk = (int32_t *)((char *)c->tlrS + 2 * slot);
+        s = mvn_tlr_potrf(c, t, dL, p->tlr_eps, MVN_TLR_ABS, (int32_t)mvn::kTile, U, V, rk, nullptr, &info);
+    } else {
+        s = mvn_potrf_ex(c, t, dL, &info, (p->method & MVN_CRD_POTRF_INT8) ? MVN_POTRF_INT8 : MVN_POTRF_FP64);
+    }
     out->info = info;
     if (s != MVN_OK) return s;
     MVN_CUDA(c, cudaEventRecord(ev[3], c->stream));

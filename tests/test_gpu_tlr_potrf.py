@@ -299,3 +299,29 @@ def test_sov_factored_update_errors(torch):
                         torch.zeros(3, dtype=torch.int32, device="cuda"), torch.zeros(3, dtype=torch.int32, device="cuda"), 0, -1)
     with pytest.raises(mvn().MvnError):
         mvn().mvn_sov_prefix_tlr(T, f, n, a, 100, 1, 1)          # kmax = 0
+
+
+def test_crd_tlr_end_to_end_vs_oracle(torch):
+    """Alg. 1 end to end through the public mvn_crd with step (a) as the TLR Cholesky (MVN_CRD_TLR,
+    P:319): against the oracle's pipeline on its own TLR factor (independent mode)."""
+    cfg = W.small_config("crdtlr", 30, 2000, 4, base="A")
+    inp = W.make_inputs(cfg)
+    eps = 1e-6
+    out = mvn().mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                        cfg.seed_lattice, cfg.conf, method=mvn().CRD_TLR, tlr_eps=eps)
+    var = np.full(cfg.n, cfg.sigma2 + cfg.nugget)
+    order, a, _ = oracle.marginal_order(inp.mu, var, cfg.u)
+    S = oracle.covariance(inp.xy[order], cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    Lt, rL, sL, rS, info = oracle.tlr_cholesky(S, eps)
+    assert out.info == -1 and info == -1
+    ref = oracle.crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                     cfg.seed_lattice, cfg.conf, chunk=500, nthreads=16, L=Lt)
+    assert np.array_equal(out.order, ref.order)
+    assert np.max(np.abs(out.logP - ref.logp)) <= 1e-8
+    assert np.array_equal(out.k_star, ref.k_star) or np.any(ref.near_tie)
+    dense = mvn().mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                          cfg.seed_lattice, cfg.conf)
+    assert np.max(np.abs(out.logP - dense.logP)) <= 1e-3          # eps = 1e-6 truncation, P:439
+    with pytest.raises(mvn().MvnError):
+        mvn().mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
+                      cfg.seed_lattice, cfg.conf, method=mvn().CRD_TLR | mvn().CRD_POTRF_INT8, tlr_eps=eps)
