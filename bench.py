@@ -637,8 +637,9 @@ def main():
     ap.add_argument("--sov-method", type=int, default=0, choices=[0, 1],
                     help="crd: 0 = SOV GEMM on fp64 DMMA (default, the headline); 1 = on the int8 tensor cores "
                          "(NEXT-4 mixed precision, Ozaki split, reading R24) - its own bench line")
-    ap.add_argument("--potrf-method", type=int, default=0, choices=[0, 1],
-                    help="crd: 0 = Cholesky updates on fp64 DMMA (default); 1 = on the int8 tensor cores (NEXT-4, R25)")
+    ap.add_argument("--potrf-method", type=int, default=0, choices=[0, 1, 2],
+                    help="crd: 0 = Cholesky updates on fp64 DMMA (default); 1 = on the int8 tensor cores (NEXT-4, R25); "
+                         "2 = the TLR Cholesky at --tlr-eps (NEXT-3, R26)")
     ap.add_argument("--shard", default="1,2,4,8", help="--workload shard: the world sizes W whose rank-0 share is timed")
     ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr", "tlr-potrf", "shard"],
                     help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
@@ -713,7 +714,7 @@ def main():
     else:
         L = mvn.alloc_tiles(n)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # 256 MB > 126 MB L2
-    step_ops = parallel.crd_ops(args.sov_method, args.potrf_method)
+    step_ops = parallel.crd_ops(args.sov_method, args.potrf_method, args.tlr_eps)
     if mode == "dstore":
         step_ops = type("LibmvnCrdOpsPhases", (step_ops,), {"phase_rows": args.phase_rows})
 
@@ -776,7 +777,9 @@ def main():
         for it in range(4):                      # one warm-up call (allocations), three timed
             t0 = time.perf_counter()
             out = mvn.mvn_crd(inp.xy, inp.mu, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, cfg.u, cfg.N, cfg.R,
-                              cfg.seed_lattice, cfg.conf, method=args.sov_method | (args.potrf_method << 1))
+                              cfg.seed_lattice, cfg.conf,
+                              method=args.sov_method | (2 if args.potrf_method == 1 else 4 if args.potrf_method == 2 else 0),
+                              tlr_eps=args.tlr_eps)
             t1 = time.perf_counter()
             if it > 0:
                 ts.append(t1 - t0)
@@ -859,7 +862,8 @@ def main():
     if mode in ("dist", "dstore"):
         n_potrf = parallel.potrf_launches(n, world, rank)
     else:
-        n_potrf = parallel.potrf_launches(n) if rank == 0 else 0
+        n_potrf = (parallel.potrf_launches(n) if args.potrf_method != 2 else tlr_potrf_launches(-(-n // 128))) \
+            if rank == 0 else 0
     # cov + potrf + (check_limits, k_sov, k_reduce_blocks) + finalize [+ rescale]; int8: + rowscale,
     # lslice, k_sov_oz (memset of the flag is a copy-engine op)
     launches = (1 if (mode in ("dist", "dstore") or rank == 0) else 0) + n_potrf + 3 + 1 + (1 if multi else 0) + \
@@ -879,6 +883,7 @@ def main():
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64" if (args.sov_method, args.potrf_method) == (0, 0) else
+                 f"f64 (Cholesky as the TLR factorisation at eps = {args.tlr_eps:g}, NEXT-3 R26)" if args.potrf_method == 2 else
                  "f64 (" + " and ".join(x for x, on in [("SOV GEMM (R24)", args.sov_method), ("Cholesky updates (R25)",
                                                         args.potrf_method)] if on) + " as exact int8 tensor-core products)",
         "data": "synthetic",
@@ -890,12 +895,14 @@ def main():
         "stage_ms": stage_mean,
         "stage_ms_per_rank": stage_per_rank,
         "sov_method": "int8 tensor cores (NEXT-4, R24)" if args.sov_method == 1 else "fp64 DMMA",
-        "potrf_method": "int8 tensor cores (NEXT-4, R25)" if args.potrf_method == 1 else "fp64 DMMA",
+        "potrf_method": {0: "fp64 DMMA", 1: "int8 tensor cores (NEXT-4, R25)",
+                         2: f"TLR Cholesky at eps = {args.tlr_eps:g} (NEXT-3, R26)"}[args.potrf_method],
         "roofline": sov_roof,
         "potrf_roofline": {"achieved": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12, "peak": PEAK_FP64_TFLOPS,
                            "frac": (n ** 3 / 3) / (potrf_ms / 1e3) / 1e12 / PEAK_FP64_TFLOPS,
                            "unit": "TFLOP/s" if args.potrf_method == 0 else
-                           "fp64-equivalent TFLOP/s (trailing updates on the int8 tensor cores, R25) over the fp64 peak"},
+                           "fp64-equivalent TFLOP/s (trailing updates on the int8 tensor cores, R25) over the fp64 peak"
+                           if args.potrf_method == 1 else "dense-equivalent TFLOP/s (n^3/3 over the TLR Cholesky time)"},
         "clocks": clk,
         "gpu_launches": launches * args.steps,
         "e2e": e2e,

@@ -99,11 +99,23 @@ class LibmvnCrdOps:
         from . import mvn_cov_matern
         mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, out=L)
 
-    potrf_method = 0         # 0: fp64 DMMA (default), 1: the trailing updates on the int8 tensor cores
+    potrf_method = 0         # 0: fp64 DMMA (default), 1: the trailing updates on the int8 tensor cores,
+    tlr_eps = 1e-3           # 2: the TLR Cholesky at accuracy tlr_eps (NEXT-3, R26; slots cached per n)
+    _tlr_slots = {}
 
     @classmethod
     def potrf(cls, L, n):
-        from . import mvn_potrf_ex
+        from . import mvn_potrf_ex, mvn_tlr_potrf
+        if cls.potrf_method == 2:
+            key = (L.device.index, n)
+            if key not in cls._tlr_slots:
+                nt = -(-n // 128)
+                noff = max(nt * (nt - 1) // 2, 1)
+                cls._tlr_slots.clear()
+                cls._tlr_slots[key] = tuple(torch.empty((noff, 128, 128), dtype=torch.float64, device=L.device)
+                                            for _ in range(2))
+            U, V = cls._tlr_slots[key]
+            return mvn_tlr_potrf(L, n, cls.tlr_eps, U=U, V=V).info
         return mvn_potrf_ex(L, n, cls.potrf_method)
 
     @staticmethod
@@ -145,11 +157,13 @@ class LibmvnCrdOps:
         return mvn_prefix_finalize(M, S, NR)
 
 
-def crd_ops(sov_method: int = 0, potrf_method: int = 0):
-    """LibmvnCrdOps with the chosen arithmetic for the SOV GEMM and the Cholesky updates (NEXT-4)."""
+def crd_ops(sov_method: int = 0, potrf_method: int = 0, tlr_eps: float = 1e-3):
+    """LibmvnCrdOps with the chosen arithmetic for the SOV GEMM and the Cholesky updates (NEXT-4), or
+    the TLR Cholesky (potrf_method 2, NEXT-3)."""
     if sov_method == 0 and potrf_method == 0:
         return LibmvnCrdOps
-    return type("LibmvnCrdOpsMixed", (LibmvnCrdOps,), {"sov_method": sov_method, "potrf_method": potrf_method})
+    return type("LibmvnCrdOpsMixed", (LibmvnCrdOps,), {"sov_method": sov_method, "potrf_method": potrf_method,
+                                                       "tlr_eps": tlr_eps})
 
 
 def crd_step(d_xy_sorted: torch.Tensor, d_a: torch.Tensor, L: torch.Tensor, cfg, group=None, events=None,
