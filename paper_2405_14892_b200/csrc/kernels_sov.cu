@@ -574,7 +574,7 @@ constexpr int NG = sovk::NGEMM, NTH = NG + sovk::NCHAIN;  // 8 GEMM warps + 4 ch
 constexpr int BAR_G = 4;                                   // the GEMM warps' staging barrier
 constexpr int SW = sovk::NB + 4;                           // W / staged-Y row stride (== 4 mod 16)
 constexpr int OFF_W = 0, OFF_BS = OFF_W + 64 * SW;         // inside k_sov's ring region (unused here)
-static_assert(OFF_BS + 16 * SW <= sovk::OFF_S, "TLR staging must fit the ring region");
+static_assert(OFF_BS + 2 * 16 * SW <= sovk::OFF_S, "TLR staging (W + two B buffers) must fit the ring region");
 }  // namespace sovt
 
 // acc(8 rows of warp wp x w) += A(8 x K) * B(K x w): A fragments straight from global (a(m, k) =
@@ -587,30 +587,43 @@ __device__ __forceinline__ void tlr_rows_gemm(double (&acc)[16][2], const double
     using namespace sovt;
     const int lane = tid & 31, wp = tid >> 5;
     const int mrow = 8 * wp + (lane >> 2);
-    for (int k0 = 0; k0 < K; k0 += 16) {
+    // the next chunk's A fragments (4 per lane) are loaded into registers while the current chunk's
+    // DMMAs run; the staged B rows go to a double-buffered BS (one barrier per chunk orders the
+    // stores against the previous readers)
+    double aN[4];
+    auto loadA = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int kr = 4 * q + (lane & 3);
+            aN[q] = (k0 + kr < K) ? __ldg(A + (int64_t)mrow * am + (int64_t)(k0 + kr) * ak) : 0.0;
+        }
+    };
+    loadA(0);
+    if (Y) named_sync(BAR_G, NG);                         // the previous users of both BS buffers are done
+    for (int k0 = 0, c = 0; k0 < K; k0 += 16, ++c) {
+        double a[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[q] = aN[q];
         const double *Bs;
-        int bstride;
         if (Y) {
-            named_sync(BAR_G, NG);                        // the previous chunk's reads of BS are done
+            double *buf = BS + (c & 1) * 16 * SW;
             for (int e = tid; e < 16 * w; e += NG) {
                 const int kk = e / w, nn = e - kk * w;
-                BS[kk * SW + nn] = (k0 + kk < K) ? __ldcg(Y + (y0 + k0 + kk) * sbw + nn) : 0.0;
+                buf[kk * SW + nn] = (k0 + kk < K) ? __ldcg(Y + (y0 + k0 + kk) * sbw + nn) : 0.0;
             }
             named_sync(BAR_G, NG);
-            Bs = BS;
-            bstride = SW;
+            Bs = buf;
         } else {
             Bs = Wsm + (int64_t)k0 * SW;
-            bstride = SW;
         }
+        if (k0 + 16 < K) loadA(k0 + 16);
 #pragma unroll
         for (int kk = 0; kk < 16; kk += 4) {
             const int kr = kk + (lane & 3);
-            const double a = (k0 + kr < K) ? __ldg(A + (int64_t)mrow * am + (int64_t)(k0 + kr) * ak) : 0.0;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-                const double b = Bs[kr * bstride + 8 * f + (lane >> 2)];
-                dmma(acc[f][0], acc[f][1], a, b);
+                const double b = Bs[kr * SW + 8 * f + (lane >> 2)];
+                dmma(acc[f][0], acc[f][1], a[kk >> 2], b);
             }
         }
     }
