@@ -587,9 +587,9 @@ __device__ __forceinline__ void tlr_rows_gemm(double (&acc)[16][2], const double
     using namespace sovt;
     const int lane = tid & 31, wp = tid >> 5;
     const int mrow = 8 * wp + (lane >> 2);
-    // the next chunk's A fragments (4 per lane) are loaded into registers while the current chunk's
-    // DMMAs run; the staged B rows go to a double-buffered BS (one barrier per chunk orders the
-    // stores against the previous readers)
+    // the next chunk's A fragments (4 per lane) are loaded into registers and the next chunk's B rows
+    // copied into the other half of a double-buffered BS by cp.async (16-byte pieces, zero-filled
+    // past K) while the current chunk's DMMAs run; one barrier per chunk
     double aN[4];
     auto loadA = [&](int k0) {
 #pragma unroll
@@ -598,21 +598,30 @@ __device__ __forceinline__ void tlr_rows_gemm(double (&acc)[16][2], const double
             aN[q] = (k0 + kr < K) ? __ldg(A + (int64_t)mrow * am + (int64_t)(k0 + kr) * ak) : 0.0;
         }
     };
+    const int hw = w >> 1;                                // 16-byte pieces per staged row
+    auto issueB = [&](int k0, double *buf) {
+        for (int e = tid; e < 16 * hw; e += NG) {
+            const int kk = e / hw, pc = e - kk * hw;
+            const bool in = k0 + kk < K;
+            cp_async16_zfill(buf + kk * SW + 2 * pc, in ? Y + (y0 + k0 + kk) * sbw + 2 * pc : Y, in ? 16 : 0);
+        }
+        cp_async_commit();
+    };
     loadA(0);
-    if (Y) named_sync(BAR_G, NG);                         // the previous users of both BS buffers are done
+    if (Y) {
+        named_sync(BAR_G, NG);                            // the previous users of both BS buffers are done
+        issueB(0, BS);
+    }
     for (int k0 = 0, c = 0; k0 < K; k0 += 16, ++c) {
         double a[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) a[q] = aN[q];
         const double *Bs;
         if (Y) {
-            double *buf = BS + (c & 1) * 16 * SW;
-            for (int e = tid; e < 16 * w; e += NG) {
-                const int kk = e / w, nn = e - kk * w;
-                buf[kk * SW + nn] = (k0 + kk < K) ? __ldcg(Y + (y0 + k0 + kk) * sbw + nn) : 0.0;
-            }
-            named_sync(BAR_G, NG);
-            Bs = buf;
+            cp_async_wait<0>();
+            named_sync(BAR_G, NG);                        // chunk c landed; chunk c - 1's readers are done
+            if (k0 + 16 < K) issueB(k0 + 16, BS + ((c + 1) & 1) * 16 * SW);
+            Bs = BS + (c & 1) * 16 * SW;
         } else {
             Bs = Wsm + (int64_t)k0 * SW;
         }
