@@ -477,6 +477,43 @@ __device__ __forceinline__ void tlr_seg_gemm(double (&c)[4][4][2], const double 
     }
 }
 
+__device__ __forceinline__ void tlr_cp16(void *smem, const void *gmem, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes));
+}
+
+// acc(64 x 64 block at (m0, n0)) += A B over k < K for operands contiguous along the staged rows,
+// A(m, k) = A[k 128 + m], B(k, n) = B[k 128 + n] (the expansions U V^T and the accumulation Z U^T):
+// a 2-stage cp.async double buffer (rows k >= K zero-filled), one barrier per chunk
+__device__ __forceinline__ void tlr_seg_gemm_async(double (&c)[4][4][2], const double *__restrict__ A,
+                                                   const double *__restrict__ B, int K, int m0, int n0, double *As2,
+                                                   double *Bs2) {
+    using namespace tlrg;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 32;
+    const int nch = (K + BK - 1) / BK;
+    if (nch == 0) return;
+    auto issue = [&](int ch, int st) {
+        const int k0 = ch * BK;
+        double *as = As2 + st * BK * SA, *bs = Bs2 + st * BK * SB;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {                     // 16 rows x 32 pieces of 16 bytes, each operand
+            const int e = tid + q * NT, kk = e >> 5, pc = e & 31;
+            const bool in = k0 + kk < K;
+            tlr_cp16(as + kk * SA + 2 * pc, in ? A + (int64_t)(k0 + kk) * 128 + m0 + 2 * pc : A, in ? 16 : 0);
+            tlr_cp16(bs + kk * SB + 2 * pc, in ? B + (int64_t)(k0 + kk) * 128 + n0 + 2 * pc : B, in ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+    __syncthreads();                                      // the previous segment's readers are done
+    issue(0, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+        cp_async_wait<0>();
+        __syncthreads();                                  // chunk ch landed; chunk ch - 1's readers are done
+        if (ch + 1 < nch) issue(ch + 1, (ch + 1) & 1);
+        mma_chunk<BK, SA, SB, 4, 4>(As2 + (ch & 1) * BK * SA, Bs2 + (ch & 1) * BK * SB, wm0, wn0, lane, c);
+    }
+}
+
 struct TlrGemm {
     int mode = 0, nt = 0, j = 0, k0 = 0, kc = 0, kmax = 0, nsplit = 1;
     double *tiles = nullptr, *pnl = nullptr, *U = nullptr, *V = nullptr, *Mw = nullptr, *Zw = nullptr;
@@ -488,7 +525,9 @@ struct TlrGemm {
 template <int MODE>
 __global__ void __launch_bounds__(tlrg::NT) k_tlr_gemm(const TlrGemm g) {
     using namespace tlrg;
-    __shared__ __align__(16) double As[BK * SA], Bs[BK * SB];
+    __shared__ __align__(16) double smb[2 * BK * (SA + SB)];
+    double *As = smb, *Bs = smb + BK * SA;              // register-staged path (M, Z)
+    double *As2 = smb, *Bs2 = smb + 2 * BK * SA;        // cp.async path (expansions, accumulation)
     const int m0 = (blockIdx.y & 1) * BM, n0 = (blockIdx.y >> 1) * BN;
     const int64_t e = blockIdx.x, S = (int64_t)128 * g.kmax, T2 = (int64_t)128 * 128;
     double c[4][4][2];
@@ -512,8 +551,8 @@ __global__ void __launch_bounds__(tlrg::NT) k_tlr_gemm(const TlrGemm g) {
             while ((int64_t)(I + 1) * I / 2 <= t) ++I;
             C = g.tiles + tile_offset(I, t - (int64_t)I * (I - 1) / 2);
         }
-        tlr_seg_gemm<false, false>(c, g.U + t * S, g.V + t * S, MODE == kExpandPanel ? g.ranks_s[t] : g.ranks[t], 128, 128,
-                                   m0, n0, As, Bs);
+        tlr_seg_gemm_async(c, g.U + t * S, g.V + t * S, MODE == kExpandPanel ? g.ranks_s[t] : g.ranks[t], m0, n0, As2,
+                           Bs2);
     } else if (MODE == kM || MODE == kZ) {
         const int64_t i = g.j + e / g.kc, k = g.k0 + e % g.kc;
         const int64_t tik = i * (i - 1) / 2 + k, tjk = (int64_t)g.j * (g.j - 1) / 2 + k;
@@ -544,8 +583,7 @@ __global__ void __launch_bounds__(tlrg::NT) k_tlr_gemm(const TlrGemm g) {
         }
         for (int kk = kb; kk < ke; ++kk) {
             const int64_t tjk = (int64_t)g.j * (g.j - 1) / 2 + g.k0 + kk;
-            tlr_seg_gemm<false, false>(c, g.Zw + (ii * g.kc + kk) * T2, g.U + tjk * S, g.ranks[tjk], 128, 128, m0, n0,
-                                       As, Bs);
+            tlr_seg_gemm_async(c, g.Zw + (ii * g.kc + kk) * T2, g.U + tjk * S, g.ranks[tjk], m0, n0, As2, Bs2);
         }
     }
     // c[a][b][h]: row m0 + wm0 + 8a + lane/4, column n0 + wn0 + 8b + 2(lane%4) + h; C column-major (ld 128)
