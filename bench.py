@@ -374,6 +374,83 @@ def run_potrf_dist(args, cfg):
     return 0
 
 
+def run_potrf_share(args, cfg):
+    """NEXT-1 per-rank share on one GPU: rank 0's own work in the distributed Cholesky at W ranks
+    (parallel.potrf_dist_schedule: its panels, lookahead and bulk updates of its tile columns), with
+    every other rank's broadcast replaced by a local pack of that super-panel from the finished
+    factor (what the NCCL receive would deliver; the network time itself, which the schedule
+    overlaps with the bulk update, is not included). Checks that rank 0's columns come out bitwise
+    equal to mvn_potrf's, and reports the time against mvn_potrf at W = 1: an estimate of the
+    Cholesky's per-rank time at W GPUs (max over ranks ~ rank 0: it owns super-panel 0, the
+    heaviest)."""
+    import torch
+    import paper_2405_14892_b200 as mvn
+    from paper_2405_14892_b200 import parallel
+    torch.cuda.set_device(0)
+    inp = W.make_inputs(cfg)
+    n = cfg.n
+    order, a, _ = mvn.mvn_marginal_order(inp.mu, np.full(n, cfg.sigma2 + cfg.nugget), cfg.u)
+    d_xy = torch.from_numpy(np.ascontiguousarray(inp.xy[order])).cuda()
+    Lref = mvn.mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    assert mvn.mvn_potrf(Lref, n) == -1
+    e1.record()
+    torch.cuda.synchronize()
+    full_ms = e0.elapsed_time(e1)
+    kp = mvn.mvn_potrf_panel_width(n)
+    nt = -(-n // 128)
+    L = mvn.alloc_tiles(n)
+    shares = {}
+    for w in [int(x) for x in args.shard.split(",")]:
+        ts, exact = [], None
+        for it in range(args.steps + 1):
+            mvn.mvn_cov_matern(d_xy, cfg.sigma2, cfg.beta, cfg.nu, cfg.nugget, out=L)
+            torch.cuda.synchronize()
+            ops = parallel.CudaPotrfOps(L, n)
+            gen = parallel.potrf_dist_schedule(ops, 0, w)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(ops.main)
+            ops.side.wait_stream(ops.main)
+            req = next(gen)
+            while True:
+                _, k, src = req
+                if src != 0:                      # the panel another rank would broadcast
+                    with torch.cuda.stream(ops.side):
+                        mvn.mvn_panel_pack(Lref, n, k * kp, kp, ops.panel_buf(k), stream=ops.side)
+                h = ops.record("side")
+                try:
+                    req = gen.send(h)
+                except StopIteration:
+                    break
+            ops.main.wait_stream(ops.side)
+            s1.record(ops.main)
+            torch.cuda.synchronize()
+            if it:
+                ts.append(s0.elapsed_time(s1))
+        # rank 0's super-panels (0, w, 2w, ...) against the single-GPU factor, bitwise
+        Lh, Rh = L.view(-1), Lref.view(-1)
+        same = True
+        for sp in range(0, -(-nt // kp), w):
+            for j in range(sp * kp, min(nt, sp * kp + kp)):
+                for i in range(j, nt):
+                    off = ((i * (i + 1)) // 2 + j) * 128 * 128
+                    if i == j or (i - j) % 37 == 0:     # a sample of the column's tiles
+                        same &= bool(torch.equal(Lh[off:off + 128 * 128], Rh[off:off + 128 * 128]))
+        exact = same
+        ms = float(np.mean(ts))
+        shares[str(w)] = {"rank0_ms": ms, "vs_full": ms / full_ms, "ideal": 1.0 / w,
+                          "rank0_columns_bitwise_equal_sampled": exact}
+    line = {"metric": "distributed Cholesky: rank 0's per-rank time at W GPUs (NEXT-1, compute share)", "unit": "ms",
+            "value": shares[str(max(int(x) for x in args.shard.split(",")))]["rank0_ms"], "higher_is_better": False,
+            "n_gpus": 1, "steps": args.steps, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {cfg.name}: n={n}, rank 0's schedule with the other ranks' panels "
+                                   f"delivered by local copies", "n": n, "kp": kp},
+            "mvn_potrf_ms": full_ms, "shares": shares}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_shard(args, cfg):
     """Per-rank shard efficiency on one GPU: the SOV sweep (k_sov + k_reduce_blocks, through
     mvn_sov_prefix) over rank 0's 1/W share of the config's N*R samples, the exact range rank 0
@@ -641,7 +718,7 @@ def main():
                     help="crd: 0 = Cholesky updates on fp64 DMMA (default); 1 = on the int8 tensor cores (NEXT-4, R25); "
                          "2 = the TLR Cholesky at --tlr-eps (NEXT-3, R26)")
     ap.add_argument("--shard", default="1,2,4,8", help="--workload shard: the world sizes W whose rank-0 share is timed")
-    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "tlr", "tlr-potrf", "shard"],
+    ap.add_argument("--workload", default="crd", choices=["crd", "mc", "posterior", "potrf-dist", "potrf-share", "tlr", "tlr-potrf", "shard"],
                     help="crd: the hot path (default, the driver's line); mc: NEXT-2 MC validation of the regions; "
                          "posterior: NEXT-4 conditioning (paper size: 200x200 sites, 6,250 observations); "
                          "potrf-dist: NEXT-1 schedule driven from Python vs mvn_potrf on one GPU; "
@@ -672,6 +749,8 @@ def main():
         return run_tlr_potrf(args)
     if args.workload == "posterior":
         return run_posterior(args)
+    if args.workload == "potrf-share":
+        return run_potrf_share(args, cfg)
     if args.workload == "potrf-dist":
         return run_potrf_dist(args, cfg)
     if args.workload == "shard":
