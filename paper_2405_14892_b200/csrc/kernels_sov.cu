@@ -780,17 +780,63 @@ __global__ void __launch_bounds__(sovt::NTH, 1) k_sov_tlr(SovArgs p) {
     }
 }
 
-// K6: combine block partials per prefix in ascending block order.
-__global__ void k_reduce_blocks(const double *__restrict__ part, int64_t nblk, int64_t n, int64_t n_pad,
-                                double *__restrict__ Mo, double *__restrict__ So) {
+// K6: combine block partials per prefix in a fixed order (deterministic for a given nblk). A CTA
+// takes 32 prefixes (lane = prefix: 512-byte coalesced reads of the (max, sum) pairs) and RS
+// contiguous slices of the blocks (threadIdx.y); each thread combines its slice in ascending block
+// order, then lane-wise one warp combines the RS slice results in ascending slice order. One thread
+// per prefix looping over all ~890 blocks was 0.50 ms of config A's 4.7 ms step
+// (profiles/r02_sov_A_ncu.md).
+constexpr int RS = 16;
+__global__ void __launch_bounds__(32 * RS)
+k_reduce_blocks(const double *__restrict__ part, int64_t nblk, int64_t n, int64_t n_pad,
+                double *__restrict__ Mo, double *__restrict__ So) {
+    __shared__ double sm[RS][32], ss[RS][32];
+    const int lane = threadIdx.x, j = threadIdx.y;
+    const int64_t k = blockIdx.x * (int64_t)32 + lane;
+    const int64_t per = (nblk + RS - 1) / RS, b0 = j * per, b1 = b0 + per < nblk ? b0 + per : nblk;
+    double m = -CUDART_INF, s = 0.0;
+    if (k < n) {
+        const double2 *p = reinterpret_cast<const double2 *>(part) + k;
+#pragma unroll 4
+        for (int64_t b = b0; b < b1; ++b) m = fmax(m, p[b * n_pad].x);
+        if (m != -CUDART_INF) {
+#pragma unroll 4
+            for (int64_t b = b0; b < b1; ++b) {
+                const double2 v = p[b * n_pad];
+                if (v.x != -CUDART_INF) s += v.y * exp(v.x - m);
+            }
+        }
+    }
+    sm[j][lane] = m;
+    ss[j][lane] = s;
+    __syncthreads();
+    if (j != 0 || k >= n) return;
+    double mm = -CUDART_INF;
+#pragma unroll
+    for (int q = 0; q < RS; ++q) mm = fmax(mm, sm[q][lane]);
+    double t = 0.0;
+    if (mm != -CUDART_INF) {
+#pragma unroll
+        for (int q = 0; q < RS; ++q)
+            if (sm[q][lane] != -CUDART_INF) t += ss[q][lane] * exp(sm[q][lane] - mm);
+    }
+    Mo[k] = mm;
+    So[k] = t;
+}
+
+// The caller's per-unit partials (mvn_prefix_reduce): one thread per prefix, strictly ascending unit
+// order, (-inf, 0) units skipped, so the bits do not depend on how the units were split over ranks
+// or padded (SURVEY 8(e)'s deterministic combine; parallel.combine_units_deterministic).
+__global__ void k_reduce_units(const double *__restrict__ part, int64_t units, int64_t n,
+                               double *__restrict__ Mo, double *__restrict__ So) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     double m = -CUDART_INF;
-    for (int64_t b = 0; b < nblk; ++b) m = fmax(m, part[(b * n_pad + k) * 2]);
+    for (int64_t b = 0; b < units; ++b) m = fmax(m, part[(b * n + k) * 2]);
     double s = 0.0;
     if (m != -CUDART_INF)
-        for (int64_t b = 0; b < nblk; ++b) {
-            const double mb = part[(b * n_pad + k) * 2], sb = part[(b * n_pad + k) * 2 + 1];
+        for (int64_t b = 0; b < units; ++b) {
+            const double mb = part[(b * n + k) * 2], sb = part[(b * n + k) * 2 + 1];
             if (mb != -CUDART_INF) s += sb * exp(mb - m);
         }
     Mo[k] = m;
@@ -880,7 +926,12 @@ cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st) {
 
 cudaError_t launch_reduce_blocks(const double *part, int64_t nblk, int64_t n, int64_t n_pad, double *M, double *S,
                                  cudaStream_t st) {
-    k_reduce_blocks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nblk, n, n_pad, M, S);
+    k_reduce_blocks<<<(unsigned)((n + 31) / 32), dim3(32, RS), 0, st>>>(part, nblk, n, n_pad, M, S);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_units(const double *part, int64_t units, int64_t n, double *M, double *S, cudaStream_t st) {
+    k_reduce_units<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(part, units, n, M, S);
     return cudaGetLastError();
 }
 

@@ -793,7 +793,7 @@ mvn_status mvn_drows_unpack(mvn_ctx *c, mvn_dtiles d, const double *d_piece, int
 mvn_status mvn_prefix_reduce(mvn_ctx *c, int64_t n, int64_t units, const double *d_partial, double *d_M, double *d_S) {
     DevGuard dev_guard(c);
     if (!c || n < 1 || units < 1 || !d_partial || !d_M || !d_S) return fail(c, MVN_E_USAGE, "mvn_prefix_reduce: bad arguments");
-    MVN_CUDA(c, mvn::launch_reduce_blocks(d_partial, units, n, n, d_M, d_S, c->stream));
+    MVN_CUDA(c, mvn::launch_reduce_units(d_partial, units, n, d_M, d_S, c->stream));
     return MVN_OK;
 }
 

@@ -97,6 +97,7 @@ int64_t sov_partition_units(int64_t u0, int64_t u1, int64_t g_end, int grid, int
 cudaError_t launch_sov(const SovLaunch &L, cudaStream_t st);
 cudaError_t launch_reduce_blocks(const double *part, int64_t nblk, int64_t n, int64_t n_pad, double *M, double *S,
                                  cudaStream_t st);
+cudaError_t launch_reduce_units(const double *part, int64_t units, int64_t n, double *M, double *S, cudaStream_t st);
 
 // NEXT-4: the SOV GEMM on the int8 tensor cores (kernels_sov_oz.cu)
 struct SovOzLaunch {
