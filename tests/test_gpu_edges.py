@@ -134,3 +134,31 @@ def test_sov_block_widths(torch, per_cta):
     Mo, So = P.oracle_range(L, a, np.full(n, np.inf), N, R, 41, begin, end, nthreads=8)
     d = np.max(np.abs(logp(M, S, total) - logp(Mo, So, total)))
     assert d <= 1e-11, d
+
+
+# ---------------------------------------------------------------------- K6 block-slice boundaries
+@pytest.mark.parametrize("count", [2, 15, 16, 17, 31, 33, 47])
+def test_sov_reduce_slice_boundaries(torch, count):
+    """K6 (`k_reduce_blocks`) combines the block partials in 16 contiguous slices: sample counts
+    below the SM count give one sample block per sample, so `count` is the number of partials —
+    fewer than, equal to and just above the slice count, with empty and ragged last slices — against
+    the oracle in shared-L mode. The last limit (a = 60) puts every factor of the last prefix far below
+    the fp64 range (log P_n ~ -4,000: the log-space path of reading R10), so the partials combined
+    there differ by hundreds in their maxima."""
+    import test_gpu_parity as P
+    n = 70
+    rng = np.random.default_rng(300 + count)
+    xy = rng.uniform(size=(n, 2))
+    T = mvn().mvn_cov_matern(torch.from_numpy(xy).cuda(), 1.0, 0.2, 0.5, 1e-8)
+    assert mvn().mvn_potrf(T, n) == -1
+    a = np.sort(rng.uniform(-1.5, 0.5, n))
+    a[-1] = 60.0                                      # 1 - Phi(a') underflows fp64: log space only
+    N, R, seed = 40, 2, 23
+    begin, end = 11, 11 + count
+    M, S = P.gpu_sov(torch, T, n, a, N, R, seed, begin, end)
+    L = P.to_dense_lower(T, n)
+    Mo, So = P.oracle_range(L, a, np.full(n, np.inf), N, R, seed, begin, end, nthreads=2)
+    lg, lo = logp(M, S, count), logp(Mo, So, count)
+    assert np.all(np.isfinite(lo)) and lo[-1] < -1000.0 and np.all(np.isfinite(lg))
+    assert np.max(np.abs(lg[:-1] - lo[:-1])) <= 1e-11
+    assert abs(lg[-1] - lo[-1]) <= 1e-12 * abs(lo[-1]), (lg[-1], lo[-1])
